@@ -1,0 +1,302 @@
+#!/usr/bin/env python3
+"""Benchmark of the expmv hot path (BASELINE.json metric).
+
+A "step" is one full `series` call — the reference's time-series driver
+(expm.cpp:214-325) — over the BASELINE workload: by default config 2, G-QSW
+on the 32x32 periodic torus (dim 1,048,576, 42,991,616 nnz), 101 output
+times on [0, 20], populations extracted on the device at every output.
+
+  value     output steps/s with rho(0) and the superoperator resident in HBM
+            (assembly and norms excluded; reported separately)
+  e2e       the same through the public C ABI with host buffers: upload of
+            vec(rho(0)) from pinned memory + series + download of all
+            populations, every step
+  roofline  the fused series-term kernel (SpMV + axpys + norms): algorithmic
+            bytes per launch / mean launch time (CUDA events, same stream)
+
+Multi-GPU: one process per GPU under torchrun; the superoperator is
+row-sharded (strong scaling of one series).  `--impl reference` times the
+unmodified reference library (oracle/_ref) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "superop SpMV HBM GB/s (% roofline); expmv steps/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "output steps/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload_desc(w, extra=None):
+    d = {"workload": f"{w.name}: {'L-QSW' if w.kind == 'local' else 'G-QSW'} n={w.n} omega={w.omega} "
+                     f"t=[{w.t1},{w.tq}] outputs={w.steps + 1}",
+         "dim": w.dim, "outputs": w.steps + 1, "omega": w.omega, "kind": w.kind, "seed": w.seed,
+         "l2_policy": "inputs larger than L2 (CSR > 126 MB), no flush"}
+    d.update(extra or {})
+    return d
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return 0
+    from oracle.oracle import Oracle, rho0_vec
+    o = Oracle("reference")
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    h = o.build(w, workers=cores)
+    build_s = time.perf_counter() - t0
+    v0 = rho0_vec(w.n, w.rho0)
+    for _ in range(args.warmup):
+        h.series(v0, w.t1, w.tq, w.steps, states=False, pops=True)
+    times, spmvs = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, _, nsp = h.series(v0, w.t1, w.tq, w.steps, states=False, pops=True)
+        times.append(time.perf_counter() - t0)
+        spmvs = nsp
+    sec = float(np.mean(times))
+    value = w.steps / sec
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
+            "data": "synthetic (seeded, BASELINE.json config)",
+            "config": workload_desc(w, {"parallelism": f"{cores} host threads (reference WorkerPool)",
+                                        "build_norms_s": build_s, "spmvs_per_step": spmvs,
+                                        "library": os.path.relpath(o.path, ROOT)}),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"full {w.name} series ({w.steps + 1} outputs) per step, "
+                                       f"n_workers={cores}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(w):
+    """The reference on this box's host cores, one bounded sample (one full
+    series of the same workload)."""
+    from oracle.oracle import Oracle, rho0_vec
+    try:
+        o = Oracle("reference")
+        kind = "reference"
+    except FileNotFoundError:
+        o = Oracle("port")
+        kind = "port"
+    cores = (os.cpu_count() or 1) if kind == "reference" else 1
+    h = o.build(w, workers=cores) if kind == "reference" else o.build(w)
+    t0 = time.perf_counter()
+    _, _, nsp = h.series(rho0_vec(w.n, w.rho0), w.t1, w.tq, w.steps, states=False, pops=True)
+    sec = time.perf_counter() - t0
+    return {"value": w.steps / sec, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"one full {w.name} series ({w.steps + 1} outputs, {nsp} SpMVs) in {sec:.2f} s; "
+                      f"library {os.path.relpath(o.path, ROOT)}"}
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="qswg", choices=["qswg", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--size", type=int, default=None, help="shrink the graph (debug only)")
+    ap.add_argument("--group", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2003_02450_b200 import graphs
+    w = graphs.config(args.config, size=args.size)
+
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch
+    from paper_2003_02450_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        comm = api.Comm.create(rank, world, local_rank)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    t0 = time.perf_counter()
+    if w.kind == "local":
+        l = api.build_local(w.omega, w.h, w.ops[0], device=local_rank, group=args.group, comm=comm)
+    else:
+        l = api.build_global(w.omega, w.h, w.ops, device=local_rank, group=args.group, comm=comm)
+    barrier()
+    build_s = time.perf_counter() - t0
+
+    stream = torch.cuda.ExternalStream(l.stream(), device=torch.device("cuda", local_rank))
+    v = l.state().from_probabilities(w.rho0)
+
+    for _ in range(args.warmup):
+        r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
+
+    # ---- device-resident timed region ----
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        ev0.record(stream)
+        launches = 0
+        for _ in range(args.steps):
+            r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
+            launches += r.info.launches
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    info = r.info
+    value = w.steps / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API, host buffers ----
+    vec_host = torch.zeros(2 * l.rows, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    diag = np.arange(w.n) * (w.n + 1) - l.row0
+    own = (diag >= 0) & (diag < l.rows)
+    vec_host[diag[own]] = w.rho0[own]
+    full_vec = vec_host if world == 1 else None
+    pops_host = torch.zeros((w.steps + 1) * w.n, dtype=torch.float64, pin_memory=True).numpy().reshape(w.steps + 1, w.n)
+    e2e_state = l.state()
+    for _ in range(1):
+        e2e_state.upload_local(vec_host)
+        api.series(l, e2e_state, w.t1, w.tq, w.steps, pops_out=pops_host)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e2e_state.upload_local(vec_host)                                   # H2D of vec(rho(0))
+        api.series(l, e2e_state, w.t1, w.tq, w.steps, pops_out=pops_host)  # + D2H populations
+    ev1.record(stream)
+    barrier()
+    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    del full_vec
+
+    # ---- roofline of the dominant kernel (fused series term) ----
+    d_active = int(info.d) if info.path == 2 else 1
+    term_ms = l.time_series_term(iters=20, count=d_active)
+    nnz_local = int(l.info.nnz_local)
+    term_bytes = 20 * nnz_local + 8 * (l.rows + 1) + 16 * l.dim + 16 * l.rows + 32 * d_active * l.rows
+    peak, peak_src = load_peaks()
+    achieved = term_bytes / (term_ms * 1e-3) / 1e9
+    share = info.spmvs * term_ms / ms_per_step
+
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "complex128",
+        "data": "synthetic (seeded graph of BASELINE.json config; no public dataset exists for this path)",
+        "config": workload_desc(w, {
+            "parallelism": f"row-block x{world}" if world > 1 else "1 GPU", "nnz": int(l.nnz),
+            "build_norms_s": build_s, "one_norms": l.one_norms().tolist(), "group": int(l.group),
+            "plan": {"path": int(info.path), "span": [int(info.span_m_star), int(info.span_s)],
+                     "d": int(info.d), "n_super": int(info.n_super), "remainder": int(info.remainder),
+                     "sub_m_star": int(info.sub_m_star)},
+            "spmvs_per_step": int(info.spmvs)}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "series_term_kernel",
+                     "bytes_per_launch": term_bytes, "ms_per_launch": term_ms, "peak_source": peak_src,
+                     "share_of_step": share},
+        "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,
+                "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,157 @@
+/* qswg — B200-native Lindblad expmv for quantum stochastic walks: C ABI.
+ *
+ * The drop-in boundary for the reference's hot path.  The
+ * reference (/root/reference/proj, C++20) exposes no plugin/FFI layer; its
+ * boundary is the C++ library surface below, and every entry point here names
+ * the reference declaration it replaces (paths under proj/core/include/qsw/).
+ * INTEGRATION.md shows the ctypes / C++ bindings a maintainer would add.
+ *
+ * Conventions
+ *  - Complex values are interleaved (re, im) doubles; indices are int64.
+ *  - vec(rho) is column-major: element k = n*j + i holds rho(i, j)
+ *    (state.hpp:10-12).
+ *  - Host arrays passed in are borrowed for the duration of the call.
+ *  - Handles own device memory; they are not thread-safe per handle.
+ *  - Every function returns QSWG_OK or an error code; qswg_last_error()
+ *    returns the thread-local message.  No exception crosses the ABI.
+ *  - There is no CPU fallback: without a CUDA device the device entry points
+ *    fail with QSWG_ECUDA.
+ */
+#ifndef QSWG_H
+#define QSWG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSWG_VERSION_MAJOR 0
+#define QSWG_VERSION_MINOR 1
+
+enum {
+  QSWG_OK = 0,
+  QSWG_EINVAL = 1,     /* std::invalid_argument  */
+  QSWG_ERANGE = 2,     /* std::out_of_range      */
+  QSWG_ENUMERICAL = 3, /* qsw::NumericalError    */
+  QSWG_ESTATE = 4,     /* std::logic_error       */
+  QSWG_ECUDA = 5,
+  QSWG_ENCCL = 6,
+  QSWG_ENOMEM = 7,
+  QSWG_EINTERNAL = 9
+};
+
+typedef struct qswg_sparse qswg_sparse;           /* host canonical CSR, complex128 */
+typedef struct qswg_liouvillian qswg_liouvillian; /* device superoperator (row block) */
+typedef struct qswg_state qswg_state;             /* device vec(rho) (row block)     */
+typedef struct qswg_comm qswg_comm;               /* multi-GPU communicator          */
+
+typedef struct { int64_t target; double rate; } qswg_source_arc; /* graph.hpp:17-20 SourceArc */
+typedef struct { int64_t origin; double rate; } qswg_sink_arc;   /* graph.hpp:23-26 SinkArc   */
+
+typedef struct {
+  int device;       /* CUDA ordinal */
+  int group;        /* SpMV lanes per row (2..32); 1 = bitwise reference order; 0 = autotune */
+  qswg_comm* comm;  /* NULL for one GPU */
+} qswg_device_config;
+
+typedef struct {
+  int64_t n, dim, nnz, nnz_local, row0, rows;
+  double omega;
+  double one_norms[9]; /* DistributedLiouvillian::one_norms(), liouvillian.hpp:31 */
+  int group, device, rank, world;
+} qswg_liouvillian_info;
+
+typedef struct { int64_t m_star, s, spmvs, launches; } qswg_step_info;
+
+typedef struct {
+  int path; /* 0 zero generator, 1 sequential steps, 2 shared-term super-steps */
+  int64_t span_m_star, span_s, d, n_super, remainder, sub_m_star, spmvs;
+  int64_t launches; /* qswg kernels enqueued by the call */
+  double device_ms; /* CUDA-event time of the whole series on the library stream */
+} qswg_series_info;
+
+const char* qswg_last_error(void);
+int qswg_version(int* major, int* minor);
+int qswg_device_count(int* count);
+
+/* ---- host sparse matrices (sparse.hpp:29-84) ---------------------------- */
+/* SparseMatrix::from_triplets (sparse.hpp:35-37): sort, sum duplicates, drop zeros. */
+int qswg_sparse_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t* row,
+                              const int64_t* col, const double* val, qswg_sparse** out);
+/* Canonicalising import of CSR arrays. */
+int qswg_sparse_from_csr(int64_t rows, int64_t cols, const int64_t* rowptr, const int64_t* col,
+                         const double* val, qswg_sparse** out);
+int qswg_sparse_shape(const qswg_sparse* m, int64_t* rows, int64_t* cols, int64_t* nnz);
+int qswg_sparse_export(const qswg_sparse* m, int64_t* rowptr, int64_t* col, double* val);
+void qswg_sparse_destroy(qswg_sparse* m);
+
+/* ---- graph -> operators (graph.hpp:78-96, operators.hpp:53-57) ---------- */
+int qswg_symmetrize(const qswg_sparse* adjacency, qswg_sparse** out);
+int qswg_generator_matrix(double gamma, const qswg_sparse* adjacency, qswg_sparse** out);
+int qswg_markov_chain_matrix(const qswg_sparse* adjacency, qswg_sparse** out);
+int qswg_local_lindblad(const qswg_sparse* m, qswg_sparse** out);
+int qswg_augment(const qswg_sparse* adjacency, const qswg_source_arc* sources, int64_t n_sources,
+                 const qswg_sink_arc* sinks, int64_t n_sinks, qswg_sparse** out);
+
+/* ---- superoperator (liouvillian.hpp:65-93) ------------------------------ */
+/* build_local(omega, h, m_l, sources, sinks, n_workers), liouvillian.hpp:65-71 */
+int qswg_build_local(double omega, const qswg_sparse* h, const qswg_sparse* m_l,
+                     const qswg_source_arc* sources, int64_t n_sources, const qswg_sink_arc* sinks,
+                     int64_t n_sinks, const qswg_device_config* cfg, qswg_liouvillian** out);
+/* build_global(omega, h, lindblads, h_rot, n_workers), liouvillian.hpp:73-85 */
+int qswg_build_global(double omega, const qswg_sparse* h, const qswg_sparse* const* lindblads,
+                      int64_t n_lindblads, const qswg_sparse* h_rot /* nullable */,
+                      const qswg_device_config* cfg, qswg_liouvillian** out);
+int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* info);
+/* gather_full() of the local row block (liouvillian.hpp:34): rowptr[rows+1], col[nnz_local], val[2*nnz_local] */
+int qswg_liouvillian_download(const qswg_liouvillian* l, int64_t* rowptr, int64_t* col, double* val);
+void qswg_liouvillian_destroy(qswg_liouvillian* l);
+/* spmv(l, x), liouvillian.hpp:93: y = L x; x: dim complex (host), y: rows complex (host) */
+int qswg_spmv(const qswg_liouvillian* l, const double* x, double* y);
+/* Mean device time of one plain SpMV kernel over `iters` back-to-back launches. */
+int qswg_time_spmv(const qswg_liouvillian* l, int iters, int group, double* ms);
+/* Mean device time of one fused series-term kernel (SpMV + `count` axpys +
+ * norms) over `iters` back-to-back launches on the library stream. */
+int qswg_time_series_term(const qswg_liouvillian* l, int iters, int count, double* ms);
+/* The CUDA stream (cudaStream_t) every kernel of this handle runs on. */
+int qswg_liouvillian_stream(const qswg_liouvillian* l, void** stream);
+
+/* ---- states (state.hpp:13-27, walk.hpp:57-66) --------------------------- */
+int qswg_state_create(const qswg_liouvillian* l, qswg_state** out);
+/* StateVector::scatter(full) — uploads this rank's rows of a full host vec(rho) */
+int qswg_state_upload(qswg_state* s, const double* vec);
+/* WalkSystem::initial_state(probabilities) (walk.cpp:101-126), built on the device */
+int qswg_state_from_probabilities(qswg_state* s, const double* p, int64_t n);
+/* StateVector::gather() of this rank's rows */
+int qswg_state_download(const qswg_state* s, double* vec);
+/* populations_of(state) (walk.cpp:177-186): out[n] (zeros for diagonals owned by other ranks) */
+int qswg_state_populations(const qswg_state* s, double* out);
+void qswg_state_destroy(qswg_state* s);
+
+/* ---- Taylor parameters (expm.hpp:19-45) --------------------------------- */
+int qswg_theta_table(double tolerance, double* theta55);
+int qswg_select_parameters(const double* one_norms9, double t, double tolerance, int64_t* m_star,
+                           int64_t* s);
+
+/* ---- evolution (expm.hpp:47-63) ----------------------------------------- */
+/* out = exp(t L) v  (qsw::step). out must be a distinct state of the same L. */
+int qswg_step(const qswg_liouvillian* l, const qswg_state* v, double t, double tolerance,
+              qswg_state* out, qswg_step_info* info);
+/* qsw::series over [t1, tq] with `steps` intervals.  pops_host: (steps+1)*n
+ * doubles or NULL (populations then stay on the device); states_host:
+ * (steps+1)*rows complex or NULL; final_state: receives the tq state or NULL. */
+int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, double tq, int64_t steps,
+                double tolerance, double* pops_host, double* states_host, qswg_state* final_state,
+                qswg_series_info* info);
+
+/* ---- multi-GPU (one process per GPU) ------------------------------------ */
+int qswg_comm_unique_id_size(void);
+int qswg_comm_get_unique_id(uint8_t* id);
+int qswg_comm_create(const uint8_t* id, int rank, int world, int device, qswg_comm** out);
+void qswg_comm_destroy(qswg_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSWG_H */

@@ -1,0 +1,544 @@
+// extern "C" boundary (include/qswg.h).  Exceptions are mapped to codes
+// exactly as the reference's exception classes:
+//   std::invalid_argument -> QSWG_EINVAL, std::out_of_range -> QSWG_ERANGE,
+//   NumericalError -> QSWG_ENUMERICAL, std::logic_error -> QSWG_ESTATE,
+//   CUDA failures -> QSWG_ECUDA, allocation -> QSWG_ENOMEM.
+#include "../../include/qswg.h"
+
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "host/comm.hpp"
+#include "host/device.hpp"
+#include "host/expm.hpp"
+#include "host/graph.hpp"
+#include "host/liouvillian.hpp"
+#include "host/sparse.hpp"
+#include "host/taylor.hpp"
+
+struct qswg_sparse {
+  qswg::SparseMatrix m;
+};
+struct qswg_liouvillian {
+  std::unique_ptr<qswg::Liouvillian> l;
+  qswg::DeviceBuffer<double> pops;  // (steps + 1) * n populations of the last series
+};
+struct qswg_state {
+  const qswg_liouvillian* owner;
+  qswg::DeviceBuffer<double2> v;  // local rows
+};
+
+namespace qswg {
+Comm* comm_from_handle(qswg_comm* c);                       // comm_nccl.cpp
+int comm_create(const uint8_t* id, int rank, int world, int device, qswg_comm** out);
+void comm_destroy(qswg_comm* c);
+int comm_unique_id_size();
+int comm_get_unique_id(uint8_t* id);
+}  // namespace qswg
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_err.clear();
+    f();
+    return QSWG_OK;
+  } catch (const qswg::NumericalError& e) {
+    return fail(QSWG_ENUMERICAL, e.what());
+  } catch (const std::out_of_range& e) {
+    return fail(QSWG_ERANGE, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(QSWG_EINVAL, e.what());
+  } catch (const std::logic_error& e) {
+    return fail(QSWG_ESTATE, e.what());
+  } catch (const qswg::CudaError& e) {
+    return fail(QSWG_ECUDA, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(QSWG_ENOMEM, "out of memory");
+  } catch (const std::exception& e) {
+    return fail(QSWG_EINTERNAL, e.what());
+  } catch (...) {
+    return fail(QSWG_EINTERNAL, "unknown error");
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + " must not be NULL");
+}
+
+qswg::DeviceConfig device_config(const qswg_device_config* cfg) {
+  qswg::DeviceConfig c;
+  if (cfg) {
+    c.device = cfg->device;
+    c.group = cfg->group;
+    c.comm = cfg->comm ? qswg::comm_from_handle(cfg->comm) : nullptr;
+  } else {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    c.device = dev;
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw qswg::CudaError("no CUDA device available (qswg has no CPU fallback)");
+  }
+  if (c.device < 0 || c.device >= count) throw std::invalid_argument("CUDA device ordinal out of range");
+  return c;
+}
+
+qswg_sparse* wrap(qswg::SparseMatrix m) { return new qswg_sparse{std::move(m)}; }
+
+void check_state(const qswg_liouvillian* l, const qswg_state* s, const char* what) {
+  need(s, what);
+  if (s->owner != l) throw std::invalid_argument("state vector partition does not match the Liouvillian");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qswg_last_error(void) { return g_err.c_str(); }
+
+int qswg_version(int* major, int* minor) {
+  return guarded([&] {
+    need(major, "major");
+    need(minor, "minor");
+    *major = QSWG_VERSION_MAJOR;
+    *minor = QSWG_VERSION_MINOR;
+  });
+}
+
+int qswg_device_count(int* count) {
+  return guarded([&] {
+    need(count, "count");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+// ---------------------------------------------------------------- sparse
+int qswg_sparse_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t* row,
+                              const int64_t* col, const double* val, qswg_sparse** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (count < 0) throw std::invalid_argument("negative triplet count");
+    std::vector<qswg::Triplet> t(static_cast<std::size_t>(count));
+    for (int64_t k = 0; k < count; ++k)
+      t[static_cast<std::size_t>(k)] = {row[k], col[k], qswg::Complex{val[2 * k], val[2 * k + 1]}};
+    *out = wrap(qswg::SparseMatrix::from_triplets(rows, cols, std::move(t)));
+  });
+}
+
+int qswg_sparse_from_csr(int64_t rows, int64_t cols, const int64_t* rowptr, const int64_t* col,
+                         const double* val, qswg_sparse** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(rowptr, "rowptr");
+    *out = wrap(qswg::SparseMatrix::from_csr(rows, cols, rowptr, col, val));
+  });
+}
+
+int qswg_sparse_shape(const qswg_sparse* m, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  return guarded([&] {
+    need(m, "matrix");
+    if (rows) *rows = m->m.rows();
+    if (cols) *cols = m->m.cols();
+    if (nnz) *nnz = m->m.nnz();
+  });
+}
+
+int qswg_sparse_export(const qswg_sparse* m, int64_t* rowptr, int64_t* col, double* val) {
+  return guarded([&] {
+    need(m, "matrix");
+    const auto& rs = m->m.row_starts();
+    if (rowptr) std::memcpy(rowptr, rs.data(), rs.size() * sizeof(int64_t));
+    if (col) std::memcpy(col, m->m.col_indices().data(), m->m.col_indices().size() * sizeof(int64_t));
+    if (val) std::memcpy(val, m->m.values().data(), m->m.values().size() * sizeof(qswg::Complex));
+  });
+}
+
+void qswg_sparse_destroy(qswg_sparse* m) { delete m; }
+
+// ---------------------------------------------------------------- graph
+int qswg_symmetrize(const qswg_sparse* a, qswg_sparse** out) {
+  return guarded([&] {
+    need(a, "adjacency");
+    need(out, "out");
+    *out = wrap(qswg::symmetrize(a->m));
+  });
+}
+
+int qswg_generator_matrix(double gamma, const qswg_sparse* a, qswg_sparse** out) {
+  return guarded([&] {
+    need(a, "adjacency");
+    need(out, "out");
+    *out = wrap(qswg::generator_matrix(gamma, a->m));
+  });
+}
+
+int qswg_markov_chain_matrix(const qswg_sparse* a, qswg_sparse** out) {
+  return guarded([&] {
+    need(a, "adjacency");
+    need(out, "out");
+    *out = wrap(qswg::markov_chain_matrix(a->m));
+  });
+}
+
+int qswg_local_lindblad(const qswg_sparse* m, qswg_sparse** out) {
+  return guarded([&] {
+    need(m, "matrix");
+    need(out, "out");
+    *out = wrap(qswg::local_lindblad(m->m));
+  });
+}
+
+int qswg_augment(const qswg_sparse* a, const qswg_source_arc* sources, int64_t n_sources,
+                 const qswg_sink_arc* sinks, int64_t n_sinks, qswg_sparse** out) {
+  return guarded([&] {
+    need(a, "adjacency");
+    need(out, "out");
+    std::vector<qswg::SourceArc> src;
+    std::vector<qswg::SinkArc> snk;
+    for (int64_t k = 0; k < n_sources; ++k) src.push_back({sources[k].target, sources[k].rate});
+    for (int64_t k = 0; k < n_sinks; ++k) snk.push_back({sinks[k].origin, sinks[k].rate});
+    *out = wrap(qswg::augment(a->m, src, snk));
+  });
+}
+
+// ---------------------------------------------------------- liouvillian
+int qswg_build_local(double omega, const qswg_sparse* h, const qswg_sparse* m_l,
+                     const qswg_source_arc* sources, int64_t n_sources, const qswg_sink_arc* sinks,
+                     int64_t n_sinks, const qswg_device_config* cfg, qswg_liouvillian** out) {
+  return guarded([&] {
+    need(h, "h");
+    need(m_l, "m_l");
+    need(out, "out");
+    if (n_sources < 0 || n_sinks < 0) throw std::invalid_argument("negative source/sink count");
+    std::vector<qswg::SourceArc> src;
+    std::vector<qswg::SinkArc> snk;
+    for (int64_t k = 0; k < n_sources; ++k) src.push_back({sources[k].target, sources[k].rate});
+    for (int64_t k = 0; k < n_sinks; ++k) snk.push_back({sinks[k].origin, sinks[k].rate});
+    const qswg::DeviceConfig c = device_config(cfg);
+    auto l = std::make_unique<qswg_liouvillian>();
+    l->l = qswg::build_local(omega, h->m, m_l->m, src, snk, c);
+    *out = l.release();
+  });
+}
+
+int qswg_build_global(double omega, const qswg_sparse* h, const qswg_sparse* const* lindblads,
+                      int64_t n_lindblads, const qswg_sparse* h_rot, const qswg_device_config* cfg,
+                      qswg_liouvillian** out) {
+  return guarded([&] {
+    need(h, "h");
+    need(out, "out");
+    if (n_lindblads < 0) throw std::invalid_argument("negative Lindblad count");
+    std::vector<qswg::SparseMatrix> ls;
+    for (int64_t k = 0; k < n_lindblads; ++k) {
+      need(lindblads[k], "lindblad operator");
+      ls.push_back(lindblads[k]->m);
+    }
+    std::optional<qswg::SparseMatrix> hr;
+    if (h_rot) hr = h_rot->m;
+    const qswg::DeviceConfig c = device_config(cfg);
+    auto l = std::make_unique<qswg_liouvillian>();
+    l->l = qswg::build_global(omega, h->m, ls, hr, c);
+    *out = l.release();
+  });
+}
+
+int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* info) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(info, "info");
+    const qswg::Liouvillian& L = *l->l;
+    info->n = L.n();
+    info->dim = L.dim();
+    info->nnz = L.nnz_total();
+    info->nnz_local = L.nnz_local();
+    info->row0 = L.block().row0;
+    info->rows = L.block().rows;
+    info->omega = L.omega();
+    for (int p = 0; p < 9; ++p) info->one_norms[p] = L.one_norms()[static_cast<std::size_t>(p)];
+    info->group = L.group();
+    info->device = L.device();
+    info->rank = L.comm() ? L.comm()->rank() : 0;
+    info->world = L.comm() ? L.comm()->world() : 1;
+  });
+}
+
+int qswg_liouvillian_download(const qswg_liouvillian* l, int64_t* rowptr, int64_t* col, double* val) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    std::vector<int64_t> rp, c;
+    std::vector<qswg::Complex> v;
+    l->l->download(rp, c, v);
+    if (rowptr) std::memcpy(rowptr, rp.data(), rp.size() * sizeof(int64_t));
+    if (col) std::memcpy(col, c.data(), c.size() * sizeof(int64_t));
+    if (val) std::memcpy(val, v.data(), v.size() * sizeof(qswg::Complex));
+  });
+}
+
+void qswg_liouvillian_destroy(qswg_liouvillian* l) {
+  if (!l) return;
+  try {
+    qswg::DeviceGuard g(l->l ? l->l->device() : 0);
+    l->pops.reset();
+    delete l;
+  } catch (...) {
+  }
+}
+
+int qswg_spmv(const qswg_liouvillian* l, const double* x, double* y) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(x, "x");
+    need(y, "y");
+    const qswg::Liouvillian& L = *l->l;
+    if (L.comm() && L.comm()->world() > 1) throw std::logic_error("qswg_spmv is single-GPU");
+    qswg::DeviceGuard g(L.device());
+    qswg::DeviceBuffer<double2> dx(static_cast<std::size_t>(L.dim())), dy(static_cast<std::size_t>(L.block().rows));
+    QSWG_CHECK(cudaMemcpyAsync(dx.get(), x, dx.bytes(), cudaMemcpyHostToDevice, L.stream()));
+    L.multiply(dx.get(), dy.get(), 1.0);
+    QSWG_CHECK(cudaMemcpyAsync(y, dy.get(), dy.bytes(), cudaMemcpyDeviceToHost, L.stream()));
+    QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+  });
+}
+
+int qswg_time_spmv(const qswg_liouvillian* l, int iters, int group, double* ms) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(ms, "ms");
+    if (iters < 1) throw std::invalid_argument("iters must be >= 1");
+    const int g = group ? group : l->l->group();
+    if (!qswg::dev::valid_group(g)) throw std::invalid_argument("group must be 1, 2, 4, 8, 16 or 32");
+    *ms = l->l->time_spmv(iters, g);
+  });
+}
+
+int qswg_time_series_term(const qswg_liouvillian* l, int iters, int count, double* ms) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(ms, "ms");
+    *ms = qswg::time_series_term(*l->l, iters, count);
+  });
+}
+
+int qswg_liouvillian_stream(const qswg_liouvillian* l, void** stream) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(stream, "stream");
+    *stream = static_cast<void*>(l->l->stream());
+  });
+}
+
+// ---------------------------------------------------------------- states
+int qswg_state_create(const qswg_liouvillian* l, qswg_state** out) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(out, "out");
+    qswg::DeviceGuard g(l->l->device());
+    auto s = std::make_unique<qswg_state>();
+    s->owner = l;
+    s->v.resize(static_cast<std::size_t>(std::max<int64_t>(l->l->block().rows, 1)));
+    QSWG_CHECK(cudaMemsetAsync(s->v.get(), 0, s->v.bytes(), l->l->stream()));
+    QSWG_CHECK(cudaStreamSynchronize(l->l->stream()));
+    *out = s.release();
+  });
+}
+
+int qswg_state_upload(qswg_state* s, const double* vec) {
+  return guarded([&] {
+    need(s, "state");
+    need(vec, "vec");
+    const qswg::Liouvillian& L = *s->owner->l;
+    qswg::DeviceGuard g(L.device());
+    QSWG_CHECK(cudaMemcpyAsync(s->v.get(), vec + 2 * L.block().row0,
+                               static_cast<std::size_t>(L.block().rows) * sizeof(double2),
+                               cudaMemcpyHostToDevice, L.stream()));
+    QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+  });
+}
+
+int qswg_state_from_probabilities(qswg_state* s, const double* p, int64_t n) {
+  return guarded([&] {
+    need(s, "state");
+    need(p, "probabilities");
+    const qswg::Liouvillian& L = *s->owner->l;
+    // walk.cpp:120-125
+    if (n != L.n()) throw std::invalid_argument("probability vector length " + std::to_string(n) +
+                                                " does not match the walk dimension");
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (p[i] < 0.0) throw std::invalid_argument("probabilities must be non-negative");
+      total += p[i];
+    }
+    if (std::abs(total - 1.0) > 1e-12) throw std::invalid_argument("probability vector is not normalized");
+    qswg::DeviceGuard g(L.device());
+    qswg::DeviceBuffer<double> dp(static_cast<std::size_t>(n));
+    QSWG_CHECK(cudaMemcpyAsync(dp.get(), p, dp.bytes(), cudaMemcpyHostToDevice, L.stream()));
+    qswg::dev::state_from_probabilities(s->v.get(), L.block().row0, L.block().rows, L.n(), dp.get(), L.stream());
+    QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+  });
+}
+
+int qswg_state_download(const qswg_state* s, double* vec) {
+  return guarded([&] {
+    need(s, "state");
+    need(vec, "vec");
+    const qswg::Liouvillian& L = *s->owner->l;
+    qswg::DeviceGuard g(L.device());
+    QSWG_CHECK(cudaMemcpyAsync(vec, s->v.get(), static_cast<std::size_t>(L.block().rows) * sizeof(double2),
+                               cudaMemcpyDeviceToHost, L.stream()));
+    QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+  });
+}
+
+int qswg_state_populations(const qswg_state* s, double* out) {
+  return guarded([&] {
+    need(s, "state");
+    need(out, "out");
+    const qswg::Liouvillian& L = *s->owner->l;
+    qswg::DeviceGuard g(L.device());
+    qswg::DeviceBuffer<double> d(static_cast<std::size_t>(L.n()));
+    QSWG_CHECK(cudaMemsetAsync(d.get(), 0, d.bytes(), L.stream()));
+    qswg::dev::diag_real(s->v.get(), L.block().row0, L.block().rows, L.n(), d.get(), L.stream());
+    QSWG_CHECK(cudaMemcpyAsync(out, d.get(), d.bytes(), cudaMemcpyDeviceToHost, L.stream()));
+    QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+  });
+}
+
+void qswg_state_destroy(qswg_state* s) {
+  if (!s) return;
+  try {
+    qswg::DeviceGuard g(s->owner->l->device());
+    delete s;
+  } catch (...) {
+  }
+}
+
+// ---------------------------------------------------------------- Taylor
+int qswg_theta_table(double tolerance, double* theta55) {
+  return guarded([&] {
+    need(theta55, "theta");
+    const auto& t = qswg::build_theta_table(tolerance);
+    std::memcpy(theta55, t.theta.data(), sizeof(double) * 55);
+  });
+}
+
+int qswg_select_parameters(const double* norms9, double t, double tolerance, int64_t* m_star, int64_t* s) {
+  return guarded([&] {
+    need(norms9, "one_norms");
+    need(m_star, "m_star");
+    need(s, "s");
+    const auto sp = qswg::select_parameters(norms9, t, qswg::build_theta_table(tolerance));
+    *m_star = sp.m_star;
+    *s = sp.s;
+  });
+}
+
+// ------------------------------------------------------------- evolution
+int qswg_step(const qswg_liouvillian* l, const qswg_state* v, double t, double tolerance, qswg_state* out,
+              qswg_step_info* info) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    check_state(l, v, "v");
+    check_state(l, out, "out");
+    if (out == v) throw std::invalid_argument("step output must not alias its input");
+    const auto& params = qswg::build_theta_table(tolerance);
+    const qswg::StepInfo si = qswg::step(*l->l, v->v.get(), t, params, out->v.get());
+    if (info) *info = {si.m_star, si.s, si.spmvs, si.launches};
+  });
+}
+
+int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, double tq, int64_t steps,
+                double tolerance, double* pops_host, double* states_host, qswg_state* final_state,
+                qswg_series_info* info) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    check_state(l, v, "v");
+    if (final_state) check_state(l, final_state, "final_state");
+    const auto& params = qswg::build_theta_table(tolerance);
+    qswg_liouvillian* lm = const_cast<qswg_liouvillian*>(l);
+    const qswg::Liouvillian& L = *l->l;
+    qswg::DeviceGuard g(L.device());
+    cudaStream_t s = L.stream();
+    const int64_t n = L.n(), rows = L.block().rows;
+    if (steps >= 1) {
+      lm->pops.resize(static_cast<std::size_t>((steps + 1) * n));
+      QSWG_CHECK(cudaMemsetAsync(lm->pops.get(), 0, lm->pops.bytes(), s));
+    }
+    cudaEvent_t e0, e1;
+    QSWG_CHECK(cudaEventCreate(&e0));
+    QSWG_CHECK(cudaEventCreate(&e1));
+    QSWG_CHECK(cudaEventRecord(e0, s));
+    int64_t emit_launches = 0;
+    auto emit = [&](int64_t k, const double2* state) {
+      ++emit_launches;
+      qswg::dev::diag_real(state, L.block().row0, rows, n, lm->pops.get() + k * n, s);
+      if (states_host)
+        QSWG_CHECK(cudaMemcpyAsync(states_host + 2 * rows * k, state, static_cast<std::size_t>(rows) * sizeof(double2),
+                                   cudaMemcpyDeviceToHost, s));
+      if (final_state && k == steps)
+        QSWG_CHECK(cudaMemcpyAsync(final_state->v.get(), state, static_cast<std::size_t>(rows) * sizeof(double2),
+                                   cudaMemcpyDeviceToDevice, s));
+    };
+    const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit);
+    QSWG_CHECK(cudaEventRecord(e1, s));
+    if (pops_host)
+      QSWG_CHECK(cudaMemcpyAsync(pops_host, lm->pops.get(), lm->pops.bytes(), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    QSWG_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (info) {
+      info->path = si.path;
+      info->span_m_star = si.span_m_star;
+      info->span_s = si.span_s;
+      info->d = si.d;
+      info->n_super = si.n_super;
+      info->remainder = si.remainder;
+      info->sub_m_star = si.sub_m_star;
+      info->spmvs = si.spmvs;
+      info->launches = si.launches + emit_launches;
+      info->device_ms = ms;
+    }
+  });
+}
+
+// ------------------------------------------------------------------ comm
+int qswg_comm_unique_id_size(void) { return qswg::comm_unique_id_size(); }
+int qswg_comm_get_unique_id(uint8_t* id) {
+  return guarded([&] {
+    need(id, "id");
+    const int rc = qswg::comm_get_unique_id(id);
+    if (rc) throw qswg::CudaError("ncclGetUniqueId failed");
+  });
+}
+int qswg_comm_create(const uint8_t* id, int rank, int world, int device, qswg_comm** out) {
+  int rc = QSWG_OK;
+  const int g = guarded([&] {
+    need(id, "id");
+    need(out, "out");
+    rc = qswg::comm_create(id, rank, world, device, out);
+  });
+  return g ? g : rc;
+}
+void qswg_comm_destroy(qswg_comm* c) { qswg::comm_destroy(c); }
+
+}  // extern "C"

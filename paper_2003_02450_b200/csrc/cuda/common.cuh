@@ -1,0 +1,83 @@
+// Shared device helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../host/device.hpp"
+
+namespace qswg::dev {
+
+inline void check(cudaError_t e, const char* what) { ::qswg::cuda_check(e, what); }
+
+#define QSWG_CUDA(x) ::qswg::dev::check((x), #x)
+#define QSWG_LAUNCH_CHECK(name) ::qswg::dev::check(cudaGetLastError(), name)
+
+constexpr int kThreads = 256;
+
+inline int sm_count() {
+  static thread_local int cached_dev = -1, cached = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    cached_dev = dev;
+  }
+  return cached > 0 ? cached : 148;
+}
+
+// Non-negative doubles order like their uint64 bit patterns; NaN patterns
+// sort above +Inf, so a max over bits flags any non-finite value.
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+__device__ __forceinline__ unsigned long long warp_max_bits(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// Block-wide max of bit patterns; result valid in thread 0. `red` holds >= 32.
+__device__ __forceinline__ unsigned long long block_max_bits(unsigned long long v,
+                                                             unsigned long long* red) {
+  v = warp_max_bits(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < static_cast<int>(blockDim.x >> 5) ? red[l] : 0ull;
+    v = warp_max_bits(v);
+  }
+  return v;
+}
+
+// Streaming loads for data touched once per SpMV (values, columns): no L1
+// allocation and an L2 evict-first policy, so L2 keeps the gathered vector.
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p, unsigned long long pol) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+      : "=d"(r.x), "=d"(r.y)
+      : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
+  int r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+}  // namespace qswg::dev

@@ -1,0 +1,228 @@
+// Host control flow of the exponential action.  Mirrors expm.cpp:146-325
+// step for step; every Taylor term is one fused kernel launch and every stop
+// test is evaluated on the device (see cuda/taylor.cu), so a whole step or
+// series is enqueued without host round-trips and synchronised once.
+#include "expm.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "comm.hpp"
+
+namespace qswg {
+
+namespace {
+
+// Workspace slots.
+enum Slot : std::size_t { kT0 = 0, kT1 = 1, kSOther = 2, kNext = 3, kZ = 4, kSums = 8 };
+
+dev::StepCtl* step_ctl(const Liouvillian& l) {
+  Workspace& ws = l.workspace();
+  if (!ws.step_ctl.get()) ws.step_ctl.resize(1);
+  return ws.step_ctl.get();
+}
+
+dev::SeriesCtl* series_ctl(const Liouvillian& l) {
+  Workspace& ws = l.workspace();
+  if (!ws.series_ctl.get()) ws.series_ctl.resize(1);
+  return ws.series_ctl.get();
+}
+
+struct Flags {
+  int error = 0;
+  std::int64_t spmvs = 0;
+};
+
+Flags read_flags(const Liouvillian& l, bool with_series) {
+  int se[2] = {0, 0}, re[2] = {0, 0};
+  cudaStream_t s = l.stream();
+  QSWG_CHECK(cudaMemcpyAsync(&se[0], &step_ctl(l)->error, sizeof(int), cudaMemcpyDeviceToHost, s));
+  QSWG_CHECK(cudaMemcpyAsync(&se[1], &step_ctl(l)->spmvs, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (with_series) {
+    QSWG_CHECK(cudaMemcpyAsync(&re[0], &series_ctl(l)->error, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaMemcpyAsync(&re[1], &series_ctl(l)->spmvs, sizeof(int), cudaMemcpyDeviceToHost, s));
+  }
+  QSWG_CHECK(cudaStreamSynchronize(s));
+  return {se[0] | re[0], static_cast<std::int64_t>(se[1]) + re[1]};
+}
+
+void reset_ctls(const Liouvillian& l, bool with_series) {
+  QSWG_CHECK(cudaMemsetAsync(step_ctl(l), 0, sizeof(dev::StepCtl), l.stream()));
+  if (with_series) QSWG_CHECK(cudaMemsetAsync(series_ctl(l), 0, sizeof(dev::SeriesCtl), l.stream()));
+}
+
+// Enqueues one step (expm.cpp:146-212) without synchronising.  `out` receives
+// the result; scratch vectors come from the workspace.
+StepParameters enqueue_step(const Liouvillian& l, const double2* v, double t,
+                            const TaylorParameters& params, double2* out, std::int64_t& launches) {
+  const std::int64_t len = l.dim();
+  cudaStream_t s = l.stream();
+  const StepParameters sp = select_parameters(l.one_norms().data(), t, params);
+  if (sp.m_star == 0) {  // expm.cpp:152
+    QSWG_CHECK(cudaMemcpyAsync(out, v, static_cast<std::size_t>(l.block().rows) * sizeof(double2),
+                               cudaMemcpyDeviceToDevice, s));
+    return sp;
+  }
+  Workspace& ws = l.workspace();
+  double2* term[2] = {ws.get(kT0, static_cast<std::size_t>(len)), ws.get(kT1, static_cast<std::size_t>(len))};
+  double2* sums[2];
+  // stage st accumulates into sums[st % 2]; the last stage lands in `out`.
+  sums[(sp.s - 1) % 2] = out;
+  sums[sp.s % 2] = ws.get(kSOther, static_cast<std::size_t>(len));
+  dev::StepCtl* ctl = step_ctl(l);
+  const dev::CsrView view = l.view();
+  dev::step_init(v, l.block().rows, ctl, s);  // c1 = ||v||_inf (expm.cpp:165-170)
+  launches += 1 + sp.s * sp.m_star;
+  const double s_count = static_cast<double>(sp.s);
+  for (std::int64_t st = 0; st < sp.s; ++st) {
+    // stage input: v, then the previous stage's sum (term = sum, expm.cpp:197-205)
+    const double2* x_stage = st == 0 ? v : sums[(st - 1) % 2];
+    double2* acc = sums[st % 2];
+    for (std::int64_t j = 1; j <= sp.m_star; ++j) {
+      const double2* x = j == 1 ? x_stage : term[(j - 1) % 2];
+      double2* y = term[j % 2];
+      const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
+      dev::step_term(view, l.group(), x, y, j == 1 ? x_stage : acc, acc, scale, j == 1,
+                     static_cast<int>(st), params.tolerance, ctl, s);
+    }
+  }
+  return sp;
+}
+
+}  // namespace
+
+StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorParameters& params,
+              double2* out) {
+  if (l.comm() && l.comm()->world() > 1) throw std::logic_error("multi-GPU step goes through step_dist");
+  DeviceGuard g(l.device());
+  reset_ctls(l, false);
+  std::int64_t launches = 0;
+  const StepParameters sp = enqueue_step(l, v, t, params, out, launches);
+  const Flags f = read_flags(l, false);
+  if (f.error) throw NumericalError("non-finite values encountered in exponential action");
+  return {sp.m_star, sp.s, f.spmvs, launches};
+}
+
+SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
+                  const TaylorParameters& params,
+                  const std::function<void(std::int64_t, const double2*)>& emit) {
+  // expm.cpp:216-217
+  if (!(tq > t1)) throw std::invalid_argument("series requires tq > t1");
+  if (steps < 1) throw std::invalid_argument("series requires at least one step");
+  if (l.comm() && l.comm()->world() > 1) throw std::logic_error("multi-GPU series goes through series_dist");
+  DeviceGuard g(l.device());
+  cudaStream_t s = l.stream();
+  const std::int64_t len = l.dim();
+  const std::int64_t q = steps;
+  const double h = (tq - t1) / static_cast<double>(q);
+  Workspace& ws = l.workspace();
+  reset_ctls(l, true);
+  SeriesInfo info;
+
+  // states[0] = step(v, t1) (expm.cpp:225)
+  double2* z = ws.get(kZ, static_cast<std::size_t>(len));
+  enqueue_step(l, v, t1, params, z, info.launches);
+  emit(0, z);
+
+  const StepParameters span = select_parameters(l.one_norms().data(), tq - t1, params);
+  info.span_m_star = span.m_star;
+  info.span_s = span.s;
+  if (span.m_star == 0) {  // zero generator (expm.cpp:228-232)
+    info.path = 0;
+    for (std::int64_t k = 1; k <= q; ++k) emit(k, z);
+  } else if (q <= span.s) {  // q sequential steps (expm.cpp:234-240)
+    info.path = 1;
+    double2* cur = z;
+    double2* nxt = ws.get(kNext, static_cast<std::size_t>(len));
+    for (std::int64_t k = 1; k <= q; ++k) {
+      enqueue_step(l, cur, h, params, nxt, info.launches);
+      emit(k, nxt);
+      std::swap(cur, nxt);
+    }
+  } else {  // super-steps sharing K_p = (hL)^p Z / p! (expm.cpp:242-323)
+    info.path = 2;
+    std::int64_t d = q / span.s;
+    const double d_cap = std::pow(1e280, 1.0 / static_cast<double>(TaylorParameters::m_max));
+    d = std::min(d, static_cast<std::int64_t>(d_cap));
+    const std::int64_t n_super = q / d;
+    const std::int64_t remainder = q - d * n_super;
+    const StepParameters sub = select_parameters(l.one_norms().data(), h * static_cast<double>(d), params);
+    const std::int64_t m_star = std::max<std::int64_t>(sub.m_star, 1);  // sub.s unused, as in the reference
+    info.d = d;
+    info.n_super = n_super;
+    info.remainder = remainder;
+    info.sub_m_star = m_star;
+    if (d > dev::kMaxSeriesD) throw std::logic_error("super-step size exceeds the device limit");
+
+    double2* kbuf[2] = {ws.get(kT0, static_cast<std::size_t>(len)), ws.get(kT1, static_cast<std::size_t>(len))};
+    std::vector<double2*> sums(static_cast<std::size_t>(d));
+    for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ws.get(kSums + static_cast<std::size_t>(k), static_cast<std::size_t>(len));
+    dev::SeriesCtl* ctl = series_ctl(l);
+    const dev::CsrView view = l.view();
+    for (std::int64_t super = 0; super <= n_super; ++super) {
+      const std::int64_t count = super < n_super ? d : remainder;
+      if (count == 0) break;
+      dev::series_init(z, l.block().rows, static_cast<int>(count), ctl, s);
+      info.launches += 1 + m_star;
+      dev::SeriesSums ss{};
+      for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
+      for (std::int64_t p = 1; p <= m_star; ++p) {
+        const double2* x = p == 1 ? z : kbuf[(p - 1) % 2];
+        double2* kp = kbuf[p % 2];
+        dev::series_term(view, l.group(), x, kp, z, ss, static_cast<int>(count), static_cast<int>(p),
+                         h / static_cast<double>(p), params.tolerance, ctl, s);
+      }
+      for (std::int64_t k = 1; k <= count; ++k) emit(super * d + k, sums[static_cast<std::size_t>(k - 1)]);
+      // the next super-step starts from states[(super + 1) d] = the last output
+      std::swap(z, sums[static_cast<std::size_t>(count - 1)]);
+    }
+  }
+  const Flags f = read_flags(l, info.path == 2);
+  info.spmvs = f.spmvs;
+  if (f.error) throw NumericalError("non-finite values encountered in series evolution");
+  return info;
+}
+
+double time_series_term(const Liouvillian& l, int iters, int count) {
+  if (count < 1 || count > dev::kMaxSeriesD) throw std::invalid_argument("count out of range");
+  if (iters < 1) throw std::invalid_argument("iters must be >= 1");
+  DeviceGuard g(l.device());
+  cudaStream_t s = l.stream();
+  const std::size_t len = static_cast<std::size_t>(l.dim());
+  Workspace& ws = l.workspace();
+  double2* k[2] = {ws.get(kT0, len), ws.get(kT1, len)};
+  double2* z = ws.get(kZ, len);
+  dev::SeriesSums ss{};
+  for (int c = 0; c < count; ++c) ss.s[c] = ws.get(kSums + static_cast<std::size_t>(c), len);
+  dev::fill_pattern(k[0], l.dim(), s);
+  dev::fill_pattern(z, l.dim(), s);
+  for (int c = 0; c < count; ++c) dev::fill_pattern(ss.s[c], l.dim(), s);
+  dev::SeriesCtl* ctl = series_ctl(l);
+  QSWG_CHECK(cudaMemsetAsync(ctl, 0, sizeof(dev::SeriesCtl), s));
+  dev::series_init(z, l.block().rows, count, ctl, s);
+  // tol = 0 keeps every output active (c1 + c2 <= 0 never holds for non-zero
+  // terms); scale 1/||L||_1 keeps the iterates bounded.
+  const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
+  auto launch = [&](int i) {
+    dev::series_term(l.view(), l.group(), k[i % 2], k[(i + 1) % 2], z, ss, count, 2 + (i % 2), scale, 0.0,
+                     ctl, s);
+  };
+  launch(0);  // warm-up
+  cudaEvent_t e0, e1;
+  QSWG_CHECK(cudaEventCreate(&e0));
+  QSWG_CHECK(cudaEventCreate(&e1));
+  QSWG_CHECK(cudaEventRecord(e0, s));
+  for (int i = 1; i <= iters; ++i) launch(i);
+  QSWG_CHECK(cudaEventRecord(e1, s));
+  QSWG_CHECK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  QSWG_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return static_cast<double>(ms) / iters;
+}
+
+}  // namespace qswg

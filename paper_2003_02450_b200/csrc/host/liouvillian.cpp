@@ -1,0 +1,496 @@
+// Superoperator construction: host operand preparation (small n x n
+// operators) + device assembly and norms.  Validation and the emitted values
+// follow proj/core/src/liouvillian.cpp (cited per block); the O(nnz) work
+// runs on the GPU (cuda/assemble.cu, cuda/norms.cu).
+#include "liouvillian.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <type_traits>
+#include <stdexcept>
+#include <string>
+
+#include "comm.hpp"
+
+namespace qswg {
+
+namespace {
+
+constexpr std::int64_t kExactNormDimLimit = 4096;  // liouvillian.cpp:13
+constexpr std::int64_t kMaxVertices = 46340;       // n^2 must fit int32 columns
+
+double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
+
+// Host-side multi-CSR (see dev::KronList): per-row entries in emission order,
+// stably sorted by column.
+struct MultiCsr {
+  std::int64_t n = 0;
+  std::vector<int> ptr, col;
+  std::vector<double2> val;
+  bool empty() const { return col.empty(); }
+};
+
+struct Entry {
+  std::int64_t row, col;
+  Complex v;
+};
+
+MultiCsr make_multi(std::int64_t n, const std::vector<Entry>& e) {
+  MultiCsr m;
+  m.n = n;
+  m.ptr.assign(static_cast<std::size_t>(n) + 1, 0);
+  for (const Entry& x : e) ++m.ptr[static_cast<std::size_t>(x.row) + 1];
+  std::partial_sum(m.ptr.begin(), m.ptr.end(), m.ptr.begin());
+  std::vector<std::size_t> order(e.size());
+  {
+    std::vector<int> cur(m.ptr.begin(), m.ptr.end() - 1);
+    for (std::size_t k = 0; k < e.size(); ++k) order[static_cast<std::size_t>(cur[static_cast<std::size_t>(e[k].row)]++)] = k;
+  }
+  for (std::int64_t i = 0; i < n; ++i) {
+    auto b = order.begin() + m.ptr[static_cast<std::size_t>(i)], en = order.begin() + m.ptr[static_cast<std::size_t>(i) + 1];
+    std::stable_sort(b, en, [&](std::size_t x, std::size_t y) { return e[x].col < e[y].col; });
+  }
+  m.col.resize(e.size());
+  m.val.resize(e.size());
+  for (std::size_t k = 0; k < e.size(); ++k) {
+    m.col[k] = static_cast<int>(e[order[k]].col);
+    m.val[k] = make_double2(e[order[k]].v.real(), e[order[k]].v.imag());
+  }
+  return m;
+}
+
+// Stable transpose: duplicates of one (i, c) keep their emission order.
+MultiCsr transpose_multi(const MultiCsr& a) {
+  std::vector<Entry> e;
+  e.reserve(a.col.size());
+  for (std::int64_t i = 0; i < a.n; ++i)
+    for (int k = a.ptr[static_cast<std::size_t>(i)]; k < a.ptr[static_cast<std::size_t>(i) + 1]; ++k)
+      e.push_back({a.col[static_cast<std::size_t>(k)], i,
+                   Complex{a.val[static_cast<std::size_t>(k)].x, a.val[static_cast<std::size_t>(k)].y}});
+  return make_multi(a.n, e);
+}
+
+MultiCsr from_sparse(const SparseMatrix& s, const std::function<Complex(Complex)>& f) {
+  std::vector<Entry> e;
+  e.reserve(static_cast<std::size_t>(s.nnz()));
+  for (std::int64_t i = 0; i < s.rows(); ++i)
+    for (std::int64_t k = s.row_begin(i); k < s.row_end(i); ++k)
+      e.push_back({i, s.col_indices()[static_cast<std::size_t>(k)], f(s.values()[static_cast<std::size_t>(k)])});
+  return make_multi(s.rows(), e);
+}
+
+void append_entries(std::vector<Entry>& e, const SparseMatrix& s, const std::function<Complex(Complex)>& f) {
+  for (std::int64_t i = 0; i < s.rows(); ++i)
+    for (std::int64_t k = s.row_begin(i); k < s.row_end(i); ++k)
+      e.push_back({i, s.col_indices()[static_cast<std::size_t>(k)], f(s.values()[static_cast<std::size_t>(k)])});
+}
+
+// Operands of L = I(x)A + B(x)I + sum_k P_k(x)Q_k + T_diag + decay (kernels.hpp).
+struct HostOperands {
+  std::int64_t n = 0;
+  MultiCsr a, b, t;
+  std::vector<MultiCsr> p, q;
+  std::vector<double> d_loc, d_ss;  // empty -> no decay term
+  double omega = 0.0;
+
+  HostOperands transposed() const {
+    HostOperands o;
+    o.n = n;
+    o.a = transpose_multi(a);
+    o.b = transpose_multi(b);
+    o.t = transpose_multi(t);
+    for (const auto& x : p) o.p.push_back(transpose_multi(x));
+    for (const auto& x : q) o.q.push_back(transpose_multi(x));
+    o.d_loc = d_loc;
+    o.d_ss = d_ss;
+    o.omega = omega;
+    return o;
+  }
+};
+
+// Device copy of HostOperands.
+class DeviceOperands {
+ public:
+  DeviceOperands(const HostOperands& h, cudaStream_t s) {
+    ops_.n = static_cast<int>(h.n);
+    ops_.a = upload(h.a, s);
+    ops_.b = upload(h.b, s);
+    ops_.t = upload(h.t, s);
+    ops_.nk = static_cast<int>(h.p.size());
+    for (std::size_t k = 0; k < h.p.size(); ++k) {
+      ops_.p[k] = upload(h.p[k], s, true);
+      ops_.q[k] = upload(h.q[k], s, true);
+    }
+    if (!h.d_loc.empty()) {
+      ops_.d_loc = upload_vec(h.d_loc, s);
+      ops_.d_ss = upload_vec(h.d_ss, s);
+    }
+    ops_.omega = h.omega;
+    QSWG_CHECK(cudaStreamSynchronize(s));
+  }
+  const dev::KronOperands& get() const { return ops_; }
+
+ private:
+  dev::KronList upload(const MultiCsr& m, cudaStream_t s, bool keep_empty = false) {
+    if (m.empty() && !keep_empty) return {};
+    dev::KronList l;
+    l.ptr = upload_vec(m.ptr, s);
+    l.col = m.col.empty() ? nullptr : upload_vec(m.col, s);
+    l.val = m.val.empty() ? nullptr : upload_vec(m.val, s);
+    return l;
+  }
+  template <class T>
+  const T* upload_vec(const std::vector<T>& v, cudaStream_t s) {
+    bufs_.emplace_back(v.size() * sizeof(T));
+    QSWG_CHECK(cudaMemcpyAsync(bufs_.back().get(), v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return reinterpret_cast<const T*>(bufs_.back().get());
+  }
+  dev::KronOperands ops_;
+  std::vector<DeviceBuffer<unsigned char>> bufs_;
+};
+
+void validate_common(double omega, const SparseMatrix& h) {
+  if (h.cols() != h.rows()) throw std::invalid_argument("Hamiltonian must be square");
+  if (!(omega >= 0.0 && omega <= 1.0)) throw std::invalid_argument("omega must be in [0, 1]");
+  if (!h.is_hermitian(hermiticity_tolerance(h))) throw std::invalid_argument("Hamiltonian must be Hermitian");
+  if (h.rows() > kMaxVertices)
+    throw std::invalid_argument("operator dimension " + std::to_string(h.rows()) +
+                                " exceeds the int32 column range of the device CSR");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ builder
+class LiouvillianBuilder {
+ public:
+  static std::unique_ptr<Liouvillian> build(double omega, std::int64_t n, const HostOperands& ops,
+                                            const DeviceConfig& cfg);
+};
+
+Liouvillian::~Liouvillian() {
+  if (stream_) {
+    DeviceGuard g(device_);
+    cudaStreamSynchronize(stream_);
+    rowptr_.reset();
+    col_.reset();
+    val_.reset();
+    ws_ = Workspace{};
+    cudaStreamDestroy(stream_);
+  }
+}
+
+dev::CsrView Liouvillian::view() const {
+  dev::CsrView v;
+  v.rowptr = rowptr_.get();
+  v.col = col_.get();
+  v.val = val_.get();
+  v.rows = block_.rows;
+  v.row0 = block_.row0;
+  return v;
+}
+
+void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
+                           std::vector<Complex>& val) const {
+  DeviceGuard g(device_);
+  rowptr.resize(static_cast<std::size_t>(block_.rows) + 1);
+  std::vector<int> c32(static_cast<std::size_t>(nnz_local_));
+  val.resize(static_cast<std::size_t>(nnz_local_));
+  QSWG_CHECK(cudaMemcpyAsync(rowptr.data(), rowptr_.get(), rowptr.size() * sizeof(std::int64_t),
+                             cudaMemcpyDeviceToHost, stream_));
+  if (nnz_local_) {
+    QSWG_CHECK(cudaMemcpyAsync(c32.data(), col_.get(), c32.size() * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    QSWG_CHECK(cudaMemcpyAsync(val.data(), val_.get(), val.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+  }
+  QSWG_CHECK(cudaStreamSynchronize(stream_));
+  col.assign(c32.begin(), c32.end());
+}
+
+void Liouvillian::multiply(const double2* x, double2* y, double scale) const {
+  DeviceGuard g(device_);
+  dev::spmv(view(), group_, x, y, scale, stream_);
+}
+
+double Liouvillian::time_spmv(int iters, int group) const {
+  DeviceGuard g(device_);
+  DeviceBuffer<double2> x(static_cast<std::size_t>(dim())), y(static_cast<std::size_t>(std::max<std::int64_t>(block_.rows, 1)));
+  QSWG_CHECK(cudaMemsetAsync(x.get(), 0, x.bytes(), stream_));
+  cudaEvent_t e0, e1;
+  QSWG_CHECK(cudaEventCreate(&e0));
+  QSWG_CHECK(cudaEventCreate(&e1));
+  dev::spmv(view(), group, x.get(), y.get(), 1.0, stream_);  // warm-up
+  QSWG_CHECK(cudaEventRecord(e0, stream_));
+  for (int i = 0; i < iters; ++i) dev::spmv(view(), group, x.get(), y.get(), 1.0, stream_);
+  QSWG_CHECK(cudaEventRecord(e1, stream_));
+  QSWG_CHECK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  QSWG_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return static_cast<double>(ms) / iters;
+}
+
+namespace {
+
+// Counts every row of the operator described by `ops` and scans them into a
+// global int64 row pointer on the device (all ranks do this, so they agree on
+// the partition without communication).  Returns colptr[j] = rowptr[j*n],
+// the nnz prefix at every rho-column boundary.
+std::vector<std::int64_t> count_scan(const dev::KronOperands& ops, std::int64_t n,
+                                     DeviceBuffer<std::int64_t>& grp, cudaStream_t s) {
+  const std::int64_t dim = n * n;
+  DeviceBuffer<std::int64_t> counts(static_cast<std::size_t>(dim) + 1);
+  QSWG_CHECK(cudaMemsetAsync(counts.get(), 0, counts.bytes(), s));
+  dev::assemble_count(ops, 0, dim, counts.get(), s);
+  grp.resize(static_cast<std::size_t>(dim) + 1);
+  std::size_t tmp_bytes = 0;
+  dev::exclusive_scan(counts.get(), grp.get(), dim + 1, nullptr, tmp_bytes, s);
+  DeviceBuffer<unsigned char> tmp(tmp_bytes);
+  dev::exclusive_scan(counts.get(), grp.get(), dim + 1, tmp.get(), tmp_bytes, s);
+  std::vector<std::int64_t> colptr(static_cast<std::size_t>(n) + 1);
+  QSWG_CHECK(cudaMemcpy2DAsync(colptr.data(), sizeof(std::int64_t), grp.get(),
+                               static_cast<std::size_t>(n) * sizeof(std::int64_t), sizeof(std::int64_t),
+                               static_cast<std::size_t>(n) + 1, cudaMemcpyDeviceToHost, s));
+  QSWG_CHECK(cudaStreamSynchronize(s));
+  return colptr;
+}
+
+// Contiguous row blocks on rho-column boundaries (multiples of n rows),
+// balanced by nnz: block w ends at the column boundary nearest to w/world of
+// the total nnz.
+std::vector<std::int64_t> partition_rows(const std::vector<std::int64_t>& colptr, std::int64_t n, int world) {
+  std::vector<std::int64_t> starts(static_cast<std::size_t>(world) + 1, 0);
+  starts[static_cast<std::size_t>(world)] = n * n;
+  const std::int64_t total = colptr.back();
+  std::int64_t j = 0;
+  for (int w = 1; w < world; ++w) {
+    const long double target = static_cast<long double>(total) * w / world;
+    while (j < n && static_cast<long double>(colptr[static_cast<std::size_t>(j)]) +
+                            (colptr[static_cast<std::size_t>(j) + 1] - colptr[static_cast<std::size_t>(j)]) / 2.0L <
+                        target)
+      ++j;
+    starts[static_cast<std::size_t>(w)] = std::max(j * n, starts[static_cast<std::size_t>(w) - 1]);
+  }
+  return starts;
+}
+
+template <class V>
+void fill_block(const dev::KronOperands& ops, const DeviceBuffer<std::int64_t>& grp,
+                const std::vector<std::int64_t>& colptr, std::int64_t n, const RowBlock& blk,
+                DeviceBuffer<std::int64_t>& rowptr, DeviceBuffer<int>& col, DeviceBuffer<V>& val,
+                std::int64_t& nnz, cudaStream_t s) {
+  const std::int64_t j0 = blk.row0 / n, j1 = (blk.row0 + blk.rows) / n;
+  const std::int64_t base = colptr[static_cast<std::size_t>(j0)];
+  nnz = colptr[static_cast<std::size_t>(j1)] - base;
+  rowptr.resize(static_cast<std::size_t>(blk.rows) + 1);
+  dev::rebase_rowptr(grp.get() + blk.row0, base, rowptr.get(), blk.rows + 1, s);
+  col.resize(static_cast<std::size_t>(std::max<std::int64_t>(nnz, 1)));
+  val.resize(static_cast<std::size_t>(std::max<std::int64_t>(nnz, 1)));
+  if constexpr (std::is_same_v<V, double2>) {
+    dev::assemble_fill(ops, blk.row0, blk.rows, rowptr.get(), col.get(), val.get(), s);
+  } else {
+    dev::assemble_fill_abs(ops, blk.row0, blk.rows, rowptr.get(), col.get(), val.get(), s);
+  }
+  QSWG_CHECK(cudaStreamSynchronize(s));
+}
+
+int heuristic_group(double mean_row) {
+  if (mean_row <= 6) return 4;
+  if (mean_row <= 20) return 8;
+  if (mean_row <= 48) return 16;
+  return 32;
+}
+
+}  // namespace
+
+std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_t n, const HostOperands& hops,
+                                                       const DeviceConfig& cfg) {
+  std::unique_ptr<Liouvillian> l(new Liouvillian);
+  l->n_ = n;
+  l->omega_ = omega;
+  l->device_ = cfg.device;
+  l->comm_ = cfg.comm;
+  DeviceGuard guard(cfg.device);
+  QSWG_CHECK(cudaStreamCreateWithFlags(&l->stream_, cudaStreamNonBlocking));
+  cudaStream_t s = l->stream_;
+  const std::int64_t dim = n * n;
+  const int world = cfg.comm ? cfg.comm->world() : 1;
+  const int rank = cfg.comm ? cfg.comm->rank() : 0;
+
+  DeviceOperands ops(hops, s);
+  DeviceBuffer<std::int64_t> grp;
+  const std::vector<std::int64_t> colptr = count_scan(ops.get(), n, grp, s);
+  l->nnz_total_ = colptr.back();
+  l->starts_ = partition_rows(colptr, n, world);
+  l->block_ = {l->starts_[static_cast<std::size_t>(rank)],
+               l->starts_[static_cast<std::size_t>(rank) + 1] - l->starts_[static_cast<std::size_t>(rank)]};
+
+  // ---- 1-norm power series (liouvillian.cpp:309-344) ----
+  if (dim <= kExactNormDimLimit) {
+    // exact: every rank assembles the (small) full matrix
+    DeviceBuffer<std::int64_t> rp;
+    DeviceBuffer<int> cc;
+    DeviceBuffer<double2> vv;
+    std::int64_t nz = 0;
+    fill_block(ops.get(), grp, colptr, n, RowBlock{0, dim}, rp, cc, vv, nz, s);
+    dev::CsrView full{rp.get(), cc.get(), vv.get(), dim, 0};
+    DeviceBuffer<double2> w0(static_cast<std::size_t>(dim * dim)), w1(static_cast<std::size_t>(dim * dim));
+    DeviceBuffer<double> colsum(static_cast<std::size_t>(dim));
+    dev::exact_norms(full, dim, w0.get(), w1.get(), colsum.get(), l->norms_.data(), s);
+  } else {
+    // bound: v <- |L|^T v from v = 1, over |L^T| assembled from transposed operands
+    const HostOperands th = hops.transposed();
+    DeviceOperands tops(th, s);
+    DeviceBuffer<std::int64_t> tgrp;
+    const std::vector<std::int64_t> tcolptr = count_scan(tops.get(), n, tgrp, s);
+    DeviceBuffer<std::int64_t> rp;
+    DeviceBuffer<int> cc;
+    DeviceBuffer<double> vv;
+    std::int64_t nz = 0;
+    fill_block(tops.get(), tgrp, tcolptr, n, l->block_, rp, cc, vv, nz, s);
+    tgrp.reset();
+    dev::RealCsrView lt{rp.get(), cc.get(), vv.get(), l->block_.rows, l->block_.row0};
+    DeviceBuffer<double> v(static_cast<std::size_t>(dim)), next(static_cast<std::size_t>(dim));
+    DeviceBuffer<unsigned long long> mx(9);
+    QSWG_CHECK(cudaMemsetAsync(mx.get(), 0, mx.bytes(), s));
+    {
+      std::vector<double> ones(static_cast<std::size_t>(dim), 1.0);
+      QSWG_CHECK(cudaMemcpyAsync(v.get(), ones.data(), v.bytes(), cudaMemcpyHostToDevice, s));
+      QSWG_CHECK(cudaStreamSynchronize(s));
+    }
+    for (int p = 0; p < 9; ++p) {
+      dev::abs_transpose_product(lt, v.get(), next.get() + l->block_.row0, s);
+      if (cfg.comm) cfg.comm->allgather_rows(next.get(), l->starts_, sizeof(double), s);
+      dev::max_reduce(next.get(), dim, mx.get() + p, s);
+      std::swap(v, next);
+    }
+    unsigned long long bits[9];
+    QSWG_CHECK(cudaMemcpyAsync(bits, mx.get(), sizeof(bits), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+    for (int p = 0; p < 9; ++p) std::memcpy(&l->norms_[static_cast<std::size_t>(p)], &bits[p], sizeof(double));
+  }
+
+  // ---- the superoperator row block ----
+  fill_block(ops.get(), grp, colptr, n, l->block_, l->rowptr_, l->col_, l->val_, l->nnz_local_, s);
+  grp.reset();
+
+  // ---- SpMV lanes per row ----
+  const double mean_row = l->block_.rows ? static_cast<double>(l->nnz_local_) / l->block_.rows : 1.0;
+  if (cfg.group) {
+    if (!dev::valid_group(cfg.group)) throw std::invalid_argument("group must be 1, 2, 4, 8, 16 or 32");
+    l->group_ = cfg.group;
+  } else if (l->nnz_local_ < (1 << 22)) {
+    l->group_ = heuristic_group(mean_row);
+  } else {
+    double best = 1e300;
+    for (int g : {4, 8, 16, 32}) {
+      if (g > 4 * mean_row + 4) continue;
+      const double t = l->time_spmv(3, g);
+      if (t < best) {
+        best = t;
+        l->group_ = g;
+      }
+    }
+  }
+  return l;
+}
+
+// ------------------------------------------------------------ build_local
+std::unique_ptr<Liouvillian> build_local(double omega, const SparseMatrix& h, const SparseMatrix& m_l,
+                                         const std::vector<SourceArc>& sources,
+                                         const std::vector<SinkArc>& sinks, const DeviceConfig& cfg) {
+  // validation: liouvillian.cpp:133-151
+  const std::int64_t n = h.rows();
+  if (h.cols() != n) throw std::invalid_argument("Hamiltonian must be square");
+  if (m_l.rows() != n || m_l.cols() != n)
+    throw std::invalid_argument("condensed Lindblad matrix dimension mismatch");
+  validate_common(omega, h);
+  const std::int64_t nsrc = static_cast<std::int64_t>(sources.size());
+  const std::int64_t nsnk = static_cast<std::int64_t>(sinks.size());
+  if (n < nsrc + nsnk) throw std::invalid_argument("operator dimension smaller than the augmentation");
+  const std::int64_t n_base = n - nsrc - nsnk;
+  for (const SourceArc& s : sources)
+    if (s.target < 0 || s.target >= n_base) throw std::out_of_range("source target out of range");
+  for (const SinkArc& s : sinks)
+    if (s.origin < 0 || s.origin >= n_base) throw std::out_of_range("sink origin out of range");
+
+  HostOperands o;
+  o.n = n;
+  o.omega = omega;
+  const Complex coh{0.0, -(1.0 - omega)};
+  const SparseMatrix ht = h.transpose();
+  if (coh != Complex{}) {
+    o.a = from_sparse(h, [&](Complex v) { return coh * v; });    // -i(1-w) I(x)H
+    o.b = from_sparse(ht, [&](Complex v) { return -coh * v; });  // +i(1-w) H^T(x)I
+  } else {
+    o.a = make_multi(n, {});
+    o.b = make_multi(n, {});
+  }
+  // decay: d = column sums of |m_l|^2 (liouvillian.cpp:19-26), d_ss from rates
+  o.d_loc.assign(static_cast<std::size_t>(n), 0.0);
+  for (std::int64_t k = 0; k < m_l.nnz(); ++k)
+    o.d_loc[static_cast<std::size_t>(m_l.col_indices()[static_cast<std::size_t>(k)])] += std::norm(m_l.values()[static_cast<std::size_t>(k)]);
+  o.d_ss.assign(static_cast<std::size_t>(n), 0.0);
+  for (std::int64_t k = 0; k < nsrc; ++k) o.d_ss[static_cast<std::size_t>(n_base + k)] += sources[static_cast<std::size_t>(k)].rate;
+  for (const SinkArc& s : sinks) o.d_ss[static_cast<std::size_t>(s.origin)] += s.rate;
+  // transfer onto the vec diagonal (liouvillian.cpp:185-206), emission order
+  std::vector<Entry> te;
+  if (omega != 0.0) append_entries(te, m_l, [&](Complex v) { return Complex{omega * std::norm(v), 0.0}; });
+  for (std::int64_t k = 0; k < nsrc; ++k) {
+    const std::int64_t u = n_base + k;
+    te.push_back({sources[static_cast<std::size_t>(k)].target, u, Complex{sources[static_cast<std::size_t>(k)].rate, 0.0}});
+  }
+  for (std::int64_t k = 0; k < nsnk; ++k)
+    te.push_back({n_base + nsrc + k, sinks[static_cast<std::size_t>(k)].origin, Complex{sinks[static_cast<std::size_t>(k)].rate, 0.0}});
+  o.t = make_multi(n, te);
+  return LiouvillianBuilder::build(omega, n, o, cfg);
+}
+
+// ----------------------------------------------------------- build_global
+std::unique_ptr<Liouvillian> build_global(double omega, const SparseMatrix& h,
+                                          const std::vector<SparseMatrix>& lindblads,
+                                          const std::optional<SparseMatrix>& h_rot,
+                                          const DeviceConfig& cfg) {
+  // validation: liouvillian.cpp:216-229
+  const std::int64_t n = h.rows();
+  validate_common(omega, h);
+  for (const SparseMatrix& l : lindblads)
+    if (l.rows() != n || l.cols() != n) throw std::invalid_argument("Lindblad operator dimension mismatch");
+  if (h_rot && (h_rot->rows() != n || h_rot->cols() != n))
+    throw std::invalid_argument("rotating Hamiltonian dimension mismatch");
+  if (static_cast<int>(lindblads.size()) > dev::kMaxKron)
+    throw std::invalid_argument("at most " + std::to_string(dev::kMaxKron) + " Lindblad operators are supported");
+
+  HostOperands o;
+  o.n = n;
+  o.omega = omega;
+  const Complex coh{0.0, -(1.0 - omega)};
+  const Complex rot{0.0, omega};
+  const SparseMatrix ht = h.transpose();
+  std::vector<Entry> ae, be;
+  if (coh != Complex{}) {
+    append_entries(ae, h, [&](Complex v) { return coh * v; });
+    append_entries(be, ht, [&](Complex v) { return -coh * v; });
+  }
+  if (h_rot && rot != Complex{}) {
+    append_entries(ae, *h_rot, [&](Complex v) { return rot * v; });
+    append_entries(be, h_rot->transpose(), [&](Complex v) { return -rot * v; });
+  }
+  if (omega != 0.0) {
+    for (const SparseMatrix& l : lindblads) {
+      const SparseMatrix ll = l.conjugate_transpose() * l;  // liouvillian.cpp:236-242
+      append_entries(ae, ll, [&](Complex v) { return -0.5 * omega * v; });
+      append_entries(be, ll.transpose(), [&](Complex v) { return -0.5 * omega * v; });
+      o.p.push_back(from_sparse(l, [&](Complex v) { return omega * std::conj(v); }));  // w L*
+      o.q.push_back(from_sparse(l, [](Complex v) { return v; }));                      // L
+    }
+  }
+  o.a = make_multi(n, ae);
+  o.b = make_multi(n, be);
+  o.t = make_multi(n, {});
+  return LiouvillianBuilder::build(omega, n, o, cfg);
+}
+
+}  // namespace qswg

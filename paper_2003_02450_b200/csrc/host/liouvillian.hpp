@@ -1,0 +1,111 @@
+// The device-resident superoperator: the B200 counterpart of
+// qsw::DistributedLiouvillian (proj/core/include/qsw/liouvillian.hpp:21-93).
+//
+// One Liouvillian lives on one GPU and owns a contiguous row block of L
+// (the whole matrix when world == 1) in CSR with int64 row pointers, int32
+// global columns and complex128 values.  Rows are split on rho-column
+// boundaries (r = n*j + i, so block = a range of rho columns j) balanced by
+// nnz.  Construction assembles the rows on the device (cuda/assemble.cu) and
+// computes the 1-norm power series (cuda/norms.cu).
+#pragma once
+
+#include <array>
+#include <memory>
+#include <optional>
+#include <vector>
+
+#include "../kernels.hpp"
+#include "device.hpp"
+#include "graph.hpp"
+#include "sparse.hpp"
+
+namespace qswg {
+
+class Comm;  // multi-GPU exchange (comm.hpp); nullptr when world == 1
+
+struct DeviceConfig {
+  int device = 0;       // CUDA ordinal
+  int group = 0;        // lanes per row for the SpMV kernels; 0 = autotune
+  Comm* comm = nullptr; // borrowed; shared by every handle on this rank
+};
+
+// Lazily grown scratch vectors and device control blocks reused by every
+// step/series call on one Liouvillian (not thread-safe per handle, like the
+// reference's per-object use).
+struct Workspace {
+  std::vector<DeviceBuffer<double2>> vec;
+  DeviceBuffer<dev::StepCtl> step_ctl;
+  DeviceBuffer<dev::SeriesCtl> series_ctl;
+  double2* get(std::size_t idx, std::size_t len) {
+    if (vec.size() <= idx) vec.resize(idx + 1);
+    if (vec[idx].size() < len) vec[idx].resize(len);
+    return vec[idx].get();
+  }
+};
+
+struct RowBlock {
+  std::int64_t row0 = 0;  // first global row owned
+  std::int64_t rows = 0;  // rows owned
+};
+
+class Liouvillian {
+ public:
+  ~Liouvillian();
+  Liouvillian(const Liouvillian&) = delete;
+  Liouvillian& operator=(const Liouvillian&) = delete;
+
+  std::int64_t n() const { return n_; }             // operator (vertex) dimension
+  std::int64_t dim() const { return n_ * n_; }
+  double omega() const { return omega_; }
+  std::int64_t nnz_local() const { return nnz_local_; }
+  std::int64_t nnz_total() const { return nnz_total_; }
+  const RowBlock& block() const { return block_; }
+  const std::vector<std::int64_t>& partition() const { return starts_; }  // world + 1 row starts
+  /// Upper bounds on ||L^p||_1, p = 1..9 (exact when dim <= 4096).
+  const std::array<double, 9>& one_norms() const { return norms_; }
+  int group() const { return group_; }
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+  Comm* comm() const { return comm_; }
+  dev::CsrView view() const;
+
+  /// Local row block downloaded as CSR with global columns (parity / debug).
+  void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
+                std::vector<Complex>& val) const;
+  /// y = scale * L x for device vectors: x full-length (dim), y local (rows).
+  void multiply(const double2* x, double2* y, double scale) const;
+  /// Mean device time (ms) of one term kernel launch over `iters` launches.
+  double time_spmv(int iters, int group) const;
+  Workspace& workspace() const { return ws_; }
+
+ private:
+  Liouvillian() = default;
+  friend class LiouvillianBuilder;
+
+  std::int64_t n_ = 0;
+  double omega_ = 0.0;
+  int device_ = 0;
+  int group_ = 8;
+  cudaStream_t stream_ = nullptr;
+  Comm* comm_ = nullptr;
+  RowBlock block_;
+  std::vector<std::int64_t> starts_;
+  std::int64_t nnz_local_ = 0, nnz_total_ = 0;
+  std::array<double, 9> norms_{};
+  DeviceBuffer<std::int64_t> rowptr_;
+  DeviceBuffer<int> col_;
+  DeviceBuffer<double2> val_;
+  mutable Workspace ws_;
+};
+
+/// L-QSW (liouvillian.hpp:65-71, liouvillian.cpp:129-210).
+std::unique_ptr<Liouvillian> build_local(double omega, const SparseMatrix& h, const SparseMatrix& m_l,
+                                         const std::vector<SourceArc>& sources,
+                                         const std::vector<SinkArc>& sinks, const DeviceConfig& cfg);
+/// G-QSW / NM-G-QSW (liouvillian.hpp:73-85, liouvillian.cpp:212-307).
+std::unique_ptr<Liouvillian> build_global(double omega, const SparseMatrix& h,
+                                          const std::vector<SparseMatrix>& lindblads,
+                                          const std::optional<SparseMatrix>& h_rot,
+                                          const DeviceConfig& cfg);
+
+}  // namespace qswg

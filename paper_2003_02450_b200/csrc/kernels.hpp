@@ -1,0 +1,149 @@
+// Launch interface between the C++ host layer (host/*.cpp) and the sm_100a
+// kernels (cuda/*.cu).  Plain structs of device pointers; no torch types.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace qswg::dev {
+
+inline constexpr int kMaxKron = 8;      // Lindblad operators per G-QSW
+inline constexpr int kMaxSeriesD = 128; // super-step outputs (d <= floor(1e280^(1/55)) = 123)
+inline constexpr int kSeriesRegD = 8;   // per-thread register maxima in the series kernel
+
+// A "multi-CSR" over the n x n operator space: rows sorted by column with
+// duplicates kept adjacent in emission order (they are summed on the device
+// in that order).  ptr == nullptr means the list is empty.
+struct KronList {
+  const int* ptr = nullptr;
+  const int* col = nullptr;
+  const double2* val = nullptr;
+};
+
+// Every superoperator variant of the reference (liouvillian.cpp:129-307) is
+//   L = I (x) A + B (x) I + sum_k P_k (x) Q_k + T_diag + decay
+// in the column-major vec convention: row r = n*j + i of L picks up
+//   A(i, c)           at column n*j + c,
+//   B(j, c)           at column n*c + i,
+//   P_k(j,a) Q_k(i,b) at column n*a + b,
+//   T(i, c)           at column n*c + c     (only when i == j),
+//   -0.5*(omega*(dl_i + dl_j) + ds_i + ds_j) at column r (when d_loc != null).
+struct KronOperands {
+  int n = 0;
+  KronList a, b;
+  int nk = 0;
+  KronList p[kMaxKron], q[kMaxKron];
+  KronList t;
+  const double* d_loc = nullptr;
+  const double* d_ss = nullptr;
+  double omega = 0.0;
+};
+
+// Row block [row0, row0 + rows) of a device CSR: int64 row pointers (local,
+// starting at 0), int32 global column indices, complex128 values.
+struct CsrView {
+  const std::int64_t* rowptr = nullptr;
+  const int* col = nullptr;
+  const double2* val = nullptr;
+  std::int64_t rows = 0;
+  std::int64_t row0 = 0;
+};
+
+struct RealCsrView {
+  const std::int64_t* rowptr = nullptr;
+  const int* col = nullptr;
+  const double* val = nullptr;
+  std::int64_t rows = 0;
+  std::int64_t row0 = 0;
+};
+
+// ---- assembly (cuda/assemble.cu) -------------------------------------------
+void assemble_count(const KronOperands& o, std::int64_t row0, std::int64_t rows,
+                    std::int64_t* counts, cudaStream_t s);
+// counts (rows + 1 entries, last one ignored) -> exclusive prefix sum.
+void exclusive_scan(const std::int64_t* counts, std::int64_t* rowptr, std::int64_t n,
+                    void* tmp, std::size_t& tmp_bytes, cudaStream_t s);
+// dst[k] = src[k] - base, k < n (local row pointers of a row block).
+void rebase_rowptr(const std::int64_t* src, std::int64_t base, std::int64_t* dst, std::int64_t n,
+                   cudaStream_t s);
+void assemble_fill(const KronOperands& o, std::int64_t row0, std::int64_t rows,
+                   const std::int64_t* rowptr, int* col, double2* val, cudaStream_t s);
+void assemble_fill_abs(const KronOperands& o, std::int64_t row0, std::int64_t rows,
+                       const std::int64_t* rowptr, int* col, double* val, cudaStream_t s);
+
+// ---- norms (cuda/norms.cu) ---------------------------------------------------
+// Exact ||L^p||_1 (p = 1..9) through dense powers of L applied to the
+// identity; dim <= 4096.  work: 2 * dim * dim double2 + dim doubles.
+void exact_norms(const CsrView& l, std::int64_t dim, double2* work0, double2* work1,
+                 double* colsum, double* norms9_host, cudaStream_t s);
+// next[r] = sum_c v[c] |L^T|(r, c), ascending c, no FMA (liouvillian.cpp:321-343).
+void abs_transpose_product(const RealCsrView& lt, const double* v, double* next,
+                           cudaStream_t s);
+// max over n non-negative doubles -> *out (device); uses the uint64 bit order.
+void max_reduce(const double* v, std::int64_t n, unsigned long long* out_bits, cudaStream_t s);
+
+// ---- Taylor loop (cuda/taylor.cu) -----------------------------------------
+struct StepCtl {
+  unsigned long long term_bits;
+  unsigned long long sum_bits;
+  unsigned int arrivals;
+  int done;
+  int error;
+  int spmvs;
+  double c1;
+  double last_nf;
+};
+
+struct SeriesCtl {
+  unsigned long long term_bits;
+  unsigned int arrivals;
+  int n_active;
+  int error;
+  int spmvs;
+  int count;
+  int pad_;
+  double z_norm;
+  unsigned long long sum_bits[kMaxSeriesD];
+  double factor[kMaxSeriesD];
+  double c1[kMaxSeriesD];
+  int active[kMaxSeriesD];
+};
+
+struct SeriesSums {
+  double2* s[kMaxSeriesD];
+};
+
+// Lanes per row for the row-group SpMV kernels: 2, 4, 8, 16 or 32; 1 selects
+// the bitwise reference-order mode (sequential rows, no FMA).
+int valid_group(int g);
+
+// ctl <- zero; ctl->c1 = ||v||_inf over n local elements.
+void step_init(const double2* v, std::int64_t n, StepCtl* ctl, cudaStream_t s);
+// One Taylor term of `step` (expm.cpp:175-195):
+//   y = scale * (L x);  sum_out = sum_in + y;  c2 = ||y||, nf = ||sum_out||;
+//   stop test c1 + c2 <= tol * nf decided on the device.  Skips itself when
+//   the stage is already done (unless first_of_stage) or on error.
+void step_term(const CsrView& l, int group, const double2* x, double2* y, const double2* sum_in,
+               double2* sum_out, double scale, bool first_of_stage, int stage, double tol,
+               StepCtl* ctl, cudaStream_t s);
+// Super-step start of `series` (expm.cpp:267-276): z_norm = ||Z||, count
+// outputs active, factor_k = k, c1_k = z_norm.
+void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, cudaStream_t s);
+// K_p = scale * (L K_{p-1}); for every active k: S_k = (p == 1 ? Z : S_k) + k^p K_p
+// with per-k stop tests (expm.cpp:278-316, evaluated p-major).
+void series_term(const CsrView& l, int group, const double2* x, double2* kp, const double2* z,
+                 const SeriesSums& sums, int count, int p, double scale, double tol,
+                 SeriesCtl* ctl, cudaStream_t s);
+// y = scale * (L x) (liouvillian.cpp:346-360).
+void spmv(const CsrView& l, int group, const double2* x, double2* y, double scale, cudaStream_t s);
+// pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).
+void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
+               double* pops, cudaStream_t s);
+// Deterministic non-zero test pattern (benchmark inputs).
+void fill_pattern(double2* v, std::int64_t n, cudaStream_t s);
+// v = 0 except v[i*(n+1)] = p[i] (walk.cpp:101-126 without the dense host rho).
+void state_from_probabilities(double2* v_local, std::int64_t row0, std::int64_t rows,
+                              std::int64_t n, const double* p, cudaStream_t s);
+
+}  // namespace qswg::dev

@@ -1,0 +1,27 @@
+#!/usr/bin/env python3
+"""One build + one series of a BASELINE config through the C ABI: the
+command profiled under ncu (launch list / --set full capture)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2003_02450_b200 import api, graphs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--size", type=int, default=None)
+ap.add_argument("--series", type=int, default=1)
+ap.add_argument("--group", type=int, default=0)
+a = ap.parse_args()
+w = graphs.config(a.config, size=a.size)
+if w.kind == "local":
+    l = api.build_local(w.omega, w.h, w.ops[0], group=a.group)
+else:
+    l = api.build_global(w.omega, w.h, w.ops, group=a.group)
+v = l.state().from_probabilities(w.rho0)
+for _ in range(a.series):
+    r = api.series(l, v, w.t1, w.tq, w.steps)
+print(f"{a.config}: dim={l.dim} nnz={l.nnz} group={l.group} spmvs={r.info.spmvs} launches={r.info.launches} "
+      f"device_ms={r.info.device_ms:.3f} pop0={r.populations[-1][0]:.15f}")
