@@ -80,4 +80,31 @@ __device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
   return r;
 }
 
+__device__ __forceinline__ unsigned long long evict_last_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// Gathered SpMV input (reused ~nnz/row times): read-only path, L2 evict-last.
+__device__ __forceinline__ double2 ld_gather(const double2* p, unsigned long long pol) {
+  double2 r;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
+// Read-modify-write vectors touched once per kernel (running sums): no L1
+// allocation, L2 evict-first.  Volatile keeps the issue order the caller
+// wrote (all loads of a chunk before its stores).
+__device__ __forceinline__ double2 ld_once(const double2* p, unsigned long long pol) {
+  double2 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x),
+               "d"(v.y), "l"(pol)
+               : "memory");
+}
+
 }  // namespace qswg::dev

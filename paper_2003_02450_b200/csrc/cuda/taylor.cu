@@ -6,14 +6,22 @@
 //   (expm.cpp:175-195) and the series lazy-term SpMV + per-k axpy/norm loops
 //   (expm.cpp:283-316).
 // The path is HBM-bound complex128 SpMV (~0.4 flop/B), so there are no
-// tensor-core ops here: rows are processed by groups of G lanes (G in
-// {2,4,8,16,32}, autotuned per matrix) in a persistent grid-stride loop;
-// values/columns stream with an L2 evict-first policy so the gathered vector
-// stays L2-resident; the axpy and both inf-norms are fused into the epilogue;
-// the grid-wide maxima use the uint64 bit order of non-negative doubles
-// (order-independent, hence deterministic) and the LAST block to arrive
+// tensor-core ops here.  Each block owns tiles of kTile = 256 consecutive
+// rows (persistent grid-stride over tiles):
+//   phase A  row groups of G lanes (G in {2,4,8,16,32}, autotuned per matrix)
+//            compute the tile's row dot products from a shared-memory copy of
+//            the tile's row pointers; values/columns stream with an L2
+//            evict-first policy so the gathered vector stays L2-resident;
+//   phase B  one thread per row runs the fused epilogue (scale, term write,
+//            running-sum axpys for every active output, inf-norms) with fully
+//            coalesced 16-byte accesses and all sum loads in flight at once.
+// Grid-wide maxima use the uint64 bit order of non-negative doubles
+// (order-independent, hence deterministic); the LAST block to arrive
 // evaluates the stop test c1 + c2 <= tol * ||sum|| and publishes it for the
 // next launch, so the host never synchronises inside a step or a series.
+#include <cstdlib>
+#include <string>
+
 #include "../kernels.hpp"
 #include "common.cuh"
 
@@ -21,64 +29,64 @@ namespace qswg::dev {
 
 namespace {
 
+constexpr int kTile = kThreads;  // rows per block tile
+
 __device__ __forceinline__ double cabs2(double2 v) { return hypot(v.x, v.y); }
 
-// Row-group SpMV core: returns the full row sum in every lane of the group.
-// G == 1 is the bitwise "reference order" mode: one thread per row, columns
-// in CSR order, every product and sum rounded separately (no FMA) — exactly
-// `acc += vals[k] * x[...]` of liouvillian.cpp:120-124 in a no-FMA build.
+// Sum of one row, computed by the G lanes of a group; every lane returns the
+// full sum.  G == 1 is the bitwise "reference order" mode: one thread per
+// row, columns in CSR order, every product and sum rounded separately (no
+// FMA) — exactly `acc += vals[k] * x[...]` of liouvillian.cpp:120-124 in a
+// no-FMA build.
 template <int G>
-__device__ __forceinline__ double2 row_dot(const CsrView& l, long long row, bool valid,
+__device__ __forceinline__ double2 row_dot(const CsrView& l, long long b, long long e,
                                            const double2* __restrict__ x, int lane,
-                                           unsigned long long pol) {
+                                           unsigned long long pol, unsigned long long xpol) {
   double2 acc = make_double2(0.0, 0.0);
   if constexpr (G == 1) {
-    if (valid) {
-      const long long b = __ldg(l.rowptr + row), e = __ldg(l.rowptr + row + 1);
-      for (long long k = b; k < e; ++k) {
-        const double2 v = ld_stream(l.val + k, pol);
-        const double2 xv = __ldg(x + ld_stream(l.col + k, pol));
-        acc.x = __dadd_rn(acc.x, __dsub_rn(__dmul_rn(v.x, xv.x), __dmul_rn(v.y, xv.y)));
-        acc.y = __dadd_rn(acc.y, __dadd_rn(__dmul_rn(v.x, xv.y), __dmul_rn(v.y, xv.x)));
+    for (long long k = b; k < e; ++k) {
+      const double2 v = ld_stream(l.val + k, pol);
+      const double2 xv = ld_gather(x + ld_stream(l.col + k, pol), xpol);
+      acc.x = __dadd_rn(acc.x, __dsub_rn(__dmul_rn(v.x, xv.x), __dmul_rn(v.y, xv.y)));
+      acc.y = __dadd_rn(acc.y, __dadd_rn(__dmul_rn(v.x, xv.y), __dmul_rn(v.y, xv.x)));
+    }
+    return acc;
+  } else {
+    constexpr int U = G <= 8 ? 4 : 2;  // independent loads in flight per lane
+    long long k = b + lane;
+    for (; k + (U - 1) * G < e; k += U * G) {
+      int c[U];
+      double2 v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = ld_stream(l.col + k + u * G, pol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(l.val + k + u * G, pol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_gather(x + c[u], xpol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc.x = fma(v[u].x, xv[u].x, acc.x);
+        acc.x = fma(-v[u].y, xv[u].y, acc.x);
+        acc.y = fma(v[u].x, xv[u].y, acc.y);
+        acc.y = fma(v[u].y, xv[u].x, acc.y);
       }
+    }
+    for (; k < e; k += G) {
+      const int c0 = ld_stream(l.col + k, pol);
+      const double2 v0 = ld_stream(l.val + k, pol);
+      const double2 x0 = ld_gather(x + c0, xpol);
+      acc.x = fma(v0.x, x0.x, acc.x);
+      acc.x = fma(-v0.y, x0.y, acc.x);
+      acc.y = fma(v0.x, x0.y, acc.y);
+      acc.y = fma(v0.y, x0.x, acc.y);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
     return acc;
   }
-  if (valid) {
-    const long long b = __ldg(l.rowptr + row), e = __ldg(l.rowptr + row + 1);
-    long long k = b + lane;
-    for (; k + G < e; k += 2 * G) {
-      const int c0 = ld_stream(l.col + k, pol);
-      const int c1 = ld_stream(l.col + k + G, pol);
-      const double2 v0 = ld_stream(l.val + k, pol);
-      const double2 v1 = ld_stream(l.val + k + G, pol);
-      const double2 x0 = __ldg(x + c0);
-      const double2 x1 = __ldg(x + c1);
-      acc.x = fma(v0.x, x0.x, acc.x);
-      acc.x = fma(-v0.y, x0.y, acc.x);
-      acc.y = fma(v0.x, x0.y, acc.y);
-      acc.y = fma(v0.y, x0.x, acc.y);
-      acc.x = fma(v1.x, x1.x, acc.x);
-      acc.x = fma(-v1.y, x1.y, acc.x);
-      acc.y = fma(v1.x, x1.y, acc.y);
-      acc.y = fma(v1.y, x1.x, acc.y);
-    }
-    if (k < e) {
-      const int c0 = ld_stream(l.col + k, pol);
-      const double2 v0 = ld_stream(l.val + k, pol);
-      const double2 x0 = __ldg(x + c0);
-      acc.x = fma(v0.x, x0.x, acc.x);
-      acc.x = fma(-v0.y, x0.y, acc.x);
-      acc.y = fma(v0.x, x0.y, acc.y);
-      acc.y = fma(v0.y, x0.x, acc.y);
-    }
-  }
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) {
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-  }
-  return acc;
 }
 
 // s + f * k; separately rounded in the bitwise mode (G == 1).
@@ -91,22 +99,36 @@ __device__ __forceinline__ double2 axpy(double2 s, double f, double2 k) {
   }
 }
 
-// Grid-stride iteration over rows in warp-uniform steps (all lanes of a warp
-// run the same trip count, so the group shuffles are always convergent).
-template <int G>
-struct RowIter {
-  long long first, stride;
-  int lane, sub;
-  __device__ RowIter() {
-    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
-    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const int wl = threadIdx.x & 31;
-    sub = wl / G;
-    lane = wl & (G - 1);
-    first = warp * (32 / G);
-    stride = nwarps * (32 / G);
+// Persistent loop over row tiles.  Phase A fills tile_acc[] with the raw row
+// sums (L x)_r of the tile; phase B calls epi(row, acc, valid) on every
+// thread (one row each; `valid` is false past the last row, so epilogues may
+// use full-warp shuffles).  Every thread of the block reaches both barriers.
+template <int G, class Epi>
+__device__ __forceinline__ void tile_loop(const CsrView& l, const double2* __restrict__ x, Epi&& epi) {
+  __shared__ long long tile_ptr[kTile + 1];
+  __shared__ double2 tile_acc[kTile];
+  const unsigned long long pol = evict_first_policy(), xpol = evict_last_policy();
+  constexpr int kGroups = kThreads / G;
+  const int g = threadIdx.x / G, lane = threadIdx.x % G;
+  for (long long base = static_cast<long long>(blockIdx.x) * kTile; base < l.rows;
+       base += static_cast<long long>(gridDim.x) * kTile) {
+    const int n_rows = static_cast<int>(min(static_cast<long long>(kTile), l.rows - base));
+    __syncthreads();  // previous tile's phase B is done with tile_acc / tile_ptr
+    for (int t = threadIdx.x; t <= n_rows; t += blockDim.x) tile_ptr[t] = __ldg(l.rowptr + base + t);
+    __syncthreads();
+#pragma unroll 1
+    for (int j = 0; j < kTile / kGroups; ++j) {
+      const int r = j * kGroups + g;
+      const bool valid = r < n_rows;
+      const long long b = valid ? tile_ptr[r] : 0, e = valid ? tile_ptr[r + 1] : 0;
+      const double2 acc = row_dot<G>(l, b, e, x, lane, pol, xpol);
+      if (lane == 0 && valid) tile_acc[r] = acc;
+    }
+    __syncthreads();
+    const bool valid = static_cast<int>(threadIdx.x) < n_rows;
+    epi(base + threadIdx.x, valid ? tile_acc[threadIdx.x] : make_double2(0.0, 0.0), valid);
   }
-};
+}
 
 // ---------------------------------------------------------------- step term
 struct StepTermArgs {
@@ -128,43 +150,36 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
   if (*(volatile int*)&ctl->error) return;
   if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
   __shared__ unsigned long long red[32];
-  __shared__ bool last;
-  const unsigned long long pol = evict_first_policy();
-  RowIter<G> it;
   unsigned long long tmax = 0, smax = 0;
-  for (long long r0 = it.first; r0 < a.l.rows; r0 += it.stride) {
-    const long long row = r0 + it.sub;
-    const bool valid = row < a.l.rows;
-    const double2 acc = row_dot<G>(a.l, row, valid, a.x, it.lane, pol);
-    if (valid && it.lane == 0) {
-      // y = scale * acc, scale = Complex{t/(s*j), 0} (liouvillian.cpp:125)
-      const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
-      a.y[row] = yv;
-      const double2 sv0 = a.sum_in[row];
-      const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
-      a.sum_out[row] = sv;
-      tmax = umax64(tmax, dbits(cabs2(yv)));
-      smax = umax64(smax, dbits(cabs2(sv)));
-    }
-  }
+  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
+  tile_loop<G>(a.l, a.x, [&](long long row, double2 acc, bool valid) {
+    if (!valid) return;
+    // y = scale * acc with scale = Complex{t/(s*j), 0} (liouvillian.cpp:125)
+    const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
+    const double2 sv0 = ld_once(a.sum_in + row, once);
+    st_hint(a.y + row, yv, keep);  // next term's SpMV input
+    const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
+    st_hint(a.sum_out + row, sv, once);
+    tmax = umax64(tmax, dbits(cabs2(yv)));
+    smax = umax64(smax, dbits(cabs2(sv)));
+  });
   tmax = block_max_bits(tmax, red);
   smax = block_max_bits(smax, red);
   if (threadIdx.x == 0) {
     atomicMax(&ctl->term_bits, tmax);
     atomicMax(&ctl->sum_bits, smax);
     __threadfence();
-    last = atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1;
-    if (last) {
+    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      const double c2 = bitsd(atomicAdd(&ctl->term_bits, 0ull));
-      const double nf = bitsd(atomicAdd(&ctl->sum_bits, 0ull));
+      const double c2 = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
+      const double nf = bitsd(*(volatile unsigned long long*)&ctl->sum_bits);
       ctl->spmvs += 1;
       if (!isfinite(c2) || !isfinite(nf)) {  // expm.cpp:191-193
         ctl->error = 1;
         ctl->done = 1;
       } else {
         // stage start: c1 = ||v|| (stage 0, from step_init) or ||sum|| of the
-        // previous stage (expm.cpp:197-205) which is that stage's last nf.
+        // previous stage (expm.cpp:197-205), which is that stage's last nf.
         const double c1 = a.first_of_stage ? (a.stage == 0 ? ctl->c1 : ctl->last_nf) : ctl->c1;
         ctl->done = (c1 + c2 <= a.tol * nf) ? 1 : 0;  // expm.cpp:194
         ctl->c1 = c2;
@@ -205,7 +220,6 @@ __device__ void series_control(SeriesCtl* ctl, int count, double tol) {
   ctl->arrivals = 0;
 }
 
-
 struct SeriesTermArgs {
   CsrView l;
   const double2* x;
@@ -233,56 +247,126 @@ __global__ void __launch_bounds__(kThreads) series_term_kernel(SeriesTermArgs a)
     smax_sh[k] = 0;
   }
   __syncthreads();
-  const unsigned long long pol = evict_first_policy();
-  RowIter<G> it;
   unsigned long long tmax = 0;
-  unsigned long long smax[kSeriesRegD];
-#pragma unroll
-  for (int k = 0; k < kSeriesRegD; ++k) smax[k] = 0;
   const bool first = a.p == 1;
-  for (long long r0 = it.first; r0 < a.l.rows; r0 += it.stride) {
-    const long long row = r0 + it.sub;
-    const bool valid = row < a.l.rows;
-    const double2 acc = row_dot<G>(a.l, row, valid, a.x, it.lane, pol);
-    if (valid && it.lane == 0) {
-      const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));  // (h/p) L K_{p-1}
-      a.kp[row] = kv;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
+  tile_loop<G>(a.l, a.x, [&](long long row, double2 acc, bool valid) {
+    // K_p = (h/p) L K_{p-1}  (expm.cpp:286-287)
+    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
+    if (valid) {
+      st_hint(a.kp + row, kv, keep);  // next term's SpMV input
       tmax = umax64(tmax, dbits(cabs2(kv)));
-      const double2 zv = first ? a.z[row] : make_double2(0.0, 0.0);
+    }
+    const double2 zv = (first && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
+    // sum_k += k^p K_p for every active output k (expm.cpp:300-305), in
+    // chunks of kSeriesRegD with all loads of a chunk in flight together.
+#pragma unroll 1
+    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
+      double2 sv[kSeriesRegD];
 #pragma unroll
-      for (int k = 0; k < kSeriesRegD; ++k) {
-        if (k < a.count && act[k]) {
-          double2* s = a.sums.s[k];
-          const double2 sv0 = first ? zv : s[row];
-          const double f = fac[k];
-          const double2 sv = axpy<G>(sv0, f, kv);  // expm.cpp:303
-          s[row] = sv;
-          smax[k] = umax64(smax[k], dbits(cabs2(sv)));
-        }
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
       }
-      for (int k = kSeriesRegD; k < a.count; ++k) {
-        if (act[k]) {
-          double2* s = a.sums.s[k];
-          const double2 sv0 = first ? zv : s[row];
-          const double f = fac[k];
-          const double2 sv = axpy<G>(sv0, f, kv);
-          s[row] = sv;
-          atomicMax(&smax_sh[k], dbits(cabs2(sv)));
+#pragma unroll
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (k >= a.count) break;  // warp-uniform
+        unsigned long long m = 0;
+        if (valid && act[k]) {
+          sv[u] = axpy<G>(sv[u], fac[k], kv);
+          st_hint(a.sums.s[k] + row, sv[u], once);
+          m = dbits(cabs2(sv[u]));
         }
+        m = warp_max_bits(m);
+        if (lane == 0 && m) atomicMax(&smax_sh[k], m);
       }
     }
-  }
+  });
   tmax = block_max_bits(tmax, red);
   if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
+  __syncthreads();
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
+    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
+      __threadfence();
+      series_control(ctl, a.count, a.tol);
+    }
+  }
+}
+
+// Split variant of series_term: the SpMV kernel writes K_p and its norm,
+// a streaming kernel then updates every active running sum.  Costs one
+// extra read of K_p but keeps the SpMV's memory-level parallelism free of
+// the sum traffic (selected at runtime, see series_term()).
+template <int G>
+__global__ void __launch_bounds__(kThreads) series_spmv_kernel(SeriesTermArgs a) {
+  SeriesCtl* ctl = a.ctl;
+  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+  __shared__ unsigned long long red[32];
+  unsigned long long tmax = 0;
+  const unsigned long long keep = evict_last_policy();
+  tile_loop<G>(a.l, a.x, [&](long long row, double2 acc, bool valid) {
+    if (!valid) return;
+    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
+    st_hint(a.kp + row, kv, keep);
+    tmax = umax64(tmax, dbits(cabs2(kv)));
+  });
+  tmax = block_max_bits(tmax, red);
+  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kThreads) series_axpy_kernel(SeriesTermArgs a) {
+  SeriesCtl* ctl = a.ctl;
+  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+  __shared__ double fac[kMaxSeriesD];
+  __shared__ int act[kMaxSeriesD];
+  __shared__ unsigned long long smax_sh[kMaxSeriesD];
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
+    fac[k] = ctl->factor[k];
+    act[k] = ctl->active[k];
+    smax_sh[k] = 0;
+  }
+  __syncthreads();
+  const bool first = a.p == 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long once = evict_first_policy();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.l.rows; base += stride) {
+    const long long row = base + threadIdx.x;
+    const bool valid = row < a.l.rows;
+    const double2 kv = valid ? __ldg(a.kp + row) : make_double2(0.0, 0.0);
+    const double2 zv = (first && valid) ? __ldg(a.z + row) : make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
+      double2 sv[kSeriesRegD];
 #pragma unroll
-  for (int k = 0; k < kSeriesRegD; ++k) {
-    if (k < a.count) {  // block-uniform
-      const unsigned long long m = block_max_bits(smax[k], red);
-      if (threadIdx.x == 0 && act[k]) atomicMax(&ctl->sum_bits[k], m);
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
+      }
+#pragma unroll
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (k >= a.count) break;
+        unsigned long long m = 0;
+        if (valid && act[k]) {
+          sv[u] = axpy<G>(sv[u], fac[k], kv);  // sum += k^p K_p (expm.cpp:300-305)
+          st_hint(a.sums.s[k] + row, sv[u], once);
+          m = dbits(cabs2(sv[u]));
+        }
+        m = warp_max_bits(m);
+        if (lane == 0 && m) atomicMax(&smax_sh[k], m);
+      }
     }
   }
   __syncthreads();
-  for (int k = kSeriesRegD + threadIdx.x; k < a.count; k += blockDim.x)
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
     if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -346,14 +430,9 @@ __global__ void __launch_bounds__(kThreads) series_init_kernel(const double2* z,
 // --------------------------------------------------------------- plain SpMV
 template <int G>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(CsrView l, const double2* x, double2* y, double scale) {
-  const unsigned long long pol = evict_first_policy();
-  RowIter<G> it;
-  for (long long r0 = it.first; r0 < l.rows; r0 += it.stride) {
-    const long long row = r0 + it.sub;
-    const bool valid = row < l.rows;
-    const double2 acc = row_dot<G>(l, row, valid, x, it.lane, pol);
-    if (valid && it.lane == 0) y[row] = make_double2(scale * acc.x, scale * acc.y);
-  }
+  tile_loop<G>(l, x, [&](long long row, double2 acc, bool valid) {
+    if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
+  });
 }
 
 __global__ void diag_kernel(const double2* v, long long row0, long long rows, long long n, double* pops) {
@@ -384,12 +463,12 @@ __global__ void pattern_kernel(double2* v, long long n) {
 
 // ------------------------------------------------------------ launch helpers
 template <class K>
-int persistent_grid(K kernel, long long work_items) {
+int persistent_grid(K kernel, long long rows) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
-  long long want = (work_items + kThreads - 1) / kThreads;
+  long long want = (rows + kTile - 1) / kTile;
   if (want < 1) want = 1;
   return static_cast<int>(want < cap ? want : cap);
 }
@@ -402,11 +481,11 @@ int small_grid(long long n) {
 template <template <int> class KT, class... Args>
 void dispatch_group(int g, long long rows, cudaStream_t s, Args... args) {
   switch (g) {
-#define QSWG_G(GV)                                                                   \
-  case GV: {                                                                         \
-    auto k = KT<GV>::fn;                                                             \
-    k<<<persistent_grid(k, rows * GV), kThreads, 0, s>>>(args...);                  \
-    break;                                                                           \
+#define QSWG_G(GV)                                                          \
+  case GV: {                                                                \
+    auto k = KT<GV>::fn;                                                    \
+    k<<<persistent_grid(k, rows), kThreads, 0, s>>>(args...);              \
+    break;                                                                  \
   }
     QSWG_G(1)
     QSWG_G(2)
@@ -423,6 +502,18 @@ void dispatch_group(int g, long long rows, cudaStream_t s, Args... args) {
 template <int G> struct StepTermK { static constexpr auto fn = step_term_kernel<G>; };
 template <int G> struct SeriesTermK { static constexpr auto fn = series_term_kernel<G>; };
 template <int G> struct SpmvK { static constexpr auto fn = spmv_kernel<G>; };
+template <int G> struct SeriesSpmvK { static constexpr auto fn = series_spmv_kernel<G>; };
+
+// QSWG_SERIES_MODE: "split" (default) or "fused"; "spmv_only" / "axpy_only"
+// launch one half of the split pair (kernel timing experiments only).
+int series_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("QSWG_SERIES_MODE");
+    const std::string m = e ? e : "split";
+    return m == "fused" ? 0 : m == "spmv_only" ? 2 : m == "axpy_only" ? 3 : 1;
+  }();
+  return mode;
+}
 
 }  // namespace
 
@@ -451,7 +542,18 @@ void series_term(const CsrView& l, int group, const double2* x, double2* kp, con
                  const SeriesSums& sums, int count, int p, double scale, double tol,
                  SeriesCtl* ctl, cudaStream_t s) {
   SeriesTermArgs a{l, x, kp, z, sums, count, p, scale, tol, ctl};
-  dispatch_group<SeriesTermK>(group, l.rows, s, a);
+  const int mode = series_mode();
+  if (mode == 0) {
+    dispatch_group<SeriesTermK>(group, l.rows, s, a);
+  } else {
+    if (mode != 3) dispatch_group<SeriesSpmvK>(group, l.rows, s, a);
+    if (mode == 2) {
+    } else if (group == 1) {
+      series_axpy_kernel<1><<<persistent_grid(series_axpy_kernel<1>, l.rows), kThreads, 0, s>>>(a);
+    } else {
+      series_axpy_kernel<2><<<persistent_grid(series_axpy_kernel<2>, l.rows), kThreads, 0, s>>>(a);
+    }
+  }
   QSWG_LAUNCH_CHECK("series_term");
 }
 

@@ -203,11 +203,11 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   dev::SeriesCtl* ctl = series_ctl(l);
   QSWG_CHECK(cudaMemsetAsync(ctl, 0, sizeof(dev::SeriesCtl), s));
   dev::series_init(z, l.block().rows, count, ctl, s);
-  // tol = 0 keeps every output active (c1 + c2 <= 0 never holds for non-zero
-  // terms); scale 1/||L||_1 keeps the iterates bounded.
+  // tol = -1 keeps every output active (c1 + c2 <= -nf never holds); scale
+  // 1/||L||_1 keeps the iterates bounded.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
   auto launch = [&](int i) {
-    dev::series_term(l.view(), l.group(), k[i % 2], k[(i + 1) % 2], z, ss, count, 2 + (i % 2), scale, 0.0,
+    dev::series_term(l.view(), l.group(), k[i % 2], k[(i + 1) % 2], z, ss, count, 2 + (i % 2), scale, -1.0,
                      ctl, s);
   };
   launch(0);  // warm-up

@@ -10,7 +10,7 @@ namespace qswg::dev {
 
 inline constexpr int kMaxKron = 8;      // Lindblad operators per G-QSW
 inline constexpr int kMaxSeriesD = 128; // super-step outputs (d <= floor(1e280^(1/55)) = 123)
-inline constexpr int kSeriesRegD = 8;   // per-thread register maxima in the series kernel
+inline constexpr int kSeriesRegD = 4;   // running sums updated per chunk in the series kernel
 
 // A "multi-CSR" over the n x n operator space: rows sorted by column with
 // duplicates kept adjacent in emission order (they are summed on the device
