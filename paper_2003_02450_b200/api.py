@@ -171,6 +171,8 @@ class Liouvillian:
     group = property(lambda self: self.info.group)
     row0 = property(lambda self: self.info.row0)
     rows = property(lambda self: self.info.rows)
+    format = property(lambda self: {1: "csr", 2: "sell"}[self.info.format])
+    padding = property(lambda self: self.info.padding)
 
     def one_norms(self) -> np.ndarray:
         return np.array(list(self.info.one_norms))
@@ -211,14 +213,18 @@ class Liouvillian:
         return StateVector(self)
 
 
-def _config(device, group, comm):
-    return _lib.DeviceConfig(device, group, comm._h if comm is not None else None)
+FORMATS = {"auto": 0, "csr": 1, "sell": 2}
 
 
-def build_local(omega, h, m_l, sources=(), sinks=(), device: int = 0, group: int = 0, comm=None) -> Liouvillian:
+def _config(device, group, comm, format="auto"):
+    return _lib.DeviceConfig(device, group, FORMATS[format], comm._h if comm is not None else None)
+
+
+def build_local(omega, h, m_l, sources=(), sinks=(), device: int = 0, group: int = 0, comm=None,
+                format: str = "auto") -> Liouvillian:
     """build_local (liouvillian.hpp:65-71)."""
     src, snk = _arcs(sources, sinks)
-    cfg = _config(device, group, comm)
+    cfg = _config(device, group, comm, format)
     out = C.c_void_p()
     hs, ms = SparseMatrix.of(h), SparseMatrix.of(m_l)
     check(lib.qswg_build_local(float(omega), hs._h, ms._h, src, len(sources), snk, len(sinks),
@@ -226,9 +232,10 @@ def build_local(omega, h, m_l, sources=(), sinks=(), device: int = 0, group: int
     return Liouvillian(out)
 
 
-def build_global(omega, h, lindblads, h_rot=None, device: int = 0, group: int = 0, comm=None) -> Liouvillian:
+def build_global(omega, h, lindblads, h_rot=None, device: int = 0, group: int = 0, comm=None,
+                 format: str = "auto") -> Liouvillian:
     """build_global (liouvillian.hpp:73-85)."""
-    cfg = _config(device, group, comm)
+    cfg = _config(device, group, comm, format)
     hs = SparseMatrix.of(h)
     ls = [SparseMatrix.of(x) for x in lindblads]
     arr = (C.c_void_p * max(len(ls), 1))(*[x._h.value for x in ls])

@@ -82,6 +82,8 @@ qswg::DeviceConfig device_config(const qswg_device_config* cfg) {
   if (cfg) {
     c.device = cfg->device;
     c.group = cfg->group;
+    if (cfg->format < 0 || cfg->format > 2) throw std::invalid_argument("unknown storage format");
+    c.format = cfg->format;
     c.comm = cfg->comm ? qswg::comm_from_handle(cfg->comm) : nullptr;
   } else {
     int dev = 0;
@@ -278,6 +280,8 @@ int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* inf
     info->device = L.device();
     info->rank = L.comm() ? L.comm()->rank() : 0;
     info->world = L.comm() ? L.comm()->world() : 1;
+    info->format = L.format() == qswg::dev::Format::Sell ? QSWG_FORMAT_SELL : QSWG_FORMAT_CSR;
+    info->padding = L.padding();
   });
 }
 

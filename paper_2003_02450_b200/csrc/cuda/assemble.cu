@@ -165,6 +165,46 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(KronOperands o, long lon
   }
 }
 
+__global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, long long row0, long long rows,
+                                                             const long long* slice_ptr, int* col, double2* val) {
+  // every lane of every slice, including the lanes past the last row of a
+  // partial final slice (pure padding)
+  const long long padded_rows = (rows + kSlice - 1) / kSlice * kSlice;
+  for (long long lr = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; lr < padded_rows;
+       lr += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long sl = lr / kSlice;
+    const long long base = slice_ptr[sl] + (lr - sl * kSlice);
+    const long long len = (slice_ptr[sl + 1] - slice_ptr[sl]) / kSlice;
+    long long k = 0;
+    if (lr < rows) {
+      RowMerge m;
+      merge_init(o, row0 + lr, m);
+      long long c;
+      double2 v;
+      while (merge_next(o, m, c, v)) {
+        col[base + k * kSlice] = static_cast<int>(c);
+        val[base + k * kSlice] = v;
+        ++k;
+      }
+    }
+    const int pad_col = static_cast<int>(row0 + (lr < rows ? lr : rows - 1));
+    for (; k < len; ++k) {  // padding: x[row] * 0
+      col[base + k * kSlice] = pad_col;
+      val[base + k * kSlice] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+__global__ void slice_len_kernel(const long long* grp, long long rows, long long n_slices, long long* out) {
+  for (long long sl = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; sl < n_slices;
+       sl += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long mx = 0;
+    const long long r1 = min(rows, (sl + 1) * kSlice);
+    for (long long r = sl * kSlice; r < r1; ++r) mx = max(mx, grp[r + 1] - grp[r]);
+    out[sl] = mx * kSlice;
+  }
+}
+
 __global__ void rebase_kernel(const long long* src, long long base, long long* dst, long long n) {
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -204,6 +244,23 @@ void assemble_fill(const KronOperands& o, std::int64_t row0, std::int64_t rows,
   fill_kernel<false><<<grid_for(rows), kThreads, 0, s>>>(
       o, row0, rows, reinterpret_cast<const long long*>(rowptr), col, val);
   QSWG_LAUNCH_CHECK("assemble_fill");
+}
+
+void sell_slice_entries(const std::int64_t* grp_local, std::int64_t rows, std::int64_t* slice_entries,
+                        cudaStream_t s) {
+  const long long n_slices = (rows + kSlice - 1) / kSlice;
+  if (n_slices <= 0) return;
+  slice_len_kernel<<<grid_for(n_slices), kThreads, 0, s>>>(reinterpret_cast<const long long*>(grp_local), rows,
+                                                           n_slices, reinterpret_cast<long long*>(slice_entries));
+  QSWG_LAUNCH_CHECK("sell_slice_entries");
+}
+
+void assemble_fill_sell(const KronOperands& o, std::int64_t row0, std::int64_t rows, const std::int64_t* slice_ptr,
+                        int* col, double2* val, cudaStream_t s) {
+  if (rows <= 0) return;
+  fill_sell_kernel<<<grid_for(rows + kSlice), kThreads, 0, s>>>(o, row0, rows, reinterpret_cast<const long long*>(slice_ptr),
+                                                       col, val);
+  QSWG_LAUNCH_CHECK("assemble_fill_sell");
 }
 
 void assemble_fill_abs(const KronOperands& o, std::int64_t row0, std::int64_t rows,

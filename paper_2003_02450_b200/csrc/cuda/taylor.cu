@@ -131,6 +131,28 @@ __device__ __forceinline__ void tile_loop(const CsrView& l, const double2* __res
 }
 
 // ---------------------------------------------------------------- step term
+// Stop test after one step term (expm.cpp:188-195), run by one thread of the
+// last block to arrive.
+__device__ void step_control(StepCtl* ctl, int first_of_stage, int stage, double tol) {
+  const double c2 = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
+  const double nf = bitsd(*(volatile unsigned long long*)&ctl->sum_bits);
+  ctl->spmvs += 1;
+  if (!isfinite(c2) || !isfinite(nf)) {  // expm.cpp:191-193
+    ctl->error = 1;
+    ctl->done = 1;
+  } else {
+    // stage start: c1 = ||v|| (stage 0, from step_init) or ||sum|| of the
+    // previous stage (expm.cpp:197-205), which is that stage's last nf.
+    const double c1 = first_of_stage ? (stage == 0 ? ctl->c1 : ctl->last_nf) : ctl->c1;
+    ctl->done = (c1 + c2 <= tol * nf) ? 1 : 0;  // expm.cpp:194
+    ctl->c1 = c2;
+    ctl->last_nf = nf;
+  }
+  ctl->term_bits = 0;
+  ctl->sum_bits = 0;
+  ctl->arrivals = 0;
+}
+
 struct StepTermArgs {
   CsrView l;
   const double2* x;
@@ -171,23 +193,7 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      const double c2 = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
-      const double nf = bitsd(*(volatile unsigned long long*)&ctl->sum_bits);
-      ctl->spmvs += 1;
-      if (!isfinite(c2) || !isfinite(nf)) {  // expm.cpp:191-193
-        ctl->error = 1;
-        ctl->done = 1;
-      } else {
-        // stage start: c1 = ||v|| (stage 0, from step_init) or ||sum|| of the
-        // previous stage (expm.cpp:197-205), which is that stage's last nf.
-        const double c1 = a.first_of_stage ? (a.stage == 0 ? ctl->c1 : ctl->last_nf) : ctl->c1;
-        ctl->done = (c1 + c2 <= a.tol * nf) ? 1 : 0;  // expm.cpp:194
-        ctl->c1 = c2;
-        ctl->last_nf = nf;
-      }
-      ctl->term_bits = 0;
-      ctl->sum_bits = 0;
-      ctl->arrivals = 0;
+      step_control(ctl, a.first_of_stage, a.stage, a.tol);
     }
   }
 }
@@ -378,6 +384,182 @@ __global__ void __launch_bounds__(kThreads) series_axpy_kernel(SeriesTermArgs a)
   }
 }
 
+// ------------------------------------------------------------- SELL path
+// One warp per 32-row slice, one lane per row (kernels.hpp: SellView).
+template <bool kStrict>
+__device__ __forceinline__ double2 sell_dot(const SellView& m, long long b, int len, int lane,
+                                            const double2* __restrict__ x, unsigned long long pol,
+                                            unsigned long long xpol) {
+  double2 acc = make_double2(0.0, 0.0);
+  const int* cp = m.col + b + lane;
+  const double2* vp = m.val + b + lane;
+  int k = 0;
+  if constexpr (!kStrict) {
+    constexpr int U = 4;
+    for (; k + U <= len; k += U) {
+      int c[U];
+      double2 v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = ld_stream(cp + (k + u) * kSlice, pol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(vp + (k + u) * kSlice, pol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_gather(x + c[u], xpol);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc.x = fma(v[u].x, xv[u].x, acc.x);
+        acc.x = fma(-v[u].y, xv[u].y, acc.x);
+        acc.y = fma(v[u].x, xv[u].y, acc.y);
+        acc.y = fma(v[u].y, xv[u].x, acc.y);
+      }
+    }
+  }
+  for (; k < len; ++k) {
+    const double2 v = ld_stream(vp + k * kSlice, pol);
+    const double2 xv = ld_gather(x + ld_stream(cp + k * kSlice, pol), xpol);
+    if constexpr (kStrict) {  // CSR order, separately rounded (liouvillian.cpp:120-124)
+      acc.x = __dadd_rn(acc.x, __dsub_rn(__dmul_rn(v.x, xv.x), __dmul_rn(v.y, xv.y)));
+      acc.y = __dadd_rn(acc.y, __dadd_rn(__dmul_rn(v.x, xv.y), __dmul_rn(v.y, xv.x)));
+    } else {
+      acc.x = fma(v.x, xv.x, acc.x);
+      acc.x = fma(-v.y, xv.y, acc.x);
+      acc.y = fma(v.x, xv.y, acc.y);
+      acc.y = fma(v.y, xv.x, acc.y);
+    }
+  }
+  return acc;
+}
+
+// Warp-uniform loop over slices; epi(row, acc, valid) runs on every lane.
+template <bool kStrict, class Epi>
+__device__ __forceinline__ void slice_loop(const SellView& m, const double2* __restrict__ x, Epi&& epi) {
+  const unsigned long long pol = evict_first_policy(), xpol = evict_last_policy();
+  const int lane = threadIdx.x & 31;
+  const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long sl = warp; sl < m.n_slices; sl += nwarps) {
+    const long long b = __ldg(m.slice_ptr + sl);
+    const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
+    const double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
+    const long long row = sl * kSlice + lane;
+    epi(row, acc, row < m.rows);
+  }
+}
+
+template <bool kStrict>
+__global__ void __launch_bounds__(kThreads) sell_spmv_kernel(SellView m, const double2* x, double2* y, double scale) {
+  slice_loop<kStrict>(m, x, [&](long long row, double2 acc, bool valid) {
+    if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
+  });
+}
+
+struct SellStepArgs {
+  SellView m;
+  const double2* x;
+  double2* y;
+  const double2* sum_in;
+  double2* sum_out;
+  double scale;
+  double tol;
+  StepCtl* ctl;
+  int first_of_stage;
+  int stage;
+};
+
+template <bool kStrict>
+__global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a) {
+  StepCtl* ctl = a.ctl;
+  if (*(volatile int*)&ctl->error) return;
+  if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
+  __shared__ unsigned long long red[32];
+  unsigned long long tmax = 0, smax = 0;
+  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
+  slice_loop<kStrict>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+    if (!valid) return;
+    const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
+    const double2 sv0 = ld_once(a.sum_in + row, once);
+    st_hint(a.y + row, yv, keep);
+    const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
+    st_hint(a.sum_out + row, sv, once);
+    tmax = umax64(tmax, dbits(cabs2(yv)));
+    smax = umax64(smax, dbits(cabs2(sv)));
+  });
+  tmax = block_max_bits(tmax, red);
+  smax = block_max_bits(smax, red);
+  if (threadIdx.x == 0) {
+    atomicMax(&ctl->term_bits, tmax);
+    atomicMax(&ctl->sum_bits, smax);
+    __threadfence();
+    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
+      __threadfence();
+      step_control(ctl, a.first_of_stage, a.stage, a.tol);
+    }
+  }
+}
+
+template <bool kStrict>
+__global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermArgs a, SellView m) {
+  SeriesCtl* ctl = a.ctl;
+  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+  __shared__ unsigned long long red[32];
+  __shared__ double fac[kMaxSeriesD];
+  __shared__ int act[kMaxSeriesD];
+  __shared__ unsigned long long smax_sh[kMaxSeriesD];
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
+    fac[k] = ctl->factor[k];
+    act[k] = ctl->active[k];
+    smax_sh[k] = 0;
+  }
+  __syncthreads();
+  unsigned long long tmax = 0;
+  const bool first = a.p == 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
+  slice_loop<kStrict>(m, a.x, [&](long long row, double2 acc, bool valid) {
+    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));  // K_p
+    if (valid) {
+      st_hint(a.kp + row, kv, keep);
+      tmax = umax64(tmax, dbits(cabs2(kv)));
+    }
+    const double2 zv = (first && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
+      double2 sv[kSeriesRegD];
+#pragma unroll
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
+      }
+#pragma unroll
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (k >= a.count) break;  // warp-uniform
+        unsigned long long mk = 0;
+        if (valid && act[k]) {
+          sv[u] = kStrict ? axpy<1>(sv[u], fac[k], kv) : axpy<2>(sv[u], fac[k], kv);  // expm.cpp:300-305
+          st_hint(a.sums.s[k] + row, sv[u], once);
+          mk = dbits(cabs2(sv[u]));
+        }
+        mk = warp_max_bits(mk);
+        if (lane == 0 && mk) atomicMax(&smax_sh[k], mk);
+      }
+    }
+  });
+  tmax = block_max_bits(tmax, red);
+  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
+  __syncthreads();
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
+    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
+      __threadfence();
+      series_control(ctl, a.count, a.tol);
+    }
+  }
+}
+
 // ------------------------------------------------------------ norm kernels
 // Grid-wide max |v| into *bits, last block runs `fin`.
 template <class Fin>
@@ -473,6 +655,17 @@ int persistent_grid(K kernel, long long rows) {
   return static_cast<int>(want < cap ? want : cap);
 }
 
+template <class K>
+int sell_grid(K kernel, const SellView& m) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const long long cap = static_cast<long long>(sm_count()) * per_sm;
+  long long want = (m.n_slices + kThreads / 32 - 1) / (kThreads / 32);
+  if (want < 1) want = 1;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
 int small_grid(long long n) {
   long long want = (n + kThreads - 1) / kThreads, cap = sm_count() * 4LL;
   return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
@@ -524,11 +717,19 @@ void step_init(const double2* v, std::int64_t n, StepCtl* ctl, cudaStream_t s) {
   QSWG_LAUNCH_CHECK("step_init");
 }
 
-void step_term(const CsrView& l, int group, const double2* x, double2* y, const double2* sum_in,
-               double2* sum_out, double scale, bool first_of_stage, int stage, double tol,
-               StepCtl* ctl, cudaStream_t s) {
-  StepTermArgs a{l, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage};
-  dispatch_group<StepTermK>(group, l.rows, s, a);
+void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,
+               double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, cudaStream_t s) {
+  if (m.format == Format::Sell) {
+    SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage};
+    if (m.group == 1) {
+      sell_step_term_kernel<true><<<sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s>>>(a);
+    } else {
+      sell_step_term_kernel<false><<<sell_grid(sell_step_term_kernel<false>, m.sell), kThreads, 0, s>>>(a);
+    }
+  } else {
+    StepTermArgs a{m.csr, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage};
+    dispatch_group<StepTermK>(m.group, m.csr.rows, s, a);
+  }
   QSWG_LAUNCH_CHECK("step_term");
 }
 
@@ -538,10 +739,21 @@ void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, cu
   QSWG_LAUNCH_CHECK("series_init");
 }
 
-void series_term(const CsrView& l, int group, const double2* x, double2* kp, const double2* z,
+void series_term(const DevMatrix& m, const double2* x, double2* kp, const double2* z,
                  const SeriesSums& sums, int count, int p, double scale, double tol,
                  SeriesCtl* ctl, cudaStream_t s) {
-  SeriesTermArgs a{l, x, kp, z, sums, count, p, scale, tol, ctl};
+  SeriesTermArgs a{m.csr, x, kp, z, sums, count, p, scale, tol, ctl};
+  if (m.format == Format::Sell) {
+    if (m.group == 1) {
+      sell_series_term_kernel<true><<<sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s>>>(a, m.sell);
+    } else {
+      sell_series_term_kernel<false><<<sell_grid(sell_series_term_kernel<false>, m.sell), kThreads, 0, s>>>(a, m.sell);
+    }
+    QSWG_LAUNCH_CHECK("series_term");
+    return;
+  }
+  const int group = m.group;
+  const CsrView& l = m.csr;
   const int mode = series_mode();
   if (mode == 0) {
     dispatch_group<SeriesTermK>(group, l.rows, s, a);
@@ -557,8 +769,16 @@ void series_term(const CsrView& l, int group, const double2* x, double2* kp, con
   QSWG_LAUNCH_CHECK("series_term");
 }
 
-void spmv(const CsrView& l, int group, const double2* x, double2* y, double scale, cudaStream_t s) {
-  dispatch_group<SpmvK>(group, l.rows, s, l, x, y, scale);
+void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaStream_t s) {
+  if (m.format == Format::Sell) {
+    if (m.group == 1) {
+      sell_spmv_kernel<true><<<sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);
+    } else {
+      sell_spmv_kernel<false><<<sell_grid(sell_spmv_kernel<false>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);
+    }
+  } else {
+    dispatch_group<SpmvK>(m.group, m.csr.rows, s, m.csr, x, y, scale);
+  }
   QSWG_LAUNCH_CHECK("spmv");
 }
 

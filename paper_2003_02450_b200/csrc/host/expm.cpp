@@ -73,7 +73,7 @@ StepParameters enqueue_step(const Liouvillian& l, const double2* v, double t,
   sums[(sp.s - 1) % 2] = out;
   sums[sp.s % 2] = ws.get(kSOther, static_cast<std::size_t>(len));
   dev::StepCtl* ctl = step_ctl(l);
-  const dev::CsrView view = l.view();
+  const dev::DevMatrix mat = l.matrix();
   dev::step_init(v, l.block().rows, ctl, s);  // c1 = ||v||_inf (expm.cpp:165-170)
   launches += 1 + sp.s * sp.m_star;
   const double s_count = static_cast<double>(sp.s);
@@ -85,7 +85,7 @@ StepParameters enqueue_step(const Liouvillian& l, const double2* v, double t,
       const double2* x = j == 1 ? x_stage : term[(j - 1) % 2];
       double2* y = term[j % 2];
       const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
-      dev::step_term(view, l.group(), x, y, j == 1 ? x_stage : acc, acc, scale, j == 1,
+      dev::step_term(mat, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1,
                      static_cast<int>(st), params.tolerance, ctl, s);
     }
   }
@@ -161,7 +161,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
     std::vector<double2*> sums(static_cast<std::size_t>(d));
     for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ws.get(kSums + static_cast<std::size_t>(k), static_cast<std::size_t>(len));
     dev::SeriesCtl* ctl = series_ctl(l);
-    const dev::CsrView view = l.view();
+    const dev::DevMatrix mat = l.matrix();
     for (std::int64_t super = 0; super <= n_super; ++super) {
       const std::int64_t count = super < n_super ? d : remainder;
       if (count == 0) break;
@@ -172,7 +172,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
       for (std::int64_t p = 1; p <= m_star; ++p) {
         const double2* x = p == 1 ? z : kbuf[(p - 1) % 2];
         double2* kp = kbuf[p % 2];
-        dev::series_term(view, l.group(), x, kp, z, ss, static_cast<int>(count), static_cast<int>(p),
+        dev::series_term(mat, x, kp, z, ss, static_cast<int>(count), static_cast<int>(p),
                          h / static_cast<double>(p), params.tolerance, ctl, s);
       }
       for (std::int64_t k = 1; k <= count; ++k) emit(super * d + k, sums[static_cast<std::size_t>(k - 1)]);
@@ -207,7 +207,7 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   // 1/||L||_1 keeps the iterates bounded.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
   auto launch = [&](int i) {
-    dev::series_term(l.view(), l.group(), k[i % 2], k[(i + 1) % 2], z, ss, count, 2 + (i % 2), scale, -1.0,
+    dev::series_term(l.matrix(), k[i % 2], k[(i + 1) % 2], z, ss, count, 2 + (i % 2), scale, -1.0,
                      ctl, s);
   };
   launch(0);  // warm-up

@@ -21,6 +21,7 @@ namespace {
 
 constexpr std::int64_t kExactNormDimLimit = 4096;  // liouvillian.cpp:13
 constexpr std::int64_t kMaxVertices = 46340;       // n^2 must fit int32 columns
+constexpr double kSellMaxPadding = 1.03;            // SELL-32 if stored/nnz <= this
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
 
@@ -192,9 +193,53 @@ dev::CsrView Liouvillian::view() const {
   return v;
 }
 
+dev::DevMatrix Liouvillian::matrix(int group_override) const {
+  dev::DevMatrix m;
+  m.format = format_;
+  m.group = group_override ? group_override : group_;
+  m.csr = view();
+  m.sell.slice_ptr = slice_ptr_.get();
+  m.sell.col = col_.get();
+  m.sell.val = val_.get();
+  m.sell.rows = block_.rows;
+  m.sell.row0 = block_.row0;
+  m.sell.n_slices = n_slices_;
+  return m;
+}
+
 void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
                            std::vector<Complex>& val) const {
   DeviceGuard g(device_);
+  if (format_ == dev::Format::Sell) {
+    // de-pad: a row's genuine entries precede its padding (val == 0 exactly;
+    // canonical entries are never zero)
+    std::vector<std::int64_t> sp(static_cast<std::size_t>(n_slices_) + 1);
+    QSWG_CHECK(cudaMemcpy(sp.data(), slice_ptr_.get(), sp.size() * sizeof(std::int64_t), cudaMemcpyDeviceToHost));
+    const std::size_t total = static_cast<std::size_t>(sp.back());
+    std::vector<int> c32(total);
+    std::vector<Complex> v(total);
+    if (total) {
+      QSWG_CHECK(cudaMemcpy(c32.data(), col_.get(), total * sizeof(int), cudaMemcpyDeviceToHost));
+      QSWG_CHECK(cudaMemcpy(v.data(), val_.get(), total * sizeof(double2), cudaMemcpyDeviceToHost));
+    }
+    rowptr.assign(static_cast<std::size_t>(block_.rows) + 1, 0);
+    col.clear();
+    val.clear();
+    col.reserve(static_cast<std::size_t>(nnz_local_));
+    val.reserve(static_cast<std::size_t>(nnz_local_));
+    for (std::int64_t r = 0; r < block_.rows; ++r) {
+      const std::int64_t sl = r / dev::kSlice, lane = r % dev::kSlice;
+      const std::int64_t len = (sp[static_cast<std::size_t>(sl) + 1] - sp[static_cast<std::size_t>(sl)]) / dev::kSlice;
+      for (std::int64_t k = 0; k < len; ++k) {
+        const std::size_t e = static_cast<std::size_t>(sp[static_cast<std::size_t>(sl)] + k * dev::kSlice + lane);
+        if (v[e] == Complex{}) break;
+        col.push_back(c32[e]);
+        val.push_back(v[e]);
+      }
+      rowptr[static_cast<std::size_t>(r) + 1] = static_cast<std::int64_t>(col.size());
+    }
+    return;
+  }
   rowptr.resize(static_cast<std::size_t>(block_.rows) + 1);
   std::vector<int> c32(static_cast<std::size_t>(nnz_local_));
   val.resize(static_cast<std::size_t>(nnz_local_));
@@ -210,7 +255,7 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
 
 void Liouvillian::multiply(const double2* x, double2* y, double scale) const {
   DeviceGuard g(device_);
-  dev::spmv(view(), group_, x, y, scale, stream_);
+  dev::spmv(matrix(), x, y, scale, stream_);
 }
 
 double Liouvillian::time_spmv(int iters, int group) const {
@@ -220,9 +265,10 @@ double Liouvillian::time_spmv(int iters, int group) const {
   cudaEvent_t e0, e1;
   QSWG_CHECK(cudaEventCreate(&e0));
   QSWG_CHECK(cudaEventCreate(&e1));
-  dev::spmv(view(), group, x.get(), y.get(), 1.0, stream_);  // warm-up
+  const dev::DevMatrix m = matrix(group);
+  dev::spmv(m, x.get(), y.get(), 1.0, stream_);  // warm-up
   QSWG_CHECK(cudaEventRecord(e0, stream_));
-  for (int i = 0; i < iters; ++i) dev::spmv(view(), group, x.get(), y.get(), 1.0, stream_);
+  for (int i = 0; i < iters; ++i) dev::spmv(m, x.get(), y.get(), 1.0, stream_);
   QSWG_CHECK(cudaEventRecord(e1, stream_));
   QSWG_CHECK(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -372,8 +418,41 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     for (int p = 0; p < 9; ++p) std::memcpy(&l->norms_[static_cast<std::size_t>(p)], &bits[p], sizeof(double));
   }
 
-  // ---- the superoperator row block ----
-  fill_block(ops.get(), grp, colptr, n, l->block_, l->rowptr_, l->col_, l->val_, l->nnz_local_, s);
+  // ---- the superoperator row block: SELL-32 when its padding is small ----
+  {
+    const std::int64_t j0 = l->block_.row0 / n, j1 = (l->block_.row0 + l->block_.rows) / n;
+    l->nnz_local_ = colptr[static_cast<std::size_t>(j1)] - colptr[static_cast<std::size_t>(j0)];
+  }
+  l->n_slices_ = (l->block_.rows + dev::kSlice - 1) / dev::kSlice;
+  std::int64_t sell_entries = 0;
+  if (l->n_slices_ > 0) {
+    DeviceBuffer<std::int64_t> se(static_cast<std::size_t>(l->n_slices_) + 1);
+    QSWG_CHECK(cudaMemsetAsync(se.get(), 0, se.bytes(), s));
+    dev::sell_slice_entries(grp.get() + l->block_.row0, l->block_.rows, se.get(), s);
+    l->slice_ptr_.resize(static_cast<std::size_t>(l->n_slices_) + 1);
+    std::size_t tmp_bytes = 0;
+    dev::exclusive_scan(se.get(), l->slice_ptr_.get(), l->n_slices_ + 1, nullptr, tmp_bytes, s);
+    DeviceBuffer<unsigned char> tmp(tmp_bytes);
+    dev::exclusive_scan(se.get(), l->slice_ptr_.get(), l->n_slices_ + 1, tmp.get(), tmp_bytes, s);
+    QSWG_CHECK(cudaMemcpyAsync(&sell_entries, l->slice_ptr_.get() + l->n_slices_, sizeof(std::int64_t),
+                               cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+  }
+  const double pad = l->nnz_local_ ? static_cast<double>(sell_entries) / static_cast<double>(l->nnz_local_) : 1.0;
+  const bool use_sell = l->nnz_local_ > 0 && (cfg.format == 2 || (cfg.format == 0 && pad <= kSellMaxPadding));
+  if (use_sell) {
+    l->format_ = dev::Format::Sell;
+    l->padding_ = pad;
+    l->col_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));
+    l->val_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));
+    dev::assemble_fill_sell(ops.get(), l->block_.row0, l->block_.rows, l->slice_ptr_.get(), l->col_.get(),
+                            l->val_.get(), s);
+    QSWG_CHECK(cudaStreamSynchronize(s));
+  } else {
+    l->slice_ptr_.reset();
+    l->format_ = dev::Format::Csr;
+    fill_block(ops.get(), grp, colptr, n, l->block_, l->rowptr_, l->col_, l->val_, l->nnz_local_, s);
+  }
   grp.reset();
 
   // ---- SpMV lanes per row ----
@@ -381,6 +460,8 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   if (cfg.group) {
     if (!dev::valid_group(cfg.group)) throw std::invalid_argument("group must be 1, 2, 4, 8, 16 or 32");
     l->group_ = cfg.group;
+  } else if (l->format_ == dev::Format::Sell) {
+    l->group_ = 32;  // lane per row; `group` only distinguishes the bitwise mode (1)
   } else if (l->nnz_local_ < (1 << 22)) {
     l->group_ = heuristic_group(mean_row);
   } else {

@@ -26,6 +26,7 @@ class Comm;  // multi-GPU exchange (comm.hpp); nullptr when world == 1
 struct DeviceConfig {
   int device = 0;       // CUDA ordinal
   int group = 0;        // lanes per row for the SpMV kernels; 0 = autotune
+  int format = 0;       // 0 auto, 1 CSR, 2 SELL-32
   Comm* comm = nullptr; // borrowed; shared by every handle on this rank
 };
 
@@ -68,6 +69,11 @@ class Liouvillian {
   cudaStream_t stream() const { return stream_; }
   Comm* comm() const { return comm_; }
   dev::CsrView view() const;
+  /// The local block as the Taylor kernels see it (format + lanes per row).
+  dev::DevMatrix matrix(int group_override = 0) const;
+  dev::Format format() const { return format_; }
+  /// Stored entries / nnz (SELL padding; 1.0 for CSR).
+  double padding() const { return padding_; }
 
   /// Local row block downloaded as CSR with global columns (parity / debug).
   void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
@@ -92,7 +98,11 @@ class Liouvillian {
   std::vector<std::int64_t> starts_;
   std::int64_t nnz_local_ = 0, nnz_total_ = 0;
   std::array<double, 9> norms_{};
-  DeviceBuffer<std::int64_t> rowptr_;
+  dev::Format format_ = dev::Format::Csr;
+  double padding_ = 1.0;
+  std::int64_t n_slices_ = 0;
+  DeviceBuffer<std::int64_t> slice_ptr_;  // SELL
+  DeviceBuffer<std::int64_t> rowptr_;     // CSR
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;
   mutable Workspace ws_;

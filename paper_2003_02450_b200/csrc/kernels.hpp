@@ -50,6 +50,36 @@ struct CsrView {
   std::int64_t row0 = 0;
 };
 
+// Sliced ELLPACK with slices of kSlice = 32 consecutive rows: entry k of the
+// rows of slice s lives at slice_ptr[s] + k * 32 + lane (lane = row % 32),
+// k < (slice_ptr[s+1] - slice_ptr[s]) / 32; rows shorter than the slice's
+// longest row are padded with (col = row, val = 0).  Entries of a row keep
+// the canonical CSR order.  One warp per slice, one lane per row: the matrix
+// stream, the x gathers of structured (lattice) superoperators and the
+// epilogue vectors are all coalesced.
+inline constexpr int kSlice = 32;
+struct SellView {
+  const std::int64_t* slice_ptr = nullptr;
+  const int* col = nullptr;
+  const double2* val = nullptr;
+  std::int64_t rows = 0;
+  std::int64_t row0 = 0;
+  std::int64_t n_slices = 0;
+};
+
+enum class Format : int { Csr = 0, Sell = 1 };
+
+// The device superoperator block as the Taylor kernels see it.  group: CSR
+// lanes per row (2..32); group == 1 selects the bitwise reference-order mode
+// for either format.
+struct DevMatrix {
+  Format format = Format::Csr;
+  int group = 8;
+  CsrView csr;
+  SellView sell;
+  std::int64_t rows() const { return format == Format::Csr ? csr.rows : sell.rows; }
+};
+
 struct RealCsrView {
   const std::int64_t* rowptr = nullptr;
   const int* col = nullptr;
@@ -69,6 +99,12 @@ void rebase_rowptr(const std::int64_t* src, std::int64_t base, std::int64_t* dst
                    cudaStream_t s);
 void assemble_fill(const KronOperands& o, std::int64_t row0, std::int64_t rows,
                    const std::int64_t* rowptr, int* col, double2* val, cudaStream_t s);
+// slice_entries[s] = 32 * (longest row of slice s), s < ceil(rows / 32);
+// grp_local holds rows + 1 row offsets (any base).
+void sell_slice_entries(const std::int64_t* grp_local, std::int64_t rows, std::int64_t* slice_entries,
+                        cudaStream_t s);
+void assemble_fill_sell(const KronOperands& o, std::int64_t row0, std::int64_t rows,
+                        const std::int64_t* slice_ptr, int* col, double2* val, cudaStream_t s);
 void assemble_fill_abs(const KronOperands& o, std::int64_t row0, std::int64_t rows,
                        const std::int64_t* rowptr, int* col, double* val, cudaStream_t s);
 
@@ -124,7 +160,7 @@ void step_init(const double2* v, std::int64_t n, StepCtl* ctl, cudaStream_t s);
 //   y = scale * (L x);  sum_out = sum_in + y;  c2 = ||y||, nf = ||sum_out||;
 //   stop test c1 + c2 <= tol * nf decided on the device.  Skips itself when
 //   the stage is already done (unless first_of_stage) or on error.
-void step_term(const CsrView& l, int group, const double2* x, double2* y, const double2* sum_in,
+void step_term(const DevMatrix& l, const double2* x, double2* y, const double2* sum_in,
                double2* sum_out, double scale, bool first_of_stage, int stage, double tol,
                StepCtl* ctl, cudaStream_t s);
 // Super-step start of `series` (expm.cpp:267-276): z_norm = ||Z||, count
@@ -132,11 +168,11 @@ void step_term(const CsrView& l, int group, const double2* x, double2* y, const 
 void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, cudaStream_t s);
 // K_p = scale * (L K_{p-1}); for every active k: S_k = (p == 1 ? Z : S_k) + k^p K_p
 // with per-k stop tests (expm.cpp:278-316, evaluated p-major).
-void series_term(const CsrView& l, int group, const double2* x, double2* kp, const double2* z,
+void series_term(const DevMatrix& l, const double2* x, double2* kp, const double2* z,
                  const SeriesSums& sums, int count, int p, double scale, double tol,
                  SeriesCtl* ctl, cudaStream_t s);
 // y = scale * (L x) (liouvillian.cpp:346-360).
-void spmv(const CsrView& l, int group, const double2* x, double2* y, double scale, cudaStream_t s);
+void spmv(const DevMatrix& l, const double2* x, double2* y, double scale, cudaStream_t s);
 // pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).
 void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
                double* pops, cudaStream_t s);

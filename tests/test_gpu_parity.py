@@ -19,7 +19,9 @@ pytestmark = pytest.mark.gpu
 api = pytest.importorskip("paper_2003_02450_b200.api")
 from paper_2003_02450_b200 import graphs  # noqa: E402
 
-MODES = [0, 1]  # autotuned fast kernels, bitwise reference order (group=1)
+# (group, storage format): autotuned fast kernels and the bitwise reference
+# order (group=1), each over CSR and SELL-32 storage.
+MODES = [(0, "csr"), (0, "sell"), (1, "csr"), (1, "sell")]
 RHO_TOL = 1e-10
 TRACE_TOL = 1e-12
 
@@ -29,10 +31,12 @@ def trace_err(states, n):
     return np.abs(np.trace(s, axis1=1, axis2=2) - 1.0).max()
 
 
+@pytest.mark.parametrize("fmt", ["csr", "sell"])
 @pytest.mark.parametrize("name", CASE_NAMES)
-def test_csr_and_norms_match_reference(name):
+def test_csr_and_norms_match_reference(name, fmt):
     c = Case(name)
-    l = c.build_gpu(api)
+    l = c.build_gpu(api, format=fmt)
+    assert l.format == fmt
     assert l.dim == c.dim and l.nnz == c.nnz
     L = l.gather_full()
     assert np.array_equal(L.indptr, c.L.indptr)
@@ -41,11 +45,11 @@ def test_csr_and_norms_match_reference(name):
     np.testing.assert_allclose(l.one_norms(), c.norms, rtol=1e-13, atol=0)
 
 
-@pytest.mark.parametrize("group", MODES)
+@pytest.mark.parametrize("group,fmt", MODES)
 @pytest.mark.parametrize("name", CASE_NAMES)
-def test_spmv_matches_reference(name, group):
+def test_spmv_matches_reference(name, group, fmt):
     c = Case(name)
-    l = c.build_gpu(api, group=group)
+    l = c.build_gpu(api, group=group, format=fmt)
     y = l.spmv(c.z["spmv_x"])
     scale = max(1.0, np.abs(c.z["spmv_y"]).max())
     assert np.abs(y - c.z["spmv_y"]).max() <= 1e-13 * scale
@@ -62,11 +66,24 @@ def counts_must_match(name, group):
     return group == 1 or name.startswith("c")
 
 
-@pytest.mark.parametrize("group", MODES)
-@pytest.mark.parametrize("name", CASE_NAMES)
-def test_series_matches_reference(name, group):
+@pytest.mark.parametrize("name", ["c1_n64", "c2_n36", "c5_n64"])
+def test_bitwise_mode_formats_agree(name):
+    """Both storage formats visit a row's entries in CSR order, so the
+    bitwise mode gives bit-identical states."""
     c = Case(name)
-    l = c.build_gpu(api, group=group)
+    t1, tq, q = c.series
+    out = []
+    for fmt in ("csr", "sell"):
+        l = c.build_gpu(api, group=1, format=fmt)
+        out.append(api.series(l, l.state().from_probabilities(c.rho0), t1, tq, int(q), states=True).states)
+    assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("group,fmt", MODES)
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_series_matches_reference(name, group, fmt):
+    c = Case(name)
+    l = c.build_gpu(api, group=group, format=fmt)
     v = l.state().from_probabilities(c.rho0)
     t1, tq, q = c.series
     r = api.series(l, v, t1, tq, int(q), states=True)
@@ -79,11 +96,11 @@ def test_series_matches_reference(name, group):
     np.testing.assert_allclose(r.times, [t1 + (tq - t1) / q * k for k in range(int(q) + 1)])
 
 
-@pytest.mark.parametrize("group", MODES)
+@pytest.mark.parametrize("group,fmt", MODES)
 @pytest.mark.parametrize("name", CASE_NAMES)
-def test_step_matches_reference(name, group):
+def test_step_matches_reference(name, group, fmt):
     c = Case(name)
-    l = c.build_gpu(api, group=group)
+    l = c.build_gpu(api, group=group, format=fmt)
     v = l.state().from_probabilities(c.rho0)
     for t, want, nsp in zip(c.z["step_t"], c.z["step_states"], c.z["step_spmvs"]):
         w, info = api.step(l, v, float(t))

@@ -14,14 +14,15 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--size", type=int, default=None)
 ap.add_argument("--series", type=int, default=1)
 ap.add_argument("--group", type=int, default=0)
+ap.add_argument("--format", default="auto")
 a = ap.parse_args()
 w = graphs.config(a.config, size=a.size)
 if w.kind == "local":
-    l = api.build_local(w.omega, w.h, w.ops[0], group=a.group)
+    l = api.build_local(w.omega, w.h, w.ops[0], group=a.group, format=a.format)
 else:
-    l = api.build_global(w.omega, w.h, w.ops, group=a.group)
+    l = api.build_global(w.omega, w.h, w.ops, group=a.group, format=a.format)
 v = l.state().from_probabilities(w.rho0)
 for _ in range(a.series):
     r = api.series(l, v, w.t1, w.tq, w.steps)
-print(f"{a.config}: dim={l.dim} nnz={l.nnz} group={l.group} spmvs={r.info.spmvs} launches={r.info.launches} "
+print(f"{a.config}: dim={l.dim} nnz={l.nnz} format={l.format} pad={l.padding:.3f} group={l.group} spmvs={r.info.spmvs} launches={r.info.launches} "
       f"device_ms={r.info.device_ms:.3f} pop0={r.populations[-1][0]:.15f}")
