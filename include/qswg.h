@@ -152,10 +152,26 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
                 qswg_series_info* info);
 
 /* ---- multi-GPU (one process per GPU) ------------------------------------ */
+/* Row partition on rho-column boundaries balanced by nnz (the device build
+ * uses the same function; replaces RowPartition::even, partition.cpp:8-19):
+ * colptr[j] = nnz before rho column j (n+1 entries) -> starts[world+1]. */
+int qswg_plan_rows(int64_t n, const int64_t* colptr, int world, int64_t* starts);
+/* Halo plan of one rank (replaces plan_communication, partition.cpp:26-59):
+ * hull [lo[q], hi[q]) of the columns in cols[] owned by peer q (empty: lo == hi). */
+int qswg_plan_halo(const int64_t* cols, int64_t nnz, const int64_t* starts, int world, int rank, int64_t* lo,
+                   int64_t* hi);
+/* The partition (starts[world+1]) and halo table (world x world, row r =
+ * what rank r receives from each peer) of a built superoperator. */
+int qswg_liouvillian_partition(const qswg_liouvillian* l, int64_t* starts, int64_t* halo_lo, int64_t* halo_hi);
 int qswg_comm_unique_id_size(void);
 int qswg_comm_get_unique_id(uint8_t* id);
 int qswg_comm_create(const uint8_t* id, int rank, int world, int device, qswg_comm** out);
 void qswg_comm_destroy(qswg_comm* c);
+/* `world` linked in-process communicators, one per host thread: runs the
+ * multi-GPU control flow (halo exchanges, allreduces) inside one process,
+ * e.g. several ranks on one GPU for testing; collectives are host-side
+ * rendezvous, so no kernel waits on another rank. */
+int qswg_comm_create_local(int world, qswg_comm** outs);
 
 #ifdef __cplusplus
 }

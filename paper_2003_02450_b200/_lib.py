@@ -129,10 +129,14 @@ SIGNATURES = {
     "qswg_step": (C.c_int, [vp, vp, C.c_double, C.c_double, vp, C.POINTER(StepInfo)]),
     "qswg_series": (C.c_int, [vp, vp, C.c_double, C.c_double, i64, C.c_double, dp, dp, vp,
                               C.POINTER(SeriesInfo)]),
+    "qswg_plan_rows": (C.c_int, [i64, i64p, C.c_int, i64p]),
+    "qswg_plan_halo": (C.c_int, [i64p, i64, i64p, C.c_int, C.c_int, i64p, i64p]),
+    "qswg_liouvillian_partition": (C.c_int, [vp, i64p, i64p, i64p]),
     "qswg_comm_unique_id_size": (C.c_int, []),
     "qswg_comm_get_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "qswg_comm_create": (C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "qswg_comm_destroy": (None, [vp]),
+    "qswg_comm_create_local": (C.c_int, [C.c_int, C.POINTER(vp)]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

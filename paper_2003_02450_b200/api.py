@@ -198,6 +198,14 @@ class Liouvillian:
         check(lib.qswg_time_spmv(self._h, iters, group, C.byref(ms)))
         return ms.value
 
+    def partition(self):
+        """(starts[world+1], halo_lo[world, world], halo_hi[world, world])."""
+        w = self.info.world
+        st = np.zeros(w + 1, np.int64)
+        lo, hi = np.zeros((w, w), np.int64), np.zeros((w, w), np.int64)
+        check(lib.qswg_liouvillian_partition(self._h, _i64p(st), _i64p(lo), _i64p(hi)))
+        return st, lo, hi
+
     def time_series_term(self, iters: int = 20, count: int = 1) -> float:
         ms = C.c_double()
         check(lib.qswg_time_series_term(self._h, iters, count, C.byref(ms)))
@@ -345,6 +353,24 @@ def series(l: Liouvillian, v: StateVector, t1: float, tq: float, steps: int, tol
 
 
 # -------------------------------------------------------------- multi-GPU
+def plan_rows(n: int, colptr, world: int) -> np.ndarray:
+    """Row partition on rho-column boundaries balanced by nnz (host planner)."""
+    cp = np.ascontiguousarray(colptr, dtype=np.int64)
+    out = np.zeros(world + 1, np.int64)
+    check(lib.qswg_plan_rows(n, _i64p(cp), world, _i64p(out)))
+    return out
+
+
+def plan_halo(cols, starts, rank: int):
+    """Per-peer hull [lo, hi) of the columns a rank's block references."""
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    st = np.ascontiguousarray(starts, dtype=np.int64)
+    world = len(st) - 1
+    lo, hi = np.zeros(world, np.int64), np.zeros(world, np.int64)
+    check(lib.qswg_plan_halo(_i64p(cols) if cols.size else None, cols.size, _i64p(st), world, rank,
+                             _i64p(lo), _i64p(hi)))
+    return lo, hi
+
 class Comm:
     """NCCL communicator for one rank (qswg_comm_*); one process per GPU."""
 
@@ -370,6 +396,13 @@ class Comm:
         h = C.c_void_p()
         check(lib.qswg_comm_create(buf, rank, world, device, C.byref(h)))
         return Comm(h)
+
+    @staticmethod
+    def local_group(world: int) -> list:
+        """`world` linked in-process communicators (one per host thread)."""
+        arr = (C.c_void_p * world)()
+        check(lib.qswg_comm_create_local(world, arr))
+        return [Comm(C.c_void_p(arr[r])) for r in range(world)]
 
     @staticmethod
     def create(rank: int, world: int, device: int) -> "Comm":

@@ -13,6 +13,7 @@
 
 #include "host/comm.hpp"
 #include "host/device.hpp"
+#include "host/dist.hpp"
 #include "host/expm.hpp"
 #include "host/graph.hpp"
 #include "host/liouvillian.hpp"
@@ -421,6 +422,7 @@ int qswg_state_populations(const qswg_state* s, double* out) {
     qswg::DeviceBuffer<double> d(static_cast<std::size_t>(L.n()));
     QSWG_CHECK(cudaMemsetAsync(d.get(), 0, d.bytes(), L.stream()));
     qswg::dev::diag_real(s->v.get(), L.block().row0, L.block().rows, L.n(), d.get(), L.stream());
+    if (L.comm() && L.comm()->world() > 1) L.comm()->allreduce_sum_f64(d.get(), static_cast<std::size_t>(L.n()), L.stream());
     QSWG_CHECK(cudaMemcpyAsync(out, d.get(), d.bytes(), cudaMemcpyDeviceToHost, L.stream()));
     QSWG_CHECK(cudaStreamSynchronize(L.stream()));
   });
@@ -502,6 +504,8 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
                                    cudaMemcpyDeviceToDevice, s));
     };
     const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit);
+    if (L.comm() && L.comm()->world() > 1)  // every diagonal element has exactly one owner
+      L.comm()->allreduce_sum_f64(lm->pops.get(), static_cast<std::size_t>((steps + 1) * n), s);
     QSWG_CHECK(cudaEventRecord(e1, s));
     if (pops_host)
       QSWG_CHECK(cudaMemcpyAsync(pops_host, lm->pops.get(), lm->pops.bytes(), cudaMemcpyDeviceToHost, s));
@@ -525,6 +529,47 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
   });
 }
 
+// ------------------------------------------------------------ planning
+int qswg_plan_rows(int64_t n, const int64_t* colptr, int world, int64_t* starts) {
+  return guarded([&] {
+    need(colptr, "colptr");
+    need(starts, "starts");
+    const std::vector<int64_t> cp(colptr, colptr + n + 1);
+    const std::vector<int64_t> st = qswg::partition_rows(cp, n, world);
+    std::memcpy(starts, st.data(), st.size() * sizeof(int64_t));
+  });
+}
+
+int qswg_plan_halo(const int64_t* cols, int64_t nnz, const int64_t* starts, int world, int rank, int64_t* lo,
+                   int64_t* hi) {
+  return guarded([&] {
+    need(starts, "starts");
+    need(lo, "lo");
+    need(hi, "hi");
+    if (rank < 0 || rank >= world) throw std::invalid_argument("rank out of range");
+    const std::vector<int64_t> st(starts, starts + world + 1);
+    const auto needs = qswg::halo_needs_host(cols, nnz, st, rank);
+    for (int q = 0; q < world; ++q) {
+      lo[q] = needs[static_cast<std::size_t>(q)].lo;
+      hi[q] = needs[static_cast<std::size_t>(q)].hi;
+    }
+  });
+}
+
+int qswg_liouvillian_partition(const qswg_liouvillian* l, int64_t* starts, int64_t* halo_lo, int64_t* halo_hi) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    const auto& st = l->l->partition();
+    const std::size_t w = st.size() - 1;
+    if (starts) std::memcpy(starts, st.data(), st.size() * sizeof(int64_t));
+    for (std::size_t r = 0; r < w; ++r)
+      for (std::size_t q = 0; q < w; ++q) {
+        if (halo_lo) halo_lo[r * w + q] = l->l->halo_lo()[r][q];
+        if (halo_hi) halo_hi[r * w + q] = l->l->halo_hi()[r][q];
+      }
+  });
+}
+
 // ------------------------------------------------------------------ comm
 int qswg_comm_unique_id_size(void) { return qswg::comm_unique_id_size(); }
 int qswg_comm_get_unique_id(uint8_t* id) {
@@ -544,5 +589,17 @@ int qswg_comm_create(const uint8_t* id, int rank, int world, int device, qswg_co
   return g ? g : rc;
 }
 void qswg_comm_destroy(qswg_comm* c) { qswg::comm_destroy(c); }
+
+int qswg_comm_create_local(int world, qswg_comm** outs) {
+  return guarded([&] {
+    need(outs, "outs");
+    auto comms = qswg::make_local_comms(world);
+    for (int r = 0; r < world; ++r) {
+      auto h = std::make_unique<qswg_comm>();
+      h->c = std::move(comms[static_cast<std::size_t>(r)]);
+      outs[r] = h.release();
+    }
+  });
+}
 
 }  // extern "C"

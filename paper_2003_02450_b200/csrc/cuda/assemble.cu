@@ -211,6 +211,34 @@ __global__ void rebase_kernel(const long long* src, long long base, long long* d
     dst[k] = src[k] - base;
 }
 
+__global__ void hull_kernel(const int* col, long long n, const long long* starts, int world, int rank,
+                            long long* lo, long long* hi) {
+  long long mn[8], mx[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    mn[q] = LLONG_MAX;
+    mx[q] = LLONG_MIN;
+  }
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = col[k];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < world && q != rank && c >= starts[q] && c < starts[q + 1]) {
+        mn[q] = min(mn[q], c);
+        mx[q] = max(mx[q], c + 1);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q < world && mn[q] != LLONG_MAX) {
+      atomicMin(lo + q, mn[q]);
+      atomicMax(hi + q, mx[q]);
+    }
+  }
+}
+
 int grid_for(long long rows) {
   long long want = (rows + kThreads - 1) / kThreads;
   long long cap = static_cast<long long>(sm_count()) * 8;
@@ -229,6 +257,15 @@ void assemble_count(const KronOperands& o, std::int64_t row0, std::int64_t rows,
 void exclusive_scan(const std::int64_t* counts, std::int64_t* rowptr, std::int64_t n, void* tmp,
                     std::size_t& tmp_bytes, cudaStream_t s) {
   QSWG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, rowptr, n, s));
+}
+
+void halo_hulls(const int* col, std::int64_t n, const std::int64_t* starts, int world, int rank, std::int64_t* lo,
+                std::int64_t* hi, cudaStream_t s) {
+  if (world > 8) throw std::invalid_argument("at most 8 ranks per communicator");
+  if (n <= 0) return;
+  hull_kernel<<<grid_for(n), kThreads, 0, s>>>(col, n, reinterpret_cast<const long long*>(starts), world, rank,
+                                               reinterpret_cast<long long*>(lo), reinterpret_cast<long long*>(hi));
+  QSWG_LAUNCH_CHECK("halo_hulls");
 }
 
 void rebase_rowptr(const std::int64_t* src, std::int64_t base, std::int64_t* dst, std::int64_t n,

@@ -164,6 +164,7 @@ struct StepTermArgs {
   StepCtl* ctl;
   int first_of_stage;
   int stage;
+  int decide;
 };
 
 template <int G>
@@ -193,7 +194,11 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      step_control(ctl, a.first_of_stage, a.stage, a.tol);
+      if (a.decide) {
+        step_control(ctl, a.first_of_stage, a.stage, a.tol);
+      } else {
+        ctl->arrivals = 0;  // maxima stay for the allreduce + step_control_kernel
+      }
     }
   }
 }
@@ -237,6 +242,7 @@ struct SeriesTermArgs {
   double scale;
   double tol;
   SeriesCtl* ctl;
+  int decide;
 };
 
 template <int G>
@@ -300,7 +306,11 @@ __global__ void __launch_bounds__(kThreads) series_term_kernel(SeriesTermArgs a)
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      series_control(ctl, a.count, a.tol);
+      if (a.decide) {
+        series_control(ctl, a.count, a.tol);
+      } else {
+        ctl->arrivals = 0;
+      }
     }
   }
 }
@@ -379,7 +389,11 @@ __global__ void __launch_bounds__(kThreads) series_axpy_kernel(SeriesTermArgs a)
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      series_control(ctl, a.count, a.tol);
+      if (a.decide) {
+        series_control(ctl, a.count, a.tol);
+      } else {
+        ctl->arrivals = 0;
+      }
     }
   }
 }
@@ -464,6 +478,7 @@ struct SellStepArgs {
   StepCtl* ctl;
   int first_of_stage;
   int stage;
+  int decide;
 };
 
 template <bool kStrict>
@@ -492,7 +507,11 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      step_control(ctl, a.first_of_stage, a.stage, a.tol);
+      if (a.decide) {
+        step_control(ctl, a.first_of_stage, a.stage, a.tol);
+      } else {
+        ctl->arrivals = 0;  // maxima stay for the allreduce + step_control_kernel
+      }
     }
   }
 }
@@ -555,7 +574,11 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
-      series_control(ctl, a.count, a.tol);
+      if (a.decide) {
+        series_control(ctl, a.count, a.tol);
+      } else {
+        ctl->arrivals = 0;
+      }
     }
   }
 }
@@ -581,32 +604,62 @@ __device__ __forceinline__ void norm_body(const double2* __restrict__ v, long lo
   }
 }
 
-__global__ void __launch_bounds__(kThreads) step_init_kernel(const double2* v, long long n, StepCtl* ctl) {
-  norm_body(v, n, &ctl->term_bits, &ctl->arrivals, [ctl](double nv) {
-    ctl->c1 = nv;  // expm.cpp:165-170
-    ctl->last_nf = nv;
-    ctl->done = 0;  // `error` and `spmvs` are sticky across calls
-    ctl->sum_bits = 0;
-    ctl->term_bits = 0;
-    ctl->arrivals = 0;
+__device__ void step_init_apply(StepCtl* ctl, double nv) {
+  ctl->c1 = nv;  // expm.cpp:165-170
+  ctl->last_nf = nv;
+  ctl->done = 0;  // `error` and `spmvs` are sticky across calls
+  ctl->sum_bits = 0;
+  ctl->term_bits = 0;
+  ctl->arrivals = 0;
+}
+
+__device__ void series_init_apply(SeriesCtl* ctl, int count, double nz) {
+  ctl->z_norm = nz;  // expm.cpp:271-276
+  ctl->count = count;
+  ctl->n_active = ctl->error ? 0 : count;  // `error` and `spmvs` are sticky
+  for (int k = 0; k < count; ++k) {
+    ctl->active[k] = 1;
+    ctl->factor[k] = static_cast<double>(k + 1);  // factor *= k at p = 1
+    ctl->c1[k] = nz;
+    ctl->sum_bits[k] = 0;
+  }
+  ctl->term_bits = 0;
+  ctl->arrivals = 0;
+}
+
+__global__ void __launch_bounds__(kThreads) step_init_kernel(const double2* v, long long n, StepCtl* ctl, int decide) {
+  norm_body(v, n, &ctl->term_bits, &ctl->arrivals, [ctl, decide](double nv) {
+    if (decide) {
+      step_init_apply(ctl, nv);
+    } else {
+      ctl->arrivals = 0;
+    }
   });
 }
 
 __global__ void __launch_bounds__(kThreads) series_init_kernel(const double2* z, long long n, int count,
-                                                              SeriesCtl* ctl) {
-  norm_body(z, n, &ctl->term_bits, &ctl->arrivals, [ctl, count](double nz) {
-    ctl->z_norm = nz;  // expm.cpp:271-276
-    ctl->count = count;
-    ctl->n_active = ctl->error ? 0 : count;  // `error` and `spmvs` are sticky
-    for (int k = 0; k < count; ++k) {
-      ctl->active[k] = 1;
-      ctl->factor[k] = static_cast<double>(k + 1);  // factor *= k at p = 1
-      ctl->c1[k] = nz;
-      ctl->sum_bits[k] = 0;
+                                                              SeriesCtl* ctl, int decide) {
+  norm_body(z, n, &ctl->term_bits, &ctl->arrivals, [ctl, count, decide](double nz) {
+    if (decide) {
+      series_init_apply(ctl, count, nz);
+    } else {
+      ctl->arrivals = 0;
     }
-    ctl->term_bits = 0;
-    ctl->arrivals = 0;
   });
+}
+
+// Control steps after a cross-GPU allreduce(max) of the maxima (one thread).
+__global__ void step_init_fin_kernel(StepCtl* ctl) {
+  step_init_apply(ctl, bitsd(ctl->term_bits));
+}
+__global__ void series_init_fin_kernel(SeriesCtl* ctl, int count) {
+  series_init_apply(ctl, count, bitsd(ctl->term_bits));
+}
+__global__ void step_control_kernel(StepCtl* ctl, int first_of_stage, int stage, double tol) {
+  step_control(ctl, first_of_stage, stage, tol);
+}
+__global__ void series_control_kernel(SeriesCtl* ctl, int count, double tol) {
+  series_control(ctl, count, tol);
 }
 
 // --------------------------------------------------------------- plain SpMV
@@ -712,37 +765,57 @@ int series_mode() {
 
 int valid_group(int g) { return (g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32) ? g : 0; }
 
-void step_init(const double2* v, std::int64_t n, StepCtl* ctl, cudaStream_t s) {
-  step_init_kernel<<<small_grid(n), kThreads, 0, s>>>(v, n, ctl);
+void step_init(const double2* v, std::int64_t n, StepCtl* ctl, bool decide, cudaStream_t s) {
+  step_init_kernel<<<small_grid(n), kThreads, 0, s>>>(v, n, ctl, decide ? 1 : 0);
   QSWG_LAUNCH_CHECK("step_init");
 }
 
+void step_init_fin(StepCtl* ctl, cudaStream_t s) {
+  step_init_fin_kernel<<<1, 1, 0, s>>>(ctl);
+  QSWG_LAUNCH_CHECK("step_init_fin");
+}
+
+void step_control(StepCtl* ctl, bool first_of_stage, int stage, double tol, cudaStream_t s) {
+  step_control_kernel<<<1, 1, 0, s>>>(ctl, first_of_stage ? 1 : 0, stage, tol);
+  QSWG_LAUNCH_CHECK("step_control");
+}
+
+void series_init_fin(SeriesCtl* ctl, int count, cudaStream_t s) {
+  series_init_fin_kernel<<<1, 1, 0, s>>>(ctl, count);
+  QSWG_LAUNCH_CHECK("series_init_fin");
+}
+
+void series_control(SeriesCtl* ctl, int count, double tol, cudaStream_t s) {
+  series_control_kernel<<<1, 1, 0, s>>>(ctl, count, tol);
+  QSWG_LAUNCH_CHECK("series_control");
+}
+
 void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,
-               double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, cudaStream_t s) {
+               double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, bool decide, cudaStream_t s) {
   if (m.format == Format::Sell) {
-    SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage};
+    SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
       sell_step_term_kernel<true><<<sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s>>>(a);
     } else {
       sell_step_term_kernel<false><<<sell_grid(sell_step_term_kernel<false>, m.sell), kThreads, 0, s>>>(a);
     }
   } else {
-    StepTermArgs a{m.csr, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage};
+    StepTermArgs a{m.csr, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     dispatch_group<StepTermK>(m.group, m.csr.rows, s, a);
   }
   QSWG_LAUNCH_CHECK("step_term");
 }
 
-void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, cudaStream_t s) {
+void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, bool decide, cudaStream_t s) {
   if (count < 1 || count > kMaxSeriesD) throw std::invalid_argument("series super-step size out of range");
-  series_init_kernel<<<small_grid(n), kThreads, 0, s>>>(z, n, count, ctl);
+  series_init_kernel<<<small_grid(n), kThreads, 0, s>>>(z, n, count, ctl, decide ? 1 : 0);
   QSWG_LAUNCH_CHECK("series_init");
 }
 
 void series_term(const DevMatrix& m, const double2* x, double2* kp, const double2* z,
                  const SeriesSums& sums, int count, int p, double scale, double tol,
-                 SeriesCtl* ctl, cudaStream_t s) {
-  SeriesTermArgs a{m.csr, x, kp, z, sums, count, p, scale, tol, ctl};
+                 SeriesCtl* ctl, bool decide, cudaStream_t s) {
+  SeriesTermArgs a{m.csr, x, kp, z, sums, count, p, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_series_term_kernel<true><<<sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s>>>(a, m.sell);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 namespace qswg {
@@ -34,4 +35,13 @@ class Comm {
   virtual void allreduce_sum_f64(double* buf, std::size_t n, cudaStream_t s) = 0;
 };
 
+/// `world` linked in-process communicators (comm_local.cpp): the multi-GPU
+/// control flow driven by `world` host threads, e.g. on one GPU in tests.
+std::vector<std::unique_ptr<Comm>> make_local_comms(int world);
+
 }  // namespace qswg
+
+/// C-ABI handle (include/qswg.h).
+struct qswg_comm {
+  std::unique_ptr<qswg::Comm> c;
+};

@@ -135,10 +135,6 @@ class NcclComm final : public Comm {
 
 }  // namespace qswg
 
-struct qswg_comm {
-  std::unique_ptr<qswg::NcclComm> c;
-};
-
 namespace qswg {
 
 Comm* comm_from_handle(qswg_comm* c) { return c ? c->c.get() : nullptr; }

@@ -1,7 +1,13 @@
 // Host control flow of the exponential action.  Mirrors expm.cpp:146-325
 // step for step; every Taylor term is one fused kernel launch and every stop
-// test is evaluated on the device (see cuda/taylor.cu), so a whole step or
-// series is enqueued without host round-trips and synchronised once.
+// test is evaluated on the device (see cuda/taylor.cu).
+//
+// One GPU: a whole step or series is enqueued without host round-trips and
+// synchronised once — the last block of each term kernel decides.
+// Several GPUs (one process each): each term kernel leaves its local maxima,
+// an allreduce(max) over NCCL combines them, a one-thread control kernel runs
+// the same decision, and the host reads the stop flag before exchanging the
+// new term's halo (so terms after the stop are neither computed nor sent).
 #include "expm.hpp"
 
 #include <algorithm>
@@ -17,7 +23,7 @@ namespace qswg {
 namespace {
 
 // Workspace slots.
-enum Slot : std::size_t { kT0 = 0, kT1 = 1, kSOther = 2, kNext = 3, kZ = 4, kSums = 8 };
+enum Slot : std::size_t { kT0 = 0, kT1 = 1, kSOther = 2, kNext = 3, kZ = 4, kXStage = 5, kZFull = 6, kSums = 8 };
 
 dev::StepCtl* step_ctl(const Liouvillian& l) {
   Workspace& ws = l.workspace();
@@ -54,40 +60,94 @@ void reset_ctls(const Liouvillian& l, bool with_series) {
   if (with_series) QSWG_CHECK(cudaMemsetAsync(series_ctl(l), 0, sizeof(dev::SeriesCtl), l.stream()));
 }
 
-// Enqueues one step (expm.cpp:146-212) without synchronising.  `out` receives
-// the result; scratch vectors come from the workspace.
-StepParameters enqueue_step(const Liouvillian& l, const double2* v, double t,
-                            const TaylorParameters& params, double2* out, std::int64_t& launches) {
-  const std::int64_t len = l.dim();
-  cudaStream_t s = l.stream();
+// Execution context: one GPU, or one rank of a row-partitioned run.
+struct Exec {
+  const Liouvillian& l;
+  Comm* comm;
+  cudaStream_t s;
+  bool single;
+  std::int64_t row0, rows, dim;
+
+  explicit Exec(const Liouvillian& lv)
+      : l(lv), comm(lv.comm()), s(lv.stream()), single(!lv.comm() || lv.comm()->world() == 1),
+        row0(lv.block().row0), rows(lv.block().rows), dim(lv.dim()) {}
+
+  // Full-length (dim) vectors are SpMV inputs; local (rows) vectors are states.
+  double2* full(std::size_t slot) const { return l.workspace().get(slot, static_cast<std::size_t>(dim)); }
+  double2* local(std::size_t slot) const {
+    return l.workspace().get(slot, static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)));
+  }
+
+  // Receive every peer segment this block's columns reference.
+  void exchange(double2* full_vec) const {
+    if (!single) comm->exchange_ranges(full_vec, l.halo_lo(), l.halo_hi(), sizeof(double2), s);
+  }
+
+  // SpMV input from a local state: on one GPU the state itself; otherwise
+  // its rows copied into a full-length buffer whose halo is then exchanged.
+  const double2* spmv_input(const double2* local_vec, std::size_t slot) const {
+    if (single) return local_vec;
+    double2* f = full(slot);
+    QSWG_CHECK(cudaMemcpyAsync(f + row0, local_vec, static_cast<std::size_t>(rows) * sizeof(double2),
+                               cudaMemcpyDeviceToDevice, s));
+    exchange(f);
+    return f;
+  }
+
+  template <class T>
+  T read(const T* dev_ptr) const {
+    T v{};
+    QSWG_CHECK(cudaMemcpyAsync(&v, dev_ptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+    return v;
+  }
+};
+
+// Enqueues one step (expm.cpp:146-212).  `out` (local) receives the result;
+// scratch vectors come from the workspace.
+StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const TaylorParameters& params,
+                            double2* out, std::int64_t& launches) {
+  const Liouvillian& l = ex.l;
+  cudaStream_t s = ex.s;
   const StepParameters sp = select_parameters(l.one_norms().data(), t, params);
   if (sp.m_star == 0) {  // expm.cpp:152
-    QSWG_CHECK(cudaMemcpyAsync(out, v, static_cast<std::size_t>(l.block().rows) * sizeof(double2),
+    QSWG_CHECK(cudaMemcpyAsync(out, v, static_cast<std::size_t>(ex.rows) * sizeof(double2),
                                cudaMemcpyDeviceToDevice, s));
     return sp;
   }
-  Workspace& ws = l.workspace();
-  double2* term[2] = {ws.get(kT0, static_cast<std::size_t>(len)), ws.get(kT1, static_cast<std::size_t>(len))};
+  double2* term[2] = {ex.full(kT0), ex.full(kT1)};
   double2* sums[2];
   // stage st accumulates into sums[st % 2]; the last stage lands in `out`.
   sums[(sp.s - 1) % 2] = out;
-  sums[sp.s % 2] = ws.get(kSOther, static_cast<std::size_t>(len));
+  sums[sp.s % 2] = ex.local(kSOther);
   dev::StepCtl* ctl = step_ctl(l);
   const dev::DevMatrix mat = l.matrix();
-  dev::step_init(v, l.block().rows, ctl, s);  // c1 = ||v||_inf (expm.cpp:165-170)
+  dev::step_init(v, ex.rows, ctl, ex.single, s);  // c1 = ||v||_inf (expm.cpp:165-170)
+  if (!ex.single) {
+    ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
+    dev::step_init_fin(ctl, s);
+  }
   launches += 1 + sp.s * sp.m_star;
   const double s_count = static_cast<double>(sp.s);
   for (std::int64_t st = 0; st < sp.s; ++st) {
     // stage input: v, then the previous stage's sum (term = sum, expm.cpp:197-205)
     const double2* x_stage = st == 0 ? v : sums[(st - 1) % 2];
+    const double2* x_stage_full = ex.spmv_input(x_stage, kXStage);
     double2* acc = sums[st % 2];
     for (std::int64_t j = 1; j <= sp.m_star; ++j) {
-      const double2* x = j == 1 ? x_stage : term[(j - 1) % 2];
-      double2* y = term[j % 2];
+      const double2* x = j == 1 ? x_stage_full : term[(j - 1) % 2];
+      double2* y = term[j % 2] + ex.row0;
       const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
-      dev::step_term(mat, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1,
-                     static_cast<int>(st), params.tolerance, ctl, s);
+      dev::step_term(mat, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1, static_cast<int>(st),
+                     params.tolerance, ctl, ex.single, s);
+      if (!ex.single) {
+        ex.comm->allreduce_max_u64(&ctl->term_bits, 2, s);  // term_bits, sum_bits
+        dev::step_control(ctl, j == 1, static_cast<int>(st), params.tolerance, s);
+        if (ex.read(&ctl->done) || ex.read(&ctl->error)) break;  // expm.cpp:191-194
+        if (j < sp.m_star) ex.exchange(term[j % 2]);
+      }
     }
+    if (!ex.single && ex.read(&ctl->error)) break;
   }
   return sp;
 }
@@ -96,11 +156,11 @@ StepParameters enqueue_step(const Liouvillian& l, const double2* v, double t,
 
 StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorParameters& params,
               double2* out) {
-  if (l.comm() && l.comm()->world() > 1) throw std::logic_error("multi-GPU step goes through step_dist");
   DeviceGuard g(l.device());
+  const Exec ex(l);
   reset_ctls(l, false);
   std::int64_t launches = 0;
-  const StepParameters sp = enqueue_step(l, v, t, params, out, launches);
+  const StepParameters sp = enqueue_step(ex, v, t, params, out, launches);
   const Flags f = read_flags(l, false);
   if (f.error) throw NumericalError("non-finite values encountered in exponential action");
   return {sp.m_star, sp.s, f.spmvs, launches};
@@ -112,19 +172,17 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
   // expm.cpp:216-217
   if (!(tq > t1)) throw std::invalid_argument("series requires tq > t1");
   if (steps < 1) throw std::invalid_argument("series requires at least one step");
-  if (l.comm() && l.comm()->world() > 1) throw std::logic_error("multi-GPU series goes through series_dist");
   DeviceGuard g(l.device());
-  cudaStream_t s = l.stream();
-  const std::int64_t len = l.dim();
+  const Exec ex(l);
+  cudaStream_t s = ex.s;
   const std::int64_t q = steps;
   const double h = (tq - t1) / static_cast<double>(q);
-  Workspace& ws = l.workspace();
   reset_ctls(l, true);
   SeriesInfo info;
 
   // states[0] = step(v, t1) (expm.cpp:225)
-  double2* z = ws.get(kZ, static_cast<std::size_t>(len));
-  enqueue_step(l, v, t1, params, z, info.launches);
+  double2* z = ex.local(kZ);
+  enqueue_step(ex, v, t1, params, z, info.launches);
   emit(0, z);
 
   const StepParameters span = select_parameters(l.one_norms().data(), tq - t1, params);
@@ -136,9 +194,9 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
   } else if (q <= span.s) {  // q sequential steps (expm.cpp:234-240)
     info.path = 1;
     double2* cur = z;
-    double2* nxt = ws.get(kNext, static_cast<std::size_t>(len));
+    double2* nxt = ex.local(kNext);
     for (std::int64_t k = 1; k <= q; ++k) {
-      enqueue_step(l, cur, h, params, nxt, info.launches);
+      enqueue_step(ex, cur, h, params, nxt, info.launches);
       emit(k, nxt);
       std::swap(cur, nxt);
     }
@@ -157,27 +215,39 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
     info.sub_m_star = m_star;
     if (d > dev::kMaxSeriesD) throw std::logic_error("super-step size exceeds the device limit");
 
-    double2* kbuf[2] = {ws.get(kT0, static_cast<std::size_t>(len)), ws.get(kT1, static_cast<std::size_t>(len))};
+    double2* kbuf[2] = {ex.full(kT0), ex.full(kT1)};
     std::vector<double2*> sums(static_cast<std::size_t>(d));
-    for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ws.get(kSums + static_cast<std::size_t>(k), static_cast<std::size_t>(len));
+    for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ex.local(kSums + static_cast<std::size_t>(k));
     dev::SeriesCtl* ctl = series_ctl(l);
     const dev::DevMatrix mat = l.matrix();
     for (std::int64_t super = 0; super <= n_super; ++super) {
       const std::int64_t count = super < n_super ? d : remainder;
       if (count == 0) break;
-      dev::series_init(z, l.block().rows, static_cast<int>(count), ctl, s);
+      dev::series_init(z, ex.rows, static_cast<int>(count), ctl, ex.single, s);
+      if (!ex.single) {
+        ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
+        dev::series_init_fin(ctl, static_cast<int>(count), s);
+      }
       info.launches += 1 + m_star;
       dev::SeriesSums ss{};
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
+      const double2* z_full = ex.spmv_input(z, kZFull);
       for (std::int64_t p = 1; p <= m_star; ++p) {
-        const double2* x = p == 1 ? z : kbuf[(p - 1) % 2];
-        double2* kp = kbuf[p % 2];
+        const double2* x = p == 1 ? z_full : kbuf[(p - 1) % 2];
+        double2* kp = kbuf[p % 2] + ex.row0;
         dev::series_term(mat, x, kp, z, ss, static_cast<int>(count), static_cast<int>(p),
-                         h / static_cast<double>(p), params.tolerance, ctl, s);
+                         h / static_cast<double>(p), params.tolerance, ctl, ex.single, s);
+        if (!ex.single) {
+          ex.comm->allreduce_max_u64(&ctl->term_bits, 1 + static_cast<std::size_t>(count), s);
+          dev::series_control(ctl, static_cast<int>(count), params.tolerance, s);
+          if (ex.read(&ctl->n_active) == 0) break;
+          if (p < m_star) ex.exchange(kbuf[p % 2]);
+        }
       }
       for (std::int64_t k = 1; k <= count; ++k) emit(super * d + k, sums[static_cast<std::size_t>(k - 1)]);
       // the next super-step starts from states[(super + 1) d] = the last output
       std::swap(z, sums[static_cast<std::size_t>(count - 1)]);
+      if (!ex.single && ex.read(&ctl->error)) break;
     }
   }
   const Flags f = read_flags(l, info.path == 2);
@@ -190,25 +260,25 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   if (count < 1 || count > dev::kMaxSeriesD) throw std::invalid_argument("count out of range");
   if (iters < 1) throw std::invalid_argument("iters must be >= 1");
   DeviceGuard g(l.device());
-  cudaStream_t s = l.stream();
-  const std::size_t len = static_cast<std::size_t>(l.dim());
-  Workspace& ws = l.workspace();
-  double2* k[2] = {ws.get(kT0, len), ws.get(kT1, len)};
-  double2* z = ws.get(kZ, len);
+  const Exec ex(l);
+  cudaStream_t s = ex.s;
+  double2* k[2] = {ex.full(kT0), ex.full(kT1)};
+  double2* z = ex.local(kZ);
   dev::SeriesSums ss{};
-  for (int c = 0; c < count; ++c) ss.s[c] = ws.get(kSums + static_cast<std::size_t>(c), len);
-  dev::fill_pattern(k[0], l.dim(), s);
-  dev::fill_pattern(z, l.dim(), s);
-  for (int c = 0; c < count; ++c) dev::fill_pattern(ss.s[c], l.dim(), s);
+  for (int c = 0; c < count; ++c) ss.s[c] = ex.local(kSums + static_cast<std::size_t>(c));
+  dev::fill_pattern(k[0], ex.dim, s);
+  dev::fill_pattern(z, ex.rows, s);
+  for (int c = 0; c < count; ++c) dev::fill_pattern(ss.s[c], ex.rows, s);
   dev::SeriesCtl* ctl = series_ctl(l);
   QSWG_CHECK(cudaMemsetAsync(ctl, 0, sizeof(dev::SeriesCtl), s));
-  dev::series_init(z, l.block().rows, count, ctl, s);
+  dev::series_init(z, ex.rows, count, ctl, true, s);
   // tol = -1 keeps every output active (c1 + c2 <= -nf never holds); scale
-  // 1/||L||_1 keeps the iterates bounded.
+  // 1/||L||_1 keeps the iterates bounded.  Local kernel time only (no
+  // exchange), as the per-GPU roofline needs.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
   auto launch = [&](int i) {
-    dev::series_term(l.matrix(), k[i % 2], k[(i + 1) % 2], z, ss, count, 2 + (i % 2), scale, -1.0,
-                     ctl, s);
+    dev::series_term(l.matrix(), k[i % 2], k[(i + 1) % 2] + ex.row0, z, ss, count, 2 + (i % 2), scale, -1.0,
+                     ctl, true, s);
   };
   launch(0);  // warm-up
   cudaEvent_t e0, e1;

@@ -14,6 +14,7 @@
 #include <string>
 
 #include "comm.hpp"
+#include "dist.hpp"
 
 namespace qswg {
 
@@ -303,25 +304,6 @@ std::vector<std::int64_t> count_scan(const dev::KronOperands& ops, std::int64_t 
   return colptr;
 }
 
-// Contiguous row blocks on rho-column boundaries (multiples of n rows),
-// balanced by nnz: block w ends at the column boundary nearest to w/world of
-// the total nnz.
-std::vector<std::int64_t> partition_rows(const std::vector<std::int64_t>& colptr, std::int64_t n, int world) {
-  std::vector<std::int64_t> starts(static_cast<std::size_t>(world) + 1, 0);
-  starts[static_cast<std::size_t>(world)] = n * n;
-  const std::int64_t total = colptr.back();
-  std::int64_t j = 0;
-  for (int w = 1; w < world; ++w) {
-    const long double target = static_cast<long double>(total) * w / world;
-    while (j < n && static_cast<long double>(colptr[static_cast<std::size_t>(j)]) +
-                            (colptr[static_cast<std::size_t>(j) + 1] - colptr[static_cast<std::size_t>(j)]) / 2.0L <
-                        target)
-      ++j;
-    starts[static_cast<std::size_t>(w)] = std::max(j * n, starts[static_cast<std::size_t>(w) - 1]);
-  }
-  return starts;
-}
-
 template <class V>
 void fill_block(const dev::KronOperands& ops, const DeviceBuffer<std::int64_t>& grp,
                 const std::vector<std::int64_t>& colptr, std::int64_t n, const RowBlock& blk,
@@ -454,6 +436,39 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     fill_block(ops.get(), grp, colptr, n, l->block_, l->rowptr_, l->col_, l->val_, l->nnz_local_, s);
   }
   grp.reset();
+
+  // ---- halo plan: hull of every peer's columns this block references ----
+  l->halo_lo_.assign(static_cast<std::size_t>(world), std::vector<std::int64_t>(static_cast<std::size_t>(world), 0));
+  l->halo_hi_ = l->halo_lo_;
+  if (world > 1) {
+    const std::int64_t stored = l->format_ == dev::Format::Sell ? sell_entries : l->nnz_local_;
+    DeviceBuffer<std::int64_t> dstarts(static_cast<std::size_t>(world) + 1);
+    DeviceBuffer<std::int64_t> table(static_cast<std::size_t>(2 * world * world));  // [rank][lo.., hi..]
+    QSWG_CHECK(cudaMemcpyAsync(dstarts.get(), l->starts_.data(), dstarts.bytes(), cudaMemcpyHostToDevice, s));
+    std::vector<std::int64_t> init(static_cast<std::size_t>(2 * world));
+    for (int q = 0; q < world; ++q) {
+      init[static_cast<std::size_t>(q)] = INT64_MAX;
+      init[static_cast<std::size_t>(world + q)] = INT64_MIN;
+    }
+    std::int64_t* mine = table.get() + 2 * world * rank;
+    QSWG_CHECK(cudaMemcpyAsync(mine, init.data(), init.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice, s));
+    dev::halo_hulls(l->col_.get(), stored, dstarts.get(), world, rank, mine, mine + world, s);
+    std::vector<std::int64_t> tstarts(static_cast<std::size_t>(world) + 1);
+    for (int w = 0; w <= world; ++w) tstarts[static_cast<std::size_t>(w)] = 2 * world * w;
+    cfg.comm->allgather_rows(table.get(), tstarts, sizeof(std::int64_t), s);
+    std::vector<std::int64_t> h(table.size());
+    QSWG_CHECK(cudaMemcpyAsync(h.data(), table.get(), table.bytes(), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+    for (int r = 0; r < world; ++r)
+      for (int q = 0; q < world; ++q) {
+        const std::int64_t lo = h[static_cast<std::size_t>(2 * world * r + q)];
+        const std::int64_t hi = h[static_cast<std::size_t>(2 * world * r + world + q)];
+        if (lo < hi) {
+          l->halo_lo_[static_cast<std::size_t>(r)][static_cast<std::size_t>(q)] = lo;
+          l->halo_hi_[static_cast<std::size_t>(r)][static_cast<std::size_t>(q)] = hi;
+        }
+      }
+  }
 
   // ---- SpMV lanes per row ----
   const double mean_row = l->block_.rows ? static_cast<double>(l->nnz_local_) / l->block_.rows : 1.0;

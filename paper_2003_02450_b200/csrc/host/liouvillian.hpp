@@ -83,6 +83,10 @@ class Liouvillian {
   /// Mean device time (ms) of one term kernel launch over `iters` launches.
   double time_spmv(int iters, int group) const;
   Workspace& workspace() const { return ws_; }
+  /// halo_lo()[r][q], halo_hi()[r][q]: global rows of rank q's segment that
+  /// rank r gathers before every SpMV (empty when lo == hi).
+  const std::vector<std::vector<std::int64_t>>& halo_lo() const { return halo_lo_; }
+  const std::vector<std::vector<std::int64_t>>& halo_hi() const { return halo_hi_; }
 
  private:
   Liouvillian() = default;
@@ -105,6 +109,7 @@ class Liouvillian {
   DeviceBuffer<std::int64_t> rowptr_;     // CSR
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;
+  std::vector<std::vector<std::int64_t>> halo_lo_, halo_hi_;
   mutable Workspace ws_;
 };
 

@@ -108,6 +108,12 @@ void assemble_fill_sell(const KronOperands& o, std::int64_t row0, std::int64_t r
 void assemble_fill_abs(const KronOperands& o, std::int64_t row0, std::int64_t rows,
                        const std::int64_t* rowptr, int* col, double* val, cudaStream_t s);
 
+// Halo hulls: for every peer q != rank, lo[q] / hi[q] = min / max+1 of the
+// columns in col[0..n) owned by q (starts: world + 1 global row starts, on
+// the device).  lo must be preset to INT64_MAX and hi to INT64_MIN.
+void halo_hulls(const int* col, std::int64_t n, const std::int64_t* starts, int world, int rank,
+                std::int64_t* lo, std::int64_t* hi, cudaStream_t s);
+
 // ---- norms (cuda/norms.cu) ---------------------------------------------------
 // Exact ||L^p||_1 (p = 1..9) through dense powers of L applied to the
 // identity; dim <= 4096.  work: 2 * dim * dim double2 + dim doubles.
@@ -132,7 +138,8 @@ struct StepCtl {
 };
 
 struct SeriesCtl {
-  unsigned long long term_bits;
+  unsigned long long term_bits;               // adjacent to sum_bits: one
+  unsigned long long sum_bits[kMaxSeriesD];   // allreduce covers both
   unsigned int arrivals;
   int n_active;
   int error;
@@ -140,7 +147,6 @@ struct SeriesCtl {
   int count;
   int pad_;
   double z_norm;
-  unsigned long long sum_bits[kMaxSeriesD];
   double factor[kMaxSeriesD];
   double c1[kMaxSeriesD];
   int active[kMaxSeriesD];
@@ -154,23 +160,32 @@ struct SeriesSums {
 // the bitwise reference-order mode (sequential rows, no FMA).
 int valid_group(int g);
 
-// ctl <- zero; ctl->c1 = ||v||_inf over n local elements.
-void step_init(const double2* v, std::int64_t n, StepCtl* ctl, cudaStream_t s);
+// Every reduction kernel below takes `decide`: true on one GPU (the last
+// block to arrive runs the control step); false under multi-GPU, where the
+// kernel leaves its local maxima in the control block for an allreduce(max)
+// and the matching *_control / *_fin kernel then runs the same control step.
+
+// ctl->c1 = ||v||_inf over n local elements (`error`/`spmvs` are sticky).
+void step_init(const double2* v, std::int64_t n, StepCtl* ctl, bool decide, cudaStream_t s);
+void step_init_fin(StepCtl* ctl, cudaStream_t s);
+void step_control(StepCtl* ctl, bool first_of_stage, int stage, double tol, cudaStream_t s);
+void series_init_fin(SeriesCtl* ctl, int count, cudaStream_t s);
+void series_control(SeriesCtl* ctl, int count, double tol, cudaStream_t s);
 // One Taylor term of `step` (expm.cpp:175-195):
 //   y = scale * (L x);  sum_out = sum_in + y;  c2 = ||y||, nf = ||sum_out||;
 //   stop test c1 + c2 <= tol * nf decided on the device.  Skips itself when
 //   the stage is already done (unless first_of_stage) or on error.
 void step_term(const DevMatrix& l, const double2* x, double2* y, const double2* sum_in,
                double2* sum_out, double scale, bool first_of_stage, int stage, double tol,
-               StepCtl* ctl, cudaStream_t s);
+               StepCtl* ctl, bool decide, cudaStream_t s);
 // Super-step start of `series` (expm.cpp:267-276): z_norm = ||Z||, count
 // outputs active, factor_k = k, c1_k = z_norm.
-void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, cudaStream_t s);
+void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, bool decide, cudaStream_t s);
 // K_p = scale * (L K_{p-1}); for every active k: S_k = (p == 1 ? Z : S_k) + k^p K_p
 // with per-k stop tests (expm.cpp:278-316, evaluated p-major).
 void series_term(const DevMatrix& l, const double2* x, double2* kp, const double2* z,
                  const SeriesSums& sums, int count, int p, double scale, double tol,
-                 SeriesCtl* ctl, cudaStream_t s);
+                 SeriesCtl* ctl, bool decide, cudaStream_t s);
 // y = scale * (L x) (liouvillian.cpp:346-360).
 void spmv(const DevMatrix& l, const double2* x, double2* y, double scale, cudaStream_t s);
 // pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).

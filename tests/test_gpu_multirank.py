@@ -1,0 +1,81 @@
+"""The multi-GPU code path (row-sharded superoperator, per-term halo
+exchange, allreduce(max) stop tests, allreduce(sum) populations) run as
+`world` ranks on ONE GPU through the in-process communicator
+(qswg_comm_create_local: host-side rendezvous collectives, no kernel waits on
+another rank).  Results must equal the single-rank run and the reference."""
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import Case
+
+pytestmark = pytest.mark.gpu
+api = pytest.importorskip("paper_2003_02450_b200.api")
+
+
+def run_ranks(world, fn):
+    comms = api.Comm.local_group(world)
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            out[r] = fn(r, comms[r])
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["c2_n36", "c5_n64", "c3_n40", "c4_n40", "lqsw_src_snk", "gqsw_multi_rot"])
+def test_sharded_series_matches_single_and_reference(name, world):
+    c = Case(name)
+    t1, tq, q = c.series
+
+    def rank_fn(r, comm):
+        l = c.build_gpu(api, comm=comm)
+        v = l.state().from_probabilities(c.rho0)
+        res = api.series(l, v, t1, tq, int(q), states=True)
+        st, lo, hi = l.partition()
+        return l.row0, res.states, res.populations, int(res.info.spmvs), st, l.one_norms()
+
+    parts = run_ranks(world, rank_fn)
+    starts = parts[0][4]
+    assert starts[0] == 0 and starts[-1] == c.dim and np.all(starts % c.n == 0)
+    states = np.concatenate([p[1] for p in sorted(parts, key=lambda p: p[0])], axis=1)
+    for p in parts:
+        np.testing.assert_allclose(p[5], c.norms, rtol=1e-13)  # distributed norm bound
+        assert np.array_equal(p[2], parts[0][2])                # allreduced populations agree
+    keep = c.z["series_keep"]
+    assert np.abs(states[keep] - c.z["series_states"]).max() <= 1e-10
+    assert np.abs(parts[0][2] - c.z["series_pops"]).max() <= 1e-10
+    if name.startswith("c"):
+        assert parts[0][3] == c.series_spmvs
+    # same kernels, same per-row arithmetic: the sharded run is bitwise the single-rank run
+    l1 = c.build_gpu(api)
+    single = api.series(l1, l1.state().from_probabilities(c.rho0), t1, tq, int(q), states=True)
+    assert np.array_equal(states, single.states)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_step_and_overflow(world):
+    c = Case("c1_n64")
+
+    def rank_fn(r, comm):
+        l = c.build_gpu(api, comm=comm)
+        v = l.state().from_probabilities(c.rho0)
+        w, info = api.step(l, v, float(c.z["step_t"][0]))
+        return l.row0, w.gather(), info.spmvs
+
+    parts = sorted(run_ranks(world, rank_fn), key=lambda p: p[0])
+    got = np.concatenate([p[1] for p in parts])
+    assert np.abs(got - c.z["step_states"][0]).max() <= 1e-10
+    assert parts[0][2] == c.z["step_spmvs"][0]
