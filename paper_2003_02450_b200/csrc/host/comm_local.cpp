@@ -103,6 +103,9 @@ class LocalComm final : public Comm {
     const unsigned long long gen = g_->generation;
     if (++g_->arrived == g_->world) {
       fn(g_->slot);
+      // device-to-device cudaMemcpy may return before the copy completes and
+      // the ranks' non-blocking streams do not order against it: drain it
+      QSWG_CHECK(cudaDeviceSynchronize());
       g_->arrived = 0;
       ++g_->generation;
       g_->cv.notify_all();
