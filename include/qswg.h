@@ -49,13 +49,14 @@ typedef struct qswg_comm qswg_comm;               /* multi-GPU communicator     
 typedef struct { int64_t target; double rate; } qswg_source_arc; /* graph.hpp:17-20 SourceArc */
 typedef struct { int64_t origin; double rate; } qswg_sink_arc;   /* graph.hpp:23-26 SinkArc   */
 
-enum { QSWG_FORMAT_AUTO = 0, QSWG_FORMAT_CSR = 1, QSWG_FORMAT_SELL = 2 };
+enum { QSWG_FORMAT_AUTO = 0, QSWG_FORMAT_CSR = 1, QSWG_FORMAT_SELL = 2, QSWG_FORMAT_KRON = 3 };
 
 typedef struct {
   int device;       /* CUDA ordinal */
   int group;        /* CSR lanes per row (2..32); 1 = bitwise reference order; 0 = autotune */
   int format;       /* QSWG_FORMAT_*: device storage of the superoperator (AUTO: SELL-32
-                       when its padding is <= 3%, else CSR) */
+                       when its padding is <= 3%, else CSR; KRON: matrix-free action on
+                       the n x n operators, no superoperator stored) */
   qswg_comm* comm;  /* NULL for one GPU */
 } qswg_device_config;
 
@@ -64,7 +65,7 @@ typedef struct {
   double omega;
   double one_norms[9]; /* DistributedLiouvillian::one_norms(), liouvillian.hpp:31 */
   int group, device, rank, world;
-  int format;     /* QSWG_FORMAT_CSR or QSWG_FORMAT_SELL */
+  int format;     /* QSWG_FORMAT_CSR, QSWG_FORMAT_SELL or QSWG_FORMAT_KRON */
   double padding; /* stored entries / nnz_local */
 } qswg_liouvillian_info;
 

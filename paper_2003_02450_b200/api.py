@@ -171,7 +171,7 @@ class Liouvillian:
     group = property(lambda self: self.info.group)
     row0 = property(lambda self: self.info.row0)
     rows = property(lambda self: self.info.rows)
-    format = property(lambda self: {1: "csr", 2: "sell"}[self.info.format])
+    format = property(lambda self: {1: "csr", 2: "sell", 3: "kron"}[self.info.format])
     padding = property(lambda self: self.info.padding)
 
     def one_norms(self) -> np.ndarray:
@@ -221,7 +221,7 @@ class Liouvillian:
         return StateVector(self)
 
 
-FORMATS = {"auto": 0, "csr": 1, "sell": 2}
+FORMATS = {"auto": 0, "csr": 1, "sell": 2, "kron": 3}
 
 
 def _config(device, group, comm, format="auto"):

@@ -83,7 +83,7 @@ qswg::DeviceConfig device_config(const qswg_device_config* cfg) {
   if (cfg) {
     c.device = cfg->device;
     c.group = cfg->group;
-    if (cfg->format < 0 || cfg->format > 2) throw std::invalid_argument("unknown storage format");
+    if (cfg->format < 0 || cfg->format > 3) throw std::invalid_argument("unknown storage format");
     c.format = cfg->format;
     c.comm = cfg->comm ? qswg::comm_from_handle(cfg->comm) : nullptr;
   } else {
@@ -281,7 +281,9 @@ int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* inf
     info->device = L.device();
     info->rank = L.comm() ? L.comm()->rank() : 0;
     info->world = L.comm() ? L.comm()->world() : 1;
-    info->format = L.format() == qswg::dev::Format::Sell ? QSWG_FORMAT_SELL : QSWG_FORMAT_CSR;
+    info->format = L.format() == qswg::dev::Format::Sell   ? QSWG_FORMAT_SELL
+                   : L.format() == qswg::dev::Format::Kron ? QSWG_FORMAT_KRON
+                                                           : QSWG_FORMAT_CSR;
     info->padding = L.padding();
   });
 }

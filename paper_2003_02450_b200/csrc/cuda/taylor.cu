@@ -583,6 +583,214 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
   }
 }
 
+// ------------------------------------------------------------ Kron path
+// Matrix-free action (kernels.hpp: KronView).  One thread per output row
+// r = n*j + i; consecutive threads share the rho column j, so the B (x) I
+// and P (x) Q parts stream coalesced columns of X and W_k, and the I (x) A
+// gathers stay inside column j (L1-resident).
+__device__ __forceinline__ void cfma(double2& acc, double2 v, double2 xv) {
+  acc.x = fma(v.x, xv.x, acc.x);
+  acc.x = fma(-v.y, xv.y, acc.x);
+  acc.y = fma(v.x, xv.y, acc.y);
+  acc.y = fma(v.y, xv.x, acc.y);
+}
+
+__device__ __forceinline__ double2 kron_row(const KronView& m, const double2* __restrict__ x, long long g,
+                                            unsigned long long xpol) {
+  const long long n = m.n;
+  const long long j = g / n, i = g - j * n;
+  double2 acc = make_double2(0.0, 0.0);
+  if (m.a.ptr) {  // I (x) A: column j of X
+    const int e1 = __ldg(m.a.ptr + i + 1);
+    const double2* xj = x + j * n;
+#pragma unroll 4
+    for (int e = __ldg(m.a.ptr + i); e < e1; ++e) cfma(acc, __ldg(m.a.val + e), ld_gather(xj + __ldg(m.a.col + e), xpol));
+  }
+  if (m.b.ptr) {  // B (x) I: coalesced columns c of X
+    const int e1 = __ldg(m.b.ptr + j + 1);
+    const double2* xi = x + i;
+#pragma unroll 4
+    for (int e = __ldg(m.b.ptr + j); e < e1; ++e)
+      cfma(acc, __ldg(m.b.val + e), ld_gather(xi + static_cast<long long>(__ldg(m.b.col + e)) * n, xpol));
+  }
+  for (int k = 0; k < m.nk; ++k) {  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
+    const KronList& p = m.p[k];
+    const int e1 = __ldg(p.ptr + j + 1);
+    const double2* wi = m.w[k] + i;
+#pragma unroll 4
+    for (int e = __ldg(p.ptr + j); e < e1; ++e)
+      cfma(acc, __ldg(p.val + e), ld_gather(wi + static_cast<long long>(__ldg(p.col + e)) * n, xpol));
+  }
+  if (m.t.ptr && i == j) {  // transfer onto the diagonal
+    const int e1 = __ldg(m.t.ptr + i + 1);
+    for (int e = __ldg(m.t.ptr + i); e < e1; ++e)
+      cfma(acc, __ldg(m.t.val + e), ld_gather(x + static_cast<long long>(__ldg(m.t.col + e)) * (n + 1), xpol));
+  }
+  if (m.d_loc) {  // -0.5 (w (dl_i + dl_j) + ds_i + ds_j) X(i, j)
+    const double d = __dmul_rn(
+        0.5, __dadd_rn(__dadd_rn(__dmul_rn(m.omega, __dadd_rn(__ldg(m.d_loc + i), __ldg(m.d_loc + j))),
+                                 __ldg(m.d_ss + i)),
+                       __ldg(m.d_ss + j)));
+    if (d != 0.0) {
+      const double2 xg = ld_gather(x + g, xpol);
+      acc.x = fma(-d, xg.x, acc.x);
+      acc.y = fma(-d, xg.y, acc.y);
+    }
+  }
+  return acc;
+}
+
+// Block-uniform loop over local rows; epi(row, acc, valid) on every thread.
+template <class Epi>
+__device__ __forceinline__ void kron_loop(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
+  const unsigned long long xpol = evict_last_policy();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < m.rows; base += stride) {
+    const long long r = base + threadIdx.x;
+    const bool valid = r < m.rows;
+    const double2 acc = valid ? kron_row(m, x, m.row0 + r, xpol) : make_double2(0.0, 0.0);
+    epi(r, acc, valid);
+  }
+}
+
+// W_k = Q_k X on the local columns (W_k(i, a) at w[n*a + i], global index).
+__global__ void __launch_bounds__(kThreads) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {
+  const unsigned long long xpol = evict_last_policy();
+  const long long n = m.n;
+  const KronList& q = m.q[k];
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < m.rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long g = m.row0 + r;
+    const long long a = g / n, i = g - a * n;
+    const double2* xa = x + a * n;
+    double2 acc = make_double2(0.0, 0.0);
+    const int e1 = __ldg(q.ptr + i + 1);
+#pragma unroll 4
+    for (int e = __ldg(q.ptr + i); e < e1; ++e) cfma(acc, __ldg(q.val + e), ld_gather(xa + __ldg(q.col + e), xpol));
+    st_hint(m.w[k] + g, acc, xpol);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) kron_spmv_kernel(KronView m, const double2* x, double2* y, double scale) {
+  kron_loop(m, x, [&](long long row, double2 acc, bool valid) {
+    if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
+  });
+}
+
+struct KronStepArgs {
+  KronView m;
+  const double2* x;
+  double2* y;
+  const double2* sum_in;
+  double2* sum_out;
+  double scale;
+  double tol;
+  StepCtl* ctl;
+  int first_of_stage;
+  int stage;
+  int decide;
+};
+
+__global__ void __launch_bounds__(kThreads) kron_step_term_kernel(KronStepArgs a) {
+  StepCtl* ctl = a.ctl;
+  if (*(volatile int*)&ctl->error) return;
+  if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
+  __shared__ unsigned long long red[32];
+  unsigned long long tmax = 0, smax = 0;
+  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
+  kron_loop(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+    if (!valid) return;
+    const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
+    const double2 sv0 = ld_once(a.sum_in + row, once);
+    st_hint(a.y + row, yv, keep);
+    const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
+    st_hint(a.sum_out + row, sv, once);
+    tmax = umax64(tmax, dbits(cabs2(yv)));
+    smax = umax64(smax, dbits(cabs2(sv)));
+  });
+  tmax = block_max_bits(tmax, red);
+  smax = block_max_bits(smax, red);
+  if (threadIdx.x == 0) {
+    atomicMax(&ctl->term_bits, tmax);
+    atomicMax(&ctl->sum_bits, smax);
+    __threadfence();
+    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
+      __threadfence();
+      if (a.decide) {
+        step_control(ctl, a.first_of_stage, a.stage, a.tol);
+      } else {
+        ctl->arrivals = 0;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
+  SeriesCtl* ctl = a.ctl;
+  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+  __shared__ unsigned long long red[32];
+  __shared__ double fac[kMaxSeriesD];
+  __shared__ int act[kMaxSeriesD];
+  __shared__ unsigned long long smax_sh[kMaxSeriesD];
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
+    fac[k] = ctl->factor[k];
+    act[k] = ctl->active[k];
+    smax_sh[k] = 0;
+  }
+  __syncthreads();
+  unsigned long long tmax = 0;
+  const bool first = a.p == 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
+  kron_loop(m, a.x, [&](long long row, double2 acc, bool valid) {
+    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));  // K_p
+    if (valid) {
+      st_hint(a.kp + row, kv, keep);
+      tmax = umax64(tmax, dbits(cabs2(kv)));
+    }
+    const double2 zv = (first && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
+      double2 sv[kSeriesRegD];
+#pragma unroll
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
+      }
+#pragma unroll
+      for (int u = 0; u < kSeriesRegD; ++u) {
+        const int k = k0 + u;
+        if (k >= a.count) break;  // warp-uniform
+        unsigned long long mk = 0;
+        if (valid && act[k]) {
+          sv[u] = axpy<2>(sv[u], fac[k], kv);  // expm.cpp:300-305
+          st_hint(a.sums.s[k] + row, sv[u], once);
+          mk = dbits(cabs2(sv[u]));
+        }
+        mk = warp_max_bits(mk);
+        if (lane == 0 && mk) atomicMax(&smax_sh[k], mk);
+      }
+    }
+  });
+  tmax = block_max_bits(tmax, red);
+  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
+  __syncthreads();
+  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
+    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
+      __threadfence();
+      if (a.decide) {
+        series_control(ctl, a.count, a.tol);
+      } else {
+        ctl->arrivals = 0;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ norm kernels
 // Grid-wide max |v| into *bits, last block runs `fin`.
 template <class Fin>
@@ -719,6 +927,17 @@ int sell_grid(K kernel, const SellView& m) {
   return static_cast<int>(want < cap ? want : cap);
 }
 
+template <class K>
+int kron_grid(K kernel, long long rows) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const long long cap = static_cast<long long>(sm_count()) * per_sm;
+  long long want = (rows + kThreads - 1) / kThreads;
+  if (want < 1) want = 1;
+  return static_cast<int>(want < cap ? want : cap);
+}
+
 int small_grid(long long n) {
   long long want = (n + kThreads - 1) / kThreads, cap = sm_count() * 4LL;
   return static_cast<int>(want < 1 ? 1 : (want < cap ? want : cap));
@@ -792,7 +1011,10 @@ void series_control(SeriesCtl* ctl, int count, double tol, cudaStream_t s) {
 
 void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,
                double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, bool decide, cudaStream_t s) {
-  if (m.format == Format::Sell) {
+  if (m.format == Format::Kron) {
+    KronStepArgs a{m.kron, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
+    kron_step_term_kernel<<<kron_grid(kron_step_term_kernel, m.kron.rows), kThreads, 0, s>>>(a);
+  } else if (m.format == Format::Sell) {
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
       sell_step_term_kernel<true><<<sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s>>>(a);
@@ -816,6 +1038,11 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, const double
                  const SeriesSums& sums, int count, int p, double scale, double tol,
                  SeriesCtl* ctl, bool decide, cudaStream_t s) {
   SeriesTermArgs a{m.csr, x, kp, z, sums, count, p, scale, tol, ctl, decide ? 1 : 0};
+  if (m.format == Format::Kron) {
+    kron_series_term_kernel<<<kron_grid(kron_series_term_kernel, m.kron.rows), kThreads, 0, s>>>(a, m.kron);
+    QSWG_LAUNCH_CHECK("series_term");
+    return;
+  }
   if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_series_term_kernel<true><<<sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s>>>(a, m.sell);
@@ -842,8 +1069,19 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, const double
   QSWG_LAUNCH_CHECK("series_term");
 }
 
+void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
+  if (m.format != Format::Kron) return;
+  for (int k = 0; k < m.kron.nk; ++k) {
+    kron_w_kernel<<<kron_grid(kron_w_kernel, m.kron.rows), kThreads, 0, s>>>(m.kron, x, k);
+    QSWG_LAUNCH_CHECK("kron_prepare");
+  }
+}
+
 void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaStream_t s) {
-  if (m.format == Format::Sell) {
+  if (m.format == Format::Kron) {
+    kron_prepare(m, x, s);  // single-GPU product (multi-GPU callers exchange W first)
+    kron_spmv_kernel<<<kron_grid(kron_spmv_kernel, m.kron.rows), kThreads, 0, s>>>(m.kron, x, y, scale);
+  } else if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_spmv_kernel<true><<<sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);
     } else {

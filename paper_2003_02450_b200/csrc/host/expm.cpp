@@ -94,6 +94,16 @@ struct Exec {
     return f;
   }
 
+  // Before every product with input x (full-length, halo filled): the Kron
+  // format builds W_k = Q_k x on the local columns and exchanges their halos.
+  void prepare(const dev::DevMatrix& m, const double2* x) const {
+    if (m.format != dev::Format::Kron) return;
+    dev::kron_prepare(m, x, s);
+    if (!single)
+      for (int k = 0; k < m.kron.nk; ++k)
+        comm->exchange_ranges(m.kron.w[k], l.w_halo_lo(), l.w_halo_hi(), sizeof(double2), s);
+  }
+
   template <class T>
   T read(const T* dev_ptr) const {
     T v{};
@@ -138,6 +148,7 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
       const double2* x = j == 1 ? x_stage_full : term[(j - 1) % 2];
       double2* y = term[j % 2] + ex.row0;
       const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
+      ex.prepare(mat, x);
       dev::step_term(mat, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1, static_cast<int>(st),
                      params.tolerance, ctl, ex.single, s);
       if (!ex.single) {
@@ -235,6 +246,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
       for (std::int64_t p = 1; p <= m_star; ++p) {
         const double2* x = p == 1 ? z_full : kbuf[(p - 1) % 2];
         double2* kp = kbuf[p % 2] + ex.row0;
+        ex.prepare(mat, x);
         dev::series_term(mat, x, kp, z, ss, static_cast<int>(count), static_cast<int>(p),
                          h / static_cast<double>(p), params.tolerance, ctl, ex.single, s);
         if (!ex.single) {
@@ -276,8 +288,10 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   // 1/||L||_1 keeps the iterates bounded.  Local kernel time only (no
   // exchange), as the per-GPU roofline needs.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
+  const dev::DevMatrix mat = l.matrix();
   auto launch = [&](int i) {
-    dev::series_term(l.matrix(), k[i % 2], k[(i + 1) % 2] + ex.row0, z, ss, count, 2 + (i % 2), scale, -1.0,
+    dev::kron_prepare(mat, k[i % 2], s);
+    dev::series_term(mat, k[i % 2], k[(i + 1) % 2] + ex.row0, z, ss, count, 2 + (i % 2), scale, -1.0,
                      ctl, true, s);
   };
   launch(0);  // warm-up

@@ -18,7 +18,7 @@
 
 namespace qswg {
 
-namespace {
+namespace detail {
 
 constexpr std::int64_t kExactNormDimLimit = 4096;  // liouvillian.cpp:13
 constexpr std::int64_t kMaxVertices = 46340;       // n^2 must fit int32 columns
@@ -90,6 +90,35 @@ void append_entries(std::vector<Entry>& e, const SparseMatrix& s, const std::fun
       e.push_back({i, s.col_indices()[static_cast<std::size_t>(k)], f(s.values()[static_cast<std::size_t>(k)])});
 }
 
+// Summed, zero-free copy of a multi-CSR (the matrix-free path needs each
+// operand once, not its emission history).
+MultiCsr canonical(const MultiCsr& m) {
+  MultiCsr c;
+  c.n = m.n;
+  c.ptr.assign(m.ptr.size(), 0);
+  for (std::int64_t i = 0; i < m.n; ++i) {
+    for (int k = m.ptr[static_cast<std::size_t>(i)]; k < m.ptr[static_cast<std::size_t>(i) + 1];) {
+      const int col = m.col[static_cast<std::size_t>(k)];
+      double2 v = m.val[static_cast<std::size_t>(k++)];
+      while (k < m.ptr[static_cast<std::size_t>(i) + 1] && m.col[static_cast<std::size_t>(k)] == col) {
+        v.x += m.val[static_cast<std::size_t>(k)].x;
+        v.y += m.val[static_cast<std::size_t>(k)].y;
+        ++k;
+      }
+      if (v.x != 0.0 || v.y != 0.0) {
+        c.col.push_back(col);
+        c.val.push_back(v);
+      }
+    }
+    c.ptr[static_cast<std::size_t>(i) + 1] = static_cast<int>(c.col.size());
+  }
+  return c;
+}
+
+}  // namespace detail
+
+using namespace detail;
+
 // Operands of L = I(x)A + B(x)I + sum_k P_k(x)Q_k + T_diag + decay (kernels.hpp).
 struct HostOperands {
   std::int64_t n = 0;
@@ -109,6 +138,14 @@ struct HostOperands {
     o.d_loc = d_loc;
     o.d_ss = d_ss;
     o.omega = omega;
+    return o;
+  }
+
+  HostOperands summed() const {
+    HostOperands o = *this;
+    o.a = canonical(a);
+    o.b = canonical(b);
+    o.t = canonical(t);
     return o;
   }
 };
@@ -154,6 +191,15 @@ class DeviceOperands {
   std::vector<DeviceBuffer<unsigned char>> bufs_;
 };
 
+// Device copy of the summed operands kept by a Kron-format Liouvillian.
+struct KronStore {
+  KronStore(const HostOperands& h, cudaStream_t s) : host(h.summed()), ops(host, s) {}
+  HostOperands host;
+  DeviceOperands ops;
+};
+
+namespace {
+
 void validate_common(double omega, const SparseMatrix& h) {
   if (h.cols() != h.rows()) throw std::invalid_argument("Hamiltonian must be square");
   if (!(omega >= 0.0 && omega <= 1.0)) throw std::invalid_argument("omega must be in [0, 1]");
@@ -194,6 +240,16 @@ dev::CsrView Liouvillian::view() const {
   return v;
 }
 
+namespace {
+std::vector<std::int64_t> count_scan(const dev::KronOperands& ops, std::int64_t n,
+                                     DeviceBuffer<std::int64_t>& grp, cudaStream_t s);
+template <class V>
+void fill_block(const dev::KronOperands& ops, const DeviceBuffer<std::int64_t>& grp,
+                const std::vector<std::int64_t>& colptr, std::int64_t n, const RowBlock& blk,
+                DeviceBuffer<std::int64_t>& rowptr, DeviceBuffer<int>& col, DeviceBuffer<V>& val,
+                std::int64_t& nnz, cudaStream_t s);
+}  // namespace
+
 dev::DevMatrix Liouvillian::matrix(int group_override) const {
   dev::DevMatrix m;
   m.format = format_;
@@ -205,12 +261,49 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
   m.sell.rows = block_.rows;
   m.sell.row0 = block_.row0;
   m.sell.n_slices = n_slices_;
+  if (kron_) {
+    const dev::KronOperands& o = kron_->ops.get();
+    m.kron.n = static_cast<int>(n_);
+    m.kron.rows = block_.rows;
+    m.kron.row0 = block_.row0;
+    m.kron.a = o.a;
+    m.kron.b = o.b;
+    m.kron.t = o.t;
+    m.kron.nk = o.nk;
+    for (int k = 0; k < o.nk; ++k) {
+      m.kron.p[k] = o.p[k];
+      m.kron.q[k] = o.q[k];
+      m.kron.w[k] = kron_w_[static_cast<std::size_t>(k)].get();
+    }
+    m.kron.d_loc = o.d_loc;
+    m.kron.d_ss = o.d_ss;
+    m.kron.omega = o.omega;
+  }
   return m;
 }
 
 void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
                            std::vector<Complex>& val) const {
   DeviceGuard g(device_);
+  if (format_ == dev::Format::Kron) {
+    // no superoperator is stored: assemble the block's CSR from the operands
+    DeviceBuffer<std::int64_t> grp, rp;
+    DeviceBuffer<int> cc;
+    DeviceBuffer<double2> vv;
+    std::int64_t nz = 0;
+    const std::vector<std::int64_t> colptr = count_scan(kron_->ops.get(), n_, grp, stream_);
+    fill_block(kron_->ops.get(), grp, colptr, n_, block_, rp, cc, vv, nz, stream_);
+    rowptr.resize(static_cast<std::size_t>(block_.rows) + 1);
+    std::vector<int> c32(static_cast<std::size_t>(nz));
+    val.resize(static_cast<std::size_t>(nz));
+    QSWG_CHECK(cudaMemcpy(rowptr.data(), rp.get(), rowptr.size() * sizeof(std::int64_t), cudaMemcpyDeviceToHost));
+    if (nz) {
+      QSWG_CHECK(cudaMemcpy(c32.data(), cc.get(), c32.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      QSWG_CHECK(cudaMemcpy(val.data(), vv.get(), val.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    }
+    col.assign(c32.begin(), c32.end());
+    return;
+  }
   if (format_ == dev::Format::Sell) {
     // de-pad: a row's genuine entries precede its padding (val == 0 exactly;
     // canonical entries are never zero)
@@ -333,6 +426,57 @@ int heuristic_group(double mean_row) {
 
 }  // namespace
 
+namespace {
+
+// Halo tables of the Kron format, replicated on every rank from the (small,
+// identical) operands: rank r reads X columns B(j, .) and T(j, .) and W_k
+// columns P_k(j, .) for its own rho columns j; each peer's share is sent as
+// the hull of whole columns.
+void kron_halos(const HostOperands& h, std::int64_t n, const std::vector<std::int64_t>& starts,
+                std::vector<std::vector<std::int64_t>>& lo, std::vector<std::vector<std::int64_t>>& hi,
+                std::vector<std::vector<std::int64_t>>& wlo, std::vector<std::vector<std::int64_t>>& whi) {
+  const int world = static_cast<int>(starts.size()) - 1;
+  const auto W = static_cast<std::size_t>(world);
+  lo.assign(W, std::vector<std::int64_t>(W, 0));
+  hi = lo;
+  wlo = lo;
+  whi = lo;
+  if (world == 1) return;
+  auto owner = [&](std::int64_t col) {
+    int q = 0;
+    while (q + 1 < world && starts[static_cast<std::size_t>(q) + 1] <= col * n) ++q;
+    return q;
+  };
+  auto add = [&](std::vector<std::vector<std::int64_t>>& L, std::vector<std::vector<std::int64_t>>& H, int r,
+                 std::int64_t col) {
+    const int q = owner(col);
+    if (q == r) return;
+    auto& a = L[static_cast<std::size_t>(r)][static_cast<std::size_t>(q)];
+    auto& b = H[static_cast<std::size_t>(r)][static_cast<std::size_t>(q)];
+    if (a == b) {
+      a = col * n;
+      b = (col + 1) * n;
+    } else {
+      a = std::min(a, col * n);
+      b = std::max(b, (col + 1) * n);
+    }
+  };
+  auto row_cols = [](const MultiCsr& m, std::int64_t row, const std::function<void(std::int64_t)>& f) {
+    if (m.ptr.empty()) return;
+    for (int k = m.ptr[static_cast<std::size_t>(row)]; k < m.ptr[static_cast<std::size_t>(row) + 1]; ++k)
+      f(m.col[static_cast<std::size_t>(k)]);
+  };
+  for (int r = 0; r < world; ++r) {
+    for (std::int64_t j = starts[static_cast<std::size_t>(r)] / n; j < starts[static_cast<std::size_t>(r) + 1] / n; ++j) {
+      row_cols(h.b, j, [&](std::int64_t c) { add(lo, hi, r, c); });
+      row_cols(h.t, j, [&](std::int64_t c) { add(lo, hi, r, c); });
+      for (const MultiCsr& p : h.p) row_cols(p, j, [&](std::int64_t c) { add(wlo, whi, r, c); });
+    }
+  }
+}
+
+}  // namespace
+
 std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_t n, const HostOperands& hops,
                                                        const DeviceConfig& cfg) {
   std::unique_ptr<Liouvillian> l(new Liouvillian);
@@ -398,6 +542,23 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     QSWG_CHECK(cudaMemcpyAsync(bits, mx.get(), sizeof(bits), cudaMemcpyDeviceToHost, s));
     QSWG_CHECK(cudaStreamSynchronize(s));
     for (int p = 0; p < 9; ++p) std::memcpy(&l->norms_[static_cast<std::size_t>(p)], &bits[p], sizeof(double));
+  }
+
+  // ---- matrix-free Kronecker action: no superoperator stored ----
+  if (cfg.format == 3 && cfg.group != 1) {
+    const std::int64_t j0 = l->block_.row0 / n, j1 = (l->block_.row0 + l->block_.rows) / n;
+    l->nnz_local_ = colptr[static_cast<std::size_t>(j1)] - colptr[static_cast<std::size_t>(j0)];
+    l->format_ = dev::Format::Kron;
+    l->kron_ = std::make_shared<KronStore>(hops, s);
+    for (std::size_t k = 0; k < hops.p.size(); ++k) {
+      l->kron_w_.emplace_back(static_cast<std::size_t>(dim));
+      QSWG_CHECK(cudaMemsetAsync(l->kron_w_.back().get(), 0, l->kron_w_.back().bytes(), s));
+    }
+    QSWG_CHECK(cudaStreamSynchronize(s));
+    grp.reset();
+    kron_halos(l->kron_->host, n, l->starts_, l->halo_lo_, l->halo_hi_, l->whalo_lo_, l->whalo_hi_);
+    l->group_ = 32;
+    return l;
   }
 
   // ---- the superoperator row block: SELL-32 when its padding is small ----

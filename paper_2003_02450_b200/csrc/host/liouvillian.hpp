@@ -21,12 +21,13 @@
 
 namespace qswg {
 
-class Comm;  // multi-GPU exchange (comm.hpp); nullptr when world == 1
+class Comm;         // multi-GPU exchange (comm.hpp); nullptr when world == 1
+struct KronStore;   // operands of the matrix-free (Kron) format (liouvillian.cpp)
 
 struct DeviceConfig {
   int device = 0;       // CUDA ordinal
   int group = 0;        // lanes per row for the SpMV kernels; 0 = autotune
-  int format = 0;       // 0 auto, 1 CSR, 2 SELL-32
+  int format = 0;       // 0 auto, 1 CSR, 2 SELL-32, 3 matrix-free Kronecker action
   Comm* comm = nullptr; // borrowed; shared by every handle on this rank
 };
 
@@ -87,6 +88,9 @@ class Liouvillian {
   /// rank r gathers before every SpMV (empty when lo == hi).
   const std::vector<std::vector<std::int64_t>>& halo_lo() const { return halo_lo_; }
   const std::vector<std::vector<std::int64_t>>& halo_hi() const { return halo_hi_; }
+  /// Kron format: halos of the W_k = Q_k X work vectors (same layout).
+  const std::vector<std::vector<std::int64_t>>& w_halo_lo() const { return whalo_lo_; }
+  const std::vector<std::vector<std::int64_t>>& w_halo_hi() const { return whalo_hi_; }
 
  private:
   Liouvillian() = default;
@@ -110,6 +114,9 @@ class Liouvillian {
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;
   std::vector<std::vector<std::int64_t>> halo_lo_, halo_hi_;
+  std::vector<std::vector<std::int64_t>> whalo_lo_, whalo_hi_;
+  std::shared_ptr<KronStore> kron_;
+  std::vector<DeviceBuffer<double2>> kron_w_;
   mutable Workspace ws_;
 };
 

@@ -67,7 +67,27 @@ struct SellView {
   std::int64_t n_slices = 0;
 };
 
-enum class Format : int { Csr = 0, Sell = 1 };
+enum class Format : int { Csr = 0, Sell = 1, Kron = 2 };
+
+// Matrix-free Kronecker action (no superoperator stored):
+//   (L x)[n*j + i] = sum_c A(i,c) X(c,j) + sum_c B(j,c) X(i,c)
+//                  + sum_k sum_a P_k(j,a) W_k(i,a)          with W_k = Q_k X
+//                  + [i == j] sum_c T(i,c) X(c,c) - decay(i,j) X(i,j)
+// for X(i,j) = x[n*j + i] (column-major vec).  A, B, T are the summed
+// (canonical) operand lists of KronOperands; W_k are full-length work
+// vectors filled by kron_prepare() before every product.
+struct KronView {
+  int n = 0;
+  std::int64_t rows = 0;  // local rows [row0, row0 + rows), multiples of n
+  std::int64_t row0 = 0;
+  KronList a, b, t;
+  int nk = 0;
+  KronList p[kMaxKron], q[kMaxKron];
+  const double* d_loc = nullptr;
+  const double* d_ss = nullptr;
+  double omega = 0.0;
+  double2* w[kMaxKron] = {};
+};
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
 // lanes per row (2..32); group == 1 selects the bitwise reference-order mode
@@ -77,7 +97,10 @@ struct DevMatrix {
   int group = 8;
   CsrView csr;
   SellView sell;
-  std::int64_t rows() const { return format == Format::Csr ? csr.rows : sell.rows; }
+  KronView kron;
+  std::int64_t rows() const {
+    return format == Format::Csr ? csr.rows : format == Format::Sell ? sell.rows : kron.rows;
+  }
 };
 
 struct RealCsrView {
@@ -186,6 +209,9 @@ void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, bo
 void series_term(const DevMatrix& l, const double2* x, double2* kp, const double2* z,
                  const SeriesSums& sums, int count, int p, double scale, double tol,
                  SeriesCtl* ctl, bool decide, cudaStream_t s);
+// Kron format: W_k = Q_k X on the local columns (call before every product
+// with input x; multi-GPU callers then exchange the W_k halos).
+void kron_prepare(const DevMatrix& l, const double2* x, cudaStream_t s);
 // y = scale * (L x) (liouvillian.cpp:346-360).
 void spmv(const DevMatrix& l, const double2* x, double2* y, double scale, cudaStream_t s);
 // pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).

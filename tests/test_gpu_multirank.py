@@ -34,15 +34,15 @@ def run_ranks(world, fn):
     return out
 
 
-@pytest.mark.parametrize("group", [0, 1])
+@pytest.mark.parametrize("group,fmt", [(0, "auto"), (1, "auto"), (0, "kron")])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("name", ["c2_n36", "c5_n64", "c3_n40", "c4_n40", "lqsw_src_snk", "gqsw_multi_rot"])
-def test_sharded_series_matches_single_and_reference(name, world, group):
+def test_sharded_series_matches_single_and_reference(name, world, group, fmt):
     c = Case(name)
     t1, tq, q = c.series
 
     def rank_fn(r, comm):
-        l = c.build_gpu(api, comm=comm, group=group)
+        l = c.build_gpu(api, comm=comm, group=group, format=fmt)
         v = l.state().from_probabilities(c.rho0)
         res = api.series(l, v, t1, tq, int(q), states=True)
         st, lo, hi = l.partition()

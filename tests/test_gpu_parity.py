@@ -21,7 +21,7 @@ from paper_2003_02450_b200 import graphs  # noqa: E402
 
 # (group, storage format): autotuned fast kernels and the bitwise reference
 # order (group=1), each over CSR and SELL-32 storage.
-MODES = [(0, "csr"), (0, "sell"), (1, "csr"), (1, "sell")]
+MODES = [(0, "csr"), (0, "sell"), (0, "kron"), (1, "csr"), (1, "sell")]
 RHO_TOL = 1e-10
 TRACE_TOL = 1e-12
 
@@ -31,7 +31,7 @@ def trace_err(states, n):
     return np.abs(np.trace(s, axis1=1, axis2=2) - 1.0).max()
 
 
-@pytest.mark.parametrize("fmt", ["csr", "sell"])
+@pytest.mark.parametrize("fmt", ["csr", "sell", "kron"])
 @pytest.mark.parametrize("name", CASE_NAMES)
 def test_csr_and_norms_match_reference(name, fmt):
     c = Case(name)
