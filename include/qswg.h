@@ -54,9 +54,11 @@ enum { QSWG_FORMAT_AUTO = 0, QSWG_FORMAT_CSR = 1, QSWG_FORMAT_SELL = 2, QSWG_FOR
 typedef struct {
   int device;       /* CUDA ordinal */
   int group;        /* CSR lanes per row (2..32); 1 = bitwise reference order; 0 = autotune */
-  int format;       /* QSWG_FORMAT_*: device storage of the superoperator (AUTO: SELL-32
-                       when its padding is <= 3%, else CSR; KRON: matrix-free action on
-                       the n x n operators, no superoperator stored) */
+  int format;       /* QSWG_FORMAT_*: how the superoperator is applied.  KRON: matrix-free
+                       action on the n x n operators, nothing N^2 x N^2 stored; SELL: stored
+                       sliced-ELL (32-row slices); CSR: stored CSR.  AUTO = KRON, except in
+                       the bitwise mode (group = 1), where it is SELL if its padding is
+                       <= 3 %, else CSR. */
   qswg_comm* comm;  /* NULL for one GPU */
 } qswg_device_config;
 

@@ -21,6 +21,7 @@
 // next launch, so the host never synchronises inside a step or a series.
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../kernels.hpp"
 #include "common.cuh"
@@ -641,6 +642,9 @@ __device__ __forceinline__ double2 kron_row(const KronView& m, const double2* __
 }
 
 // Block-uniform loop over local rows; epi(row, acc, valid) on every thread.
+// (Staging column j in shared memory for the I (x) A gathers was measured
+// slower than L1 on c2 and c4 — 125 vs 101 ms and 5.1 vs 3.9 s per series —
+// and is not used.)
 template <class Epi>
 __device__ __forceinline__ void kron_loop(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
   const unsigned long long xpol = evict_last_policy();
@@ -658,6 +662,7 @@ __global__ void __launch_bounds__(kThreads) kron_w_kernel(KronView m, const doub
   const unsigned long long xpol = evict_last_policy();
   const long long n = m.n;
   const KronList& q = m.q[k];
+
   for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < m.rows;
        r += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long g = m.row0 + r;
@@ -927,15 +932,16 @@ int sell_grid(K kernel, const SellView& m) {
   return static_cast<int>(want < cap ? want : cap);
 }
 
+// Persistent launch geometry of a Kron kernel (no dynamic shared memory).
 template <class K>
-int kron_grid(K kernel, long long rows) {
+std::pair<int, std::size_t> kron_geom(K kernel, const KronView& m) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
-  long long want = (rows + kThreads - 1) / kThreads;
+  long long want = (m.rows + kThreads - 1) / kThreads;
   if (want < 1) want = 1;
-  return static_cast<int>(want < cap ? want : cap);
+  return {static_cast<int>(want < cap ? want : cap), std::size_t{0}};
 }
 
 int small_grid(long long n) {
@@ -1013,7 +1019,8 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
                double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, bool decide, cudaStream_t s) {
   if (m.format == Format::Kron) {
     KronStepArgs a{m.kron, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
-    kron_step_term_kernel<<<kron_grid(kron_step_term_kernel, m.kron.rows), kThreads, 0, s>>>(a);
+    const auto g = kron_geom(kron_step_term_kernel, m.kron);
+    kron_step_term_kernel<<<g.first, kThreads, g.second, s>>>(a);
   } else if (m.format == Format::Sell) {
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
@@ -1039,7 +1046,8 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, const double
                  SeriesCtl* ctl, bool decide, cudaStream_t s) {
   SeriesTermArgs a{m.csr, x, kp, z, sums, count, p, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Kron) {
-    kron_series_term_kernel<<<kron_grid(kron_series_term_kernel, m.kron.rows), kThreads, 0, s>>>(a, m.kron);
+    const auto g = kron_geom(kron_series_term_kernel, m.kron);
+    kron_series_term_kernel<<<g.first, kThreads, g.second, s>>>(a, m.kron);
     QSWG_LAUNCH_CHECK("series_term");
     return;
   }
@@ -1072,7 +1080,8 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, const double
 void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
   if (m.format != Format::Kron) return;
   for (int k = 0; k < m.kron.nk; ++k) {
-    kron_w_kernel<<<kron_grid(kron_w_kernel, m.kron.rows), kThreads, 0, s>>>(m.kron, x, k);
+    const auto g = kron_geom(kron_w_kernel, m.kron);
+    kron_w_kernel<<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
     QSWG_LAUNCH_CHECK("kron_prepare");
   }
 }
@@ -1080,7 +1089,8 @@ void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
 void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaStream_t s) {
   if (m.format == Format::Kron) {
     kron_prepare(m, x, s);  // single-GPU product (multi-GPU callers exchange W first)
-    kron_spmv_kernel<<<kron_grid(kron_spmv_kernel, m.kron.rows), kThreads, 0, s>>>(m.kron, x, y, scale);
+    const auto g = kron_geom(kron_spmv_kernel, m.kron);
+    kron_spmv_kernel<<<g.first, kThreads, g.second, s>>>(m.kron, x, y, scale);
   } else if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_spmv_kernel<true><<<sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);

@@ -545,7 +545,9 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   }
 
   // ---- matrix-free Kronecker action: no superoperator stored ----
-  if (cfg.format == 3 && cfg.group != 1) {
+  // (the default: fewest bytes and fastest on every BASELINE config; the
+  // bitwise reference-order mode needs a stored superoperator)
+  if ((cfg.format == 3 || cfg.format == 0) && cfg.group != 1) {
     const std::int64_t j0 = l->block_.row0 / n, j1 = (l->block_.row0 + l->block_.rows) / n;
     l->nnz_local_ = colptr[static_cast<std::size_t>(j1)] - colptr[static_cast<std::size_t>(j0)];
     l->format_ = dev::Format::Kron;
@@ -583,6 +585,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   }
   const double pad = l->nnz_local_ ? static_cast<double>(sell_entries) / static_cast<double>(l->nnz_local_) : 1.0;
   const bool use_sell = l->nnz_local_ > 0 && (cfg.format == 2 || (cfg.format == 0 && pad <= kSellMaxPadding));
+  if (cfg.format == 3) throw std::invalid_argument("the Kron format has no bitwise (group = 1) mode");
   if (use_sell) {
     l->format_ = dev::Format::Sell;
     l->padding_ = pad;

@@ -258,15 +258,15 @@ def test_omega_linearity():  # test_liouvillian.cpp:285-294
     g = random_digraph(rng, 5)
     h = api.generator_matrix(1.0, api.symmetrize(g))
     ml = api.local_lindblad(api.generator_matrix(1.0, g))
-    d = {om: api.build_local(om, h, ml).gather_full().to_dense() for om in (0.0, 0.3, 1.0)}
+    d = {om: api.build_local(om, h, ml, format="csr").gather_full().to_dense() for om in (0.0, 0.3, 1.0)}
     assert np.abs(d[0.3] - (0.7 * d[0.0] + 0.3 * d[1.0])).max() <= 1e-14
 
 
 def test_global_equals_local_at_omega0():  # test_liouvillian.cpp:119-127
     g = graphs.cycle_graph(5)
     h = graphs.generator_matrix(1.0, g)
-    a = api.build_local(0.0, h, graphs.markov_chain_matrix(g)).gather_full().to_dense()
-    b = api.build_global(0.0, h, [graphs.markov_chain_matrix(g)]).gather_full().to_dense()
+    a = api.build_local(0.0, h, graphs.markov_chain_matrix(g), format="csr").gather_full().to_dense()
+    b = api.build_global(0.0, h, [graphs.markov_chain_matrix(g)], format="csr").gather_full().to_dense()
     assert np.array_equal(a, b)
 
 
@@ -274,7 +274,7 @@ def test_trace_preservation_structure():  # test_liouvillian.cpp:268-283
     rng = np.random.default_rng(3)
     l, _ = random_lqsw(rng, 5, 0.7)
     n = 5
-    L = l.gather_full().to_dense()
+    L = l.gather_full().to_dense()  # assembled on demand in the Kron format
     diag_rows = [i * (n + 1) for i in range(n)]
     colsum = L[diag_rows, :].sum(axis=0)
     assert np.abs(colsum).max() <= 1e-14
@@ -283,8 +283,8 @@ def test_trace_preservation_structure():  # test_liouvillian.cpp:268-283
 @pytest.mark.parametrize("group", [1, 2, 4, 8, 16, 32])
 def test_every_row_group_width_agrees(group):
     w = graphs.config("c2", size=6)
-    l = api.build_global(w.omega, w.h, w.ops, group=group)
-    assert l.group == group
+    l = api.build_global(w.omega, w.h, w.ops, group=group, format="csr")
+    assert l.group == group and l.format == "csr"
     x = random_vec(np.random.default_rng(1), l.dim)
     L = l.gather_full()
     want = L.to_dense() @ x

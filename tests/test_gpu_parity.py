@@ -21,7 +21,7 @@ from paper_2003_02450_b200 import graphs  # noqa: E402
 
 # (group, storage format): autotuned fast kernels and the bitwise reference
 # order (group=1), each over CSR and SELL-32 storage.
-MODES = [(0, "csr"), (0, "sell"), (0, "kron"), (1, "csr"), (1, "sell")]
+MODES = [(0, "csr"), (0, "sell"), (0, "kron"), (1, "csr"), (1, "sell"), (1, "auto")]
 RHO_TOL = 1e-10
 TRACE_TOL = 1e-12
 
@@ -37,6 +37,7 @@ def test_csr_and_norms_match_reference(name, fmt):
     c = Case(name)
     l = c.build_gpu(api, format=fmt)
     assert l.format == fmt
+    assert c.build_gpu(api).format == "kron"  # the default
     assert l.dim == c.dim and l.nnz == c.nnz
     L = l.gather_full()
     assert np.array_equal(L.indptr, c.L.indptr)
