@@ -96,6 +96,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def traffic_for(config, fmt):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed ncu --set full capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(f"{config}:{fmt}")
+        return e["dram_bytes_per_launch"] if e else None
+    except Exception:
+        return None
+
+
 def workload_desc(w, extra=None):
     d = {"workload": f"{w.name}: {'L-QSW' if w.kind == 'local' else 'G-QSW'} n={w.n} omega={w.omega} "
                      f"t=[{w.t1},{w.tq}] outputs={w.steps + 1}",
@@ -171,7 +183,9 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--size", type=int, default=None, help="shrink the graph (debug only)")
     ap.add_argument("--group", type=int, default=0)
+    ap.add_argument("--format", default="auto", choices=["auto", "kron", "sell", "csr"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-superop", action="store_true", help="skip the stored-superoperator comparison")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -200,11 +214,14 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    def build(fmt):
+        if w.kind == "local":
+            return api.build_local(w.omega, w.h, w.ops[0], device=local_rank, group=args.group, comm=comm,
+                                   format=fmt)
+        return api.build_global(w.omega, w.h, w.ops, device=local_rank, group=args.group, comm=comm, format=fmt)
+
     t0 = time.perf_counter()
-    if w.kind == "local":
-        l = api.build_local(w.omega, w.h, w.ops[0], device=local_rank, group=args.group, comm=comm)
-    else:
-        l = api.build_global(w.omega, w.h, w.ops, device=local_rank, group=args.group, comm=comm)
+    l = build(args.format)
     barrier()
     build_s = time.perf_counter() - t0
 
@@ -260,14 +277,46 @@ def main():
         e2e_ms = float(t.item())
     del full_vec
 
-    # ---- roofline of the dominant kernel (fused series term) ----
+    # ---- roofline of the dominant kernel (one series term) ----
     d_active = int(info.d) if info.path == 2 else 1
-    term_ms = l.time_series_term(iters=20, count=d_active)
-    nnz_local = int(l.info.nnz_local)
-    term_bytes = 20 * nnz_local + 8 * (l.rows + 1) + 16 * l.dim + 16 * l.rows + 32 * d_active * l.rows
     peak, peak_src = load_peaks()
-    achieved = term_bytes / (term_ms * 1e-3) / 1e9
+    n_lind = len(w.ops) if w.kind == "global" else 0
+
+    def term_bytes(lv):
+        """Algorithmic HBM bytes of one series term with d_active outputs."""
+        vec = 16 * lv.dim + 16 * lv.rows + 32 * d_active * lv.rows  # x read, K_p write, sums r+w
+        if lv.format == "kron":  # W_k = Q_k x written once and read once per term
+            return vec + 32 * n_lind * lv.dim
+        return vec + 20 * int(lv.info.nnz_local) + 8 * (lv.rows + 1)
+
+    term_ms = l.time_series_term(iters=20, count=d_active)
+    achieved = term_bytes(l) / (term_ms * 1e-3) / 1e9
     share = info.spmvs * term_ms / ms_per_step
+    kernel_name = {"kron": "kron_w_kernel + kron_series_term_kernel", "sell": "sell_series_term_kernel",
+                   "csr": "series_spmv_kernel + series_axpy_kernel"}[l.format]
+
+    # ---- the stored-superoperator SpMV (BASELINE's "superop SpMV HBM GB/s") ----
+    superop = None
+    if l.format == "kron" and world == 1 and not args.no_superop:
+        del e2e_state, v
+        lk = l
+        l = None
+        ls = build("sell")
+        if ls.padding > 1.03:
+            del ls
+            ls = build("csr")
+        s_ms = ls.time_series_term(iters=20, count=d_active)
+        vs = ls.state().from_probabilities(w.rho0)
+        api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)  # warm-up
+        rs = api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)
+        sb = term_bytes(ls)
+        superop = {"format": ls.format, "kernel": "sell_series_term_kernel" if ls.format == "sell" else
+                   "series_spmv_kernel + series_axpy_kernel", "bytes_per_launch": sb, "ms_per_launch": s_ms,
+                   "achieved_gbs": sb / (s_ms * 1e-3) / 1e9, "frac": sb / (s_ms * 1e-3) / 1e9 / peak,
+                   "series_ms": float(rs.info.device_ms), "output_steps_per_s": w.steps / (rs.info.device_ms / 1e3),
+                   "bytes_note": "20 B/nnz + 8 B/row + x + K_p + 32*d*rows (SURVEY.md 8(d))"}
+        del ls, vs
+        l = lk
 
     if rank != 0:
         return 0
@@ -278,15 +327,17 @@ def main():
         "data": "synthetic (seeded graph of BASELINE.json config; no public dataset exists for this path)",
         "config": workload_desc(w, {
             "parallelism": f"row-block x{world}" if world > 1 else "1 GPU", "nnz": int(l.nnz),
+            "format": l.format,
             "build_norms_s": build_s, "one_norms": l.one_norms().tolist(), "group": int(l.group),
             "plan": {"path": int(info.path), "span": [int(info.span_m_star), int(info.span_s)],
                      "d": int(info.d), "n_super": int(info.n_super), "remainder": int(info.remainder),
                      "sub_m_star": int(info.sub_m_star)},
             "spmvs_per_step": int(info.spmvs)}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "series_term_kernel",
-                     "bytes_per_launch": term_bytes, "ms_per_launch": term_ms, "peak_source": peak_src,
-                     "share_of_step": share},
+                     "frac": achieved / peak, "traffic": traffic_for(w.name, l.format), "kernel": kernel_name,
+                     "format": l.format, "bytes_per_launch": term_bytes(l), "ms_per_launch": term_ms,
+                     "peak_source": peak_src, "share_of_step": share},
+        "superop_spmv": superop,
         "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,
                 "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),

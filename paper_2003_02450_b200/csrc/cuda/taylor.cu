@@ -601,7 +601,15 @@ __device__ __forceinline__ double2 kron_row(const KronView& m, const double2* __
   const long long n = m.n;
   const long long j = g / n, i = g - j * n;
   double2 acc = make_double2(0.0, 0.0);
-  if (m.a.ptr) {  // I (x) A: column j of X
+  if (m.a_ell.sptr) {  // I (x) A: column j of X, operand rows in sliced ELL
+    const int sl = static_cast<int>(i >> 5), lane = static_cast<int>(i & 31);
+    const int b = __ldg(m.a_ell.sptr + sl), len = (__ldg(m.a_ell.sptr + sl + 1) - b) >> 5;
+    const int* cp = m.a_ell.col + b + lane;
+    const double2* vp = m.a_ell.val + b + lane;
+    const double2* xj = x + j * n;
+#pragma unroll 4
+    for (int k = 0; k < len; ++k) cfma(acc, __ldg(vp + 32 * k), ld_gather(xj + __ldg(cp + 32 * k), xpol));
+  } else if (m.a.ptr) {  // I (x) A with CSR operand rows
     const int e1 = __ldg(m.a.ptr + i + 1);
     const double2* xj = x + j * n;
 #pragma unroll 4
@@ -661,17 +669,25 @@ __device__ __forceinline__ void kron_loop(const KronView& m, const double2* __re
 __global__ void __launch_bounds__(kThreads) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {
   const unsigned long long xpol = evict_last_policy();
   const long long n = m.n;
+  const KronEll& qe = m.q_ell[k];
   const KronList& q = m.q[k];
-
   for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < m.rows;
        r += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long g = m.row0 + r;
     const long long a = g / n, i = g - a * n;
     const double2* xa = x + a * n;
     double2 acc = make_double2(0.0, 0.0);
-    const int e1 = __ldg(q.ptr + i + 1);
+    if (qe.sptr) {
+      const int sl = static_cast<int>(i >> 5), lane = static_cast<int>(i & 31);
+      const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
 #pragma unroll 4
-    for (int e = __ldg(q.ptr + i); e < e1; ++e) cfma(acc, __ldg(q.val + e), ld_gather(xa + __ldg(q.col + e), xpol));
+      for (int e = 0; e < len; ++e)
+        cfma(acc, __ldg(qe.val + b + 32 * e + lane), ld_gather(xa + __ldg(qe.col + b + 32 * e + lane), xpol));
+    } else if (q.ptr) {
+      const int e1 = __ldg(q.ptr + i + 1);
+#pragma unroll 4
+      for (int e = __ldg(q.ptr + i); e < e1; ++e) cfma(acc, __ldg(q.val + e), ld_gather(xa + __ldg(q.col + e), xpol));
+    }
     st_hint(m.w[k] + g, acc, xpol);
   }
 }

@@ -191,11 +191,82 @@ class DeviceOperands {
   std::vector<DeviceBuffer<unsigned char>> bufs_;
 };
 
+// Sliced-ELL copy of a row-indexed operand (kernels.hpp: KronEll).
+struct EllHost {
+  std::vector<int> sptr, col;
+  std::vector<double2> val;
+};
+
+EllHost to_ell(const MultiCsr& m) {
+  EllHost e;
+  const std::int64_t ns = (m.n + 31) / 32;
+  e.sptr.assign(static_cast<std::size_t>(ns) + 1, 0);
+  for (std::int64_t sl = 0; sl < ns; ++sl) {
+    int len = 0;
+    for (std::int64_t i = sl * 32; i < std::min<std::int64_t>(m.n, sl * 32 + 32); ++i)
+      len = std::max(len, m.ptr[static_cast<std::size_t>(i) + 1] - m.ptr[static_cast<std::size_t>(i)]);
+    e.sptr[static_cast<std::size_t>(sl) + 1] = e.sptr[static_cast<std::size_t>(sl)] + 32 * len;
+  }
+  e.col.assign(static_cast<std::size_t>(e.sptr.back()), 0);
+  e.val.assign(static_cast<std::size_t>(e.sptr.back()), make_double2(0.0, 0.0));
+  for (std::int64_t sl = 0; sl < ns; ++sl) {
+    const int len = (e.sptr[static_cast<std::size_t>(sl) + 1] - e.sptr[static_cast<std::size_t>(sl)]) / 32;
+    for (int lane = 0; lane < 32; ++lane) {
+      const std::int64_t i = sl * 32 + lane;
+      const int b = i < m.n ? m.ptr[static_cast<std::size_t>(i)] : 0;
+      const int cnt = i < m.n ? m.ptr[static_cast<std::size_t>(i) + 1] - b : 0;
+      for (int k = 0; k < len; ++k) {
+        const std::size_t at = static_cast<std::size_t>(e.sptr[static_cast<std::size_t>(sl)] + 32 * k + lane);
+        if (k < cnt) {
+          e.col[at] = m.col[static_cast<std::size_t>(b + k)];
+          e.val[at] = m.val[static_cast<std::size_t>(b + k)];
+        } else {
+          e.col[at] = static_cast<int>(std::min<std::int64_t>(i, m.n - 1));  // padding: X(i, j) * 0
+        }
+      }
+    }
+  }
+  return e;
+}
+
 // Device copy of the summed operands kept by a Kron-format Liouvillian.
 struct KronStore {
-  KronStore(const HostOperands& h, cudaStream_t s) : host(h.summed()), ops(host, s) {}
+  // Sliced ELL copies unless they store more than kEllMaxPadding x the
+  // nonzeros; whether the kernels use them is autotuned per operator set at
+  // build (ELL wins on lattices and on c3, CSR on c4's 2-hop rows).
+  static constexpr double kEllMaxPadding = 2.0;
+  KronStore(const HostOperands& h, cudaStream_t s) : host(h.summed()), ops(host, s) {
+    a = maybe_ell(host.a, s);
+    for (const MultiCsr& qk : host.q) q.push_back(maybe_ell(qk, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+  }
   HostOperands host;
-  DeviceOperands ops;
+  DeviceOperands ops;  // CSR lists (B, P, T; and A, Q for on-demand assembly)
+  dev::KronEll a;
+  std::vector<dev::KronEll> q;
+
+ private:
+  dev::KronEll maybe_ell(const MultiCsr& m, cudaStream_t s) {
+    if (m.col.empty()) return {};
+    EllHost e = to_ell(m);
+    if (static_cast<double>(e.col.size()) > kEllMaxPadding * static_cast<double>(m.col.size())) return {};
+    return upload_ell(e, s);
+  }
+  dev::KronEll upload_ell(const EllHost& e, cudaStream_t s) {
+    dev::KronEll d;
+    if (e.col.empty()) return d;  // empty operand: no term
+    d.sptr = up(e.sptr, s);
+    d.col = up(e.col, s);
+    d.val = up(e.val, s);
+    return d;
+  }
+  template <class T>
+  const T* up(const std::vector<T>& v, cudaStream_t s) {
+    bufs_.emplace_back(v.size() * sizeof(T));
+    QSWG_CHECK(cudaMemcpyAsync(bufs_.back().get(), v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return reinterpret_cast<const T*>(bufs_.back().get());
+  }
+  std::vector<DeviceBuffer<unsigned char>> bufs_;
 };
 
 namespace {
@@ -266,12 +337,14 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.n = static_cast<int>(n_);
     m.kron.rows = block_.rows;
     m.kron.row0 = block_.row0;
+    m.kron.a_ell = kron_ell_ ? kron_->a : dev::KronEll{};
     m.kron.a = o.a;
     m.kron.b = o.b;
     m.kron.t = o.t;
     m.kron.nk = o.nk;
     for (int k = 0; k < o.nk; ++k) {
       m.kron.p[k] = o.p[k];
+      m.kron.q_ell[k] = kron_ell_ ? kron_->q[static_cast<std::size_t>(k)] : dev::KronEll{};
       m.kron.q[k] = o.q[k];
       m.kron.w[k] = kron_w_[static_cast<std::size_t>(k)].get();
     }
@@ -560,6 +633,16 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     grp.reset();
     kron_halos(l->kron_->host, n, l->starts_, l->halo_lo_, l->halo_hi_, l->whalo_lo_, l->whalo_hi_);
     l->group_ = 32;
+    // sliced-ELL vs CSR row-indexed operands: time both (local products only)
+    bool has_ell = l->kron_->a.sptr != nullptr;
+    for (const auto& q : l->kron_->q) has_ell = has_ell || q.sptr != nullptr;
+    l->kron_ell_ = has_ell;
+    if (has_ell && dim >= (1 << 16)) {
+      const double t_ell = l->time_spmv(3, 32);
+      l->kron_ell_ = false;
+      const double t_csr = l->time_spmv(3, 32);
+      l->kron_ell_ = t_ell <= t_csr;
+    }
     return l;
   }
 

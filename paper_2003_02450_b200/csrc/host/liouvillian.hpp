@@ -116,6 +116,7 @@ class Liouvillian {
   std::vector<std::vector<std::int64_t>> halo_lo_, halo_hi_;
   std::vector<std::vector<std::int64_t>> whalo_lo_, whalo_hi_;
   std::shared_ptr<KronStore> kron_;
+  mutable bool kron_ell_ = false;  // use the sliced-ELL copies of A / Q_k
   std::vector<DeviceBuffer<double2>> kron_w_;
   mutable Workspace ws_;
 };

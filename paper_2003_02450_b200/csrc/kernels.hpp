@@ -76,13 +76,30 @@ enum class Format : int { Csr = 0, Sell = 1, Kron = 2 };
 // for X(i,j) = x[n*j + i] (column-major vec).  A, B, T are the summed
 // (canonical) operand lists of KronOperands; W_k are full-length work
 // vectors filled by kron_prepare() before every product.
+// Row-indexed n x n operand in sliced ELL (32 rows per slice, entry k of the
+// rows of slice s at sptr[s] + 32 k + lane, padded with col = row, val = 0):
+// the 32 lanes of a warp handle 32 consecutive rows i, so their operand
+// loads are coalesced.
+struct KronEll {
+  const int* sptr = nullptr;  // n_slices + 1 entry offsets
+  const int* col = nullptr;
+  const double2* val = nullptr;
+};
+
 struct KronView {
   int n = 0;
   std::int64_t rows = 0;  // local rows [row0, row0 + rows), multiples of n
   std::int64_t row0 = 0;
-  KronList a, b, t;
+  // Row-indexed operands come in sliced ELL when its padding is small (lattice
+  // operators), else in CSR (their `ell.sptr` is then null).
+  KronEll a_ell;  // I (x) A, indexed by the rho row i
+  KronList a;
+  KronList b;     // B (x) I, indexed by the rho column j (warp-uniform)
+  KronList t;     // transfer onto the diagonal (rows i == j)
   int nk = 0;
-  KronList p[kMaxKron], q[kMaxKron];
+  KronList p[kMaxKron];      // indexed by j (warp-uniform)
+  KronEll q_ell[kMaxKron];   // W_k = Q_k X, indexed by i
+  KronList q[kMaxKron];
   const double* d_loc = nullptr;
   const double* d_ss = nullptr;
   double omega = 0.0;
