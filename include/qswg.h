@@ -103,6 +103,17 @@ int qswg_local_lindblad(const qswg_sparse* m, qswg_sparse** out);
 int qswg_augment(const qswg_sparse* adjacency, const qswg_source_arc* sources, int64_t n_sources,
                  const qswg_sink_arc* sinks, int64_t n_sinks, qswg_sparse** out);
 
+/* ---- non-moralising G-QSW operators (operators.hpp:16-83) --------------- */
+/* nm_vsets(gu): dims[i] = arcs into vertex i of the symmetric gu, at least 1. */
+int qswg_nm_vsets(const qswg_sparse* gu, int64_t* dims);
+/* nm_H(gamma, gu, V), nm_L(gamma, g, V), nm_H_rot(V, dim2) for V given by dims[n_vertices]. */
+int qswg_nm_H(double gamma, const qswg_sparse* gu, const int64_t* dims, int64_t n_vertices, qswg_sparse** out);
+int qswg_nm_L(double gamma, const qswg_sparse* g, const int64_t* dims, int64_t n_vertices, qswg_sparse** out);
+int qswg_nm_H_rot(const int64_t* dims, int64_t n_vertices, int pauli_y, qswg_sparse** out);
+/* nm_rho_map(p, V) -> expanded[sum(dims)]; nm_measure(diag, V) -> p[n_vertices]. */
+int qswg_nm_rho_map(const double* p, const int64_t* dims, int64_t n_vertices, double* expanded);
+int qswg_nm_measure(const double* diag, const int64_t* dims, int64_t n_vertices, double* p);
+
 /* ---- superoperator (liouvillian.hpp:65-93) ------------------------------ */
 /* build_local(omega, h, m_l, sources, sinks, n_workers), liouvillian.hpp:65-71 */
 int qswg_build_local(double omega, const qswg_sparse* h, const qswg_sparse* m_l,

@@ -88,6 +88,14 @@ def cases():
     out.append(dict(name="walkthrough_gqsw", kind="global", n=3, omega=1.0, h=R.graph_op("generator_matrix", gu),
                     ops=[g3], sources=[], sinks=[], h_rot=None, rho0=np.array([1.0, 0, 0]),
                     series=(0.0, 100.0, 10), steps=[100.0]))
+    vs_h, _ = R.nm_op("nm_H", g3, gu, 1.0)
+    vs_l, _ = R.nm_op("nm_L", g3, gu, 1.0)
+    vs_r, dims3 = R.nm_op("nm_H_rot", g3, gu)
+    p_nm = np.concatenate([np.full(int(d), (1.0 if v == 0 else 0.0) / d) for v, d in enumerate(dims3)])
+    for om in (1.0, 0.0):
+        out.append(dict(name=f"walkthrough_nm_w{int(om)}", kind="global", n=int(dims3.sum()), omega=om, h=vs_h,
+                        ops=[vs_l], sources=[], sinks=[], h_rot=vs_r, rho0=p_nm, series=(0.0, 100.0, 10),
+                        steps=[100.0]))
     out.append(dict(name="walkthrough_lqsw_w0", kind="local", n=3, omega=0.0, h=gu, ops=[g3], sources=[],
                     sinks=[], h_rot=None, rho0=np.array([1.0, 0, 0]), series=(0.0, 100.0, 10), steps=[100.0]))
     out.append(dict(name="walkthrough_lqsw_w1", kind="local", n=3, omega=1.0, h=gu, ops=[g3], sources=[],
@@ -130,6 +138,20 @@ def main():
         for op in ("generator_matrix", "markov_chain_matrix", "symmetrize", "local_lindblad"):
             garr.update(csr_arrays(f"g{k}_{op}", R.graph_op(op, g)))
     np.savez_compressed(os.path.join(OUT, "graph_ops.npz"), **garr)
+
+    # demoralisation operators (operators.cpp nm_*): walkthrough + random digraphs
+    narr = {}
+    g3 = Csr.from_coo(3, 3, [2, 2], [0, 1], [1.0, 1.0])
+    nm_graphs = [g3] + [random_digraph(np.random.default_rng(300 + k), 6, 0.35) for k in range(3)]
+    for k, g in enumerate(nm_graphs):
+        gu = R.graph_op("symmetrize", g)
+        narr.update(csr_arrays(f"g{k}", g))
+        for op in ("nm_H", "nm_L", "nm_H_rot"):
+            for py in ((0, 1) if op == "nm_H_rot" else (0,)):
+                m, dims = R.nm_op(op, g, gu, gamma=1.0 if k == 0 else 0.7, pauli_y=bool(py))
+                narr.update(csr_arrays(f"g{k}_{op}{'_py' if py else ''}", m))
+                narr[f"g{k}_dims"] = dims
+    np.savez_compressed(os.path.join(OUT, "nm_ops.npz"), **narr)
 
     for c in cases():
         hd = build(R, c)

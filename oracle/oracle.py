@@ -109,6 +109,8 @@ class Oracle:
             L.ref_sparse_export.argtypes = [C.c_void_p, _i64p, _i64p, _dp]
             L.ref_graph_op.restype = C.c_void_p
             L.ref_graph_op.argtypes = [C.c_int, C.c_double, C.c_void_p, C.c_char_p, C.c_int]
+            L.ref_nm_op.restype = C.c_void_p
+            L.ref_nm_op.argtypes = [C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_int, _i64p, C.c_char_p, C.c_int]
             L.ref_build_local.restype = C.c_void_p
             L.ref_build_local.argtypes = [C.c_double, C.c_void_p, C.c_void_p, C.c_int64, _i64p, _dp,
                                           C.c_int64, _i64p, _dp, C.c_int64, C.POINTER(C.c_int),
@@ -183,6 +185,26 @@ class Oracle:
             return res
         finally:
             self._sparse_free(h)
+
+    def nm_op(self, what: str, g, gu, gamma: float = 1.0, pauli_y: bool = False):
+        """Reference demoralisation operators: what in {nm_H, nm_L, nm_H_rot};
+        returns (matrix, vsets dims).  Reference library only."""
+        assert self.kind == "reference"
+        gh, k1 = self._sparse_in(g)
+        uh, k2 = self._sparse_in(gu)
+        dims = np.zeros(g.rows, np.int64)
+        err = C.create_string_buffer(512)
+        code = {"nm_H": 0, "nm_L": 1, "nm_H_rot": 2}[what]
+        try:
+            out = self.lib.ref_nm_op(code, gamma, gh, uh, int(pauli_y), _p(dims, _i64p), err, 512)
+            if not out:
+                raise OracleError(1, err.value.decode())
+            res = self._sparse_out(C.c_void_p(out))
+            self.lib.ref_sparse_free(C.c_void_p(out))
+            return res, dims
+        finally:
+            self._sparse_free(gh)
+            self._sparse_free(uh)
 
     # -------------------------------------------------------- liouvillian
     def build_local(self, omega, h, m_l, sources=(), sinks=(), workers=1):

@@ -162,6 +162,30 @@ void* ref_graph_op(int what, double gamma, void* adj, char* err, int errlen) {
   }
 }
 
+// Demoralisation operators (operators.hpp:59-83): what 0 nm_H(gamma, gu, V),
+// 1 nm_L(gamma, g, V), 2 nm_H_rot(V, dim2), with V = nm_vsets(gu); dims_out
+// (vertex count entries) receives V.dims.
+void* ref_nm_op(int what, double gamma, void* g, void* gu, int pauli_y, std::int64_t* dims_out, char* err,
+                int errlen) {
+  try {
+    const auto G = qsw::WeightedDigraph::from_adjacency(*static_cast<SparseMatrix*>(g));
+    const auto GU = qsw::WeightedDigraph::from_adjacency(*static_cast<SparseMatrix*>(gu));
+    const qsw::VertexSubspaces v = qsw::nm_vsets(GU);
+    for (std::size_t i = 0; i < v.dims.size(); ++i) dims_out[i] = static_cast<std::int64_t>(v.dims[i]);
+    switch (what) {
+      case 0: return new SparseMatrix(qsw::nm_H(gamma, GU, v));
+      case 1: return new SparseMatrix(qsw::nm_L(gamma, G, v));
+      case 2:
+        return new SparseMatrix(
+            qsw::nm_H_rot(v, pauli_y ? qsw::Dim2Rotation::PauliY : qsw::Dim2Rotation::Cancel));
+      default: set_err(err, errlen, "unknown op"); return nullptr;
+    }
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return nullptr;
+  }
+}
+
 // ---- superoperator --------------------------------------------------------
 void* ref_build_local(double omega, void* h, void* m_l, std::int64_t nsrc,
                       const std::int64_t* src_target, const double* src_rate,

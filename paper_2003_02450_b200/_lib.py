@@ -107,6 +107,12 @@ SIGNATURES = {
     "qswg_markov_chain_matrix": (C.c_int, [vp, C.POINTER(vp)]),
     "qswg_local_lindblad": (C.c_int, [vp, C.POINTER(vp)]),
     "qswg_augment": (C.c_int, [vp, C.POINTER(SourceArc), i64, C.POINTER(SinkArc), i64, C.POINTER(vp)]),
+    "qswg_nm_vsets": (C.c_int, [vp, i64p]),
+    "qswg_nm_H": (C.c_int, [C.c_double, vp, i64p, i64, C.POINTER(vp)]),
+    "qswg_nm_L": (C.c_int, [C.c_double, vp, i64p, i64, C.POINTER(vp)]),
+    "qswg_nm_H_rot": (C.c_int, [i64p, i64, C.c_int, C.POINTER(vp)]),
+    "qswg_nm_rho_map": (C.c_int, [dp, i64p, i64, dp]),
+    "qswg_nm_measure": (C.c_int, [dp, i64p, i64, dp]),
     "qswg_build_local": (C.c_int, [C.c_double, vp, vp, C.POINTER(SourceArc), i64, C.POINTER(SinkArc), i64,
                                    C.POINTER(DeviceConfig), C.POINTER(vp)]),
     "qswg_build_global": (C.c_int, [C.c_double, vp, C.POINTER(vp), i64, vp, C.POINTER(DeviceConfig),

@@ -148,6 +148,46 @@ def augment(adjacency, sources=(), sinks=()) -> SparseMatrix:  # graph.hpp:93-95
     return _unary(lib.qswg_augment, SparseMatrix.of(adjacency), src, len(sources), snk, len(sinks))
 
 
+# ------------------------------------------------- demoralisation (NM-G-QSW)
+def nm_vsets(gu) -> np.ndarray:
+    """Subspace dimension per vertex of the symmetric graph gu (operators.hpp:59-60)."""
+    m = SparseMatrix.of(gu)
+    dims = np.zeros(m.shape[0], np.int64)
+    check(lib.qswg_nm_vsets(m._h, _i64p(dims)))
+    return dims
+
+
+def nm_H(gamma, gu, dims) -> SparseMatrix:  # operators.hpp:66-68
+    d = np.ascontiguousarray(dims, np.int64)
+    return _unary(lib.qswg_nm_H, C.c_double(gamma), SparseMatrix.of(gu), _i64p(d), len(d))
+
+
+def nm_L(gamma, g, dims) -> SparseMatrix:  # operators.hpp:70-75
+    d = np.ascontiguousarray(dims, np.int64)
+    return _unary(lib.qswg_nm_L, C.c_double(gamma), SparseMatrix.of(g), _i64p(d), len(d))
+
+
+def nm_H_rot(dims, pauli_y: bool = False) -> SparseMatrix:  # operators.hpp:77-79
+    d = np.ascontiguousarray(dims, np.int64)
+    return _unary(lib.qswg_nm_H_rot, _i64p(d), len(d), int(pauli_y))
+
+
+def nm_rho_map(p, dims) -> np.ndarray:  # operators.hpp:80-81
+    d = np.ascontiguousarray(dims, np.int64)
+    p = np.ascontiguousarray(p, np.float64)
+    out = np.zeros(int(d.sum()))
+    check(lib.qswg_nm_rho_map(_dp(p), _i64p(d), len(d), _dp(out)))
+    return out
+
+
+def nm_measure(diag, dims) -> np.ndarray:  # operators.hpp:82-83
+    d = np.ascontiguousarray(dims, np.int64)
+    diag = np.ascontiguousarray(diag, np.float64)
+    out = np.zeros(len(d))
+    check(lib.qswg_nm_measure(_dp(diag), _i64p(d), len(d), _dp(out)))
+    return out
+
+
 # ----------------------------------------------------------- Liouvillian
 class Liouvillian:
     """Device superoperator (DistributedLiouvillian, liouvillian.hpp:21-63)."""
@@ -432,11 +472,18 @@ class WalkSystem:
         return w
 
     @staticmethod
-    def gqsw(omega, h, lindblads, h_rot=None, device=0, group=0, comm=None) -> "WalkSystem":
+    def gqsw(omega, h, lindblads, h_rot=None, vsets=None, device=0, group=0, comm=None) -> "WalkSystem":
+        """Pass both h_rot and vsets (subspace dims) for the non-moralising
+        walk, neither for the plain one (walk.hpp:43-48)."""
+        if (h_rot is None) != (vsets is None):
+            raise ValueError("non-moralising walks need both the rotating Hamiltonian and the vertex subspaces")
         w = WalkSystem()
         w.kind, w._omega = "global", float(omega)
         w._h, w._ops, w._src, w._snk = SparseMatrix.of(h), [SparseMatrix.of(x) for x in lindblads], [], []
         w._h_rot = SparseMatrix.of(h_rot) if h_rot is not None else None
+        w._vsets = None if vsets is None else np.asarray(vsets, np.int64)
+        if w._vsets is not None and int(w._vsets.sum()) != w._h.shape[0]:
+            raise ValueError("vertex subspaces do not match the operator dimension")
         w._dev = (device, group, comm)
         w._rebuild()
         return w
@@ -450,6 +497,10 @@ class WalkSystem:
 
     omega = property(lambda self: self._omega)
     dimension = property(lambda self: self.liouvillian.n)
+    _vsets = None
+
+    def measured_vertex_count(self) -> int:  # walk.hpp:55
+        return len(self._vsets) if self._vsets is not None else self.liouvillian.n
 
     def initial_state(self, rho):
         """Probabilities (walk.cpp:101-126) or a dense Hermitian unit-trace rho (128-139)."""
@@ -458,6 +509,8 @@ class WalkSystem:
         s = StateVector(self.liouvillian)
         if rho.ndim == 1:
             p = rho.astype(np.float64)
+            if self._vsets is not None and len(p) == len(self._vsets):
+                p = nm_rho_map(p, self._vsets)  # walk.cpp:103-105
             if self.kind == "local" and len(p) < n and len(p) == n - len(self._src) - len(self._snk):
                 p = np.concatenate([p, np.zeros(n - len(p))])
             s.from_probabilities(p)
@@ -492,6 +545,8 @@ class WalkSystem:
             raise LogicError("no initial state: call initial_state first")
         r = series(self.liouvillian, self._initial, t1, tq, steps, tolerance, True, states, True)
         self._result = r.final
+        if self._vsets is not None:
+            r.populations = np.stack([nm_measure(p, self._vsets) for p in r.populations])
         return r
 
     def _current(self):
@@ -506,7 +561,10 @@ class WalkSystem:
         return self._current().gather().reshape(n, n).T  # unvec (state.cpp:37-44)
 
     def gather_populations(self) -> np.ndarray:
-        return self._current().populations()
+        return self.populations_of(self._current())
 
     def populations_of(self, state: StateVector) -> np.ndarray:
-        return state.populations()
+        """Vertex populations; NM walks are folded back onto the original
+        vertices (walk.cpp:177-186)."""
+        p = state.populations()
+        return nm_measure(p, self._vsets) if self._vsets is not None else p

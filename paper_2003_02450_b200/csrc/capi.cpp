@@ -17,6 +17,7 @@
 #include "host/expm.hpp"
 #include "host/graph.hpp"
 #include "host/liouvillian.hpp"
+#include "host/nm.hpp"
 #include "host/sparse.hpp"
 #include "host/taylor.hpp"
 
@@ -220,6 +221,67 @@ int qswg_augment(const qswg_sparse* a, const qswg_source_arc* sources, int64_t n
     for (int64_t k = 0; k < n_sources; ++k) src.push_back({sources[k].target, sources[k].rate});
     for (int64_t k = 0; k < n_sinks; ++k) snk.push_back({sinks[k].origin, sinks[k].rate});
     *out = wrap(qswg::augment(a->m, src, snk));
+  });
+}
+
+// ------------------------------------------------------- demoralisation
+namespace {
+qswg::VertexSubspaces vsets_of(const int64_t* dims, int64_t nv) {
+  need(dims, "dims");
+  if (nv < 0) throw std::invalid_argument("negative vertex count");
+  return qswg::VertexSubspaces::from_dims(std::vector<std::int64_t>(dims, dims + nv));
+}
+}  // namespace
+
+int qswg_nm_vsets(const qswg_sparse* gu, int64_t* dims) {
+  return guarded([&] {
+    need(gu, "gu");
+    need(dims, "dims");
+    const auto v = qswg::nm_vsets(gu->m);
+    std::memcpy(dims, v.dims.data(), v.dims.size() * sizeof(int64_t));
+  });
+}
+
+int qswg_nm_H(double gamma, const qswg_sparse* gu, const int64_t* dims, int64_t nv, qswg_sparse** out) {
+  return guarded([&] {
+    need(gu, "gu");
+    need(out, "out");
+    *out = wrap(qswg::nm_H(gamma, gu->m, vsets_of(dims, nv)));
+  });
+}
+
+int qswg_nm_L(double gamma, const qswg_sparse* g, const int64_t* dims, int64_t nv, qswg_sparse** out) {
+  return guarded([&] {
+    need(g, "g");
+    need(out, "out");
+    *out = wrap(qswg::nm_L(gamma, g->m, vsets_of(dims, nv)));
+  });
+}
+
+int qswg_nm_H_rot(const int64_t* dims, int64_t nv, int pauli_y, qswg_sparse** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = wrap(qswg::nm_H_rot(vsets_of(dims, nv), pauli_y ? qswg::Dim2Rotation::PauliY : qswg::Dim2Rotation::Cancel));
+  });
+}
+
+int qswg_nm_rho_map(const double* p, const int64_t* dims, int64_t nv, double* expanded) {
+  return guarded([&] {
+    need(p, "p");
+    need(expanded, "expanded");
+    const auto v = vsets_of(dims, nv);
+    const auto e = qswg::nm_rho_map(std::vector<double>(p, p + nv), v);
+    std::memcpy(expanded, e.data(), e.size() * sizeof(double));
+  });
+}
+
+int qswg_nm_measure(const double* diag, const int64_t* dims, int64_t nv, double* p) {
+  return guarded([&] {
+    need(diag, "diag");
+    need(p, "p");
+    const auto v = vsets_of(dims, nv);
+    const auto out = qswg::nm_measure(std::vector<double>(diag, diag + v.total_dim()), v);
+    std::memcpy(p, out.data(), out.size() * sizeof(double));
   });
 }
 

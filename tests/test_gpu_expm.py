@@ -289,3 +289,38 @@ def test_every_row_group_width_agrees(group):
     L = l.gather_full()
     want = L.to_dense() @ x
     assert np.abs(l.spmv(x) - want).max() <= 1e-13 * max(1, np.abs(want).max())
+
+
+def _walkthrough_nm(omega, **kw):  # test_walk.cpp:33-39
+    g3 = Csr.from_coo(3, 3, [2, 2], [0, 1], [1.0, 1.0])
+    gu = api.symmetrize(g3)
+    dims = api.nm_vsets(gu)
+    w = api.WalkSystem.gqsw(omega, api.nm_H(1.0, gu, dims), [api.nm_L(1.0, g3, dims)], api.nm_H_rot(dims),
+                            dims, **kw)
+    w.initial_state([1.0, 0.0, 0.0])
+    return w
+
+
+@pytest.mark.parametrize("fmt", ["kron", "csr"])
+def test_demoralised_walk_reaches_the_child(fmt):  # test_walk.cpp:53-64
+    w = _walkthrough_nm(1.0, group=1 if fmt == "csr" else 0)
+    w.step(100.0)
+    p = w.gather_populations()
+    assert len(p) == 3
+    assert p[2] >= 1.0 - 1e-10
+    assert abs(p[0]) <= 1e-12 and abs(p[1]) <= 1e-12
+
+
+def test_demoralised_coherent_limit_matches_lqsw():  # test_walk.cpp:66-84
+    nm = _walkthrough_nm(0.0)
+    nm.step(100.0)
+    p_nm = nm.gather_populations()
+    np.testing.assert_allclose(p_nm, [3.80773381e-07, 9.98766244e-01, 1.23337485e-03], rtol=1e-5)
+    g3 = Csr.from_coo(3, 3, [2, 2], [0, 1], [1.0, 1.0])
+    lq = api.WalkSystem.lqsw(0.0, api.symmetrize(g3), g3)
+    lq.initial_state([1.0, 0.0, 0.0])
+    lq.step(100.0)
+    assert np.abs(p_nm - lq.gather_populations()).max() <= 1e-9
+    r = _walkthrough_nm(0.5).series(0.0, 10.0, 5)
+    assert r.populations.shape == (6, 3)
+    np.testing.assert_allclose(r.populations.sum(axis=1), 1.0, atol=1e-12)

@@ -17,7 +17,7 @@ from paper_2003_02450_b200 import _lib, graphs  # noqa: E402
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "qswg.h")).read()
-    return sorted(set(re.findall(r"\b(qswg_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(qswg_[A-Za-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol():
@@ -91,3 +91,30 @@ def test_device_entry_points_fail_loudly_without_gpu():
     w = graphs.config("c1", size=8)
     with pytest.raises(_lib.CudaError):
         api.build_local(w.omega, w.h, w.ops[0])
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_nm_operators_bit_identical_to_reference(k):
+    """operators.cpp nm_vsets / nm_H / nm_L / nm_H_rot against the reference."""
+    z = np.load(os.path.join(GOLDEN, "nm_ops.npz"))
+    g = load_csr(z, f"g{k}")
+    gamma = 1.0 if k == 0 else 0.7
+    gu = api.symmetrize(g)
+    dims = api.nm_vsets(gu)
+    assert np.array_equal(dims, z[f"g{k}_dims"])
+    for name, got in (("nm_H", api.nm_H(gamma, gu, dims)), ("nm_L", api.nm_L(gamma, g, dims)),
+                      ("nm_H_rot", api.nm_H_rot(dims)), ("nm_H_rot_py", api.nm_H_rot(dims, pauli_y=True))):
+        got, want = got.to_csr(), load_csr(z, f"g{k}_{name}")
+        assert np.array_equal(got.indptr, want.indptr) and np.array_equal(got.indices, want.indices), name
+        assert np.array_equal(got.data, want.data), name
+
+
+def test_nm_rho_map_and_measure():
+    dims = np.array([1, 1, 2])
+    e = api.nm_rho_map([0.5, 0.25, 0.25], dims)
+    assert list(e) == [0.5, 0.25, 0.125, 0.125]
+    assert list(api.nm_measure(e, dims)) == [0.5, 0.25, 0.25]
+    with pytest.raises(ValueError):
+        api.nm_rho_map([0.5, 0.5, 0.5], dims)
+    with pytest.raises(ValueError):
+        api.nm_vsets(graphs.Csr.from_coo(3, 3, [2], [0], [1.0]))  # not symmetric
