@@ -629,6 +629,19 @@ __device__ __forceinline__ double2 kron_row(const KronView& m, const double2* __
 #pragma unroll 4
     for (int e = __ldg(p.ptr + j); e < e1; ++e)
       cfma(acc, __ldg(p.val + e), ld_gather(wi + static_cast<long long>(__ldg(p.col + e)) * n, xpol));
+    if (m.factored) {
+      const KronList& r = m.r[k];  // -w/2 L'(L X): column j of W_k
+      const int r1 = __ldg(r.ptr + i + 1);
+      const double2* wj = m.w[k] + j * n;
+#pragma unroll 4
+      for (int e = __ldg(r.ptr + i); e < r1; ++e) cfma(acc, __ldg(r.val + e), ld_gather(wj + __ldg(r.col + e), xpol));
+      const KronList& sk = m.s[k];  // -w/2 (X L') L: columns of V_k
+      const int s1 = __ldg(sk.ptr + j + 1);
+      const double2* vi = m.v[k] + i;
+#pragma unroll 4
+      for (int e = __ldg(sk.ptr + j); e < s1; ++e)
+        cfma(acc, __ldg(sk.val + e), ld_gather(vi + static_cast<long long>(__ldg(sk.col + e)) * n, xpol));
+    }
   }
   if (m.t.ptr && i == j) {  // transfer onto the diagonal
     const int e1 = __ldg(m.t.ptr + i + 1);
@@ -689,6 +702,24 @@ __global__ void __launch_bounds__(kThreads) kron_w_kernel(KronView m, const doub
       for (int e = __ldg(q.ptr + i); e < e1; ++e) cfma(acc, __ldg(q.val + e), ld_gather(xa + __ldg(q.col + e), xpol));
     }
     st_hint(m.w[k] + g, acc, xpol);
+  }
+}
+
+// V_k = X L_k' on the local columns: V_k(i, a) = sum_c conj(L_k(a, c)) X(i, c).
+__global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const double2* __restrict__ x, int k) {
+  const unsigned long long xpol = evict_last_policy();
+  const long long n = m.n;
+  const KronList& u = m.u[k];
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < m.rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long g = m.row0 + r;
+    const long long a = g / n, i = g - a * n;
+    double2 acc = make_double2(0.0, 0.0);
+    const int e1 = __ldg(u.ptr + a + 1);
+#pragma unroll 4
+    for (int e = __ldg(u.ptr + a); e < e1; ++e)
+      cfma(acc, __ldg(u.val + e), ld_gather(x + static_cast<long long>(__ldg(u.col + e)) * n + i, xpol));
+    st_hint(m.v[k] + g, acc, xpol);
   }
 }
 
@@ -1099,6 +1130,11 @@ void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
     const auto g = kron_geom(kron_w_kernel, m.kron);
     kron_w_kernel<<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
     QSWG_LAUNCH_CHECK("kron_prepare");
+    if (m.kron.factored) {
+      const auto gv = kron_geom(kron_v_kernel, m.kron);
+      kron_v_kernel<<<gv.first, kThreads, gv.second, s>>>(m.kron, x, k);
+      QSWG_LAUNCH_CHECK("kron_prepare");
+    }
   }
 }
 

@@ -100,8 +100,10 @@ struct Exec {
     if (m.format != dev::Format::Kron) return;
     dev::kron_prepare(m, x, s);
     if (!single)
-      for (int k = 0; k < m.kron.nk; ++k)
+      for (int k = 0; k < m.kron.nk; ++k) {
         comm->exchange_ranges(m.kron.w[k], l.w_halo_lo(), l.w_halo_hi(), sizeof(double2), s);
+        if (m.kron.factored) comm->exchange_ranges(m.kron.v[k], l.v_halo_lo(), l.v_halo_hi(), sizeof(double2), s);
+      }
   }
 
   template <class T>
@@ -137,7 +139,7 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
     ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
     dev::step_init_fin(ctl, s);
   }
-  launches += 1 + sp.s * sp.m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk : 0));
+  launches += 1 + sp.s * sp.m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0));
   const double s_count = static_cast<double>(sp.s);
   for (std::int64_t st = 0; st < sp.s; ++st) {
     // stage input: v, then the previous stage's sum (term = sum, expm.cpp:197-205)
@@ -239,7 +241,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
         ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
         dev::series_init_fin(ctl, static_cast<int>(count), s);
       }
-      info.launches += 1 + m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk : 0));
+      info.launches += 1 + m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0));
       dev::SeriesSums ss{};
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
       const double2* z_full = ex.spmv_input(z, kZFull);

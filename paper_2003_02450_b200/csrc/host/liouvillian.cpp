@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -126,6 +127,13 @@ struct HostOperands {
   std::vector<MultiCsr> p, q;
   std::vector<double> d_loc, d_ss;  // empty -> no decay term
   double omega = 0.0;
+  // Factored dissipator of G-QSW for the matrix-free path: A = af, B = bf
+  // (no L'L terms) and per Lindblad operator R_k = -w/2 L_k' (gathers in the
+  // columns of W_k = L_k X), S_k = -w/2 L_k^T (streams the columns of
+  // V_k = X L_k'), U_k = conj(L_k) (builds V_k from the columns of X).
+  bool has_factored = false;
+  MultiCsr af, bf;
+  std::vector<MultiCsr> r, sfac, u;
 
   HostOperands transposed() const {
     HostOperands o;
@@ -146,7 +154,23 @@ struct HostOperands {
     o.a = canonical(a);
     o.b = canonical(b);
     o.t = canonical(t);
+    if (has_factored) {
+      o.af = canonical(af);
+      o.bf = canonical(bf);
+    }
     return o;
+  }
+
+  // Operand entries touched per output element (Kron kernels).
+  double kron_cost(bool factored) const {
+    const double nn = static_cast<double>(n);
+    auto e = [&](const MultiCsr& m) { return static_cast<double>(m.col.size()) / nn; };
+    double c = 0.0;
+    for (std::size_t k = 0; k < p.size(); ++k) c += e(p[k]) + e(q[k]);
+    if (!factored) return c + e(a) + e(b);
+    c += e(af) + e(bf);
+    for (std::size_t k = 0; k < r.size(); ++k) c += e(r[k]) + e(sfac[k]) + e(u[k]) + 2.0;  // + V_k pass
+    return c;
   }
 };
 
@@ -236,14 +260,29 @@ struct KronStore {
   // build (ELL wins on lattices and on c3, CSR on c4's 2-hop rows).
   static constexpr double kEllMaxPadding = 2.0;
   KronStore(const HostOperands& h, cudaStream_t s) : host(h.summed()), ops(host, s) {
-    a = maybe_ell(host.a, s);
+    // factor the L'L terms when that touches clearly fewer operand entries
+    factored = host.has_factored && host.kron_cost(true) < 0.8 * host.kron_cost(false);
+    if (const char* f = std::getenv("QSWG_KRON_FACTOR")) factored = host.has_factored && f[0] == '1';  // test knob
+    a = maybe_ell(factored ? host.af : host.a, s);
     for (const MultiCsr& qk : host.q) q.push_back(maybe_ell(qk, s));
+    if (factored) {
+      af = upload_list(host.af, s);
+      bf = upload_list(host.bf, s);
+      for (std::size_t k = 0; k < host.r.size(); ++k) {
+        r.push_back(upload_list(host.r[k], s));
+        sfac.push_back(upload_list(host.sfac[k], s));
+        u.push_back(upload_list(host.u[k], s));
+      }
+    }
     QSWG_CHECK(cudaStreamSynchronize(s));
   }
   HostOperands host;
   DeviceOperands ops;  // CSR lists (B, P, T; and A, Q for on-demand assembly)
   dev::KronEll a;
   std::vector<dev::KronEll> q;
+  bool factored = false;
+  dev::KronList af, bf;
+  std::vector<dev::KronList> r, sfac, u;
 
  private:
   dev::KronEll maybe_ell(const MultiCsr& m, cudaStream_t s) {
@@ -251,6 +290,14 @@ struct KronStore {
     EllHost e = to_ell(m);
     if (static_cast<double>(e.col.size()) > kEllMaxPadding * static_cast<double>(m.col.size())) return {};
     return upload_ell(e, s);
+  }
+  dev::KronList upload_list(const MultiCsr& m, cudaStream_t s) {
+    dev::KronList l;
+    if (m.col.empty()) return l;
+    l.ptr = up(m.ptr, s);
+    l.col = up(m.col, s);
+    l.val = up(m.val, s);
+    return l;
   }
   dev::KronEll upload_ell(const EllHost& e, cudaStream_t s) {
     dev::KronEll d;
@@ -338,14 +385,21 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.rows = block_.rows;
     m.kron.row0 = block_.row0;
     m.kron.a_ell = kron_ell_ ? kron_->a : dev::KronEll{};
-    m.kron.a = o.a;
-    m.kron.b = o.b;
+    m.kron.a = kron_->factored ? kron_->af : o.a;
+    m.kron.b = kron_->factored ? kron_->bf : o.b;
+    m.kron.factored = kron_->factored ? 1 : 0;
     m.kron.t = o.t;
     m.kron.nk = o.nk;
     for (int k = 0; k < o.nk; ++k) {
       m.kron.p[k] = o.p[k];
       m.kron.q_ell[k] = kron_ell_ ? kron_->q[static_cast<std::size_t>(k)] : dev::KronEll{};
       m.kron.q[k] = o.q[k];
+      if (kron_->factored) {
+        m.kron.r[k] = kron_->r[static_cast<std::size_t>(k)];
+        m.kron.s[k] = kron_->sfac[static_cast<std::size_t>(k)];
+        m.kron.u[k] = kron_->u[static_cast<std::size_t>(k)];
+        m.kron.v[k] = kron_v_[static_cast<std::size_t>(k)].get();
+      }
       m.kron.w[k] = kron_w_[static_cast<std::size_t>(k)].get();
     }
     m.kron.d_loc = o.d_loc;
@@ -505,15 +559,18 @@ namespace {
 // identical) operands: rank r reads X columns B(j, .) and T(j, .) and W_k
 // columns P_k(j, .) for its own rho columns j; each peer's share is sent as
 // the hull of whole columns.
-void kron_halos(const HostOperands& h, std::int64_t n, const std::vector<std::int64_t>& starts,
+void kron_halos(const HostOperands& h, bool factored, std::int64_t n, const std::vector<std::int64_t>& starts,
                 std::vector<std::vector<std::int64_t>>& lo, std::vector<std::vector<std::int64_t>>& hi,
-                std::vector<std::vector<std::int64_t>>& wlo, std::vector<std::vector<std::int64_t>>& whi) {
+                std::vector<std::vector<std::int64_t>>& wlo, std::vector<std::vector<std::int64_t>>& whi,
+                std::vector<std::vector<std::int64_t>>& vlo, std::vector<std::vector<std::int64_t>>& vhi) {
   const int world = static_cast<int>(starts.size()) - 1;
   const auto W = static_cast<std::size_t>(world);
   lo.assign(W, std::vector<std::int64_t>(W, 0));
   hi = lo;
   wlo = lo;
   whi = lo;
+  vlo = lo;
+  vhi = lo;
   if (world == 1) return;
   auto owner = [&](std::int64_t col) {
     int q = 0;
@@ -541,9 +598,13 @@ void kron_halos(const HostOperands& h, std::int64_t n, const std::vector<std::in
   };
   for (int r = 0; r < world; ++r) {
     for (std::int64_t j = starts[static_cast<std::size_t>(r)] / n; j < starts[static_cast<std::size_t>(r) + 1] / n; ++j) {
-      row_cols(h.b, j, [&](std::int64_t c) { add(lo, hi, r, c); });
+      row_cols(factored ? h.bf : h.b, j, [&](std::int64_t c) { add(lo, hi, r, c); });
       row_cols(h.t, j, [&](std::int64_t c) { add(lo, hi, r, c); });
       for (const MultiCsr& p : h.p) row_cols(p, j, [&](std::int64_t c) { add(wlo, whi, r, c); });
+      if (factored) {
+        for (const MultiCsr& u : h.u) row_cols(u, j, [&](std::int64_t c) { add(lo, hi, r, c); });  // V_k(:, j)
+        for (const MultiCsr& sk : h.sfac) row_cols(sk, j, [&](std::int64_t c) { add(vlo, vhi, r, c); });
+      }
     }
   }
 }
@@ -628,10 +689,15 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     for (std::size_t k = 0; k < hops.p.size(); ++k) {
       l->kron_w_.emplace_back(static_cast<std::size_t>(dim));
       QSWG_CHECK(cudaMemsetAsync(l->kron_w_.back().get(), 0, l->kron_w_.back().bytes(), s));
+      if (l->kron_->factored) {
+        l->kron_v_.emplace_back(static_cast<std::size_t>(dim));
+        QSWG_CHECK(cudaMemsetAsync(l->kron_v_.back().get(), 0, l->kron_v_.back().bytes(), s));
+      }
     }
     QSWG_CHECK(cudaStreamSynchronize(s));
     grp.reset();
-    kron_halos(l->kron_->host, n, l->starts_, l->halo_lo_, l->halo_hi_, l->whalo_lo_, l->whalo_hi_);
+    kron_halos(l->kron_->host, l->kron_->factored, n, l->starts_, l->halo_lo_, l->halo_hi_, l->whalo_lo_,
+               l->whalo_hi_, l->vhalo_lo_, l->vhalo_hi_);
     l->group_ = 32;
     // sliced-ELL vs CSR row-indexed operands: time both (local products only)
     bool has_ell = l->kron_->a.sptr != nullptr;
@@ -820,6 +886,16 @@ std::unique_ptr<Liouvillian> build_global(double omega, const SparseMatrix& h,
   if (h_rot && rot != Complex{}) {
     append_entries(ae, *h_rot, [&](Complex v) { return rot * v; });
     append_entries(be, h_rot->transpose(), [&](Complex v) { return -rot * v; });
+  }
+  o.af = make_multi(n, ae);  // coherent parts only (before the L'L terms)
+  o.bf = make_multi(n, be);
+  o.has_factored = omega != 0.0 && !lindblads.empty();
+  if (o.has_factored) {
+    for (const SparseMatrix& l : lindblads) {
+      o.r.push_back(from_sparse(l.conjugate_transpose(), [&](Complex v) { return -0.5 * omega * v; }));
+      o.sfac.push_back(from_sparse(l.transpose(), [&](Complex v) { return -0.5 * omega * v; }));
+      o.u.push_back(from_sparse(l, [](Complex v) { return std::conj(v); }));
+    }
   }
   if (omega != 0.0) {
     for (const SparseMatrix& l : lindblads) {

@@ -91,6 +91,8 @@ class Liouvillian {
   /// Kron format: halos of the W_k = Q_k X work vectors (same layout).
   const std::vector<std::vector<std::int64_t>>& w_halo_lo() const { return whalo_lo_; }
   const std::vector<std::vector<std::int64_t>>& w_halo_hi() const { return whalo_hi_; }
+  const std::vector<std::vector<std::int64_t>>& v_halo_lo() const { return vhalo_lo_; }
+  const std::vector<std::vector<std::int64_t>>& v_halo_hi() const { return vhalo_hi_; }
 
  private:
   Liouvillian() = default;
@@ -114,10 +116,10 @@ class Liouvillian {
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;
   std::vector<std::vector<std::int64_t>> halo_lo_, halo_hi_;
-  std::vector<std::vector<std::int64_t>> whalo_lo_, whalo_hi_;
+  std::vector<std::vector<std::int64_t>> whalo_lo_, whalo_hi_, vhalo_lo_, vhalo_hi_;
   std::shared_ptr<KronStore> kron_;
   mutable bool kron_ell_ = false;  // use the sliced-ELL copies of A / Q_k
-  std::vector<DeviceBuffer<double2>> kron_w_;
+  std::vector<DeviceBuffer<double2>> kron_w_, kron_v_;
   mutable Workspace ws_;
 };
 

@@ -100,6 +100,13 @@ struct KronView {
   KronList p[kMaxKron];      // indexed by j (warp-uniform)
   KronEll q_ell[kMaxKron];   // W_k = Q_k X, indexed by i
   KronList q[kMaxKron];
+  // Factored G-QSW dissipator (a, b then hold only the coherent parts):
+  //   + sum_b R_k(i,b) W_k(b,j)      R_k = -w/2 L_k'   (column j of W_k)
+  //   + sum_a S_k(j,a) V_k(i,a)      S_k = -w/2 L_k^T  (columns of V_k)
+  //   with V_k(:, a) = sum_c U_k(a,c) X(:, c),  U_k = conj(L_k).
+  int factored = 0;
+  KronList r[kMaxKron], s[kMaxKron], u[kMaxKron];
+  double2* v[kMaxKron] = {};
   const double* d_loc = nullptr;
   const double* d_ss = nullptr;
   double omega = 0.0;

@@ -82,3 +82,21 @@ def test_sharded_step_and_overflow(world):
     got = np.concatenate([p[1] for p in parts])
     assert np.abs(got - c.z["step_states"][0]).max() <= 1e-10
     assert parts[0][2] == c.z["step_spmvs"][0]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_kron_factored(world, monkeypatch):
+    monkeypatch.setenv("QSWG_KRON_FACTOR", "1")
+    c = Case("c4_n40")
+    t1, tq, q = c.series
+
+    def rank_fn(r, comm):
+        l = c.build_gpu(api, comm=comm, format="kron")
+        res = api.series(l, l.state().from_probabilities(c.rho0), t1, tq, int(q), states=True)
+        return l.row0, res.states, int(res.info.spmvs)
+
+    parts = sorted(run_ranks(world, rank_fn), key=lambda p: p[0])
+    states = np.concatenate([p[1] for p in parts], axis=1)
+    keep = c.z["series_keep"]
+    assert np.abs(states[keep] - c.z["series_states"]).max() <= 1e-10
+    assert parts[0][2] == c.series_spmvs

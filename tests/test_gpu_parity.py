@@ -124,3 +124,22 @@ def test_series_matches_oracle_live(port, name, size):
     assert r.info.spmvs == nref
     assert np.abs(r.states - so).max() <= RHO_TOL
     assert trace_err(r.states, w.n) <= TRACE_TOL
+
+
+@pytest.mark.parametrize("factor", ["0", "1"])
+@pytest.mark.parametrize("name", ["c2_n36", "c4_n40", "gqsw_multi_rot", "walkthrough_nm_w1", "walkthrough_gqsw"])
+def test_kron_factored_dissipator_matches_reference(name, factor, monkeypatch):
+    """G-QSW L'L terms applied as L'(L X) and (X L')L (QSWG_KRON_FACTOR
+    forces the choice the build otherwise makes from operand counts)."""
+    monkeypatch.setenv("QSWG_KRON_FACTOR", factor)
+    c = Case(name)
+    l = c.build_gpu(api, format="kron")
+    t1, tq, q = c.series
+    r = api.series(l, l.state().from_probabilities(c.rho0), t1, tq, int(q), states=True)
+    keep = c.z["series_keep"]
+    assert np.abs(r.states[keep] - c.z["series_states"]).max() <= RHO_TOL
+    assert trace_err(r.states, c.n) <= TRACE_TOL
+    if name.startswith("c"):
+        assert r.info.spmvs == c.series_spmvs
+    y = l.spmv(c.z["spmv_x"])
+    assert np.abs(y - c.z["spmv_y"]).max() <= 1e-13 * max(1.0, np.abs(c.z["spmv_y"]).max())
