@@ -285,8 +285,8 @@ def main():
     def term_bytes(lv):
         """Algorithmic HBM bytes of one series term with d_active outputs."""
         vec = 16 * lv.dim + 16 * lv.rows + 32 * d_active * lv.rows  # x read, K_p write, sums r+w
-        if lv.format == "kron":  # W_k = Q_k x written once and read once per term
-            return vec + 32 * n_lind * lv.dim
+        if lv.format == "kron":  # W_k = Q_k x (and V_k = x L_k' when factored): written + read once
+            return vec + 32 * n_lind * lv.dim * (2 if lv.info.kron_factored else 1)
         return vec + 20 * int(lv.info.nnz_local) + 8 * (lv.rows + 1)
 
     term_ms = l.time_series_term(iters=20, count=d_active)
@@ -327,7 +327,7 @@ def main():
         "data": "synthetic (seeded graph of BASELINE.json config; no public dataset exists for this path)",
         "config": workload_desc(w, {
             "parallelism": f"row-block x{world}" if world > 1 else "1 GPU", "nnz": int(l.nnz),
-            "format": l.format,
+            "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell),
             "build_norms_s": build_s, "one_norms": l.one_norms().tolist(), "group": int(l.group),
             "plan": {"path": int(info.path), "span": [int(info.span_m_star), int(info.span_s)],
                      "d": int(info.d), "n_super": int(info.n_super), "remainder": int(info.remainder),
@@ -335,7 +335,7 @@ def main():
             "spmvs_per_step": int(info.spmvs)}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_for(w.name, l.format), "kernel": kernel_name,
-                     "format": l.format, "bytes_per_launch": term_bytes(l), "ms_per_launch": term_ms,
+                     "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell), "bytes_per_launch": term_bytes(l), "ms_per_launch": term_ms,
                      "peak_source": peak_src, "share_of_step": share},
         "superop_spmv": superop,
         "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,

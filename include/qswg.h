@@ -69,6 +69,8 @@ typedef struct {
   int group, device, rank, world;
   int format;     /* QSWG_FORMAT_CSR, QSWG_FORMAT_SELL or QSWG_FORMAT_KRON */
   double padding; /* stored entries / nnz_local */
+  int kron_factored; /* KRON: G-QSW L'L terms applied in factored form */
+  int kron_ell;      /* KRON: row-indexed operands read in sliced ELL */
 } qswg_liouvillian_info;
 
 typedef struct { int64_t m_star, s, spmvs, launches; } qswg_step_info;

@@ -347,6 +347,8 @@ int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* inf
                    : L.format() == qswg::dev::Format::Kron ? QSWG_FORMAT_KRON
                                                            : QSWG_FORMAT_CSR;
     info->padding = L.padding();
+    info->kron_factored = L.kron_factored() ? 1 : 0;
+    info->kron_ell = L.kron_ell() ? 1 : 0;
   });
 }
 

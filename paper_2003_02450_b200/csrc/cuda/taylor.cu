@@ -585,6 +585,10 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
 }
 
 // ------------------------------------------------------------ Kron path
+#ifndef QSWG_KRON_MIN_BLOCKS
+#define QSWG_KRON_MIN_BLOCKS 4  // <= 64 registers: 4 resident blocks of 256 threads per SM
+#endif
+
 // Matrix-free action (kernels.hpp: KronView).  One thread per output row
 // r = n*j + i; consecutive threads share the rho column j, so the B (x) I
 // and P (x) Q parts stream coalesced columns of X and W_k, and the I (x) A
@@ -743,7 +747,7 @@ struct KronStepArgs {
   int decide;
 };
 
-__global__ void __launch_bounds__(kThreads) kron_step_term_kernel(KronStepArgs a) {
+__global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term_kernel(KronStepArgs a) {
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
   if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
@@ -777,7 +781,7 @@ __global__ void __launch_bounds__(kThreads) kron_step_term_kernel(KronStepArgs a
   }
 }
 
-__global__ void __launch_bounds__(kThreads) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
+__global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
   SeriesCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
   __shared__ unsigned long long red[32];

@@ -368,6 +368,8 @@ void fill_block(const dev::KronOperands& ops, const DeviceBuffer<std::int64_t>& 
                 std::int64_t& nnz, cudaStream_t s);
 }  // namespace
 
+bool Liouvillian::kron_factored() const { return kron_ != nullptr && kron_->factored; }
+
 dev::DevMatrix Liouvillian::matrix(int group_override) const {
   dev::DevMatrix m;
   m.format = format_;

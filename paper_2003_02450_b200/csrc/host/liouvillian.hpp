@@ -75,6 +75,8 @@ class Liouvillian {
   dev::Format format() const { return format_; }
   /// Stored entries / nnz (SELL padding; 1.0 for CSR).
   double padding() const { return padding_; }
+  bool kron_factored() const;
+  bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
 
   /// Local row block downloaded as CSR with global columns (parity / debug).
   void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
