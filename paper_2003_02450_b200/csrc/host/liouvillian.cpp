@@ -706,9 +706,13 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     for (const auto& q : l->kron_->q) has_ell = has_ell || q.sptr != nullptr;
     l->kron_ell_ = has_ell;
     if (has_ell && dim >= (1 << 16)) {
-      const double t_ell = l->time_spmv(3, 32);
-      l->kron_ell_ = false;
-      const double t_csr = l->time_spmv(3, 32);
+      double t_ell = 1e300, t_csr = 1e300;
+      for (int rep = 0; rep < 2; ++rep) {  // interleaved, best of two
+        l->kron_ell_ = true;
+        t_ell = std::min(t_ell, l->time_spmv(4, 32));
+        l->kron_ell_ = false;
+        t_csr = std::min(t_csr, l->time_spmv(4, 32));
+      }
       l->kron_ell_ = t_ell <= t_csr;
     }
     return l;
