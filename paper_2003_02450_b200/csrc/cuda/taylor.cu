@@ -205,15 +205,60 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
 }
 
 // ------------------------------------------------------------- series term
-// Per-k stop tests after term p (expm.cpp:298-316, evaluated p-major): run
-// by one thread of the last block to arrive.
-__device__ void series_control(SeriesCtl* ctl, int count, double tol) {
+// Stop tests of the super-step terms (expm.cpp:298-316, evaluated p-major)
+// with deferred running sums (kernels.hpp: SeriesCtl).  Both controls run on
+// one thread of the last block to arrive (or in a 1-thread kernel after the
+// multi-GPU allreduce).
+//
+// After term p: c2_k = k^p ||K_p||.  The exact test c1_k + c2_k <= tol ||S_k||
+// is settled without S_k when c1_k + c2_k > tol * ub_k, where
+//   ub_k = (||S_k at the last flush|| + sum of the pending k^q ||K_q||) (1 + 2^-30)
+// is computed with upward rounding: ||S_k|| <= ub_k holds through every
+// rounding of the pending axpys and norms (each at most (1 + 2^-53)), so the
+// settled outcome "continue" is the one the exact test would give.
+__device__ void series_term_control(SeriesCtl* ctl, int last, double tol) {
   ctl->spmvs += 1;
   const double tn = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
-  if (!isfinite(tn)) ctl->error = 1;  // expm.cpp:293-295
+  ctl->term_bits = 0;
+  ctl->arrivals = 0;
+  if (!isfinite(tn)) {  // expm.cpp:293-295
+    ctl->error = 1;
+    ctl->n_active = 0;
+    return;
+  }
+  const int b = ctl->n_pend;
+  const int count = ctl->count;
+  ctl->tn_last = tn;
+  int need = last || b + 1 >= ctl->pend_max;
   for (int k = 0; k < count; ++k) {
     if (!ctl->active[k]) continue;
     const double f = ctl->factor[k];
+    ctl->fac_pend[b][k] = f;
+    ctl->bound[k] = __dadd_ru(ctl->bound[k], __dmul_ru(f, tn));
+    const double ub = __dmul_ru(__dadd_ru(ctl->nf_last[k], ctl->bound[k]), 1.0 + 0x1p-30);
+    if (!(ctl->c1[k] + f * tn > tol * ub)) need = 1;  // expm.cpp:310, 315
+  }
+  ctl->n_pend = b + 1;
+  if (need) {
+    ctl->flush = 1;  // the flush control runs the exact tests of term p
+    return;
+  }
+  for (int k = 0; k < count; ++k) {
+    if (!ctl->active[k]) continue;
+    const double f = ctl->factor[k];
+    ctl->c1[k] = f * tn;                         // every test settled: continue
+    ctl->factor[k] = f * static_cast<double>(k + 1);  // factor *= k for p + 1
+  }
+}
+
+// Exact tests of the newest pending term after the flush wrote every S_k.
+__device__ void series_flush_control(SeriesCtl* ctl, double tol) {
+  const int b = ctl->n_pend - 1;
+  const int count = ctl->count;
+  const double tn = ctl->tn_last;
+  for (int k = 0; k < count; ++k) {
+    if (!ctl->active[k]) continue;
+    const double f = ctl->fac_pend[b][k];
     const double c2 = f * tn;  // expm.cpp:310
     const double nf = bitsd(*(volatile unsigned long long*)&ctl->sum_bits[k]);
     if (!isfinite(nf)) {  // expm.cpp:312-314
@@ -224,156 +269,135 @@ __device__ void series_control(SeriesCtl* ctl, int count, double tol) {
     } else {
       ctl->c1[k] = c2;
     }
-    ctl->factor[k] = f * static_cast<double>(k + 1);  // factor *= k for p + 1
+    ctl->factor[k] = f * static_cast<double>(k + 1);
+    ctl->nf_last[k] = nf;
+    ctl->bound[k] = 0.0;
     ctl->sum_bits[k] = 0;
   }
   if (ctl->error) ctl->n_active = 0;
-  ctl->term_bits = 0;
+  ctl->n_pend = 0;
+  ctl->flush = 0;
+  ctl->fresh = 0;
   ctl->arrivals = 0;
 }
 
 struct SeriesTermArgs {
-  CsrView l;
   const double2* x;
   double2* kp;
-  const double2* z;
-  SeriesSums sums;
-  int count;
-  int p;
+  int last;
   double scale;
   double tol;
   SeriesCtl* ctl;
   int decide;
 };
 
-template <int G>
-__global__ void __launch_bounds__(kThreads) series_term_kernel(SeriesTermArgs a) {
-  SeriesCtl* ctl = a.ctl;
-  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
-  __shared__ unsigned long long red[32];
-  __shared__ double fac[kMaxSeriesD];
-  __shared__ int act[kMaxSeriesD];
-  __shared__ unsigned long long smax_sh[kMaxSeriesD];
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
-    fac[k] = ctl->factor[k];
-    act[k] = ctl->active[k];
-    smax_sh[k] = 0;
-  }
-  __syncthreads();
-  unsigned long long tmax = 0;
-  const bool first = a.p == 1;
-  const int lane = threadIdx.x & 31;
-  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  tile_loop<G>(a.l, a.x, [&](long long row, double2 acc, bool valid) {
-    // K_p = (h/p) L K_{p-1}  (expm.cpp:286-287)
-    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
-    if (valid) {
-      st_hint(a.kp + row, kv, keep);  // next term's SpMV input
-      tmax = umax64(tmax, dbits(cabs2(kv)));
-    }
-    const double2 zv = (first && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
-    // sum_k += k^p K_p for every active output k (expm.cpp:300-305), in
-    // chunks of kSeriesRegD with all loads of a chunk in flight together.
-#pragma unroll 1
-    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
-      double2 sv[kSeriesRegD];
-#pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
-      }
-#pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (k >= a.count) break;  // warp-uniform
-        unsigned long long m = 0;
-        if (valid && act[k]) {
-          sv[u] = axpy<G>(sv[u], fac[k], kv);
-          st_hint(a.sums.s[k] + row, sv[u], once);
-          m = dbits(cabs2(sv[u]));
-        }
-        m = warp_max_bits(m);
-        if (lane == 0 && m) atomicMax(&smax_sh[k], m);
-      }
-    }
-  });
+__device__ __forceinline__ bool series_skip(const SeriesCtl* ctl) {
+  return *(volatile const int*)&ctl->error || *(volatile const int*)&ctl->n_active == 0;
+}
+
+// Term-kernel epilogue of one row: K_p = (h/p) L K_{p-1} (expm.cpp:286-287),
+// kept in L2 for the next term's gathers and the flush.
+__device__ __forceinline__ void series_store(double2* kp, double scale, long long row, double2 acc, bool valid,
+                                             unsigned long long keep, unsigned long long& tmax) {
+  if (!valid) return;
+  const double2 kv = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
+  st_hint(kp + row, kv, keep);
+  tmax = umax64(tmax, dbits(cabs2(kv)));
+}
+
+// Grid-wide ||K_p|| and the term control (last block).
+__device__ __forceinline__ void series_term_finish(const SeriesTermArgs& a, unsigned long long tmax,
+                                                   unsigned long long* red) {
   tmax = block_max_bits(tmax, red);
-  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
-  __syncthreads();
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
-    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
-  __syncthreads();
   if (threadIdx.x == 0) {
+    SeriesCtl* ctl = a.ctl;
+    atomicMax(&ctl->term_bits, tmax);
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
       if (a.decide) {
-        series_control(ctl, a.count, a.tol);
+        series_term_control(ctl, a.last, a.tol);
       } else {
-        ctl->arrivals = 0;
+        ctl->arrivals = 0;  // maximum stays for the allreduce + series_term_control_kernel
       }
     }
   }
 }
 
-// Split variant of series_term: the SpMV kernel writes K_p and its norm,
-// a streaming kernel then updates every active running sum.  Costs one
-// extra read of K_p but keeps the SpMV's memory-level parallelism free of
-// the sum traffic (selected at runtime, see series_term()).
 template <int G>
-__global__ void __launch_bounds__(kThreads) series_spmv_kernel(SeriesTermArgs a) {
-  SeriesCtl* ctl = a.ctl;
-  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+__global__ void __launch_bounds__(kThreads) series_term_kernel(SeriesTermArgs a, CsrView l) {
+  if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0;
   const unsigned long long keep = evict_last_policy();
-  tile_loop<G>(a.l, a.x, [&](long long row, double2 acc, bool valid) {
-    if (!valid) return;
-    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
-    st_hint(a.kp + row, kv, keep);
-    tmax = umax64(tmax, dbits(cabs2(kv)));
-  });
-  tmax = block_max_bits(tmax, red);
-  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
+  double2* const kp = a.kp;
+  const double scale = a.scale;
+  tile_loop<G>(l, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  series_term_finish(a, tmax, red);
 }
 
-template <int G>
-__global__ void __launch_bounds__(kThreads) series_axpy_kernel(SeriesTermArgs a) {
+struct SeriesFlushArgs {
+  SeriesRing ring;
+  long long row0, rows;
+  const double2* z;
+  SeriesSums sums;
+  int p;
+  double tol;
+  SeriesCtl* ctl;
+  int decide;
+};
+
+// Batched running-sum update (kernels.hpp: series_flush).  Each thread keeps
+// its row of every pending term in registers and walks the active outputs in
+// chunks of kSeriesRegD with all sum loads of a chunk in flight; the order of
+// the additions per output is the term order, as in per-term updates.
+template <bool kStrict>
+__global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs a) {
   SeriesCtl* ctl = a.ctl;
-  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
-  __shared__ double fac[kMaxSeriesD];
+  if (!*(volatile int*)&ctl->flush || series_skip(ctl)) return;
+  __shared__ double fac[kPendMax][kMaxSeriesD];
   __shared__ int act[kMaxSeriesD];
   __shared__ unsigned long long smax_sh[kMaxSeriesD];
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
-    fac[k] = ctl->factor[k];
+  __shared__ const double2* kptr[kPendMax];
+  const int nb = ctl->n_pend, count = ctl->count, fresh = ctl->fresh;
+  for (int k = threadIdx.x; k < count; k += blockDim.x) {
     act[k] = ctl->active[k];
     smax_sh[k] = 0;
+    for (int b = 0; b < nb; ++b) fac[b][k] = ctl->fac_pend[b][k];
+  }
+  if (threadIdx.x < nb) {
+    const int slot = (a.p - nb + 1 + static_cast<int>(threadIdx.x)) % a.ring.slots;
+    kptr[threadIdx.x] = a.ring.k[slot] + a.row0;
   }
   __syncthreads();
-  const bool first = a.p == 1;
   const int lane = threadIdx.x & 31;
   const unsigned long long once = evict_first_policy();
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.l.rows; base += stride) {
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.rows; base += stride) {
     const long long row = base + threadIdx.x;
-    const bool valid = row < a.l.rows;
-    const double2 kv = valid ? __ldg(a.kp + row) : make_double2(0.0, 0.0);
-    const double2 zv = (first && valid) ? __ldg(a.z + row) : make_double2(0.0, 0.0);
+    const bool valid = row < a.rows;
+    double2 kv[kPendMax];
+#pragma unroll
+    for (int b = 0; b < kPendMax; ++b)
+      kv[b] = (valid && b < nb) ? ld_once(kptr[b] + row, once) : make_double2(0.0, 0.0);
+    const double2 zv = (fresh && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
 #pragma unroll 1
-    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
+    for (int k0 = 0; k0 < count; k0 += kSeriesRegD) {
       double2 sv[kSeriesRegD];
 #pragma unroll
       for (int u = 0; u < kSeriesRegD; ++u) {
         const int k = k0 + u;
-        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
+        if (valid && k < count && act[k]) sv[u] = fresh ? zv : ld_once(a.sums.s[k] + row, once);
       }
 #pragma unroll
       for (int u = 0; u < kSeriesRegD; ++u) {
         const int k = k0 + u;
-        if (k >= a.count) break;
+        if (k >= count) break;  // block-uniform
         unsigned long long m = 0;
         if (valid && act[k]) {
-          sv[u] = axpy<G>(sv[u], fac[k], kv);  // sum += k^p K_p (expm.cpp:300-305)
+#pragma unroll
+          for (int b = 0; b < kPendMax; ++b)  // sum += k^q K_q (expm.cpp:300-305)
+            if (b < nb) sv[u] = kStrict ? axpy<1>(sv[u], fac[b][k], kv[b]) : axpy<2>(sv[u], fac[b][k], kv[b]);
           st_hint(a.sums.s[k] + row, sv[u], once);
           m = dbits(cabs2(sv[u]));
         }
@@ -383,7 +407,7 @@ __global__ void __launch_bounds__(kThreads) series_axpy_kernel(SeriesTermArgs a)
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
+  for (int k = threadIdx.x; k < count; k += blockDim.x)
     if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -391,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) series_axpy_kernel(SeriesTermArgs a)
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
       if (a.decide) {
-        series_control(ctl, a.count, a.tol);
+        series_flush_control(ctl, a.tol);
       } else {
         ctl->arrivals = 0;
       }
@@ -519,69 +543,14 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
 
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermArgs a, SellView m) {
-  SeriesCtl* ctl = a.ctl;
-  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+  if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
-  __shared__ double fac[kMaxSeriesD];
-  __shared__ int act[kMaxSeriesD];
-  __shared__ unsigned long long smax_sh[kMaxSeriesD];
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
-    fac[k] = ctl->factor[k];
-    act[k] = ctl->active[k];
-    smax_sh[k] = 0;
-  }
-  __syncthreads();
   unsigned long long tmax = 0;
-  const bool first = a.p == 1;
-  const int lane = threadIdx.x & 31;
-  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  slice_loop<kStrict>(m, a.x, [&](long long row, double2 acc, bool valid) {
-    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));  // K_p
-    if (valid) {
-      st_hint(a.kp + row, kv, keep);
-      tmax = umax64(tmax, dbits(cabs2(kv)));
-    }
-    const double2 zv = (first && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
-#pragma unroll 1
-    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
-      double2 sv[kSeriesRegD];
-#pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
-      }
-#pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (k >= a.count) break;  // warp-uniform
-        unsigned long long mk = 0;
-        if (valid && act[k]) {
-          sv[u] = kStrict ? axpy<1>(sv[u], fac[k], kv) : axpy<2>(sv[u], fac[k], kv);  // expm.cpp:300-305
-          st_hint(a.sums.s[k] + row, sv[u], once);
-          mk = dbits(cabs2(sv[u]));
-        }
-        mk = warp_max_bits(mk);
-        if (lane == 0 && mk) atomicMax(&smax_sh[k], mk);
-      }
-    }
-  });
-  tmax = block_max_bits(tmax, red);
-  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
-  __syncthreads();
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
-    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
-      __threadfence();
-      if (a.decide) {
-        series_control(ctl, a.count, a.tol);
-      } else {
-        ctl->arrivals = 0;
-      }
-    }
-  }
+  const unsigned long long keep = evict_last_policy();
+  double2* const kp = a.kp;
+  const double scale = a.scale;
+  slice_loop<kStrict>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  series_term_finish(a, tmax, red);
 }
 
 // ------------------------------------------------------------ Kron path
@@ -782,69 +751,14 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term
 }
 
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
-  SeriesCtl* ctl = a.ctl;
-  if (*(volatile int*)&ctl->error || *(volatile int*)&ctl->n_active == 0) return;
+  if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
-  __shared__ double fac[kMaxSeriesD];
-  __shared__ int act[kMaxSeriesD];
-  __shared__ unsigned long long smax_sh[kMaxSeriesD];
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x) {
-    fac[k] = ctl->factor[k];
-    act[k] = ctl->active[k];
-    smax_sh[k] = 0;
-  }
-  __syncthreads();
   unsigned long long tmax = 0;
-  const bool first = a.p == 1;
-  const int lane = threadIdx.x & 31;
-  const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  kron_loop(m, a.x, [&](long long row, double2 acc, bool valid) {
-    const double2 kv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));  // K_p
-    if (valid) {
-      st_hint(a.kp + row, kv, keep);
-      tmax = umax64(tmax, dbits(cabs2(kv)));
-    }
-    const double2 zv = (first && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
-#pragma unroll 1
-    for (int k0 = 0; k0 < a.count; k0 += kSeriesRegD) {
-      double2 sv[kSeriesRegD];
-#pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (valid && k < a.count && act[k]) sv[u] = first ? zv : ld_once(a.sums.s[k] + row, once);
-      }
-#pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (k >= a.count) break;  // warp-uniform
-        unsigned long long mk = 0;
-        if (valid && act[k]) {
-          sv[u] = axpy<2>(sv[u], fac[k], kv);  // expm.cpp:300-305
-          st_hint(a.sums.s[k] + row, sv[u], once);
-          mk = dbits(cabs2(sv[u]));
-        }
-        mk = warp_max_bits(mk);
-        if (lane == 0 && mk) atomicMax(&smax_sh[k], mk);
-      }
-    }
-  });
-  tmax = block_max_bits(tmax, red);
-  if (threadIdx.x == 0) atomicMax(&ctl->term_bits, tmax);
-  __syncthreads();
-  for (int k = threadIdx.x; k < a.count; k += blockDim.x)
-    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
-      __threadfence();
-      if (a.decide) {
-        series_control(ctl, a.count, a.tol);
-      } else {
-        ctl->arrivals = 0;
-      }
-    }
-  }
+  const unsigned long long keep = evict_last_policy();
+  double2* const kp = a.kp;
+  const double scale = a.scale;
+  kron_loop(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  series_term_finish(a, tmax, red);
 }
 
 // ------------------------------------------------------------ norm kernels
@@ -877,7 +791,7 @@ __device__ void step_init_apply(StepCtl* ctl, double nv) {
   ctl->arrivals = 0;
 }
 
-__device__ void series_init_apply(SeriesCtl* ctl, int count, double nz) {
+__device__ void series_init_apply(SeriesCtl* ctl, int count, int pend_max, double nz) {
   ctl->z_norm = nz;  // expm.cpp:271-276
   ctl->count = count;
   ctl->n_active = ctl->error ? 0 : count;  // `error` and `spmvs` are sticky
@@ -885,8 +799,14 @@ __device__ void series_init_apply(SeriesCtl* ctl, int count, double nz) {
     ctl->active[k] = 1;
     ctl->factor[k] = static_cast<double>(k + 1);  // factor *= k at p = 1
     ctl->c1[k] = nz;
+    ctl->nf_last[k] = nz;  // S_k starts as Z
+    ctl->bound[k] = 0.0;
     ctl->sum_bits[k] = 0;
   }
+  ctl->n_pend = 0;
+  ctl->flush = 0;
+  ctl->fresh = 1;
+  ctl->pend_max = pend_max < 1 ? 1 : (pend_max > kPendMax ? kPendMax : pend_max);
   ctl->term_bits = 0;
   ctl->arrivals = 0;
 }
@@ -902,10 +822,10 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(const double2* v, l
 }
 
 __global__ void __launch_bounds__(kThreads) series_init_kernel(const double2* z, long long n, int count,
-                                                              SeriesCtl* ctl, int decide) {
-  norm_body(z, n, &ctl->term_bits, &ctl->arrivals, [ctl, count, decide](double nz) {
+                                                              int pend_max, SeriesCtl* ctl, int decide) {
+  norm_body(z, n, &ctl->term_bits, &ctl->arrivals, [ctl, count, pend_max, decide](double nz) {
     if (decide) {
-      series_init_apply(ctl, count, nz);
+      series_init_apply(ctl, count, pend_max, nz);
     } else {
       ctl->arrivals = 0;
     }
@@ -916,14 +836,17 @@ __global__ void __launch_bounds__(kThreads) series_init_kernel(const double2* z,
 __global__ void step_init_fin_kernel(StepCtl* ctl) {
   step_init_apply(ctl, bitsd(ctl->term_bits));
 }
-__global__ void series_init_fin_kernel(SeriesCtl* ctl, int count) {
-  series_init_apply(ctl, count, bitsd(ctl->term_bits));
+__global__ void series_init_fin_kernel(SeriesCtl* ctl, int count, int pend_max) {
+  series_init_apply(ctl, count, pend_max, bitsd(ctl->term_bits));
 }
 __global__ void step_control_kernel(StepCtl* ctl, int first_of_stage, int stage, double tol) {
   step_control(ctl, first_of_stage, stage, tol);
 }
-__global__ void series_control_kernel(SeriesCtl* ctl, int count, double tol) {
-  series_control(ctl, count, tol);
+__global__ void series_term_control_kernel(SeriesCtl* ctl, int last, double tol) {
+  series_term_control(ctl, last, tol);
+}
+__global__ void series_flush_control_kernel(SeriesCtl* ctl, double tol) {
+  series_flush_control(ctl, tol);
 }
 
 // --------------------------------------------------------------- plain SpMV
@@ -1024,18 +947,6 @@ void dispatch_group(int g, long long rows, cudaStream_t s, Args... args) {
 template <int G> struct StepTermK { static constexpr auto fn = step_term_kernel<G>; };
 template <int G> struct SeriesTermK { static constexpr auto fn = series_term_kernel<G>; };
 template <int G> struct SpmvK { static constexpr auto fn = spmv_kernel<G>; };
-template <int G> struct SeriesSpmvK { static constexpr auto fn = series_spmv_kernel<G>; };
-
-// QSWG_SERIES_MODE: "split" (default) or "fused"; "spmv_only" / "axpy_only"
-// launch one half of the split pair (kernel timing experiments only).
-int series_mode() {
-  static const int mode = [] {
-    const char* e = std::getenv("QSWG_SERIES_MODE");
-    const std::string m = e ? e : "split";
-    return m == "fused" ? 0 : m == "spmv_only" ? 2 : m == "axpy_only" ? 3 : 1;
-  }();
-  return mode;
-}
 
 }  // namespace
 
@@ -1056,14 +967,19 @@ void step_control(StepCtl* ctl, bool first_of_stage, int stage, double tol, cuda
   QSWG_LAUNCH_CHECK("step_control");
 }
 
-void series_init_fin(SeriesCtl* ctl, int count, cudaStream_t s) {
-  series_init_fin_kernel<<<1, 1, 0, s>>>(ctl, count);
+void series_init_fin(SeriesCtl* ctl, int count, int pend_max, cudaStream_t s) {
+  series_init_fin_kernel<<<1, 1, 0, s>>>(ctl, count, pend_max);
   QSWG_LAUNCH_CHECK("series_init_fin");
 }
 
-void series_control(SeriesCtl* ctl, int count, double tol, cudaStream_t s) {
-  series_control_kernel<<<1, 1, 0, s>>>(ctl, count, tol);
-  QSWG_LAUNCH_CHECK("series_control");
+void series_term_control(SeriesCtl* ctl, int last, double tol, cudaStream_t s) {
+  series_term_control_kernel<<<1, 1, 0, s>>>(ctl, last, tol);
+  QSWG_LAUNCH_CHECK("series_term_control");
+}
+
+void series_flush_control(SeriesCtl* ctl, double tol, cudaStream_t s) {
+  series_flush_control_kernel<<<1, 1, 0, s>>>(ctl, tol);
+  QSWG_LAUNCH_CHECK("series_flush_control");
 }
 
 void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,
@@ -1086,46 +1002,42 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
   QSWG_LAUNCH_CHECK("step_term");
 }
 
-void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, bool decide, cudaStream_t s) {
+void series_init(const double2* z, std::int64_t n, int count, int pend_max, SeriesCtl* ctl, bool decide,
+                 cudaStream_t s) {
   if (count < 1 || count > kMaxSeriesD) throw std::invalid_argument("series super-step size out of range");
-  series_init_kernel<<<small_grid(n), kThreads, 0, s>>>(z, n, count, ctl, decide ? 1 : 0);
+  series_init_kernel<<<small_grid(n), kThreads, 0, s>>>(z, n, count, pend_max, ctl, decide ? 1 : 0);
   QSWG_LAUNCH_CHECK("series_init");
 }
 
-void series_term(const DevMatrix& m, const double2* x, double2* kp, const double2* z,
-                 const SeriesSums& sums, int count, int p, double scale, double tol,
-                 SeriesCtl* ctl, bool decide, cudaStream_t s) {
-  SeriesTermArgs a{m.csr, x, kp, z, sums, count, p, scale, tol, ctl, decide ? 1 : 0};
+void series_term(const DevMatrix& m, const double2* x, double2* kp, int /*p*/, bool last, double scale,
+                 double tol, SeriesCtl* ctl, bool decide, cudaStream_t s) {
+  const SeriesTermArgs a{x, kp, last ? 1 : 0, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Kron) {
     const auto g = kron_geom(kron_series_term_kernel, m.kron);
     kron_series_term_kernel<<<g.first, kThreads, g.second, s>>>(a, m.kron);
-    QSWG_LAUNCH_CHECK("series_term");
-    return;
-  }
-  if (m.format == Format::Sell) {
+  } else if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_series_term_kernel<true><<<sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s>>>(a, m.sell);
     } else {
       sell_series_term_kernel<false><<<sell_grid(sell_series_term_kernel<false>, m.sell), kThreads, 0, s>>>(a, m.sell);
     }
-    QSWG_LAUNCH_CHECK("series_term");
-    return;
-  }
-  const int group = m.group;
-  const CsrView& l = m.csr;
-  const int mode = series_mode();
-  if (mode == 0) {
-    dispatch_group<SeriesTermK>(group, l.rows, s, a);
   } else {
-    if (mode != 3) dispatch_group<SeriesSpmvK>(group, l.rows, s, a);
-    if (mode == 2) {
-    } else if (group == 1) {
-      series_axpy_kernel<1><<<persistent_grid(series_axpy_kernel<1>, l.rows), kThreads, 0, s>>>(a);
-    } else {
-      series_axpy_kernel<2><<<persistent_grid(series_axpy_kernel<2>, l.rows), kThreads, 0, s>>>(a);
-    }
+    dispatch_group<SeriesTermK>(m.group, m.csr.rows, s, a, m.csr);
   }
   QSWG_LAUNCH_CHECK("series_term");
+}
+
+void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, const double2* z,
+                  const SeriesSums& sums, int count, int p, bool strict, double tol, SeriesCtl* ctl,
+                  bool decide, cudaStream_t s) {
+  (void)count;
+  const SeriesFlushArgs a{ring, row0, rows, z, sums, p, tol, ctl, decide ? 1 : 0};
+  if (strict) {
+    series_flush_kernel<true><<<persistent_grid(series_flush_kernel<true>, rows), kThreads, 0, s>>>(a);
+  } else {
+    series_flush_kernel<false><<<persistent_grid(series_flush_kernel<false>, rows), kThreads, 0, s>>>(a);
+  }
+  QSWG_LAUNCH_CHECK("series_flush");
 }
 
 void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -23,7 +24,27 @@ namespace qswg {
 namespace {
 
 // Workspace slots.
-enum Slot : std::size_t { kT0 = 0, kT1 = 1, kSOther = 2, kNext = 3, kZ = 4, kXStage = 5, kZFull = 6, kSums = 8 };
+enum Slot : std::size_t {
+  kT0 = 0, kT1 = 1, kSOther = 2, kNext = 3, kZ = 4, kXStage = 5, kZFull = 6, kSums = 8,
+  kRing = kSums + dev::kMaxSeriesD  // series term ring slots 2.. (slots 0, 1 are kT0, kT1)
+};
+
+std::size_t ring_slot(int i) { return i < 2 ? static_cast<std::size_t>(i) : kRing + static_cast<std::size_t>(i - 2); }
+
+// Terms a series super-step may hold back (kernels.hpp: SeriesCtl): kPendMax,
+// fewer when the ring of pend_max + 1 full-length vectors would take more
+// than half of the free device memory; QSWG_PEND_MAX overrides (1 = update
+// the sums after every term).
+int series_pend_max(std::int64_t dim) {
+  int pm = dev::kPendMax;
+  if (const char* e = std::getenv("QSWG_PEND_MAX")) pm = std::max(1, std::min(dev::kPendMax, std::atoi(e)));
+  std::size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+    const double vec_b = static_cast<double>(dim) * sizeof(double2);
+    while (pm > 1 && (pm - 1) * vec_b > 0.5 * static_cast<double>(free_b)) --pm;
+  }
+  return pm;
+}
 
 dev::StepCtl* step_ctl(const Liouvillian& l) {
   Workspace& ws = l.workspace();
@@ -228,35 +249,51 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
     info.sub_m_star = m_star;
     if (d > dev::kMaxSeriesD) throw std::logic_error("super-step size exceeds the device limit");
 
-    double2* kbuf[2] = {ex.full(kT0), ex.full(kT1)};
-    std::vector<double2*> sums(static_cast<std::size_t>(d));
-    for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ex.local(kSums + static_cast<std::size_t>(k));
     dev::SeriesCtl* ctl = series_ctl(l);
     const dev::DevMatrix mat = l.matrix();
+    const int pend_max = series_pend_max(ex.dim);
+    dev::SeriesRing ring{};
+    ring.slots = pend_max + 1;
+    for (int i = 0; i < ring.slots; ++i) ring.k[i] = ex.full(ring_slot(i));
+    std::vector<double2*> sums(static_cast<std::size_t>(d));
+    for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ex.local(kSums + static_cast<std::size_t>(k));
+    const bool strict = mat.group == 1;
+    const std::int64_t per_term = 2 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0);
     for (std::int64_t super = 0; super <= n_super; ++super) {
       const std::int64_t count = super < n_super ? d : remainder;
       if (count == 0) break;
-      dev::series_init(z, ex.rows, static_cast<int>(count), ctl, ex.single, s);
+      dev::series_init(z, ex.rows, static_cast<int>(count), pend_max, ctl, ex.single, s);
       if (!ex.single) {
         ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
-        dev::series_init_fin(ctl, static_cast<int>(count), s);
+        dev::series_init_fin(ctl, static_cast<int>(count), pend_max, s);
       }
-      info.launches += 1 + m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0));
+      info.launches += 1 + m_star * per_term;
       dev::SeriesSums ss{};
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
       const double2* z_full = ex.spmv_input(z, kZFull);
       for (std::int64_t p = 1; p <= m_star; ++p) {
-        const double2* x = p == 1 ? z_full : kbuf[(p - 1) % 2];
-        double2* kp = kbuf[p % 2] + ex.row0;
+        const double2* x = p == 1 ? z_full : ring.k[(p - 1) % ring.slots];
+        double2* kp = ring.k[p % ring.slots] + ex.row0;
+        const bool last = p == m_star;
         ex.prepare(mat, x);
-        dev::series_term(mat, x, kp, z, ss, static_cast<int>(count), static_cast<int>(p),
-                         h / static_cast<double>(p), params.tolerance, ctl, ex.single, s);
-        if (!ex.single) {
-          ex.comm->allreduce_max_u64(&ctl->term_bits, 1 + static_cast<std::size_t>(count), s);
-          dev::series_control(ctl, static_cast<int>(count), params.tolerance, s);
-          if (ex.read(&ctl->n_active) == 0) break;
-          if (p < m_star) ex.exchange(kbuf[p % 2]);
+        dev::series_term(mat, x, kp, static_cast<int>(p), last, h / static_cast<double>(p), params.tolerance, ctl,
+                         ex.single, s);
+        if (ex.single) {
+          dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
+                            params.tolerance, ctl, true, s);
+          continue;
         }
+        ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
+        dev::series_term_control(ctl, last ? 1 : 0, params.tolerance, s);
+        if (ex.read(&ctl->n_active) == 0) break;
+        if (ex.read(&ctl->flush)) {
+          dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
+                            params.tolerance, ctl, false, s);
+          ex.comm->allreduce_max_u64(&ctl->sum_bits[0], static_cast<std::size_t>(count), s);
+          dev::series_flush_control(ctl, params.tolerance, s);
+          if (ex.read(&ctl->n_active) == 0) break;
+        }
+        if (p < m_star) ex.exchange(ring.k[p % ring.slots]);
       }
       for (std::int64_t k = 1; k <= count; ++k) emit(super * d + k, sums[static_cast<std::size_t>(k - 1)]);
       // the next super-step starts from states[(super + 1) d] = the last output
@@ -276,32 +313,38 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   DeviceGuard g(l.device());
   const Exec ex(l);
   cudaStream_t s = ex.s;
-  double2* k[2] = {ex.full(kT0), ex.full(kT1)};
+  const int pend_max = series_pend_max(ex.dim);
+  dev::SeriesRing ring{};
+  ring.slots = pend_max + 1;
+  for (int i = 0; i < ring.slots; ++i) ring.k[i] = ex.full(ring_slot(i));
   double2* z = ex.local(kZ);
   dev::SeriesSums ss{};
   for (int c = 0; c < count; ++c) ss.s[c] = ex.local(kSums + static_cast<std::size_t>(c));
-  dev::fill_pattern(k[0], ex.dim, s);
+  dev::fill_pattern(ring.k[0], ex.dim, s);
   dev::fill_pattern(z, ex.rows, s);
   for (int c = 0; c < count; ++c) dev::fill_pattern(ss.s[c], ex.rows, s);
   dev::SeriesCtl* ctl = series_ctl(l);
   QSWG_CHECK(cudaMemsetAsync(ctl, 0, sizeof(dev::SeriesCtl), s));
-  dev::series_init(z, ex.rows, count, ctl, true, s);
-  // tol = -1 keeps every output active (c1 + c2 <= -nf never holds); scale
-  // 1/||L||_1 keeps the iterates bounded.  Local kernel time only (no
-  // exchange), as the per-GPU roofline needs.
+  dev::series_init(z, ex.rows, count, pend_max, ctl, true, s);
+  // tol = -1 keeps every output active and settles every test without the
+  // sums (c1 + c2 > -ub), so the sums are updated once per pend_max terms, as
+  // in the converging part of a real series; scale 1/||L||_1 keeps the
+  // iterates bounded.  Local kernel time only (no exchange), as the per-GPU
+  // roofline needs.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
   const dev::DevMatrix mat = l.matrix();
   auto launch = [&](int i) {
-    dev::kron_prepare(mat, k[i % 2], s);
-    dev::series_term(mat, k[i % 2], k[(i + 1) % 2] + ex.row0, z, ss, count, 2 + (i % 2), scale, -1.0,
-                     ctl, true, s);
+    const double2* x = ring.k[i % ring.slots];
+    dev::kron_prepare(mat, x, s);
+    dev::series_term(mat, x, ring.k[(i + 1) % ring.slots] + ex.row0, i + 1, false, scale, -1.0, ctl, true, s);
+    dev::series_flush(ring, ex.row0, ex.rows, z, ss, count, i + 1, mat.group == 1, -1.0, ctl, true, s);
   };
-  launch(0);  // warm-up
+  for (int i = 0; i < pend_max; ++i) launch(i);  // warm-up (one full ring)
   cudaEvent_t e0, e1;
   QSWG_CHECK(cudaEventCreate(&e0));
   QSWG_CHECK(cudaEventCreate(&e1));
   QSWG_CHECK(cudaEventRecord(e0, s));
-  for (int i = 1; i <= iters; ++i) launch(i);
+  for (int i = pend_max; i < pend_max + iters; ++i) launch(i);
   QSWG_CHECK(cudaEventRecord(e1, s));
   QSWG_CHECK(cudaEventSynchronize(e1));
   float ms = 0.f;

@@ -11,6 +11,7 @@ namespace qswg::dev {
 inline constexpr int kMaxKron = 8;      // Lindblad operators per G-QSW
 inline constexpr int kMaxSeriesD = 128; // super-step outputs (d <= floor(1e280^(1/55)) = 123)
 inline constexpr int kSeriesRegD = 4;   // running sums updated per chunk in the series kernel
+inline constexpr int kPendMax = 8;      // series terms held back before one batched sum update
 
 // A "multi-CSR" over the n x n operator space: rows sorted by column with
 // duplicates kept adjacent in emission order (they are summed on the device
@@ -184,6 +185,14 @@ struct StepCtl {
   double last_nf;
 };
 
+// Series control block.  Running sums are updated lazily: term kernels only
+// write K_p (into a ring of kPendMax + 1 vectors) and ||K_p||; the stop test
+// of every output is first evaluated against a rigorous upper bound of
+// ||S_k|| (last exact norm + sum of the pending terms' norms, rounded up).
+// While every active output provably continues, terms stay pending; the
+// first undecidable test, a full ring or the super-step's last term set
+// `flush`, and the flush kernel then applies all pending terms in order
+// (bit-identical to per-term updates) and runs the exact test.
 struct SeriesCtl {
   unsigned long long term_bits;               // adjacent to sum_bits: one
   unsigned long long sum_bits[kMaxSeriesD];   // allreduce covers both
@@ -192,11 +201,25 @@ struct SeriesCtl {
   int error;
   int spmvs;
   int count;
-  int pad_;
+  int n_pend;      // terms written but not yet added to the sums
+  int flush;       // the flush kernel after this term must run
+  int fresh;       // the first flush of a super-step starts from Z
+  int pend_max;    // ring capacity in use (<= kPendMax)
   double z_norm;
+  double tn_last;  // ||K_p|| of the newest pending term
   double factor[kMaxSeriesD];
   double c1[kMaxSeriesD];
+  double nf_last[kMaxSeriesD];  // exact ||S_k|| at the last flush (||Z|| at the start)
+  double bound[kMaxSeriesD];    // upper bound of the pending terms' contribution
+  double fac_pend[kPendMax][kMaxSeriesD];
   int active[kMaxSeriesD];
+};
+
+// Term vectors of a series super-step: term p lives in k[p % slots]
+// (full-length, SpMV inputs); slots = pend_max + 1.
+struct SeriesRing {
+  double2* k[kPendMax + 1];
+  int slots;
 };
 
 struct SeriesSums {
@@ -216,8 +239,7 @@ int valid_group(int g);
 void step_init(const double2* v, std::int64_t n, StepCtl* ctl, bool decide, cudaStream_t s);
 void step_init_fin(StepCtl* ctl, cudaStream_t s);
 void step_control(StepCtl* ctl, bool first_of_stage, int stage, double tol, cudaStream_t s);
-void series_init_fin(SeriesCtl* ctl, int count, cudaStream_t s);
-void series_control(SeriesCtl* ctl, int count, double tol, cudaStream_t s);
+void series_init_fin(SeriesCtl* ctl, int count, int pend_max, cudaStream_t s);
 // One Taylor term of `step` (expm.cpp:175-195):
 //   y = scale * (L x);  sum_out = sum_in + y;  c2 = ||y||, nf = ||sum_out||;
 //   stop test c1 + c2 <= tol * nf decided on the device.  Skips itself when
@@ -226,13 +248,22 @@ void step_term(const DevMatrix& l, const double2* x, double2* y, const double2* 
                double2* sum_out, double scale, bool first_of_stage, int stage, double tol,
                StepCtl* ctl, bool decide, cudaStream_t s);
 // Super-step start of `series` (expm.cpp:267-276): z_norm = ||Z||, count
-// outputs active, factor_k = k, c1_k = z_norm.
-void series_init(const double2* z, std::int64_t n, int count, SeriesCtl* ctl, bool decide, cudaStream_t s);
-// K_p = scale * (L K_{p-1}); for every active k: S_k = (p == 1 ? Z : S_k) + k^p K_p
-// with per-k stop tests (expm.cpp:278-316, evaluated p-major).
-void series_term(const DevMatrix& l, const double2* x, double2* kp, const double2* z,
-                 const SeriesSums& sums, int count, int p, double scale, double tol,
-                 SeriesCtl* ctl, bool decide, cudaStream_t s);
+// outputs active, factor_k = k, c1_k = z_norm; pend_max terms may be held back.
+void series_init(const double2* z, std::int64_t n, int count, int pend_max, SeriesCtl* ctl, bool decide,
+                 cudaStream_t s);
+// K_p = scale * (L K_{p-1}) and ||K_p|| (expm.cpp:283-293); the control then
+// decides which stop tests are already settled and whether a flush is due
+// (always on the super-step's `last` term).
+void series_term(const DevMatrix& l, const double2* x, double2* kp, int p, bool last, double scale,
+                 double tol, SeriesCtl* ctl, bool decide, cudaStream_t s);
+void series_term_control(SeriesCtl* ctl, int last, double tol, cudaStream_t s);
+// When ctl->flush: for every active k, S_k = (fresh ? Z : S_k) + sum over the
+// pending terms q of k^q K_q, in term order (expm.cpp:300-305), then the
+// exact stop tests of term p (expm.cpp:306-316).  No-op otherwise.
+void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, const double2* z,
+                  const SeriesSums& sums, int count, int p, bool strict, double tol, SeriesCtl* ctl,
+                  bool decide, cudaStream_t s);
+void series_flush_control(SeriesCtl* ctl, double tol, cudaStream_t s);
 // Kron format: W_k = Q_k X on the local columns (call before every product
 // with input x; multi-GPU callers then exchange the W_k halos).
 void kron_prepare(const DevMatrix& l, const double2* x, cudaStream_t s);
