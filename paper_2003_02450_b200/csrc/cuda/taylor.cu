@@ -558,10 +558,16 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
 #define QSWG_KRON_MIN_BLOCKS 4  // <= 64 registers: 4 resident blocks of 256 threads per SM
 #endif
 
-// Matrix-free action (kernels.hpp: KronView).  One thread per output row
-// r = n*j + i; consecutive threads share the rho column j, so the B (x) I
-// and P (x) Q parts stream coalesced columns of X and W_k, and the I (x) A
-// gathers stay inside column j (L1-resident).
+// Matrix-free action (kernels.hpp: KronView), in 32 x 32 tiles of X: lane
+// = rho row i (operand rows of A, R_k per lane, coalesced in sliced ELL),
+// warp w = rho columns j0 + 4w .. j0 + 4w + 3 (operand rows of B, P_k, S_k
+// warp-uniform).  Each thread accumulates its 4 elements together, so every
+// row-indexed operand entry is loaded once per 4 outputs and 4 independent
+// gathers are in flight per entry.  The B (x) I and P (x) Q parts stream
+// coalesced columns of X and W_k; the I (x) A gathers stay inside columns j.
+constexpr int kKT = 32;                      // tile edge
+constexpr int kKR = kKT / (kThreads / 32);   // columns per thread (4)
+
 __device__ __forceinline__ void cfma(double2& acc, double2 v, double2 xv) {
   acc.x = fma(v.x, xv.x, acc.x);
   acc.x = fma(-v.y, xv.y, acc.x);
@@ -569,112 +575,226 @@ __device__ __forceinline__ void cfma(double2& acc, double2 v, double2 xv) {
   acc.y = fma(v.y, xv.x, acc.y);
 }
 
-__device__ __forceinline__ double2 kron_row(const KronView& m, const double2* __restrict__ x, long long g,
-                                            unsigned long long xpol) {
+// acc[r] = (L x) at rho element (i, j[r]) (global row i, global columns j[r]);
+// i and j[r] are clamped to valid indices by the caller.  Per element the
+// terms are summed in the order A, B, then per k: P_k, R_k, S_k, then T,
+// decay.
+__device__ __forceinline__ void kron_tile_acc(const KronView& m, const double2* __restrict__ x, int i,
+                                              const int* j, double2* acc, unsigned long long xpol) {
   const long long n = m.n;
-  const long long j = g / n, i = g - j * n;
-  double2 acc = make_double2(0.0, 0.0);
-  if (m.a_ell.sptr) {  // I (x) A: column j of X, operand rows in sliced ELL
-    const int sl = static_cast<int>(i >> 5), lane = static_cast<int>(i & 31);
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
+  if (m.a_ell.sptr) {  // I (x) A: columns j of X, operand rows in sliced ELL
+    const int sl = i >> 5, lane = i & 31;
     const int b = __ldg(m.a_ell.sptr + sl), len = (__ldg(m.a_ell.sptr + sl + 1) - b) >> 5;
     const int* cp = m.a_ell.col + b + lane;
     const double2* vp = m.a_ell.val + b + lane;
-    const double2* xj = x + j * n;
-#pragma unroll 4
-    for (int k = 0; k < len; ++k) cfma(acc, __ldg(vp + 32 * k), ld_gather(xj + __ldg(cp + 32 * k), xpol));
-  } else if (m.a.ptr) {  // I (x) A with CSR operand rows
+#pragma unroll 2
+    for (int e = 0; e < len; ++e) {
+      const int c = __ldg(cp + 32 * e);
+      const double2 v = __ldg(vp + 32 * e);
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + j[r] * n + c, xpol));
+    }
+  } else if (m.a.ptr) {
     const int e1 = __ldg(m.a.ptr + i + 1);
-    const double2* xj = x + j * n;
-#pragma unroll 4
-    for (int e = __ldg(m.a.ptr + i); e < e1; ++e) cfma(acc, __ldg(m.a.val + e), ld_gather(xj + __ldg(m.a.col + e), xpol));
+#pragma unroll 2
+    for (int e = __ldg(m.a.ptr + i); e < e1; ++e) {
+      const int c = __ldg(m.a.col + e);
+      const double2 v = __ldg(m.a.val + e);
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + j[r] * n + c, xpol));
+    }
   }
   if (m.b.ptr) {  // B (x) I: coalesced columns c of X
-    const int e1 = __ldg(m.b.ptr + j + 1);
     const double2* xi = x + i;
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const int e1 = __ldg(m.b.ptr + j[r] + 1);
 #pragma unroll 4
-    for (int e = __ldg(m.b.ptr + j); e < e1; ++e)
-      cfma(acc, __ldg(m.b.val + e), ld_gather(xi + static_cast<long long>(__ldg(m.b.col + e)) * n, xpol));
+      for (int e = __ldg(m.b.ptr + j[r]); e < e1; ++e)
+        cfma(acc[r], __ldg(m.b.val + e), ld_gather(xi + static_cast<long long>(__ldg(m.b.col + e)) * n, xpol));
+    }
   }
   for (int k = 0; k < m.nk; ++k) {  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
     const KronList& p = m.p[k];
-    const int e1 = __ldg(p.ptr + j + 1);
     const double2* wi = m.w[k] + i;
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const int e1 = __ldg(p.ptr + j[r] + 1);
 #pragma unroll 4
-    for (int e = __ldg(p.ptr + j); e < e1; ++e)
-      cfma(acc, __ldg(p.val + e), ld_gather(wi + static_cast<long long>(__ldg(p.col + e)) * n, xpol));
+      for (int e = __ldg(p.ptr + j[r]); e < e1; ++e)
+        cfma(acc[r], __ldg(p.val + e), ld_gather(wi + static_cast<long long>(__ldg(p.col + e)) * n, xpol));
+    }
     if (m.factored) {
-      const KronList& r = m.r[k];  // -w/2 L'(L X): column j of W_k
-      const int r1 = __ldg(r.ptr + i + 1);
-      const double2* wj = m.w[k] + j * n;
-#pragma unroll 4
-      for (int e = __ldg(r.ptr + i); e < r1; ++e) cfma(acc, __ldg(r.val + e), ld_gather(wj + __ldg(r.col + e), xpol));
+      const KronList& rk = m.r[k];  // -w/2 L'(L X): columns j of W_k
+      const int r1 = __ldg(rk.ptr + i + 1);
+      const double2* wk = m.w[k];
+#pragma unroll 2
+      for (int e = __ldg(rk.ptr + i); e < r1; ++e) {
+        const int c = __ldg(rk.col + e);
+        const double2 v = __ldg(rk.val + e);
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(wk + j[r] * n + c, xpol));
+      }
       const KronList& sk = m.s[k];  // -w/2 (X L') L: columns of V_k
-      const int s1 = __ldg(sk.ptr + j + 1);
       const double2* vi = m.v[k] + i;
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const int s1 = __ldg(sk.ptr + j[r] + 1);
 #pragma unroll 4
-      for (int e = __ldg(sk.ptr + j); e < s1; ++e)
-        cfma(acc, __ldg(sk.val + e), ld_gather(vi + static_cast<long long>(__ldg(sk.col + e)) * n, xpol));
+        for (int e = __ldg(sk.ptr + j[r]); e < s1; ++e)
+          cfma(acc[r], __ldg(sk.val + e), ld_gather(vi + static_cast<long long>(__ldg(sk.col + e)) * n, xpol));
+      }
     }
   }
-  if (m.t.ptr && i == j) {  // transfer onto the diagonal
-    const int e1 = __ldg(m.t.ptr + i + 1);
-    for (int e = __ldg(m.t.ptr + i); e < e1; ++e)
-      cfma(acc, __ldg(m.t.val + e), ld_gather(x + static_cast<long long>(__ldg(m.t.col + e)) * (n + 1), xpol));
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) {
+    if (m.t.ptr && i == j[r]) {  // transfer onto the diagonal
+      const int e1 = __ldg(m.t.ptr + i + 1);
+      for (int e = __ldg(m.t.ptr + i); e < e1; ++e)
+        cfma(acc[r], __ldg(m.t.val + e), ld_gather(x + static_cast<long long>(__ldg(m.t.col + e)) * (n + 1), xpol));
+    }
   }
   if (m.d_loc) {  // -0.5 (w (dl_i + dl_j) + ds_i + ds_j) X(i, j)
-    const double d = __dmul_rn(
-        0.5, __dadd_rn(__dadd_rn(__dmul_rn(m.omega, __dadd_rn(__ldg(m.d_loc + i), __ldg(m.d_loc + j))),
-                                 __ldg(m.d_ss + i)),
-                       __ldg(m.d_ss + j)));
-    if (d != 0.0) {
-      const double2 xg = ld_gather(x + g, xpol);
-      acc.x = fma(-d, xg.x, acc.x);
-      acc.y = fma(-d, xg.y, acc.y);
+    const double dli = __ldg(m.d_loc + i), dsi = __ldg(m.d_ss + i);
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const double d = __dmul_rn(
+          0.5, __dadd_rn(__dadd_rn(__dmul_rn(m.omega, __dadd_rn(dli, __ldg(m.d_loc + j[r]))), dsi),
+                         __ldg(m.d_ss + j[r])));
+      if (d != 0.0) {
+        const double2 xg = ld_gather(x + j[r] * n + i, xpol);
+        acc[r].x = fma(-d, xg.x, acc[r].x);
+        acc[r].y = fma(-d, xg.y, acc[r].y);
+      }
     }
   }
-  return acc;
 }
 
-// Block-uniform loop over local rows; epi(row, acc, valid) on every thread.
-// (Staging column j in shared memory for the I (x) A gathers was measured
-// slower than L1 on c2 and c4 — 125 vs 101 ms and 5.1 vs 3.9 s per series —
-// and is not used.)
+// Hermitian mode in effect for this launch (block-uniform).
+__device__ __forceinline__ bool kron_herm(const KronView& m) {
+  return m.herm != nullptr && *(volatile const int*)m.herm != 0;
+}
+
+// Persistent loop over 32 x 32 tiles of the local columns, J-major (blocks
+// launched together share the columns J that the I (x) A part gathers
+// from).  epi(local_row, value, valid) runs on every thread for every
+// element (valid is false outside the matrix and for the elements a
+// Hermitian tile takes from its mirror).  In Hermitian mode only tiles
+// I <= J are computed; each is written directly and, through a shared-memory
+// transpose, conjugated into tile (J, I) (coalesced both ways); diagonal
+// tiles keep their upper triangle, a real diagonal and its mirror.
 template <class Epi>
-__device__ __forceinline__ void kron_loop(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
+__device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
+  __shared__ double2 tile[kKT][kKT + 1];
   const unsigned long long xpol = evict_last_policy();
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < m.rows; base += stride) {
-    const long long r = base + threadIdx.x;
-    const bool valid = r < m.rows;
-    const double2 acc = valid ? kron_row(m, x, m.row0 + r, xpol) : make_double2(0.0, 0.0);
-    epi(r, acc, valid);
+  const int n = m.n;
+  const int nc = static_cast<int>(m.rows / n);
+  const long long c0 = m.row0 / n;
+  const bool herm = kron_herm(m);
+  const int nti = (n + kKT - 1) / kKT, ntj = (nc + kKT - 1) / kKT;
+  const long long ntiles = herm ? static_cast<long long>(nti) * (nti + 1) / 2 : static_cast<long long>(nti) * ntj;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int I, J;
+    if (herm) {
+      J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
+      while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
+      while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
+      I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
+    } else {
+      J = static_cast<int>(t / nti);
+      I = static_cast<int>(t - static_cast<long long>(J) * nti);
+    }
+    const int iu = I * kKT + lane;
+    const bool vi = iu < n;
+    const int i = vi ? iu : n - 1;
+    int jl[kKR], jg[kKR];
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      jl[r] = J * kKT + kKR * w + r;
+      jg[r] = static_cast<int>(c0) + (jl[r] < nc ? jl[r] : nc - 1);
+    }
+    double2 acc[kKR];
+    kron_tile_acc(m, x, i, jg, acc, xpol);
+    const bool diag = herm && I == J;
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const int jt = kKR * w + r;  // column within the tile
+      double2 y = acc[r];
+      if (diag && lane == jt) y.y = 0.0;
+      epi(static_cast<long long>(jl[r]) * n + iu, y, vi && jl[r] < nc && (!diag || lane <= jt));
+      if (herm) tile[jt][lane] = acc[r];
+    }
+    if (herm) {
+      __syncthreads();
+      // mirror: element (row J*32 + lane, column I*32 + it) = conj Y(I*32 + it, J*32 + lane)
+      const int jrow = J * kKT + lane;
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const int it = kKR * w + r;
+        const double2 v = tile[lane][it];
+        const int icol = I * kKT + it;
+        epi(static_cast<long long>(icol) * n + jrow, make_double2(v.x, -v.y),
+            jrow < n && icol < n && (!diag || lane > it));
+      }
+      __syncthreads();
+    }
   }
 }
 
-// W_k = Q_k X on the local columns (W_k(i, a) at w[n*a + i], global index).
+// W_k = Q_k X on the local columns (W_k(i, a) at w[n*a + i], global index),
+// in the tiles of kron_tiles (lane = row i, 4 columns a per thread).
 __global__ void __launch_bounds__(kThreads) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {
   const unsigned long long xpol = evict_last_policy();
   const long long n = m.n;
+  const int nc = static_cast<int>(m.rows / m.n);
+  const long long c0 = m.row0 / m.n;
   const KronEll& qe = m.q_ell[k];
   const KronList& q = m.q[k];
-  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < m.rows;
-       r += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long g = m.row0 + r;
-    const long long a = g / n, i = g - a * n;
-    const double2* xa = x + a * n;
-    double2 acc = make_double2(0.0, 0.0);
+  const int nti = (m.n + kKT - 1) / kKT, ntj = (nc + kKT - 1) / kKT;
+  const long long ntiles = static_cast<long long>(nti) * ntj;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int J = static_cast<int>(t / nti), I = static_cast<int>(t - static_cast<long long>(J) * nti);
+    const int iu = I * kKT + lane;
+    const bool vi = iu < m.n;
+    const int i = vi ? iu : m.n - 1;
+    long long col[kKR];
+    bool vj[kKR];
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const int jl = J * kKT + kKR * w + r;
+      vj[r] = jl < nc;
+      col[r] = (c0 + (vj[r] ? jl : nc - 1)) * n;
+    }
+    double2 acc[kKR];
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
     if (qe.sptr) {
-      const int sl = static_cast<int>(i >> 5), lane = static_cast<int>(i & 31);
+      const int sl = i >> 5, ln = i & 31;
       const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
-#pragma unroll 4
-      for (int e = 0; e < len; ++e)
-        cfma(acc, __ldg(qe.val + b + 32 * e + lane), ld_gather(xa + __ldg(qe.col + b + 32 * e + lane), xpol));
+#pragma unroll 2
+      for (int e = 0; e < len; ++e) {
+        const int c = __ldg(qe.col + b + 32 * e + ln);
+        const double2 v = __ldg(qe.val + b + 32 * e + ln);
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+      }
     } else if (q.ptr) {
       const int e1 = __ldg(q.ptr + i + 1);
-#pragma unroll 4
-      for (int e = __ldg(q.ptr + i); e < e1; ++e) cfma(acc, __ldg(q.val + e), ld_gather(xa + __ldg(q.col + e), xpol));
+#pragma unroll 2
+      for (int e = __ldg(q.ptr + i); e < e1; ++e) {
+        const int c = __ldg(q.col + e);
+        const double2 v = __ldg(q.val + e);
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+      }
     }
-    st_hint(m.w[k] + g, acc, xpol);
+#pragma unroll
+    for (int r = 0; r < kKR; ++r)
+      if (vi && vj[r]) st_hint(m.w[k] + col[r] + i, acc[r], xpol);
   }
 }
 
@@ -697,7 +817,7 @@ __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const doub
 }
 
 __global__ void __launch_bounds__(kThreads) kron_spmv_kernel(KronView m, const double2* x, double2* y, double scale) {
-  kron_loop(m, x, [&](long long row, double2 acc, bool valid) {
+  kron_tiles(m, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
@@ -723,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0, smax = 0;
   const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  kron_loop(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+  kron_tiles(a.m, a.x, [&](long long row, double2 acc, bool valid) {
     if (!valid) return;
     const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
     const double2 sv0 = ld_once(a.sum_in + row, once);
@@ -757,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_te
   const unsigned long long keep = evict_last_policy();
   double2* const kp = a.kp;
   const double scale = a.scale;
-  kron_loop(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  kron_tiles(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
   series_term_finish(a, tmax, red);
 }
 
@@ -874,6 +994,34 @@ __global__ void probs_kernel(double2* v, long long row0, long long rows, long lo
   }
 }
 
+// *flag = 0 when some X(i, j) != conj X(j, i) (i <= j); one thread per
+// upper element, lanes along i (the mirrored reads are strided).
+__global__ void hermitian_check_kernel(const double2* __restrict__ x, long long n, int* flag) {
+  const long long total = n * n;
+  bool ok = true;
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < total;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long j = k / n, i = k - j * n;
+    if (i > j) continue;
+    const double2 a = __ldg(x + k), b = __ldg(x + i * n + j);
+    ok = ok && a.x == b.x && a.y == -b.y;
+  }
+  if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) *flag = 0;
+}
+
+__global__ void pattern_hermitian_kernel(double2* v, long long n) {
+  const long long total = n * n;
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < total;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long j = k / n, i = k - j * n;
+    const long long a = i < j ? i : j, b = i < j ? j : i;
+    const unsigned long long h = (static_cast<unsigned long long>(a * n + b) + 1) * 0x9E3779B97F4A7C15ull;
+    const double re = static_cast<double>(h >> 11) * 0x1p-53 - 0.5;
+    const double im = i == j ? 0.0 : static_cast<double>((h * 0xBF58476D1CE4E5B9ull) >> 11) * 0x1p-53 - 0.5;
+    v[k] = make_double2(re, i <= j ? im : -im);
+  }
+}
+
 __global__ void pattern_kernel(double2* v, long long n) {
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -913,7 +1061,8 @@ std::pair<int, std::size_t> kron_geom(K kernel, const KronView& m) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
-  long long want = (m.rows + kThreads - 1) / kThreads;
+  const long long nti = (m.n + kKT - 1) / kKT, ntj = (m.rows / (m.n > 0 ? m.n : 1) + kKT - 1) / kKT;
+  long long want = nti * ntj;
   if (want < 1) want = 1;
   return {static_cast<int>(want < cap ? want : cap), std::size_t{0}};
 }
@@ -1054,6 +1203,15 @@ void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
   }
 }
 
+void kron_hermitian_check(const DevMatrix& m, const double2* x, cudaStream_t s) {
+  if (m.format != Format::Kron || m.kron.herm == nullptr) return;
+  QSWG_CUDA(cudaMemsetAsync(m.kron.herm, 1, sizeof(int), s));  // any non-zero value = Hermitian
+  const long long n = m.kron.n;
+  const long long want = (n * n + kThreads - 1) / kThreads, cap = sm_count() * 8LL;
+  hermitian_check_kernel<<<static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap), kThreads, 0, s>>>(x, n, m.kron.herm);
+  QSWG_LAUNCH_CHECK("kron_hermitian_check");
+}
+
 void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaStream_t s) {
   if (m.format == Format::Kron) {
     kron_prepare(m, x, s);  // single-GPU product (multi-GPU callers exchange W first)
@@ -1080,6 +1238,11 @@ void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std
 void fill_pattern(double2* v, std::int64_t n, cudaStream_t s) {
   pattern_kernel<<<small_grid(n), kThreads, 0, s>>>(v, n);
   QSWG_LAUNCH_CHECK("fill_pattern");
+}
+
+void fill_pattern_hermitian(double2* v, std::int64_t n, cudaStream_t s) {
+  pattern_hermitian_kernel<<<small_grid(n * n), kThreads, 0, s>>>(v, n);
+  QSWG_LAUNCH_CHECK("fill_pattern_hermitian");
 }
 
 void state_from_probabilities(double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,

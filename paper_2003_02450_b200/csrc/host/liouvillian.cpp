@@ -407,6 +407,7 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.d_loc = o.d_loc;
     m.kron.d_ss = o.d_ss;
     m.kron.omega = o.omega;
+    m.kron.herm = herm_flag_.get();
   }
   return m;
 }
@@ -478,7 +479,9 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
 
 void Liouvillian::multiply(const double2* x, double2* y, double scale) const {
   DeviceGuard g(device_);
-  dev::spmv(matrix(), x, y, scale, stream_);
+  const dev::DevMatrix m = matrix();
+  dev::kron_hermitian_check(m, x, stream_);
+  dev::spmv(m, x, y, scale, stream_);
 }
 
 double Liouvillian::time_spmv(int iters, int group) const {
@@ -489,6 +492,7 @@ double Liouvillian::time_spmv(int iters, int group) const {
   QSWG_CHECK(cudaEventCreate(&e0));
   QSWG_CHECK(cudaEventCreate(&e1));
   const dev::DevMatrix m = matrix(group);
+  dev::kron_hermitian_check(m, x.get(), stream_);  // x = 0 is Hermitian: the one-GPU Kron product runs in that mode
   dev::spmv(m, x.get(), y.get(), 1.0, stream_);  // warm-up
   QSWG_CHECK(cudaEventRecord(e0, stream_));
   for (int i = 0; i < iters; ++i) dev::spmv(m, x.get(), y.get(), 1.0, stream_);
@@ -695,6 +699,10 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
         l->kron_v_.emplace_back(static_cast<std::size_t>(dim));
         QSWG_CHECK(cudaMemsetAsync(l->kron_v_.back().get(), 0, l->kron_v_.back().bytes(), s));
       }
+    }
+    if (world == 1) {
+      l->herm_flag_.resize(1);
+      QSWG_CHECK(cudaMemsetAsync(l->herm_flag_.get(), 0, sizeof(int), s));
     }
     QSWG_CHECK(cudaStreamSynchronize(s));
     grp.reset();

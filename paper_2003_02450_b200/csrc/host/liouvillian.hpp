@@ -122,6 +122,7 @@ class Liouvillian {
   std::shared_ptr<KronStore> kron_;
   mutable bool kron_ell_ = false;  // use the sliced-ELL copies of A / Q_k
   std::vector<DeviceBuffer<double2>> kron_w_, kron_v_;
+  DeviceBuffer<int> herm_flag_;  // Kron on one GPU: input-is-Hermitian flag (kernels.hpp: KronView::herm)
   mutable Workspace ws_;
 };
 

@@ -112,6 +112,13 @@ struct KronView {
   const double* d_ss = nullptr;
   double omega = 0.0;
   double2* w[kMaxKron] = {};
+  // One GPU only: device flag, 1 when the current input X is exactly
+  // Hermitian (kron_hermitian_check).  Every superoperator here maps
+  // Hermitian X to Hermitian L(X) (Lindblad form), so the kernels then
+  // compute the upper-triangular 32 x 32 tiles only and write each one twice
+  // (Y(j,i) = conj Y(i,j), real diagonal); the iterates stay exactly
+  // Hermitian.  nullptr (row-partitioned runs) = always the full product.
+  int* herm = nullptr;
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
@@ -267,6 +274,9 @@ void series_flush_control(SeriesCtl* ctl, double tol, cudaStream_t s);
 // Kron format: W_k = Q_k X on the local columns (call before every product
 // with input x; multi-GPU callers then exchange the W_k halos).
 void kron_prepare(const DevMatrix& l, const double2* x, cudaStream_t s);
+// Kron format, one GPU: sets *m.kron.herm to whether x (dim) is exactly
+// Hermitian as an n x n matrix.  No-op for other formats / multi-GPU.
+void kron_hermitian_check(const DevMatrix& l, const double2* x, cudaStream_t s);
 // y = scale * (L x) (liouvillian.cpp:346-360).
 void spmv(const DevMatrix& l, const double2* x, double2* y, double scale, cudaStream_t s);
 // pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).
@@ -274,6 +284,8 @@ void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std
                double* pops, cudaStream_t s);
 // Deterministic non-zero test pattern (benchmark inputs).
 void fill_pattern(double2* v, std::int64_t n, cudaStream_t s);
+// Deterministic Hermitian n x n test pattern (column-major, n*n entries).
+void fill_pattern_hermitian(double2* v, std::int64_t n, cudaStream_t s);
 // v = 0 except v[i*(n+1)] = p[i] (walk.cpp:101-126 without the dense host rho).
 void state_from_probabilities(double2* v_local, std::int64_t row0, std::int64_t rows,
                               std::int64_t n, const double* p, cudaStream_t s);
