@@ -558,15 +558,26 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
 #define QSWG_KRON_MIN_BLOCKS 4  // <= 64 registers: 4 resident blocks of 256 threads per SM
 #endif
 
-// Matrix-free action (kernels.hpp: KronView), in 32 x 32 tiles of X: lane
-// = rho row i (operand rows of A, R_k per lane, coalesced in sliced ELL),
-// warp w = rho columns j0 + 4w .. j0 + 4w + 3 (operand rows of B, P_k, S_k
-// warp-uniform).  Each thread accumulates its 4 elements together, so every
-// row-indexed operand entry is loaded once per 4 outputs and 4 independent
-// gathers are in flight per entry.  The B (x) I and P (x) Q parts stream
-// coalesced columns of X and W_k; the I (x) A gathers stay inside columns j.
+// Matrix-free action (kernels.hpp: KronView), in 32 x 32 tiles of X.
+// Per element the terms are summed in the order
+//   A, R_1 .. R_nk (row-indexed operands),  B, P_1, S_1, .., P_nk, S_nk,
+//   T, decay (column-indexed operands and the diagonal terms),
+// in every path, so the Hermitian path reproduces the general one bit for bit.
+//
+// General path: lane = rho row i, warp w = rho columns j0 + 4w .. j0 + 4w + 3.
+// Row-indexed operands are per lane (sliced ELL when padding is small, so the
+// operand loads are coalesced), each entry loaded once for 4 columns with 4
+// gathers in flight; column-indexed operand rows are warp-uniform and their
+// gathers X(i, c), W_k(i, a), V_k(i, a) stream coalesced columns.
+//
+// Hermitian path (X = X', one GPU): only tiles I <= J, and the row-indexed
+// part is computed transposed — warp w = rows i0 + 4w + r, lane = column j —
+// from X(c, j) = conj X(j, c) = conj x[n c + j], so those gathers are
+// coalesced too and every operand row is warp-uniform; the partial sums meet
+// in shared memory, the column-indexed part continues in the normal
+// orientation, and the tile is written twice (Y(j, i) = conj Y(i, j)).
 constexpr int kKT = 32;                      // tile edge
-constexpr int kKR = kKT / (kThreads / 32);   // columns per thread (4)
+constexpr int kKR = kKT / (kThreads / 32);   // columns (rows) per thread (4)
 
 __device__ __forceinline__ void cfma(double2& acc, double2 v, double2 xv) {
   acc.x = fma(v.x, xv.x, acc.x);
@@ -574,16 +585,12 @@ __device__ __forceinline__ void cfma(double2& acc, double2 v, double2 xv) {
   acc.y = fma(v.x, xv.y, acc.y);
   acc.y = fma(v.y, xv.x, acc.y);
 }
+__device__ __forceinline__ double2 conj2(double2 v) { return make_double2(v.x, -v.y); }
 
-// acc[r] = (L x) at rho element (i, j[r]) (global row i, global columns j[r]);
-// i and j[r] are clamped to valid indices by the caller.  Per element the
-// terms are summed in the order A, B, then per k: P_k, R_k, S_k, then T,
-// decay.
-__device__ __forceinline__ void kron_tile_acc(const KronView& m, const double2* __restrict__ x, int i,
-                                              const int* j, double2* acc, unsigned long long xpol) {
+// Row-indexed part at (i, j[r]), lane = row i: A then R_k.
+__device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2* __restrict__ x, int i,
+                                               const int* j, double2* acc, unsigned long long xpol) {
   const long long n = m.n;
-#pragma unroll
-  for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
   if (m.a_ell.sptr) {  // I (x) A: columns j of X, operand rows in sliced ELL
     const int sl = i >> 5, lane = i & 31;
     const int b = __ldg(m.a_ell.sptr + sl), len = (__ldg(m.a_ell.sptr + sl + 1) - b) >> 5;
@@ -606,28 +613,9 @@ __device__ __forceinline__ void kron_tile_acc(const KronView& m, const double2* 
       for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + j[r] * n + c, xpol));
     }
   }
-  if (m.b.ptr) {  // B (x) I: coalesced columns c of X
-    const double2* xi = x + i;
-#pragma unroll
-    for (int r = 0; r < kKR; ++r) {
-      const int e1 = __ldg(m.b.ptr + j[r] + 1);
-#pragma unroll 4
-      for (int e = __ldg(m.b.ptr + j[r]); e < e1; ++e)
-        cfma(acc[r], __ldg(m.b.val + e), ld_gather(xi + static_cast<long long>(__ldg(m.b.col + e)) * n, xpol));
-    }
-  }
-  for (int k = 0; k < m.nk; ++k) {  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
-    const KronList& p = m.p[k];
-    const double2* wi = m.w[k] + i;
-#pragma unroll
-    for (int r = 0; r < kKR; ++r) {
-      const int e1 = __ldg(p.ptr + j[r] + 1);
-#pragma unroll 4
-      for (int e = __ldg(p.ptr + j[r]); e < e1; ++e)
-        cfma(acc[r], __ldg(p.val + e), ld_gather(wi + static_cast<long long>(__ldg(p.col + e)) * n, xpol));
-    }
-    if (m.factored) {
-      const KronList& rk = m.r[k];  // -w/2 L'(L X): columns j of W_k
+  if (m.factored) {
+    for (int k = 0; k < m.nk; ++k) {  // -w/2 L'(L X): columns j of W_k
+      const KronList& rk = m.r[k];
       const int r1 = __ldg(rk.ptr + i + 1);
       const double2* wk = m.w[k];
 #pragma unroll 2
@@ -637,15 +625,59 @@ __device__ __forceinline__ void kron_tile_acc(const KronView& m, const double2* 
 #pragma unroll
         for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(wk + j[r] * n + c, xpol));
       }
-      const KronList& sk = m.s[k];  // -w/2 (X L') L: columns of V_k
+    }
+  }
+}
+
+// acc += sum over operand row `row` of val * g(col) (warp-uniform row).
+template <class G>
+__device__ __forceinline__ void uniform_row(const KronList& l, int row, double2& acc, G&& g) {
+  const int e1 = __ldg(l.ptr + row + 1);
+#pragma unroll 4
+  for (int e = __ldg(l.ptr + row); e < e1; ++e) cfma(acc, __ldg(l.val + e), g(__ldg(l.col + e)));
+}
+
+// Row-indexed part, transposed (Hermitian path): acc[r] at (i[r], j), warp-
+// uniform rows i[r], lane = column j: A from conj X(j, c), R_k from the
+// row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).
+__device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
+                                                  int j, double2* acc, unsigned long long xpol) {
+  const long long n = m.n;
+  if (m.a.ptr) {
+#pragma unroll
+    for (int r = 0; r < kKR; ++r)
+      uniform_row(m.a, i[r], acc[r], [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
+  }
+  if (m.factored) {
+    for (int k = 0; k < m.nk; ++k) {
+      const double2* wt = m.wt[k];
+#pragma unroll
+      for (int r = 0; r < kKR; ++r)
+        uniform_row(m.r[k], i[r], acc[r], [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
+    }
+  }
+}
+
+// Column-indexed part and diagonal terms at (i, j[r]), lane = row i.
+__device__ __forceinline__ void kron_cols(const KronView& m, const double2* __restrict__ x, int i, const int* j,
+                                          double2* acc, unsigned long long xpol) {
+  const long long n = m.n;
+  if (m.b.ptr) {  // B (x) I: coalesced columns c of X
+    const double2* xi = x + i;
+#pragma unroll
+    for (int r = 0; r < kKR; ++r)
+      uniform_row(m.b, j[r], acc[r], [&](int c) { return ld_gather(xi + static_cast<long long>(c) * n, xpol); });
+  }
+  for (int k = 0; k < m.nk; ++k) {
+    const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
+#pragma unroll
+    for (int r = 0; r < kKR; ++r)
+      uniform_row(m.p[k], j[r], acc[r], [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
+    if (m.factored) {  // -w/2 (X L') L: columns of V_k
       const double2* vi = m.v[k] + i;
 #pragma unroll
-      for (int r = 0; r < kKR; ++r) {
-        const int s1 = __ldg(sk.ptr + j[r] + 1);
-#pragma unroll 4
-        for (int e = __ldg(sk.ptr + j[r]); e < s1; ++e)
-          cfma(acc[r], __ldg(sk.val + e), ld_gather(vi + static_cast<long long>(__ldg(sk.col + e)) * n, xpol));
-      }
+      for (int r = 0; r < kKR; ++r)
+        uniform_row(m.s[k], j[r], acc[r], [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
     }
   }
 #pragma unroll
@@ -672,129 +704,199 @@ __device__ __forceinline__ void kron_tile_acc(const KronView& m, const double2* 
   }
 }
 
-// Hermitian mode in effect for this launch (block-uniform).
-__device__ __forceinline__ bool kron_herm(const KronView& m) {
-  return m.herm != nullptr && *(volatile const int*)m.herm != 0;
+// Tile enumeration: J-major (blocks launched together share the columns J).
+// Hermitian mode enumerates the upper tiles I <= J only.
+struct TileGrid {
+  int n, nc, nti, ntj;
+  long long c0, ntiles;
+};
+
+__device__ __forceinline__ TileGrid tile_grid(const KronView& m, bool herm) {
+  TileGrid g;
+  g.n = m.n;
+  g.nc = static_cast<int>(m.rows / m.n);
+  g.c0 = m.row0 / m.n;
+  g.nti = (g.n + kKT - 1) / kKT;
+  g.ntj = (g.nc + kKT - 1) / kKT;
+  g.ntiles = herm ? static_cast<long long>(g.nti) * (g.nti + 1) / 2 : static_cast<long long>(g.nti) * g.ntj;
+  return g;
 }
 
-// Persistent loop over 32 x 32 tiles of the local columns, J-major (blocks
-// launched together share the columns J that the I (x) A part gathers
-// from).  epi(local_row, value, valid) runs on every thread for every
-// element (valid is false outside the matrix and for the elements a
-// Hermitian tile takes from its mirror).  In Hermitian mode only tiles
-// I <= J are computed; each is written directly and, through a shared-memory
-// transpose, conjugated into tile (J, I) (coalesced both ways); diagonal
-// tiles keep their upper triangle, a real diagonal and its mirror.
-template <class Epi>
-__device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
-  __shared__ double2 tile[kKT][kKT + 1];
-  const unsigned long long xpol = evict_last_policy();
-  const int n = m.n;
-  const int nc = static_cast<int>(m.rows / n);
-  const long long c0 = m.row0 / n;
-  const bool herm = kron_herm(m);
-  const int nti = (n + kKT - 1) / kKT, ntj = (nc + kKT - 1) / kKT;
-  const long long ntiles = herm ? static_cast<long long>(nti) * (nti + 1) / 2 : static_cast<long long>(nti) * ntj;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int I, J;
-    if (herm) {
-      J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
-      while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
-      while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
-      I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
-    } else {
-      J = static_cast<int>(t / nti);
-      I = static_cast<int>(t - static_cast<long long>(J) * nti);
-    }
-    const int iu = I * kKT + lane;
-    const bool vi = iu < n;
-    const int i = vi ? iu : n - 1;
-    int jl[kKR], jg[kKR];
-#pragma unroll
-    for (int r = 0; r < kKR; ++r) {
-      jl[r] = J * kKT + kKR * w + r;
-      jg[r] = static_cast<int>(c0) + (jl[r] < nc ? jl[r] : nc - 1);
-    }
-    double2 acc[kKR];
-    kron_tile_acc(m, x, i, jg, acc, xpol);
-    const bool diag = herm && I == J;
-#pragma unroll
-    for (int r = 0; r < kKR; ++r) {
-      const int jt = kKR * w + r;  // column within the tile
-      double2 y = acc[r];
-      if (diag && lane == jt) y.y = 0.0;
-      epi(static_cast<long long>(jl[r]) * n + iu, y, vi && jl[r] < nc && (!diag || lane <= jt));
-      if (herm) tile[jt][lane] = acc[r];
-    }
-    if (herm) {
-      __syncthreads();
-      // mirror: element (row J*32 + lane, column I*32 + it) = conj Y(I*32 + it, J*32 + lane)
-      const int jrow = J * kKT + lane;
-#pragma unroll
-      for (int r = 0; r < kKR; ++r) {
-        const int it = kKR * w + r;
-        const double2 v = tile[lane][it];
-        const int icol = I * kKT + it;
-        epi(static_cast<long long>(icol) * n + jrow, make_double2(v.x, -v.y),
-            jrow < n && icol < n && (!diag || lane > it));
-      }
-      __syncthreads();
-    }
+__device__ __forceinline__ void tile_coords(const TileGrid& g, bool herm, long long t, int& I, int& J) {
+  if (herm) {
+    J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
+    while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
+    while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
+    I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
+  } else {
+    J = static_cast<int>(t / g.nti);
+    I = static_cast<int>(t - static_cast<long long>(J) * g.nti);
   }
 }
 
-// W_k = Q_k X on the local columns (W_k(i, a) at w[n*a + i], global index),
-// in the tiles of kron_tiles (lane = row i, 4 columns a per thread).
-__global__ void __launch_bounds__(kThreads) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {
-  const unsigned long long xpol = evict_last_policy();
-  const long long n = m.n;
-  const int nc = static_cast<int>(m.rows / m.n);
-  const long long c0 = m.row0 / m.n;
-  const KronEll& qe = m.q_ell[k];
-  const KronList& q = m.q[k];
-  const int nti = (m.n + kKT - 1) / kKT, ntj = (nc + kKT - 1) / kKT;
-  const long long ntiles = static_cast<long long>(nti) * ntj;
+// Writes one computed tile (acc[r] at row I*32 + lane, column J*32 + 4w + r)
+// through epi(local_row, value, valid): directly and, in Hermitian mode,
+// conjugated into tile (J, I) through a shared-memory transpose (coalesced
+// both ways); diagonal tiles keep their upper triangle, a real diagonal and
+// its mirror.  Every thread of the block calls it.
+template <bool kHerm, class Epi>
+__device__ __forceinline__ void kron_tile_emit(const TileGrid& g, int I, int J, const double2* acc,
+                                               double2 (*tile)[kKT + 1], Epi&& epi) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int J = static_cast<int>(t / nti), I = static_cast<int>(t - static_cast<long long>(J) * nti);
+  const int n = g.n;
+  const int iu = I * kKT + lane;
+  const bool diag = kHerm && I == J;
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) {
+    const int jt = kKR * w + r;  // column within the tile
+    const int jl = J * kKT + jt;
+    double2 y = acc[r];
+    if (diag && lane == jt) y.y = 0.0;
+    epi(static_cast<long long>(jl) * n + iu, y, iu < n && jl < g.nc && (!diag || lane <= jt));
+    if (kHerm) tile[jt][lane] = acc[r];
+  }
+  if (kHerm) {
+    __syncthreads();
+    // mirror: element (row J*32 + lane, column I*32 + it) = conj Y(I*32 + it, J*32 + lane)
+    const int jrow = J * kKT + lane;
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const int it = kKR * w + r;
+      const double2 v = tile[lane][it];
+      const int icol = I * kKT + it;
+      epi(static_cast<long long>(icol) * n + jrow, conj2(v), jrow < n && icol < n && (!diag || lane > it));
+    }
+    __syncthreads();
+  }
+}
+
+// Persistent loop over the tiles; epi(local_row, value, valid) runs on every
+// thread for every element (valid is false outside the matrix and for the
+// elements a Hermitian tile takes from its mirror).
+template <bool kHerm, class Epi>
+__device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
+  __shared__ double2 tile[kKT][kKT + 1];
+  const unsigned long long xpol = evict_last_policy();
+  const TileGrid g = tile_grid(m, kHerm);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    int I, J;
+    tile_coords(g, kHerm, t, I, J);
     const int iu = I * kKT + lane;
-    const bool vi = iu < m.n;
-    const int i = vi ? iu : m.n - 1;
-    long long col[kKR];
-    bool vj[kKR];
+    const int i = iu < g.n ? iu : g.n - 1;
+    int jg[kKR];
 #pragma unroll
     for (int r = 0; r < kKR; ++r) {
       const int jl = J * kKT + kKR * w + r;
-      vj[r] = jl < nc;
-      col[r] = (c0 + (vj[r] ? jl : nc - 1)) * n;
+      jg[r] = static_cast<int>(g.c0) + (jl < g.nc ? jl : g.nc - 1);
     }
+    double2 acc[kKR];
+    if constexpr (kHerm) {
+      int ir[kKR];
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const int iv = I * kKT + kKR * w + r;
+        ir[r] = iv < g.n ? iv : g.n - 1;
+        acc[r] = make_double2(0.0, 0.0);
+      }
+      const int ju = J * kKT + lane;
+      kron_rows_uniform(m, x, ir, ju < g.n ? ju : g.n - 1, acc, xpol);
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) tile[kKR * w + r][lane] = acc[r];  // [row][column] of the tile
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) acc[r] = tile[lane][kKR * w + r];
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
+      kron_rows_lane(m, x, i, jg, acc, xpol);
+    }
+    kron_cols(m, x, i, jg, acc, xpol);
+    kron_tile_emit<kHerm>(g, I, J, acc, tile, epi);
+  }
+}
+
+// W_k = Q_k X on the local columns (W_k(i, a) at w[n*a + i], global index)
+// in the tiles of kron_tiles.  General path: lane = row i, 4 columns a per
+// thread (per-lane operand rows).  Hermitian path: warp-uniform rows i, lane
+// = column a, gathers conj X(a, b) coalesced; the tile is transposed through
+// shared memory for the column-major store, and (factored dissipator) also
+// stored row-major into Wt_k for the transposed R_k part.
+#ifndef QSWG_KRON_W_MIN_BLOCKS
+#define QSWG_KRON_W_MIN_BLOCKS 1
+#endif
+template <bool kHerm>
+__global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {
+  __shared__ double2 tile[kKT][kKT + 1];
+  const unsigned long long xpol = evict_last_policy();
+  const long long n = m.n;
+  const TileGrid g = tile_grid(m, false);
+  const KronEll& qe = m.q_ell[k];
+  const KronList& q = m.q[k];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    int I, J;
+    tile_coords(g, false, t, I, J);
     double2 acc[kKR];
 #pragma unroll
     for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
-    if (qe.sptr) {
-      const int sl = i >> 5, ln = i & 31;
-      const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
-#pragma unroll 2
-      for (int e = 0; e < len; ++e) {
-        const int c = __ldg(qe.col + b + 32 * e + ln);
-        const double2 v = __ldg(qe.val + b + 32 * e + ln);
+    if constexpr (kHerm) {
+      const int au = J * kKT + lane;  // column a (single GPU: c0 = 0)
+      const int a = au < g.n ? au : g.n - 1;
 #pragma unroll
-        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+      for (int r = 0; r < kKR; ++r) {
+        const int iv = I * kKT + kKR * w + r;
+        const int i = iv < g.n ? iv : g.n - 1;
+        if (q.ptr)
+          uniform_row(q, i, acc[r], [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
+        if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<long long>(iv) * n + au, acc[r], xpol);
+        tile[kKR * w + r][lane] = acc[r];
       }
-    } else if (q.ptr) {
-      const int e1 = __ldg(q.ptr + i + 1);
-#pragma unroll 2
-      for (int e = __ldg(q.ptr + i); e < e1; ++e) {
-        const int c = __ldg(q.col + e);
-        const double2 v = __ldg(q.val + e);
+      __syncthreads();
+      const int iu = I * kKT + lane;
 #pragma unroll
-        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+      for (int r = 0; r < kKR; ++r) {
+        const int at = J * kKT + kKR * w + r;
+        if (iu < g.n && at < g.n) st_hint(m.w[k] + static_cast<long long>(at) * n + iu, tile[lane][kKR * w + r], xpol);
       }
+      __syncthreads();
+    } else {
+      const int iu = I * kKT + lane;
+      const bool vi = iu < m.n;
+      const int i = vi ? iu : m.n - 1;
+      long long col[kKR];
+      bool vj[kKR];
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const int jl = J * kKT + kKR * w + r;
+        vj[r] = jl < g.nc;
+        col[r] = (g.c0 + (vj[r] ? jl : g.nc - 1)) * n;
+      }
+      if (qe.sptr) {
+        const int sl = i >> 5, ln = i & 31;
+        const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
+#pragma unroll 2
+        for (int e = 0; e < len; ++e) {
+          const int c = __ldg(qe.col + b + 32 * e + ln);
+          const double2 v = __ldg(qe.val + b + 32 * e + ln);
+#pragma unroll
+          for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+        }
+      } else if (q.ptr) {
+        const int e1 = __ldg(q.ptr + i + 1);
+#pragma unroll 2
+        for (int e = __ldg(q.ptr + i); e < e1; ++e) {
+          const int c = __ldg(q.col + e);
+          const double2 v = __ldg(q.val + e);
+#pragma unroll
+          for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kKR; ++r)
+        if (vi && vj[r]) st_hint(m.w[k] + col[r] + i, acc[r], xpol);
     }
-#pragma unroll
-    for (int r = 0; r < kKR; ++r)
-      if (vi && vj[r]) st_hint(m.w[k] + col[r] + i, acc[r], xpol);
   }
 }
 
@@ -816,8 +918,9 @@ __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const doub
   }
 }
 
+template <bool kHerm>
 __global__ void __launch_bounds__(kThreads) kron_spmv_kernel(KronView m, const double2* x, double2* y, double scale) {
-  kron_tiles(m, x, [&](long long row, double2 acc, bool valid) {
+  kron_tiles<kHerm>(m, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
@@ -836,6 +939,7 @@ struct KronStepArgs {
   int decide;
 };
 
+template <bool kHerm>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term_kernel(KronStepArgs a) {
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
@@ -843,7 +947,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0, smax = 0;
   const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  kron_tiles(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+  kron_tiles<kHerm>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
     if (!valid) return;
     const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
     const double2 sv0 = ld_once(a.sum_in + row, once);
@@ -870,6 +974,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term
   }
 }
 
+template <bool kHerm>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
   if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
@@ -877,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_te
   const unsigned long long keep = evict_last_policy();
   double2* const kp = a.kp;
   const double scale = a.scale;
-  kron_tiles(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  kron_tiles<kHerm>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
   series_term_finish(a, tmax, red);
 }
 
@@ -1135,8 +1240,13 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
                double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, bool decide, cudaStream_t s) {
   if (m.format == Format::Kron) {
     KronStepArgs a{m.kron, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
-    const auto g = kron_geom(kron_step_term_kernel, m.kron);
-    kron_step_term_kernel<<<g.first, kThreads, g.second, s>>>(a);
+    if (m.kron.herm) {
+      const auto g = kron_geom(kron_step_term_kernel<true>, m.kron);
+      kron_step_term_kernel<true><<<g.first, kThreads, g.second, s>>>(a);
+    } else {
+      const auto g = kron_geom(kron_step_term_kernel<false>, m.kron);
+      kron_step_term_kernel<false><<<g.first, kThreads, g.second, s>>>(a);
+    }
   } else if (m.format == Format::Sell) {
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
@@ -1162,8 +1272,13 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int /*p*/, b
                  double tol, SeriesCtl* ctl, bool decide, cudaStream_t s) {
   const SeriesTermArgs a{x, kp, last ? 1 : 0, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Kron) {
-    const auto g = kron_geom(kron_series_term_kernel, m.kron);
-    kron_series_term_kernel<<<g.first, kThreads, g.second, s>>>(a, m.kron);
+    if (m.kron.herm) {
+      const auto g = kron_geom(kron_series_term_kernel<true>, m.kron);
+      kron_series_term_kernel<true><<<g.first, kThreads, g.second, s>>>(a, m.kron);
+    } else {
+      const auto g = kron_geom(kron_series_term_kernel<false>, m.kron);
+      kron_series_term_kernel<false><<<g.first, kThreads, g.second, s>>>(a, m.kron);
+    }
   } else if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_series_term_kernel<true><<<sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s>>>(a, m.sell);
@@ -1192,8 +1307,13 @@ void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, 
 void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
   if (m.format != Format::Kron) return;
   for (int k = 0; k < m.kron.nk; ++k) {
-    const auto g = kron_geom(kron_w_kernel, m.kron);
-    kron_w_kernel<<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
+    if (m.kron.herm) {
+      const auto g = kron_geom(kron_w_kernel<true>, m.kron);
+      kron_w_kernel<true><<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
+    } else {
+      const auto g = kron_geom(kron_w_kernel<false>, m.kron);
+      kron_w_kernel<false><<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
+    }
     QSWG_LAUNCH_CHECK("kron_prepare");
     if (m.kron.factored) {
       const auto gv = kron_geom(kron_v_kernel, m.kron);
@@ -1203,20 +1323,29 @@ void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
   }
 }
 
-void kron_hermitian_check(const DevMatrix& m, const double2* x, cudaStream_t s) {
-  if (m.format != Format::Kron || m.kron.herm == nullptr) return;
-  QSWG_CUDA(cudaMemsetAsync(m.kron.herm, 1, sizeof(int), s));  // any non-zero value = Hermitian
+bool kron_hermitian_check(const DevMatrix& m, const double2* x, cudaStream_t s) {
+  if (m.format != Format::Kron || m.kron.herm_flag == nullptr) return false;
+  QSWG_CUDA(cudaMemsetAsync(m.kron.herm_flag, 1, sizeof(int), s));  // any non-zero value = Hermitian
   const long long n = m.kron.n;
   const long long want = (n * n + kThreads - 1) / kThreads, cap = sm_count() * 8LL;
-  hermitian_check_kernel<<<static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap), kThreads, 0, s>>>(x, n, m.kron.herm);
+  hermitian_check_kernel<<<static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap), kThreads, 0, s>>>(x, n, m.kron.herm_flag);
   QSWG_LAUNCH_CHECK("kron_hermitian_check");
+  int flag = 0;
+  QSWG_CUDA(cudaMemcpyAsync(&flag, m.kron.herm_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  QSWG_CUDA(cudaStreamSynchronize(s));
+  return flag != 0;
 }
 
 void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaStream_t s) {
   if (m.format == Format::Kron) {
     kron_prepare(m, x, s);  // single-GPU product (multi-GPU callers exchange W first)
-    const auto g = kron_geom(kron_spmv_kernel, m.kron);
-    kron_spmv_kernel<<<g.first, kThreads, g.second, s>>>(m.kron, x, y, scale);
+    if (m.kron.herm) {
+      const auto g = kron_geom(kron_spmv_kernel<true>, m.kron);
+      kron_spmv_kernel<true><<<g.first, kThreads, g.second, s>>>(m.kron, x, y, scale);
+    } else {
+      const auto g = kron_geom(kron_spmv_kernel<false>, m.kron);
+      kron_spmv_kernel<false><<<g.first, kThreads, g.second, s>>>(m.kron, x, y, scale);
+    }
   } else if (m.format == Format::Sell) {
     if (m.group == 1) {
       sell_spmv_kernel<true><<<sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);

@@ -193,7 +193,7 @@ StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorPara
   DeviceGuard g(l.device());
   const Exec ex(l);
   reset_ctls(l, false);
-  dev::kron_hermitian_check(l.matrix(), v, ex.s);  // Hermitian input: the iterates stay Hermitian
+  l.set_hermitian_input(v);  // Hermitian input: the iterates stay Hermitian
   std::int64_t launches = 0;
   const StepParameters sp = enqueue_step(ex, v, t, params, out, launches);
   const Flags f = read_flags(l, false);
@@ -213,7 +213,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
   const std::int64_t q = steps;
   const double h = (tq - t1) / static_cast<double>(q);
   reset_ctls(l, true);
-  dev::kron_hermitian_check(l.matrix(), v, s);  // Hermitian input: every state stays Hermitian
+  l.set_hermitian_input(v);  // Hermitian input: every state stays Hermitian
   SeriesInfo info;
 
   // states[0] = step(v, t1) (expm.cpp:225)
@@ -322,13 +322,13 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   double2* z = ex.local(kZ);
   dev::SeriesSums ss{};
   for (int c = 0; c < count; ++c) ss.s[c] = ex.local(kSums + static_cast<std::size_t>(c));
-  const dev::DevMatrix mat = l.matrix();
-  if (mat.format == dev::Format::Kron && mat.kron.herm) {  // density-matrix-like input, as in a real series
+  if (l.matrix().format == dev::Format::Kron && l.matrix().kron.herm_flag) {  // density-matrix-like input, as in a real series
     dev::fill_pattern_hermitian(ring.k[0], l.n(), s);
-    dev::kron_hermitian_check(mat, ring.k[0], s);
   } else {
     dev::fill_pattern(ring.k[0], ex.dim, s);
   }
+  l.set_hermitian_input(ring.k[0]);
+  const dev::DevMatrix mat = l.matrix();
   dev::fill_pattern(z, ex.rows, s);
   for (int c = 0; c < count; ++c) dev::fill_pattern(ss.s[c], ex.rows, s);
   dev::SeriesCtl* ctl = series_ctl(l);

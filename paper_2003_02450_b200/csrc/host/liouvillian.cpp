@@ -407,7 +407,9 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.d_loc = o.d_loc;
     m.kron.d_ss = o.d_ss;
     m.kron.omega = o.omega;
-    m.kron.herm = herm_flag_.get();
+    m.kron.herm_flag = herm_flag_.get();
+    m.kron.herm = herm_;
+    for (std::size_t k = 0; k < kron_wt_.size(); ++k) m.kron.wt[k] = kron_wt_[k].get();
   }
   return m;
 }
@@ -479,9 +481,13 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
 
 void Liouvillian::multiply(const double2* x, double2* y, double scale) const {
   DeviceGuard g(device_);
-  const dev::DevMatrix m = matrix();
-  dev::kron_hermitian_check(m, x, stream_);
-  dev::spmv(m, x, y, scale, stream_);
+  set_hermitian_input(x);
+  dev::spmv(matrix(), x, y, scale, stream_);
+}
+
+void Liouvillian::set_hermitian_input(const double2* x) const {
+  DeviceGuard g(device_);
+  herm_ = dev::kron_hermitian_check(matrix(), x, stream_) ? 1 : 0;
 }
 
 double Liouvillian::time_spmv(int iters, int group) const {
@@ -491,8 +497,8 @@ double Liouvillian::time_spmv(int iters, int group) const {
   cudaEvent_t e0, e1;
   QSWG_CHECK(cudaEventCreate(&e0));
   QSWG_CHECK(cudaEventCreate(&e1));
+  set_hermitian_input(x.get());  // x = 0 is Hermitian: the one-GPU Kron product runs in that mode
   const dev::DevMatrix m = matrix(group);
-  dev::kron_hermitian_check(m, x.get(), stream_);  // x = 0 is Hermitian: the one-GPU Kron product runs in that mode
   dev::spmv(m, x.get(), y.get(), 1.0, stream_);  // warm-up
   QSWG_CHECK(cudaEventRecord(e0, stream_));
   for (int i = 0; i < iters; ++i) dev::spmv(m, x.get(), y.get(), 1.0, stream_);
@@ -703,6 +709,8 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     if (world == 1) {
       l->herm_flag_.resize(1);
       QSWG_CHECK(cudaMemsetAsync(l->herm_flag_.get(), 0, sizeof(int), s));
+      if (l->kron_->factored)
+        for (std::size_t k = 0; k < hops.p.size(); ++k) l->kron_wt_.emplace_back(static_cast<std::size_t>(dim));
     }
     QSWG_CHECK(cudaStreamSynchronize(s));
     grp.reset();

@@ -81,6 +81,9 @@ class Liouvillian {
   /// Local row block downloaded as CSR with global columns (parity / debug).
   void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
                 std::vector<Complex>& val) const;
+  /// Kron on one GPU: selects the Hermitian kernels for the products that
+  /// follow when x (full-length) is exactly Hermitian (synchronises).
+  void set_hermitian_input(const double2* x) const;
   /// y = scale * L x for device vectors: x full-length (dim), y local (rows).
   void multiply(const double2* x, double2* y, double scale) const;
   /// Mean device time (ms) of one term kernel launch over `iters` launches.
@@ -122,7 +125,9 @@ class Liouvillian {
   std::shared_ptr<KronStore> kron_;
   mutable bool kron_ell_ = false;  // use the sliced-ELL copies of A / Q_k
   std::vector<DeviceBuffer<double2>> kron_w_, kron_v_;
-  DeviceBuffer<int> herm_flag_;  // Kron on one GPU: input-is-Hermitian flag (kernels.hpp: KronView::herm)
+  DeviceBuffer<int> herm_flag_;  // Kron on one GPU: device flag of the Hermiticity check
+  mutable int herm_ = 0;         // the current call's input is Hermitian (kernels.hpp: KronView::herm)
+  std::vector<DeviceBuffer<double2>> kron_wt_;  // factored + one GPU: row-major W_k for the Hermitian path
   mutable Workspace ws_;
 };
 

@@ -112,13 +112,15 @@ struct KronView {
   const double* d_ss = nullptr;
   double omega = 0.0;
   double2* w[kMaxKron] = {};
-  // One GPU only: device flag, 1 when the current input X is exactly
-  // Hermitian (kron_hermitian_check).  Every superoperator here maps
-  // Hermitian X to Hermitian L(X) (Lindblad form), so the kernels then
-  // compute the upper-triangular 32 x 32 tiles only and write each one twice
-  // (Y(j,i) = conj Y(i,j), real diagonal); the iterates stay exactly
-  // Hermitian.  nullptr (row-partitioned runs) = always the full product.
-  int* herm = nullptr;
+  // One GPU only.  Every superoperator here maps Hermitian X to Hermitian
+  // L(X) (Lindblad form); when the input of a call is exactly Hermitian
+  // (kron_hermitian_check, herm = 1) the kernels compute the upper-triangular
+  // 32 x 32 tiles only and write each one twice (Y(j,i) = conj Y(i,j), real
+  // diagonal), so the iterates stay exactly Hermitian.  herm_flag: device int
+  // for the check (nullptr in row-partitioned runs: always the full product).
+  int* herm_flag = nullptr;
+  int herm = 0;
+  double2* wt[kMaxKron] = {};  // factored + Hermitian: row-major copies of W_k
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
@@ -274,9 +276,9 @@ void series_flush_control(SeriesCtl* ctl, double tol, cudaStream_t s);
 // Kron format: W_k = Q_k X on the local columns (call before every product
 // with input x; multi-GPU callers then exchange the W_k halos).
 void kron_prepare(const DevMatrix& l, const double2* x, cudaStream_t s);
-// Kron format, one GPU: sets *m.kron.herm to whether x (dim) is exactly
-// Hermitian as an n x n matrix.  No-op for other formats / multi-GPU.
-void kron_hermitian_check(const DevMatrix& l, const double2* x, cudaStream_t s);
+// Kron format, one GPU: whether x (dim) is exactly Hermitian as an n x n
+// matrix (synchronises the stream).  false for other formats / multi-GPU.
+bool kron_hermitian_check(const DevMatrix& l, const double2* x, cudaStream_t s);
 // y = scale * (L x) (liouvillian.cpp:346-360).
 void spmv(const DevMatrix& l, const double2* x, double2* y, double scale, cudaStream_t s);
 // pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).
