@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -17,6 +18,32 @@ inline void check(cudaError_t e, const char* what) { ::qswg::cuda_check(e, what)
 #define QSWG_LAUNCH_CHECK(name) ::qswg::dev::check(cudaGetLastError(), name)
 
 constexpr int kThreads = 256;
+
+// Resident blocks per SM of `kernel` at kThreads threads (cached per device
+// and kernel: the occupancy query costs microseconds of host time, which
+// would otherwise bound short launches).
+inline int blocks_per_sm(const void* kernel, std::size_t smem = 0) {
+  struct Key {
+    int dev;
+    const void* k;
+    std::size_t smem;
+  };
+  static thread_local Key keys[64];
+  static thread_local int vals[64];
+  static thread_local int used = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < used; ++i)
+    if (keys[i].dev == dev && keys[i].k == kernel && keys[i].smem == smem) return vals[i];
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  if (used < 64) {
+    keys[used] = {dev, kernel, smem};
+    vals[used++] = per_sm;
+  }
+  return per_sm;
+}
 
 inline int sm_count() {
   static thread_local int cached_dev = -1, cached = 0;

@@ -637,23 +637,26 @@ __device__ __forceinline__ void uniform_row(const KronList& l, int row, double2&
   for (int e = __ldg(l.ptr + row); e < e1; ++e) cfma(acc, __ldg(l.val + e), g(__ldg(l.col + e)));
 }
 
+// acc[r] += sum over operand row rows[r] of val * g(col) for r < kKR, one
+// row after the other.  (Walking the kKR rows in lockstep was measured
+// slower on c2-c4.)
+template <class G>
+__device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows, double2* acc, G&& g) {
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) uniform_row(l, rows[r], acc[r], g);
+}
+
 // Row-indexed part, transposed (Hermitian path): acc[r] at (i[r], j), warp-
 // uniform rows i[r], lane = column j: A from conj X(j, c), R_k from the
 // row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).
 __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
                                                   int j, double2* acc, unsigned long long xpol) {
   const long long n = m.n;
-  if (m.a.ptr) {
-#pragma unroll
-    for (int r = 0; r < kKR; ++r)
-      uniform_row(m.a, i[r], acc[r], [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
-  }
+  if (m.a.ptr) uniform_rows(m.a, i, acc, [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
   if (m.factored) {
     for (int k = 0; k < m.nk; ++k) {
       const double2* wt = m.wt[k];
-#pragma unroll
-      for (int r = 0; r < kKR; ++r)
-        uniform_row(m.r[k], i[r], acc[r], [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
+      uniform_rows(m.r[k], i, acc, [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
     }
   }
 }
@@ -664,20 +667,14 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
   const long long n = m.n;
   if (m.b.ptr) {  // B (x) I: coalesced columns c of X
     const double2* xi = x + i;
-#pragma unroll
-    for (int r = 0; r < kKR; ++r)
-      uniform_row(m.b, j[r], acc[r], [&](int c) { return ld_gather(xi + static_cast<long long>(c) * n, xpol); });
+    uniform_rows(m.b, j, acc, [&](int c) { return ld_gather(xi + static_cast<long long>(c) * n, xpol); });
   }
   for (int k = 0; k < m.nk; ++k) {
     const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
-#pragma unroll
-    for (int r = 0; r < kKR; ++r)
-      uniform_row(m.p[k], j[r], acc[r], [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
+    uniform_rows(m.p[k], j, acc, [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
     if (m.factored) {  // -w/2 (X L') L: columns of V_k
       const double2* vi = m.v[k] + i;
-#pragma unroll
-      for (int r = 0; r < kKR; ++r)
-        uniform_row(m.s[k], j[r], acc[r], [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
+      uniform_rows(m.s[k], j, acc, [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
     }
   }
 #pragma unroll
@@ -1139,9 +1136,7 @@ __global__ void pattern_kernel(double2* v, long long n) {
 // ------------------------------------------------------------ launch helpers
 template <class K>
 int persistent_grid(K kernel, long long rows) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-  if (per_sm < 1) per_sm = 1;
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel));
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
   long long want = (rows + kTile - 1) / kTile;
   if (want < 1) want = 1;
@@ -1150,9 +1145,7 @@ int persistent_grid(K kernel, long long rows) {
 
 template <class K>
 int sell_grid(K kernel, const SellView& m) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-  if (per_sm < 1) per_sm = 1;
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel));
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
   long long want = (m.n_slices + kThreads / 32 - 1) / (kThreads / 32);
   if (want < 1) want = 1;
@@ -1162,9 +1155,7 @@ int sell_grid(K kernel, const SellView& m) {
 // Persistent launch geometry of a Kron kernel (no dynamic shared memory).
 template <class K>
 std::pair<int, std::size_t> kron_geom(K kernel, const KronView& m) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-  if (per_sm < 1) per_sm = 1;
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel));
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
   const long long nti = (m.n + kKT - 1) / kKT, ntj = (m.rows / (m.n > 0 ? m.n : 1) + kKT - 1) / kKT;
   long long want = nti * ntj;
