@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
 // is computed with upward rounding: ||S_k|| <= ub_k holds through every
 // rounding of the pending axpys and norms (each at most (1 + 2^-53)), so the
 // settled outcome "continue" is the one the exact test would give.
-__device__ void series_term_control(SeriesCtl* ctl, int last, double tol) {
+__device__ void series_term_control(SeriesCtl* ctl, int p, int last, double tol) {
   ctl->spmvs += 1;
   const double tn = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
   ctl->term_bits = 0;
@@ -226,39 +226,46 @@ __device__ void series_term_control(SeriesCtl* ctl, int last, double tol) {
     ctl->n_active = 0;
     return;
   }
-  const int b = ctl->n_pend;
   const int count = ctl->count;
+  const int slot = p % ctl->slots;
   ctl->tn_last = tn;
-  int need = last || b + 1 >= ctl->pend_max;
+  int pmin = p;
+  for (int k = 0; k < count; ++k)
+    if (ctl->active[k] && ctl->p0[k] < pmin) pmin = ctl->p0[k];
+  // the next term must not overwrite a pending one
+  int any = last || p - pmin + 1 >= ctl->pend_max;
   for (int k = 0; k < count; ++k) {
     if (!ctl->active[k]) continue;
     const double f = ctl->factor[k];
-    ctl->fac_pend[b][k] = f;
+    ctl->fac_ring[slot][k] = f;
     ctl->bound[k] = __dadd_ru(ctl->bound[k], __dmul_ru(f, tn));
     const double ub = __dmul_ru(__dadd_ru(ctl->nf_last[k], ctl->bound[k]), 1.0 + 0x1p-30);
-    if (!(ctl->c1[k] + f * tn > tol * ub)) need = 1;  // expm.cpp:310, 315
+    if (!(ctl->c1[k] + f * tn > tol * ub)) any = 1;  // undecidable (expm.cpp:310, 315)
   }
-  ctl->n_pend = b + 1;
-  if (need) {
-    ctl->flush = 1;  // the flush control runs the exact tests of term p
-    return;
-  }
+  // One undecidable test flushes every active output: each pending term is
+  // then read once per super-step, and a large ring keeps flushes to the
+  // outputs' stop events (measured cheaper than flushing the undecidable
+  // outputs alone, which re-reads the shared terms per output).
   for (int k = 0; k < count; ++k) {
     if (!ctl->active[k]) continue;
-    const double f = ctl->factor[k];
-    ctl->c1[k] = f * tn;                         // every test settled: continue
-    ctl->factor[k] = f * static_cast<double>(k + 1);  // factor *= k for p + 1
+    ctl->mark[k] = any;
+    if (!any) {  // every test settled: continue
+      const double f = ctl->factor[k];
+      ctl->c1[k] = f * tn;
+      ctl->factor[k] = f * static_cast<double>(k + 1);  // factor *= k for p + 1
+    }
   }
+  ctl->flush = any;
 }
 
-// Exact tests of the newest pending term after the flush wrote every S_k.
-__device__ void series_flush_control(SeriesCtl* ctl, double tol) {
-  const int b = ctl->n_pend - 1;
+// Exact tests of term p for the marked outputs after the flush wrote their sums.
+__device__ void series_flush_control(SeriesCtl* ctl, int p, double tol) {
   const int count = ctl->count;
+  const int slot = p % ctl->slots;
   const double tn = ctl->tn_last;
   for (int k = 0; k < count; ++k) {
-    if (!ctl->active[k]) continue;
-    const double f = ctl->fac_pend[b][k];
+    if (!ctl->active[k] || !ctl->mark[k]) continue;
+    const double f = ctl->fac_ring[slot][k];
     const double c2 = f * tn;  // expm.cpp:310
     const double nf = bitsd(*(volatile unsigned long long*)&ctl->sum_bits[k]);
     if (!isfinite(nf)) {  // expm.cpp:312-314
@@ -273,17 +280,19 @@ __device__ void series_flush_control(SeriesCtl* ctl, double tol) {
     ctl->nf_last[k] = nf;
     ctl->bound[k] = 0.0;
     ctl->sum_bits[k] = 0;
+    ctl->p0[k] = p + 1;
+    ctl->fresh[k] = 0;
+    ctl->mark[k] = 0;
   }
   if (ctl->error) ctl->n_active = 0;
-  ctl->n_pend = 0;
   ctl->flush = 0;
-  ctl->fresh = 0;
   ctl->arrivals = 0;
 }
 
 struct SeriesTermArgs {
   const double2* x;
   double2* kp;
+  int p;
   int last;
   double scale;
   double tol;
@@ -316,7 +325,7 @@ __device__ __forceinline__ void series_term_finish(const SeriesTermArgs& a, unsi
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
       if (a.decide) {
-        series_term_control(ctl, a.last, a.tol);
+        series_term_control(ctl, a.p, a.last, a.tol);
       } else {
         ctl->arrivals = 0;  // maximum stays for the allreduce + series_term_control_kernel
       }
@@ -347,28 +356,36 @@ struct SeriesFlushArgs {
   int decide;
 };
 
-// Batched running-sum update (kernels.hpp: series_flush).  Each thread keeps
-// its row of every pending term in registers and walks the active outputs in
-// chunks of kSeriesRegD with all sum loads of a chunk in flight; the order of
-// the additions per output is the term order, as in per-term updates.
+// Batched running-sum update of the marked outputs (kernels.hpp:
+// series_flush).  The marked outputs are walked in chunks of kSeriesRegD
+// with all their sum loads in flight; per chunk the pending terms are read
+// once, oldest first (each output adds only terms from its own first pending
+// one), so every output sums in term order as with per-term updates.
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs a) {
   SeriesCtl* ctl = a.ctl;
   if (!*(volatile int*)&ctl->flush || series_skip(ctl)) return;
-  __shared__ double fac[kPendMax][kMaxSeriesD];
-  __shared__ int act[kMaxSeriesD];
+  __shared__ int list[kMaxSeriesD];   // marked outputs
+  __shared__ int q0[kMaxSeriesD];     // their first pending term
+  __shared__ int fr[kMaxSeriesD];
   __shared__ unsigned long long smax_sh[kMaxSeriesD];
-  __shared__ const double2* kptr[kPendMax];
-  const int nb = ctl->n_pend, count = ctl->count, fresh = ctl->fresh;
-  for (int k = threadIdx.x; k < count; k += blockDim.x) {
-    act[k] = ctl->active[k];
-    smax_sh[k] = 0;
-    for (int b = 0; b < nb; ++b) fac[b][k] = ctl->fac_pend[b][k];
+  __shared__ int nmark;
+  const int count = ctl->count, slots = ctl->slots, p = a.p;
+  if (threadIdx.x == 0) {
+    int nm = 0;
+    for (int k = 0; k < count; ++k) {
+      if (ctl->active[k] && ctl->mark[k]) {
+        list[nm] = k;
+        q0[nm] = ctl->p0[k];
+        fr[nm] = ctl->fresh[k];
+        ++nm;
+      }
+    }
+    nmark = nm;
   }
-  if (threadIdx.x < nb) {
-    const int slot = (a.p - nb + 1 + static_cast<int>(threadIdx.x)) % a.ring.slots;
-    kptr[threadIdx.x] = a.ring.k[slot] + a.row0;
-  }
+  __syncthreads();
+  const int nm = nmark;
+  for (int u = threadIdx.x; u < nm; u += blockDim.x) smax_sh[u] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const unsigned long long once = evict_first_policy();
@@ -376,46 +393,54 @@ __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs 
   for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.rows; base += stride) {
     const long long row = base + threadIdx.x;
     const bool valid = row < a.rows;
-    double2 kv[kPendMax];
-#pragma unroll
-    for (int b = 0; b < kPendMax; ++b)
-      kv[b] = (valid && b < nb) ? ld_once(kptr[b] + row, once) : make_double2(0.0, 0.0);
-    const double2 zv = (fresh && valid) ? ld_once(a.z + row, once) : make_double2(0.0, 0.0);
 #pragma unroll 1
-    for (int k0 = 0; k0 < count; k0 += kSeriesRegD) {
+    for (int u0 = 0; u0 < nm; u0 += kSeriesRegD) {
       double2 sv[kSeriesRegD];
+      int lo = p + 1;
 #pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (valid && k < count && act[k]) sv[u] = fresh ? zv : ld_once(a.sums.s[k] + row, once);
+      for (int v = 0; v < kSeriesRegD; ++v) {
+        const int u = u0 + v;
+        if (u < nm) {
+          lo = q0[u] < lo ? q0[u] : lo;
+          if (valid) sv[v] = ld_once((fr[u] ? a.z : a.sums.s[list[u]]) + row, once);
+        }
+      }
+#pragma unroll 1
+      for (int q = lo; q <= p; ++q) {  // sum += k^q K_q (expm.cpp:300-305)
+        const int sl = q % slots;
+        const double2 kv = valid ? __ldg(a.ring.k[sl] + a.row0 + row) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int v = 0; v < kSeriesRegD; ++v) {
+          const int u = u0 + v;
+          if (u < nm && q >= q0[u] && valid) {
+            const double f = ctl->fac_ring[sl][list[u]];  // block-uniform
+            sv[v] = kStrict ? axpy<1>(sv[v], f, kv) : axpy<2>(sv[v], f, kv);
+          }
+        }
       }
 #pragma unroll
-      for (int u = 0; u < kSeriesRegD; ++u) {
-        const int k = k0 + u;
-        if (k >= count) break;  // block-uniform
-        unsigned long long m = 0;
-        if (valid && act[k]) {
-#pragma unroll
-          for (int b = 0; b < kPendMax; ++b)  // sum += k^q K_q (expm.cpp:300-305)
-            if (b < nb) sv[u] = kStrict ? axpy<1>(sv[u], fac[b][k], kv[b]) : axpy<2>(sv[u], fac[b][k], kv[b]);
-          st_hint(a.sums.s[k] + row, sv[u], once);
-          m = dbits(cabs2(sv[u]));
+      for (int v = 0; v < kSeriesRegD; ++v) {
+        const int u = u0 + v;
+        if (u >= nm) break;  // block-uniform
+        unsigned long long mk = 0;
+        if (valid) {
+          st_hint(a.sums.s[list[u]] + row, sv[v], once);
+          mk = dbits(cabs2(sv[v]));
         }
-        m = warp_max_bits(m);
-        if (lane == 0 && m) atomicMax(&smax_sh[k], m);
+        mk = warp_max_bits(mk);
+        if (lane == 0 && mk) atomicMax(&smax_sh[u], mk);
       }
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < count; k += blockDim.x)
-    if (act[k]) atomicMax(&ctl->sum_bits[k], smax_sh[k]);
+  for (int u = threadIdx.x; u < nm; u += blockDim.x) atomicMax(&ctl->sum_bits[list[u]], smax_sh[u]);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
       __threadfence();
       if (a.decide) {
-        series_flush_control(ctl, a.tol);
+        series_flush_control(ctl, p, a.tol);
       } else {
         ctl->arrivals = 0;
       }
@@ -1024,11 +1049,13 @@ __device__ void series_init_apply(SeriesCtl* ctl, int count, int pend_max, doubl
     ctl->nf_last[k] = nz;  // S_k starts as Z
     ctl->bound[k] = 0.0;
     ctl->sum_bits[k] = 0;
+    ctl->p0[k] = 1;
+    ctl->mark[k] = 0;
+    ctl->fresh[k] = 1;
   }
-  ctl->n_pend = 0;
   ctl->flush = 0;
-  ctl->fresh = 1;
   ctl->pend_max = pend_max < 1 ? 1 : (pend_max > kPendMax ? kPendMax : pend_max);
+  ctl->slots = ctl->pend_max + 1;
   ctl->term_bits = 0;
   ctl->arrivals = 0;
 }
@@ -1064,11 +1091,11 @@ __global__ void series_init_fin_kernel(SeriesCtl* ctl, int count, int pend_max) 
 __global__ void step_control_kernel(StepCtl* ctl, int first_of_stage, int stage, double tol) {
   step_control(ctl, first_of_stage, stage, tol);
 }
-__global__ void series_term_control_kernel(SeriesCtl* ctl, int last, double tol) {
-  series_term_control(ctl, last, tol);
+__global__ void series_term_control_kernel(SeriesCtl* ctl, int p, int last, double tol) {
+  series_term_control(ctl, p, last, tol);
 }
-__global__ void series_flush_control_kernel(SeriesCtl* ctl, double tol) {
-  series_flush_control(ctl, tol);
+__global__ void series_flush_control_kernel(SeriesCtl* ctl, int p, double tol) {
+  series_flush_control(ctl, p, tol);
 }
 
 // --------------------------------------------------------------- plain SpMV
@@ -1217,13 +1244,13 @@ void series_init_fin(SeriesCtl* ctl, int count, int pend_max, cudaStream_t s) {
   QSWG_LAUNCH_CHECK("series_init_fin");
 }
 
-void series_term_control(SeriesCtl* ctl, int last, double tol, cudaStream_t s) {
-  series_term_control_kernel<<<1, 1, 0, s>>>(ctl, last, tol);
+void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s) {
+  series_term_control_kernel<<<1, 1, 0, s>>>(ctl, p, last, tol);
   QSWG_LAUNCH_CHECK("series_term_control");
 }
 
-void series_flush_control(SeriesCtl* ctl, double tol, cudaStream_t s) {
-  series_flush_control_kernel<<<1, 1, 0, s>>>(ctl, tol);
+void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {
+  series_flush_control_kernel<<<1, 1, 0, s>>>(ctl, p, tol);
   QSWG_LAUNCH_CHECK("series_flush_control");
 }
 
@@ -1259,9 +1286,9 @@ void series_init(const double2* z, std::int64_t n, int count, int pend_max, Seri
   QSWG_LAUNCH_CHECK("series_init");
 }
 
-void series_term(const DevMatrix& m, const double2* x, double2* kp, int /*p*/, bool last, double scale,
+void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool last, double scale,
                  double tol, SeriesCtl* ctl, bool decide, cudaStream_t s) {
-  const SeriesTermArgs a{x, kp, last ? 1 : 0, scale, tol, ctl, decide ? 1 : 0};
+  const SeriesTermArgs a{x, kp, p, last ? 1 : 0, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Kron) {
     if (m.kron.herm) {
       const auto g = kron_geom(kron_series_term_kernel<true>, m.kron);

@@ -33,7 +33,7 @@ std::size_t ring_slot(int i) { return i < 2 ? static_cast<std::size_t>(i) : kRin
 
 // Terms a series super-step may hold back (kernels.hpp: SeriesCtl): kPendMax,
 // fewer when the ring of pend_max + 1 full-length vectors would take more
-// than half of the free device memory; QSWG_PEND_MAX overrides (1 = update
+// than 30% of the free device memory; QSWG_PEND_MAX overrides (1 = update
 // the sums after every term).
 int series_pend_max(std::int64_t dim) {
   int pm = dev::kPendMax;
@@ -41,7 +41,7 @@ int series_pend_max(std::int64_t dim) {
   std::size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
     const double vec_b = static_cast<double>(dim) * sizeof(double2);
-    while (pm > 1 && (pm - 1) * vec_b > 0.5 * static_cast<double>(free_b)) --pm;
+    while (pm > 1 && (pm - 1) * vec_b > 0.3 * static_cast<double>(free_b)) --pm;
   }
   return pm;
 }
@@ -286,13 +286,13 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
           continue;
         }
         ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
-        dev::series_term_control(ctl, last ? 1 : 0, params.tolerance, s);
+        dev::series_term_control(ctl, static_cast<int>(p), last ? 1 : 0, params.tolerance, s);
         if (ex.read(&ctl->n_active) == 0) break;
         if (ex.read(&ctl->flush)) {
           dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
                             params.tolerance, ctl, false, s);
           ex.comm->allreduce_max_u64(&ctl->sum_bits[0], static_cast<std::size_t>(count), s);
-          dev::series_flush_control(ctl, params.tolerance, s);
+          dev::series_flush_control(ctl, static_cast<int>(p), params.tolerance, s);
           if (ex.read(&ctl->n_active) == 0) break;
         }
         if (p < m_star) ex.exchange(ring.k[p % ring.slots]);

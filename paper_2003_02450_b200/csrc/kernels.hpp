@@ -11,7 +11,7 @@ namespace qswg::dev {
 inline constexpr int kMaxKron = 8;      // Lindblad operators per G-QSW
 inline constexpr int kMaxSeriesD = 128; // super-step outputs (d <= floor(1e280^(1/55)) = 123)
 inline constexpr int kSeriesRegD = 4;   // running sums updated per chunk in the series kernel
-inline constexpr int kPendMax = 8;      // series terms held back before one batched sum update
+inline constexpr int kPendMax = 64;     // series terms held back before one batched sum update
 
 // A "multi-CSR" over the n x n operator space: rows sorted by column with
 // duplicates kept adjacent in emission order (they are summed on the device
@@ -194,14 +194,15 @@ struct StepCtl {
   double last_nf;
 };
 
-// Series control block.  Running sums are updated lazily: term kernels only
-// write K_p (into a ring of kPendMax + 1 vectors) and ||K_p||; the stop test
-// of every output is first evaluated against a rigorous upper bound of
-// ||S_k|| (last exact norm + sum of the pending terms' norms, rounded up).
-// While every active output provably continues, terms stay pending; the
-// first undecidable test, a full ring or the super-step's last term set
-// `flush`, and the flush kernel then applies all pending terms in order
-// (bit-identical to per-term updates) and runs the exact test.
+// Series control block.  Running sums are updated lazily and per output:
+// term kernels only write K_p (into a ring of pend_max + 1 vectors) and
+// ||K_p||; the stop test of every active output is first evaluated against
+// a rigorous upper bound of ||S_k|| (its last exact norm + the sum of its
+// pending terms' norms, rounded up).  An output whose test is settled
+// ("continues") keeps its terms pending; an undecidable test marks that
+// output, and the flush kernel then adds its pending terms in order
+// (bit-identical to per-term updates) and runs its exact test.  A full ring
+// or the super-step's last term marks every active output.
 struct SeriesCtl {
   unsigned long long term_bits;               // adjacent to sum_bits: one
   unsigned long long sum_bits[kMaxSeriesD];   // allreduce covers both
@@ -210,17 +211,19 @@ struct SeriesCtl {
   int error;
   int spmvs;
   int count;
-  int n_pend;      // terms written but not yet added to the sums
-  int flush;       // the flush kernel after this term must run
-  int fresh;       // the first flush of a super-step starts from Z
-  int pend_max;    // ring capacity in use (<= kPendMax)
+  int flush;       // the flush kernel after this term must run (some output marked)
+  int pend_max;    // ring capacity in use (<= kPendMax); ring slots = pend_max + 1
+  int slots;
   double z_norm;
-  double tn_last;  // ||K_p|| of the newest pending term
+  double tn_last;  // ||K_p|| of the newest term
   double factor[kMaxSeriesD];
   double c1[kMaxSeriesD];
-  double nf_last[kMaxSeriesD];  // exact ||S_k|| at the last flush (||Z|| at the start)
+  double nf_last[kMaxSeriesD];  // exact ||S_k|| at its last flush (||Z|| at the start)
   double bound[kMaxSeriesD];    // upper bound of the pending terms' contribution
-  double fac_pend[kPendMax][kMaxSeriesD];
+  double fac_ring[kPendMax + 1][kMaxSeriesD];  // k^q of the term in ring slot q % slots
+  int p0[kMaxSeriesD];          // first pending term of output k
+  int mark[kMaxSeriesD];        // output k is flushed after this term
+  int fresh[kMaxSeriesD];       // output k's first flush starts from Z
   int active[kMaxSeriesD];
 };
 
@@ -265,14 +268,14 @@ void series_init(const double2* z, std::int64_t n, int count, int pend_max, Seri
 // (always on the super-step's `last` term).
 void series_term(const DevMatrix& l, const double2* x, double2* kp, int p, bool last, double scale,
                  double tol, SeriesCtl* ctl, bool decide, cudaStream_t s);
-void series_term_control(SeriesCtl* ctl, int last, double tol, cudaStream_t s);
-// When ctl->flush: for every active k, S_k = (fresh ? Z : S_k) + sum over the
-// pending terms q of k^q K_q, in term order (expm.cpp:300-305), then the
-// exact stop tests of term p (expm.cpp:306-316).  No-op otherwise.
+void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s);
+// When ctl->flush: for every marked output k, S_k = (fresh_k ? Z : S_k) +
+// sum over its pending terms q of k^q K_q, in term order (expm.cpp:300-305),
+// then its exact stop test of term p (expm.cpp:306-316).  No-op otherwise.
 void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, const double2* z,
                   const SeriesSums& sums, int count, int p, bool strict, double tol, SeriesCtl* ctl,
                   bool decide, cudaStream_t s);
-void series_flush_control(SeriesCtl* ctl, double tol, cudaStream_t s);
+void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s);
 // Kron format: W_k = Q_k X on the local columns (call before every product
 // with input x; multi-GPU callers then exchange the W_k halos).
 void kron_prepare(const DevMatrix& l, const double2* x, cudaStream_t s);
