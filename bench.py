@@ -112,7 +112,9 @@ def workload_desc(w, extra=None):
     d = {"workload": f"{w.name}: {'L-QSW' if w.kind == 'local' else 'G-QSW'} n={w.n} omega={w.omega} "
                      f"t=[{w.t1},{w.tq}] outputs={w.steps + 1}",
          "dim": w.dim, "outputs": w.steps + 1, "omega": w.omega, "kind": w.kind, "seed": w.seed,
-         "l2_policy": "inputs larger than L2 (CSR > 126 MB), no flush"}
+         "l2_policy": "no flush: one step (a whole series) streams far more than the 126 MB L2 "
+                      "(term ring, running sums, stored superoperator), so no input survives in L2 "
+                      "from one step to the next"}
     d.update(extra or {})
     return d
 
@@ -277,23 +279,39 @@ def main():
         e2e_ms = float(t.item())
     del full_vec
 
-    # ---- roofline of the dominant kernel (one series term) ----
+    # ---- roofline of the dominant kernel (the series term kernel) ----
     d_active = int(info.d) if info.path == 2 else 1
     peak, peak_src = load_peaks()
     n_lind = len(w.ops) if w.kind == "global" else 0
 
     def term_bytes(lv):
-        """Algorithmic HBM bytes of one series term with d_active outputs."""
-        vec = 16 * lv.dim + 16 * lv.rows + 32 * d_active * lv.rows  # x read, K_p write, sums r+w
-        if lv.format == "kron":  # W_k = Q_k x (and V_k = x L_k' when factored): written + read once
-            return vec + 32 * n_lind * lv.dim * (2 if lv.info.kron_factored else 1)
+        """Algorithmic HBM bytes of one term-kernel launch: the
+        input x read once, K_p written once, plus the stored superoperator
+        (20 B/nnz + 8 B/row) or, matrix-free, the W_k (and V_k) work vectors
+        read once."""
+        vec = 16 * lv.dim + 16 * lv.rows
+        if lv.format == "kron":
+            return vec + 16 * n_lind * lv.dim * (2 if lv.info.kron_factored else 1)
         return vec + 20 * int(lv.info.nnz_local) + 8 * (lv.rows + 1)
 
-    term_ms = l.time_series_term(iters=20, count=d_active)
+    def prepare_bytes(lv):
+        """Kron prepare kernels: x read, W_k (V_k) written."""
+        if lv.format != "kron":
+            return 0
+        return n_lind * (2 if lv.info.kron_factored else 1) * 32 * lv.dim
+
+    parts = l.time_series_parts(iters=20, count=d_active)
+    term_ms = parts["term"]
     achieved = term_bytes(l) / (term_ms * 1e-3) / 1e9
     share = info.spmvs * term_ms / ms_per_step
-    kernel_name = {"kron": "kron_w_kernel + kron_series_term_kernel", "sell": "sell_series_term_kernel",
-                   "csr": "series_spmv_kernel + series_axpy_kernel"}[l.format]
+    kernel_name = {"kron": "kron_series_term_kernel", "sell": "sell_series_term_kernel",
+                   "csr": "series_term_kernel"}[l.format]
+    parts_line = {"prepare_ms": parts["prepare"], "term_ms": parts["term"], "flush_ms": parts["flush"],
+                  "prepare_kernels": "kron_w_kernel" + (" + kron_v_kernel" if l.info.kron_factored else "")
+                  if l.format == "kron" else None,
+                  "prepare_gbs": prepare_bytes(l) / (parts["prepare"] * 1e-3) / 1e9 if parts["prepare"] > 0 else None,
+                  "flush_kernel": "series_flush_kernel (amortised over the term ring)",
+                  "count": d_active}
 
     # ---- the stored-superoperator SpMV (BASELINE's "superop SpMV HBM GB/s") ----
     superop = None
@@ -305,16 +323,18 @@ def main():
         if ls.padding > 1.03:
             del ls
             ls = build("csr")
-        s_ms = ls.time_series_term(iters=20, count=d_active)
+        sp = ls.time_series_parts(iters=20, count=d_active)
+        s_ms = sp["term"]
         vs = ls.state().from_probabilities(w.rho0)
         api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)  # warm-up
         rs = api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)
         sb = term_bytes(ls)
         superop = {"format": ls.format, "kernel": "sell_series_term_kernel" if ls.format == "sell" else
-                   "series_spmv_kernel + series_axpy_kernel", "bytes_per_launch": sb, "ms_per_launch": s_ms,
+                   "series_term_kernel", "bytes_per_launch": sb, "ms_per_launch": s_ms,
                    "achieved_gbs": sb / (s_ms * 1e-3) / 1e9, "frac": sb / (s_ms * 1e-3) / 1e9 / peak,
+                   "flush_ms": sp["flush"],
                    "series_ms": float(rs.info.device_ms), "output_steps_per_s": w.steps / (rs.info.device_ms / 1e3),
-                   "bytes_note": "20 B/nnz + 8 B/row + x + K_p + 32*d*rows (SURVEY.md 8(d))"}
+                   "bytes_note": "20 B/nnz + 8 B/row + x read + K_p written (SURVEY.md 8(d))"}
         del ls, vs
         l = lk
 
@@ -336,7 +356,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_for(w.name, l.format), "kernel": kernel_name,
                      "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell), "bytes_per_launch": term_bytes(l), "ms_per_launch": term_ms,
-                     "peak_source": peak_src, "share_of_step": share},
+                     "peak_source": peak_src, "share_of_step": share, "parts": parts_line},
         "superop_spmv": superop,
         "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,
                 "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms},

@@ -133,9 +133,11 @@ void qswg_liouvillian_destroy(qswg_liouvillian* l);
 int qswg_spmv(const qswg_liouvillian* l, const double* x, double* y);
 /* Mean device time of one plain SpMV kernel over `iters` back-to-back launches. */
 int qswg_time_spmv(const qswg_liouvillian* l, int iters, int group, double* ms);
-/* Mean device time of one fused series-term kernel (SpMV + `count` axpys +
- * norms) over `iters` back-to-back launches on the library stream. */
+/* Mean device time of one series term (Kron prepare + term kernel + the
+ * amortised running-sum flush of `count` outputs) over `iters` terms. */
 int qswg_time_series_term(const qswg_liouvillian* l, int iters, int count, double* ms);
+/* The same split into its parts: ms4 = {prepare, term kernel, flush, total}. */
+int qswg_time_series_parts(const qswg_liouvillian* l, int iters, int count, double* ms4);
 /* The CUDA stream (cudaStream_t) every kernel of this handle runs on. */
 int qswg_liouvillian_stream(const qswg_liouvillian* l, void** stream);
 

@@ -251,6 +251,12 @@ class Liouvillian:
         check(lib.qswg_time_series_term(self._h, iters, count, C.byref(ms)))
         return ms.value
 
+    def time_series_parts(self, iters: int = 20, count: int = 1) -> dict:
+        """Mean device ms of one series term split into prepare / term kernel / flush."""
+        ms = (C.c_double * 4)()
+        check(lib.qswg_time_series_parts(self._h, iters, count, ms))
+        return {"prepare": ms[0], "term": ms[1], "flush": ms[2], "total": ms[3]}
+
     def stream(self) -> int:
         """cudaStream_t of this handle (for CUDA events recorded by callers)."""
         s = C.c_void_p()

@@ -409,6 +409,15 @@ int qswg_time_series_term(const qswg_liouvillian* l, int iters, int count, doubl
   });
 }
 
+int qswg_time_series_parts(const qswg_liouvillian* l, int iters, int count, double* ms4) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    need(ms4, "ms4");
+    const auto t = qswg::time_series_parts(*l->l, iters, count);
+    for (int k = 0; k < 4; ++k) ms4[k] = t[static_cast<std::size_t>(k)];
+  });
+}
+
 int qswg_liouvillian_stream(const qswg_liouvillian* l, void** stream) {
   return guarded([&] {
     need(l, "liouvillian");

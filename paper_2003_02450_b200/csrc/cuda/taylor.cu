@@ -846,7 +846,7 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
 // shared memory for the column-major store, and (factored dissipator) also
 // stored row-major into Wt_k for the transposed R_k part.
 #ifndef QSWG_KRON_W_MIN_BLOCKS
-#define QSWG_KRON_W_MIN_BLOCKS 1
+#define QSWG_KRON_W_MIN_BLOCKS 4
 #endif
 template <bool kHerm>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {

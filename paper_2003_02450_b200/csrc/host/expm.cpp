@@ -11,6 +11,7 @@
 #include "expm.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -309,7 +310,11 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
   return info;
 }
 
-double time_series_term(const Liouvillian& l, int iters, int count) {
+// Mean device ms of the parts of one series term over `iters` terms: [0] the
+// Kron prepare kernels (W_k, V_k; 0 for stored formats), [1] the term
+// kernel, [2] the flush kernel (amortised: it runs its sum update once per
+// ring, as in the converging part of a real series) and [3] the whole term.
+std::array<double, 4> time_series_parts(const Liouvillian& l, int iters, int count) {
   if (count < 1 || count > dev::kMaxSeriesD) throw std::invalid_argument("count out of range");
   if (iters < 1) throw std::invalid_argument("iters must be >= 1");
   DeviceGuard g(l.device());
@@ -335,30 +340,35 @@ double time_series_term(const Liouvillian& l, int iters, int count) {
   QSWG_CHECK(cudaMemsetAsync(ctl, 0, sizeof(dev::SeriesCtl), s));
   dev::series_init(z, ex.rows, count, pend_max, ctl, true, s);
   // tol = -1 keeps every output active and settles every test without the
-  // sums (c1 + c2 > -ub), so the sums are updated once per pend_max terms, as
-  // in the converging part of a real series; scale 1/||L||_1 keeps the
-  // iterates bounded.  Local kernel time only (no exchange), as the per-GPU
-  // roofline needs.
+  // sums (c1 + c2 > -ub); scale 1/||L||_1 keeps the iterates bounded.  Local
+  // kernel time only (no exchange), as the per-GPU roofline needs.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
-  auto launch = [&](int i) {
+  cudaEvent_t ev[4];
+  for (auto& e : ev) QSWG_CHECK(cudaEventCreate(&e));
+  std::array<double, 4> acc{};
+  for (int i = 0; i < pend_max + iters; ++i) {  // the first ring is warm-up
+    const bool timed = i >= pend_max;
     const double2* x = ring.k[i % ring.slots];
+    if (timed) QSWG_CHECK(cudaEventRecord(ev[0], s));
     dev::kron_prepare(mat, x, s);
+    if (timed) QSWG_CHECK(cudaEventRecord(ev[1], s));
     dev::series_term(mat, x, ring.k[(i + 1) % ring.slots] + ex.row0, i + 1, false, scale, -1.0, ctl, true, s);
+    if (timed) QSWG_CHECK(cudaEventRecord(ev[2], s));
     dev::series_flush(ring, ex.row0, ex.rows, z, ss, count, i + 1, mat.group == 1, -1.0, ctl, true, s);
-  };
-  for (int i = 0; i < pend_max; ++i) launch(i);  // warm-up (one full ring)
-  cudaEvent_t e0, e1;
-  QSWG_CHECK(cudaEventCreate(&e0));
-  QSWG_CHECK(cudaEventCreate(&e1));
-  QSWG_CHECK(cudaEventRecord(e0, s));
-  for (int i = pend_max; i < pend_max + iters; ++i) launch(i);
-  QSWG_CHECK(cudaEventRecord(e1, s));
-  QSWG_CHECK(cudaEventSynchronize(e1));
-  float ms = 0.f;
-  QSWG_CHECK(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  return static_cast<double>(ms) / iters;
+    if (timed) {
+      QSWG_CHECK(cudaEventRecord(ev[3], s));
+      QSWG_CHECK(cudaEventSynchronize(ev[3]));
+      float t[3] = {0.f, 0.f, 0.f};
+      for (int k = 0; k < 3; ++k) QSWG_CHECK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+      for (int k = 0; k < 3; ++k) acc[static_cast<std::size_t>(k)] += t[k];
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& a : acc) a /= iters;
+  acc[3] = acc[0] + acc[1] + acc[2];
+  return acc;
 }
+
+double time_series_term(const Liouvillian& l, int iters, int count) { return time_series_parts(l, iters, count)[3]; }
 
 }  // namespace qswg

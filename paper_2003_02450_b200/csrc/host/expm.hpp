@@ -7,6 +7,7 @@
 // terms on one GPU — the stop tests run on the device (cuda/taylor.cu).
 #pragma once
 
+#include <array>
 #include <functional>
 
 #include "liouvillian.hpp"
@@ -45,5 +46,6 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
 /// active outputs (p > 1 traffic: K read, K write, count sums read+write),
 /// `iters` back-to-back launches on the Liouvillian's stream.
 double time_series_term(const Liouvillian& l, int iters, int count);
+std::array<double, 4> time_series_parts(const Liouvillian& l, int iters, int count);
 
 }  // namespace qswg
