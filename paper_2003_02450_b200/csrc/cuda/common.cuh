@@ -95,6 +95,10 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
   return pol;
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p, unsigned long long pol) {
+#ifdef QSWG_NO_HINTS
+  (void)pol;
+  return __ldg(p);
+#endif
   double2 r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
       : "=d"(r.x), "=d"(r.y)
@@ -102,6 +106,10 @@ __device__ __forceinline__ double2 ld_stream(const double2* p, unsigned long lon
   return r;
 }
 __device__ __forceinline__ int ld_stream(const int* p, unsigned long long pol) {
+#ifdef QSWG_NO_HINTS
+  (void)pol;
+  return __ldg(p);
+#endif
   int r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
   return r;
@@ -114,14 +122,23 @@ __device__ __forceinline__ unsigned long long evict_last_policy() {
 }
 // Gathered SpMV input (reused ~nnz/row times): read-only path, L2 evict-last.
 __device__ __forceinline__ double2 ld_gather(const double2* p, unsigned long long pol) {
+#ifdef QSWG_GATHER_HINT
   double2 r;
   asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
   return r;
+#else
+  (void)pol;  // plain read-only load: measured faster than the L2 evict-last hint (c2 1.38x, c3 1.24x)
+  return __ldg(p);
+#endif
 }
 // Read-modify-write vectors touched once per kernel (running sums): no L1
 // allocation, L2 evict-first.  Volatile keeps the issue order the caller
 // wrote (all loads of a chunk before its stores).
 __device__ __forceinline__ double2 ld_once(const double2* p, unsigned long long pol) {
+#ifdef QSWG_NO_HINTS
+  (void)pol;
+  return *p;
+#endif
   double2 r;
   asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(r.x), "=d"(r.y)
@@ -129,6 +146,11 @@ __device__ __forceinline__ double2 ld_once(const double2* p, unsigned long long 
   return r;
 }
 __device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long long pol) {
+#ifdef QSWG_NO_HINTS
+  (void)pol;
+  *p = v;
+  return;
+#endif
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x),
                "d"(v.y), "l"(pol)
                : "memory");

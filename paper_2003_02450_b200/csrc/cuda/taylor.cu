@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
 // ------------------------------------------------------------- series term
 // Stop tests of the super-step terms (expm.cpp:298-316, evaluated p-major)
 // with deferred running sums (kernels.hpp: SeriesCtl).  Both controls run on
-// one thread of the last block to arrive (or in a 1-thread kernel after the
-// multi-GPU allreduce).
+// the whole last block to arrive, one thread per output (or in a one-block
+// kernel after the multi-GPU allreduce); every thread of the block calls them.
 //
 // After term p: c2_k = k^p ||K_p||.  The exact test c1_k + c2_k <= tol ||S_k||
 // is settled without S_k when c1_k + c2_k > tol * ub_k, where
@@ -217,62 +217,78 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
 // rounding of the pending axpys and norms (each at most (1 + 2^-53)), so the
 // settled outcome "continue" is the one the exact test would give.
 __device__ void series_term_control(SeriesCtl* ctl, int p, int last, double tol) {
-  ctl->spmvs += 1;
+  static_assert(kMaxSeriesD <= kThreads, "one thread per output");
+  __shared__ int pmin_sh;
+  const int k = threadIdx.x;
   const double tn = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
-  ctl->term_bits = 0;
-  ctl->arrivals = 0;
+  const int count = ctl->count;
+  if (k == 0) pmin_sh = p;
+  __syncthreads();
   if (!isfinite(tn)) {  // expm.cpp:293-295
-    ctl->error = 1;
-    ctl->n_active = 0;
+    if (k == 0) {
+      ctl->spmvs += 1;
+      ctl->error = 1;
+      ctl->n_active = 0;
+      ctl->term_bits = 0;
+      ctl->arrivals = 0;
+    }
     return;
   }
-  const int count = ctl->count;
   const int slot = p % ctl->slots;
-  ctl->tn_last = tn;
-  int pmin = p;
-  for (int k = 0; k < count; ++k)
-    if (ctl->active[k] && ctl->p0[k] < pmin) pmin = ctl->p0[k];
+  const bool act = k < count && ctl->active[k];
+  if (act) atomicMin(&pmin_sh, ctl->p0[k]);
+  __syncthreads();
   // the next term must not overwrite a pending one
-  int any = last || p - pmin + 1 >= ctl->pend_max;
-  for (int k = 0; k < count; ++k) {
-    if (!ctl->active[k]) continue;
-    const double f = ctl->factor[k];
+  const bool full = last || p - pmin_sh + 1 >= ctl->pend_max;
+  double f = 0.0;
+  bool und = false;
+  if (act) {
+    f = ctl->factor[k];
     ctl->fac_ring[slot][k] = f;
-    ctl->bound[k] = __dadd_ru(ctl->bound[k], __dmul_ru(f, tn));
-    const double ub = __dmul_ru(__dadd_ru(ctl->nf_last[k], ctl->bound[k]), 1.0 + 0x1p-30);
-    if (!(ctl->c1[k] + f * tn > tol * ub)) any = 1;  // undecidable (expm.cpp:310, 315)
+    const double bnd = __dadd_ru(ctl->bound[k], __dmul_ru(f, tn));
+    ctl->bound[k] = bnd;
+    const double ub = __dmul_ru(__dadd_ru(ctl->nf_last[k], bnd), 1.0 + 0x1p-30);
+    und = !(ctl->c1[k] + f * tn > tol * ub);  // undecidable (expm.cpp:310, 315)
   }
   // One undecidable test flushes every active output: each pending term is
   // then read once per super-step, and a large ring keeps flushes to the
   // outputs' stop events (measured cheaper than flushing the undecidable
   // outputs alone, which re-reads the shared terms per output).
-  for (int k = 0; k < count; ++k) {
-    if (!ctl->active[k]) continue;
+  const bool any = __syncthreads_or(und) || full;
+  if (act) {
     ctl->mark[k] = any;
     if (!any) {  // every test settled: continue
-      const double f = ctl->factor[k];
       ctl->c1[k] = f * tn;
       ctl->factor[k] = f * static_cast<double>(k + 1);  // factor *= k for p + 1
     }
   }
-  ctl->flush = any;
+  if (k == 0) {
+    ctl->spmvs += 1;
+    ctl->tn_last = tn;
+    ctl->flush = any;
+    ctl->term_bits = 0;
+    ctl->arrivals = 0;
+  }
 }
 
 // Exact tests of term p for the marked outputs after the flush wrote their sums.
 __device__ void series_flush_control(SeriesCtl* ctl, int p, double tol) {
+  __shared__ int stopped, err;
+  const int k = threadIdx.x;
   const int count = ctl->count;
   const int slot = p % ctl->slots;
   const double tn = ctl->tn_last;
-  for (int k = 0; k < count; ++k) {
-    if (!ctl->active[k] || !ctl->mark[k]) continue;
+  if (k == 0) stopped = err = 0;
+  __syncthreads();
+  if (k < count && ctl->active[k] && ctl->mark[k]) {
     const double f = ctl->fac_ring[slot][k];
     const double c2 = f * tn;  // expm.cpp:310
     const double nf = bitsd(*(volatile unsigned long long*)&ctl->sum_bits[k]);
     if (!isfinite(nf)) {  // expm.cpp:312-314
-      ctl->error = 1;
+      err = 1;
     } else if (ctl->c1[k] + c2 <= tol * nf) {  // expm.cpp:315
       ctl->active[k] = 0;
-      ctl->n_active -= 1;
+      atomicAdd(&stopped, 1);
     } else {
       ctl->c1[k] = c2;
     }
@@ -284,9 +300,13 @@ __device__ void series_flush_control(SeriesCtl* ctl, int p, double tol) {
     ctl->fresh[k] = 0;
     ctl->mark[k] = 0;
   }
-  if (ctl->error) ctl->n_active = 0;
-  ctl->flush = 0;
-  ctl->arrivals = 0;
+  __syncthreads();
+  if (k == 0) {
+    if (err) ctl->error = 1;
+    ctl->n_active = ctl->error ? 0 : ctl->n_active - stopped;
+    ctl->flush = 0;
+    ctl->arrivals = 0;
+  }
 }
 
 struct SeriesTermArgs {
@@ -317,19 +337,21 @@ __device__ __forceinline__ void series_store(double2* kp, double scale, long lon
 // Grid-wide ||K_p|| and the term control (last block).
 __device__ __forceinline__ void series_term_finish(const SeriesTermArgs& a, unsigned long long tmax,
                                                    unsigned long long* red) {
+  __shared__ int is_last;
   tmax = block_max_bits(tmax, red);
+  SeriesCtl* ctl = a.ctl;
   if (threadIdx.x == 0) {
-    SeriesCtl* ctl = a.ctl;
     atomicMax(&ctl->term_bits, tmax);
     __threadfence();
-    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
-      __threadfence();
-      if (a.decide) {
-        series_term_control(ctl, a.p, a.last, a.tol);
-      } else {
-        ctl->arrivals = 0;  // maximum stays for the allreduce + series_term_control_kernel
-      }
-    }
+    is_last = atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1;
+    if (is_last) __threadfence();
+  }
+  __syncthreads();
+  if (!is_last) return;
+  if (a.decide) {
+    series_term_control(ctl, a.p, a.last, a.tol);
+  } else if (threadIdx.x == 0) {
+    ctl->arrivals = 0;  // maximum stays for the allreduce + series_term_control_kernel
   }
 }
 
@@ -435,16 +457,18 @@ __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs 
   __syncthreads();
   for (int u = threadIdx.x; u < nm; u += blockDim.x) atomicMax(&ctl->sum_bits[list[u]], smax_sh[u]);
   __syncthreads();
+  __shared__ int is_last;
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1) {
-      __threadfence();
-      if (a.decide) {
-        series_flush_control(ctl, p, a.tol);
-      } else {
-        ctl->arrivals = 0;
-      }
-    }
+    is_last = atomicAdd(&ctl->arrivals, 1u) == gridDim.x - 1;
+    if (is_last) __threadfence();
+  }
+  __syncthreads();
+  if (!is_last) return;
+  if (a.decide) {
+    series_flush_control(ctl, p, a.tol);
+  } else if (threadIdx.x == 0) {
+    ctl->arrivals = 0;
   }
 }
 
@@ -1091,10 +1115,10 @@ __global__ void series_init_fin_kernel(SeriesCtl* ctl, int count, int pend_max) 
 __global__ void step_control_kernel(StepCtl* ctl, int first_of_stage, int stage, double tol) {
   step_control(ctl, first_of_stage, stage, tol);
 }
-__global__ void series_term_control_kernel(SeriesCtl* ctl, int p, int last, double tol) {
+__global__ void __launch_bounds__(kThreads) series_term_control_kernel(SeriesCtl* ctl, int p, int last, double tol) {
   series_term_control(ctl, p, last, tol);
 }
-__global__ void series_flush_control_kernel(SeriesCtl* ctl, int p, double tol) {
+__global__ void __launch_bounds__(kThreads) series_flush_control_kernel(SeriesCtl* ctl, int p, double tol) {
   series_flush_control(ctl, p, tol);
 }
 
@@ -1245,12 +1269,12 @@ void series_init_fin(SeriesCtl* ctl, int count, int pend_max, cudaStream_t s) {
 }
 
 void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s) {
-  series_term_control_kernel<<<1, 1, 0, s>>>(ctl, p, last, tol);
+  series_term_control_kernel<<<1, kThreads, 0, s>>>(ctl, p, last, tol);
   QSWG_LAUNCH_CHECK("series_term_control");
 }
 
 void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {
-  series_flush_control_kernel<<<1, 1, 0, s>>>(ctl, p, tol);
+  series_flush_control_kernel<<<1, kThreads, 0, s>>>(ctl, p, tol);
   QSWG_LAUNCH_CHECK("series_flush_control");
 }
 

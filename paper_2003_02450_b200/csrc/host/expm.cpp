@@ -343,29 +343,37 @@ std::array<double, 4> time_series_parts(const Liouvillian& l, int iters, int cou
   // sums (c1 + c2 > -ub); scale 1/||L||_1 keeps the iterates bounded.  Local
   // kernel time only (no exchange), as the per-GPU roofline needs.
   const double scale = 1.0 / std::max(l.one_norms()[0], 1e-300);
-  cudaEvent_t ev[4];
+  // every launch of the timed terms is bracketed by events; one
+  // synchronisation at the end (the stream runs back to back, as in a series)
+  std::vector<cudaEvent_t> ev(static_cast<std::size_t>(4 * iters));
   for (auto& e : ev) QSWG_CHECK(cudaEventCreate(&e));
-  std::array<double, 4> acc{};
   for (int i = 0; i < pend_max + iters; ++i) {  // the first ring is warm-up
-    const bool timed = i >= pend_max;
+    const int it = i - pend_max;
     const double2* x = ring.k[i % ring.slots];
-    if (timed) QSWG_CHECK(cudaEventRecord(ev[0], s));
+    auto mark = [&](int k) {
+      if (it >= 0) QSWG_CHECK(cudaEventRecord(ev[static_cast<std::size_t>(4 * it + k)], s));
+    };
+    mark(0);
     dev::kron_prepare(mat, x, s);
-    if (timed) QSWG_CHECK(cudaEventRecord(ev[1], s));
+    mark(1);
     dev::series_term(mat, x, ring.k[(i + 1) % ring.slots] + ex.row0, i + 1, false, scale, -1.0, ctl, true, s);
-    if (timed) QSWG_CHECK(cudaEventRecord(ev[2], s));
+    mark(2);
     dev::series_flush(ring, ex.row0, ex.rows, z, ss, count, i + 1, mat.group == 1, -1.0, ctl, true, s);
-    if (timed) {
-      QSWG_CHECK(cudaEventRecord(ev[3], s));
-      QSWG_CHECK(cudaEventSynchronize(ev[3]));
-      float t[3] = {0.f, 0.f, 0.f};
-      for (int k = 0; k < 3; ++k) QSWG_CHECK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
-      for (int k = 0; k < 3; ++k) acc[static_cast<std::size_t>(k)] += t[k];
-    }
+    mark(3);
   }
+  QSWG_CHECK(cudaEventSynchronize(ev.back()));
+  std::array<double, 4> acc{};
+  for (int it = 0; it < iters; ++it)
+    for (int k = 0; k < 3; ++k) {
+      float t = 0.f;
+      QSWG_CHECK(cudaEventElapsedTime(&t, ev[static_cast<std::size_t>(4 * it + k)], ev[static_cast<std::size_t>(4 * it + k + 1)]));
+      acc[static_cast<std::size_t>(k)] += t;
+    }
+  float total = 0.f;
+  QSWG_CHECK(cudaEventElapsedTime(&total, ev.front(), ev.back()));
   for (auto& e : ev) cudaEventDestroy(e);
-  for (auto& a : acc) a /= iters;
-  acc[3] = acc[0] + acc[1] + acc[2];
+  for (int k = 0; k < 3; ++k) acc[static_cast<std::size_t>(k)] /= iters;
+  acc[3] = static_cast<double>(total) / iters;  // first prepare to last flush, per term
   return acc;
 }
 

@@ -497,7 +497,10 @@ void Liouvillian::set_hermitian_input(const double2* x) const {
 double Liouvillian::time_spmv(int iters, int group) const {
   DeviceGuard g(device_);
   DeviceBuffer<double2> x(static_cast<std::size_t>(dim())), y(static_cast<std::size_t>(std::max<std::int64_t>(block_.rows, 1)));
-  QSWG_CHECK(cudaMemsetAsync(x.get(), 0, x.bytes(), stream_));
+  if (std::getenv("QSWG_TIME_PATTERN") && format_ == dev::Format::Kron && herm_flag_.get())
+    dev::fill_pattern_hermitian(x.get(), n_, stream_);  // experiment knob: density-matrix-like input
+  else
+    QSWG_CHECK(cudaMemsetAsync(x.get(), 0, x.bytes(), stream_));
   cudaEvent_t e0, e1;
   QSWG_CHECK(cudaEventCreate(&e0));
   QSWG_CHECK(cudaEventCreate(&e1));

@@ -28,7 +28,8 @@ class Case:
         meta = json.load(open(os.path.join(GOLDEN, "cases.json")))["cases"][name]
         self.name = name
         self.__dict__.update(meta)
-        z = np.load(os.path.join(GOLDEN, f"case_{name}.npz"))
+        with np.load(os.path.join(GOLDEN, f"case_{name}.npz")) as f:
+            z = {k: f[k] for k in f.files}  # eager: rank threads read it concurrently
         self.z = z
         self.h = load_csr(z, "h")
         self.ops = [load_csr(z, f"op{k}") for k in range(self.n_ops)]

@@ -28,7 +28,7 @@ def run_ranks(world, fn):
     for t in ts:
         t.start()
     for t in ts:
-        t.join(timeout=600)
+        t.join(timeout=300)
     if errs:
         raise errs[0]
     return out
