@@ -383,10 +383,17 @@ struct SeriesFlushArgs {
 // with all their sum loads in flight; per chunk the pending terms are read
 // once, oldest first (each output adds only terms from its own first pending
 // one), so every output sums in term order as with per-term updates.
+// Whether the flush after term a.p must run (block-uniform: the flag was set
+// by the previous kernel).
+__device__ __forceinline__ bool flush_due(const SeriesFlushArgs& a) {
+  return *(volatile const int*)&a.ctl->flush && !series_skip(a.ctl);
+}
+
+// The flush work of one block (every thread calls it; the last block to
+// arrive runs the exact stop tests).
 template <bool kStrict>
-__global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs a) {
+__device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
   SeriesCtl* ctl = a.ctl;
-  if (!*(volatile int*)&ctl->flush || series_skip(ctl)) return;
   __shared__ int list[kMaxSeriesD];   // marked outputs
   __shared__ int q0[kMaxSeriesD];     // their first pending term
   __shared__ int fr[kMaxSeriesD];
@@ -470,6 +477,11 @@ __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs 
   } else if (threadIdx.x == 0) {
     ctl->arrivals = 0;
   }
+}
+
+template <bool kStrict>
+__global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs a) {
+  if (flush_due(a)) flush_body<kStrict>(a);
 }
 
 // ------------------------------------------------------------- SELL path
@@ -872,8 +884,11 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
 #ifndef QSWG_KRON_W_MIN_BLOCKS
 #define QSWG_KRON_W_MIN_BLOCKS 4
 #endif
-template <bool kHerm>
-__global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kernel(KronView m, const double2* __restrict__ x, int k) {
+// kFlush: the same launch then runs the flush after the previous term
+// (series_flush; its HBM streaming overlaps the gathers of W).
+template <bool kHerm, bool kFlush>
+__global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kernel(KronView m, const double2* __restrict__ x, int k,
+                                                                               SeriesFlushArgs fa) {
   __shared__ double2 tile[kKT][kKT + 1];
   const unsigned long long xpol = evict_last_policy();
   const long long n = m.n;
@@ -943,6 +958,9 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
       for (int r = 0; r < kKR; ++r)
         if (vi && vj[r]) st_hint(m.w[k] + col[r] + i, acc[r], xpol);
     }
+  }
+  if constexpr (kFlush) {
+    if (flush_due(fa)) flush_body<false>(fa);
   }
 }
 
@@ -1346,16 +1364,45 @@ void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, 
   QSWG_LAUNCH_CHECK("series_flush");
 }
 
+namespace {
+template <bool kFlush>
+void launch_w(const DevMatrix& m, const double2* x, int k, const SeriesFlushArgs& fa, cudaStream_t s) {
+  if (m.kron.herm) {
+    const auto g = kron_geom(kron_w_kernel<true, kFlush>, m.kron);
+    kron_w_kernel<true, kFlush><<<g.first, kThreads, g.second, s>>>(m.kron, x, k, fa);
+  } else {
+    const auto g = kron_geom(kron_w_kernel<false, kFlush>, m.kron);
+    kron_w_kernel<false, kFlush><<<g.first, kThreads, g.second, s>>>(m.kron, x, k, fa);
+  }
+}
+}  // namespace
+
+bool kron_prepare_flush(const DevMatrix& m, const double2* x, const SeriesRing& ring, std::int64_t row0,
+                        std::int64_t rows, const double2* z, const SeriesSums& sums, int p, double tol,
+                        SeriesCtl* ctl, cudaStream_t s) {
+  if (m.format != Format::Kron || m.kron.nk == 0) return false;
+  const SeriesFlushArgs fa{ring, row0, rows, z, sums, p, tol, ctl, 1};
+  launch_w<true>(m, x, 0, fa, s);
+  QSWG_LAUNCH_CHECK("kron_prepare_flush");
+  for (int k = 0; k < m.kron.nk; ++k) {
+    if (k > 0) {
+      launch_w<false>(m, x, k, fa, s);
+      QSWG_LAUNCH_CHECK("kron_prepare_flush");
+    }
+    if (m.kron.factored) {
+      const auto gv = kron_geom(kron_v_kernel, m.kron);
+      kron_v_kernel<<<gv.first, kThreads, gv.second, s>>>(m.kron, x, k);
+      QSWG_LAUNCH_CHECK("kron_prepare_flush");
+    }
+  }
+  return true;
+}
+
 void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
   if (m.format != Format::Kron) return;
+  const SeriesFlushArgs none{};
   for (int k = 0; k < m.kron.nk; ++k) {
-    if (m.kron.herm) {
-      const auto g = kron_geom(kron_w_kernel<true>, m.kron);
-      kron_w_kernel<true><<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
-    } else {
-      const auto g = kron_geom(kron_w_kernel<false>, m.kron);
-      kron_w_kernel<false><<<g.first, kThreads, g.second, s>>>(m.kron, x, k);
-    }
+    launch_w<false>(m, x, k, none, s);
     QSWG_LAUNCH_CHECK("kron_prepare");
     if (m.kron.factored) {
       const auto gv = kron_geom(kron_v_kernel, m.kron);

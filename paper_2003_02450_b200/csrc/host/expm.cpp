@@ -261,7 +261,10 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
     std::vector<double2*> sums(static_cast<std::size_t>(d));
     for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ex.local(kSums + static_cast<std::size_t>(k));
     const bool strict = mat.group == 1;
-    const std::int64_t per_term = 2 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0);
+    // One GPU, Kron with Lindblad terms: the flush after term p runs in the
+    // launch that prepares W for term p + 1.
+    const bool fused = ex.single && mat.format == dev::Format::Kron && mat.kron.nk > 0;
+    const std::int64_t per_term = (fused ? 1 : 2) + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0);
     for (std::int64_t super = 0; super <= n_super; ++super) {
       const std::int64_t count = super < n_super ? d : remainder;
       if (count == 0) break;
@@ -270,7 +273,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
         ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
         dev::series_init_fin(ctl, static_cast<int>(count), pend_max, s);
       }
-      info.launches += 1 + m_star * per_term;
+      info.launches += 1 + m_star * per_term + (fused ? 1 : 0);
       dev::SeriesSums ss{};
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
       const double2* z_full = ex.spmv_input(z, kZFull);
@@ -278,12 +281,15 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
         const double2* x = p == 1 ? z_full : ring.k[(p - 1) % ring.slots];
         double2* kp = ring.k[p % ring.slots] + ex.row0;
         const bool last = p == m_star;
-        ex.prepare(mat, x);
+        if (!fused || p == 1) ex.prepare(mat, x);
         dev::series_term(mat, x, kp, static_cast<int>(p), last, h / static_cast<double>(p), params.tolerance, ctl,
                          ex.single, s);
         if (ex.single) {
-          dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
-                            params.tolerance, ctl, true, s);
+          if (!(fused && !last &&
+                dev::kron_prepare_flush(mat, ring.k[p % ring.slots], ring, ex.row0, ex.rows, z, ss,
+                                        static_cast<int>(p), params.tolerance, ctl, s)))
+            dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
+                              params.tolerance, ctl, true, s);
           continue;
         }
         ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);

@@ -279,6 +279,13 @@ void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s);
 // Kron format: W_k = Q_k X on the local columns (call before every product
 // with input x; multi-GPU callers then exchange the W_k halos).
 void kron_prepare(const DevMatrix& l, const double2* x, cudaStream_t s);
+// One GPU, Kron with Lindblad terms: kron_prepare(x) for the next term fused
+// in one launch with series_flush(..., p, decide = true) for the term just
+// computed (the flush streams from HBM while W gathers from L2).  Returns
+// false (nothing launched) for other matrices.
+bool kron_prepare_flush(const DevMatrix& l, const double2* x, const SeriesRing& ring, std::int64_t row0,
+                        std::int64_t rows, const double2* z, const SeriesSums& sums, int p, double tol,
+                        SeriesCtl* ctl, cudaStream_t s);
 // Kron format, one GPU: whether x (dim) is exactly Hermitian as an n x n
 // matrix (synchronises the stream).  false for other formats / multi-GPU.
 bool kron_hermitian_check(const DevMatrix& l, const double2* x, cudaStream_t s);
