@@ -723,6 +723,9 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
 }
 
 // Column-indexed part and diagonal terms at (i, j[r]), lane = row i.
+// kHerm: V_k = X L_k' = W_k' for Hermitian X, so V_k(i, a) = conj Wt_k[n a + i]
+// and no V_k is built.
+template <bool kHerm>
 __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __restrict__ x, int i, const int* j,
                                           double2* acc, unsigned long long xpol) {
   const long long n = m.n;
@@ -734,8 +737,13 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
     const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
     uniform_rows(m.p[k], j, acc, [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
     if (m.factored) {  // -w/2 (X L') L: columns of V_k
-      const double2* vi = m.v[k] + i;
-      uniform_rows(m.s[k], j, acc, [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
+      if constexpr (kHerm) {
+        const double2* vi = m.wt[k] + i;
+        uniform_rows(m.s[k], j, acc, [&](int c) { return conj2(ld_gather(vi + static_cast<long long>(c) * n, xpol)); });
+      } else {
+        const double2* vi = m.v[k] + i;
+        uniform_rows(m.s[k], j, acc, [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
+      }
     }
   }
 #pragma unroll
@@ -870,7 +878,7 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
       for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
       kron_rows_lane(m, x, i, jg, acc, xpol);
     }
-    kron_cols(m, x, i, jg, acc, xpol);
+    kron_cols<kHerm>(m, x, i, jg, acc, xpol);
     kron_tile_emit<kHerm>(g, I, J, acc, tile, epi);
   }
 }
@@ -1389,7 +1397,7 @@ bool kron_prepare_flush(const DevMatrix& m, const double2* x, const SeriesRing& 
       launch_w<false>(m, x, k, fa, s);
       QSWG_LAUNCH_CHECK("kron_prepare_flush");
     }
-    if (m.kron.factored) {
+    if (m.kron.factored && !m.kron.herm) {
       const auto gv = kron_geom(kron_v_kernel, m.kron);
       kron_v_kernel<<<gv.first, kThreads, gv.second, s>>>(m.kron, x, k);
       QSWG_LAUNCH_CHECK("kron_prepare_flush");
@@ -1404,7 +1412,7 @@ void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
   for (int k = 0; k < m.kron.nk; ++k) {
     launch_w<false>(m, x, k, none, s);
     QSWG_LAUNCH_CHECK("kron_prepare");
-    if (m.kron.factored) {
+    if (m.kron.factored && !m.kron.herm) {  // Hermitian path: V_k = W_k', read from Wt_k
       const auto gv = kron_geom(kron_v_kernel, m.kron);
       kron_v_kernel<<<gv.first, kThreads, gv.second, s>>>(m.kron, x, k);
       QSWG_LAUNCH_CHECK("kron_prepare");

@@ -161,7 +161,7 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
     ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
     dev::step_init_fin(ctl, s);
   }
-  launches += 1 + sp.s * sp.m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0));
+  launches += 1 + sp.s * sp.m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + (mat.kron.factored && !mat.kron.herm)) : 0));
   const double s_count = static_cast<double>(sp.s);
   for (std::int64_t st = 0; st < sp.s; ++st) {
     // stage input: v, then the previous stage's sum (term = sum, expm.cpp:197-205)
@@ -264,7 +264,8 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
     // One GPU, Kron with Lindblad terms: the flush after term p runs in the
     // launch that prepares W for term p + 1.
     const bool fused = ex.single && mat.format == dev::Format::Kron && mat.kron.nk > 0;
-    const std::int64_t per_term = (fused ? 1 : 2) + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + mat.kron.factored) : 0);
+    const std::int64_t per_term =
+        (fused ? 1 : 2) + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + (mat.kron.factored && !mat.kron.herm)) : 0);
     for (std::int64_t super = 0; super <= n_super; ++super) {
       const std::int64_t count = super < n_super ? d : remainder;
       if (count == 0) break;
