@@ -126,6 +126,10 @@ int qswg_build_global(double omega, const qswg_sparse* h, const qswg_sparse* con
                       int64_t n_lindblads, const qswg_sparse* h_rot /* nullable */,
                       const qswg_device_config* cfg, qswg_liouvillian** out);
 int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* info);
+/* KRON on one GPU: 1 (default) lets step/series/spmv take the Hermitian tile
+ * kernels when their input is exactly Hermitian, 0 always uses the general
+ * kernels (results agree to rounding; no reference counterpart). */
+int qswg_liouvillian_set_hermitian_mode(qswg_liouvillian* l, int mode);
 /* gather_full() of the local row block (liouvillian.hpp:34): rowptr[rows+1], col[nnz_local], val[2*nnz_local] */
 int qswg_liouvillian_download(const qswg_liouvillian* l, int64_t* rowptr, int64_t* col, double* val);
 void qswg_liouvillian_destroy(qswg_liouvillian* l);

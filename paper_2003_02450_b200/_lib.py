@@ -124,6 +124,7 @@ SIGNATURES = {
     "qswg_time_spmv": (C.c_int, [vp, C.c_int, C.c_int, dp]),
     "qswg_time_series_term": (C.c_int, [vp, C.c_int, C.c_int, dp]),
     "qswg_time_series_parts": (C.c_int, [vp, C.c_int, C.c_int, dp]),
+    "qswg_liouvillian_set_hermitian_mode": (C.c_int, [vp, C.c_int]),
     "qswg_liouvillian_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "qswg_state_create": (C.c_int, [vp, C.POINTER(vp)]),
     "qswg_state_upload": (C.c_int, [vp, dp]),

@@ -251,6 +251,10 @@ class Liouvillian:
         check(lib.qswg_time_series_term(self._h, iters, count, C.byref(ms)))
         return ms.value
 
+    def set_hermitian_mode(self, on: bool) -> None:
+        """KRON on one GPU: allow (default) or forbid the Hermitian tile kernels."""
+        check(lib.qswg_liouvillian_set_hermitian_mode(self._h, 1 if on else 0))
+
     def time_series_parts(self, iters: int = 20, count: int = 1) -> dict:
         """Mean device ms of one series term split into prepare / term kernel / flush."""
         ms = (C.c_double * 4)()

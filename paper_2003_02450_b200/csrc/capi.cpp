@@ -409,6 +409,13 @@ int qswg_time_series_term(const qswg_liouvillian* l, int iters, int count, doubl
   });
 }
 
+int qswg_liouvillian_set_hermitian_mode(qswg_liouvillian* l, int mode) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    l->l->set_hermitian_mode(mode);
+  });
+}
+
 int qswg_time_series_parts(const qswg_liouvillian* l, int iters, int count, double* ms4) {
   return guarded([&] {
     need(l, "liouvillian");

@@ -491,7 +491,7 @@ void Liouvillian::set_hermitian_input(const double2* x) const {
     const char* e = std::getenv("QSWG_KRON_HERM");  // experiment knob: 0 = always the general kernels
     return e != nullptr && e[0] == '0';
   }();
-  herm_ = !off && dev::kron_hermitian_check(matrix(), x, stream_) ? 1 : 0;
+  herm_ = !off && herm_mode_ && dev::kron_hermitian_check(matrix(), x, stream_) ? 1 : 0;
 }
 
 double Liouvillian::time_spmv(int iters, int group) const {

@@ -84,6 +84,8 @@ class Liouvillian {
   /// Kron on one GPU: selects the Hermitian kernels for the products that
   /// follow when x (full-length) is exactly Hermitian (synchronises).
   void set_hermitian_input(const double2* x) const;
+  /// 0: never take the Hermitian kernels; 1 (default): when the input is Hermitian.
+  void set_hermitian_mode(int mode) { herm_mode_ = mode ? 1 : 0; }
   /// y = scale * L x for device vectors: x full-length (dim), y local (rows).
   void multiply(const double2* x, double2* y, double scale) const;
   /// Mean device time (ms) of one term kernel launch over `iters` launches.
@@ -127,6 +129,7 @@ class Liouvillian {
   std::vector<DeviceBuffer<double2>> kron_w_, kron_v_;
   DeviceBuffer<int> herm_flag_;  // Kron on one GPU: device flag of the Hermiticity check
   mutable int herm_ = 0;         // the current call's input is Hermitian (kernels.hpp: KronView::herm)
+  int herm_mode_ = 1;            // set_hermitian_mode
   std::vector<DeviceBuffer<double2>> kron_wt_;  // factored + one GPU: row-major W_k for the Hermitian path
   mutable Workspace ws_;
 };

@@ -1,0 +1,122 @@
+"""Device paths specific to this implementation (no reference counterpart,
+checked against the reference-pinned C oracle and against each other):
+
+* the Hermitian tile kernels (KRON, one GPU) — taken when the input is an
+  exactly Hermitian matrix — against the general kernels on the same input;
+* non-Hermitian inputs, which must take the general path;
+* the lazily updated running sums of `series` (term ring, bound-settled stop
+  tests, flushes) — the ring size must not change a single bit or term count.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import rho0_vec
+from conftest import Case
+
+pytestmark = pytest.mark.gpu
+api = pytest.importorskip("paper_2003_02450_b200.api")
+from paper_2003_02450_b200 import graphs  # noqa: E402
+
+
+def hermitian(rng, n):
+    a = rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))
+    h = a + a.conj().T
+    return h.reshape(-1, order="F")  # column-major vec
+
+
+def as_matrix(v, n):
+    return np.asarray(v).reshape(n, n, order="F")
+
+
+CASES = ["c2_n36", "c3_n40", "c4_n40", "c5_n64", "gqsw_multi_rot", "lqsw_src_snk", "walkthrough_nm_w1"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_hermitian_spmv_matches_general(name):
+    c = Case(name)
+    l = c.build_gpu(api, format="kron")
+    rng = np.random.default_rng(5)
+    x = hermitian(rng, c.n)
+    y_h = l.spmv(x)                  # Hermitian kernels
+    l.set_hermitian_mode(False)
+    y_g = l.spmv(x)                  # general kernels
+    Yh, Yg = as_matrix(y_h, c.n), as_matrix(y_g, c.n)
+    iu = np.triu_indices(c.n, 1)
+    # upper triangle: the same formula, the same order -> the same bits
+    assert np.array_equal(Yh[iu], Yg[iu])
+    assert np.array_equal(np.diag(Yh).real, np.diag(Yg).real)
+    # the Hermitian result is exactly Hermitian with a real diagonal
+    assert np.array_equal(Yh, Yh.conj().T)
+    # the general lower triangle agrees to rounding
+    scale = np.abs(Yg).max()
+    assert np.abs(Yh - Yg).max() <= 1e-14 * scale
+    # and both are L x of the reference's superoperator
+    ref = c.L.to_dense() @ x
+    assert np.abs(y_h - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", ["c2_n36", "c4_n40", "gqsw_multi_rot", "lqsw_src_snk"])
+def test_hermitian_series_matches_general_and_reference(name):
+    c = Case(name)
+    t1, tq, q = c.series
+    l = c.build_gpu(api, format="kron")
+    v = l.state().from_probabilities(c.rho0)
+    r_h = api.series(l, v, t1, tq, int(q), states=True)
+    l.set_hermitian_mode(False)
+    r_g = api.series(l, v, t1, tq, int(q), states=True)
+    assert r_h.info.spmvs == r_g.info.spmvs == c.series_spmvs
+    assert np.abs(r_h.states - r_g.states).max() <= 1e-13
+    keep = c.z["series_keep"]
+    assert np.abs(r_h.states[keep] - c.z["series_states"]).max() <= 1e-10
+    for s in r_h.states:  # every output of the Hermitian path is exactly Hermitian
+        S = as_matrix(s, c.n)
+        assert np.array_equal(S, S.conj().T)
+
+
+@pytest.mark.parametrize("name", ["c2_n36", "lqsw_src_snk"])
+def test_non_hermitian_input_takes_general_path(name, port):
+    c = Case(name)
+    rng = np.random.default_rng(17)
+    x = rng.uniform(-1, 1, c.n * c.n) + 1j * rng.uniform(-1, 1, c.n * c.n)  # not Hermitian
+    l = c.build_gpu(api, format="kron")
+    w, info = api.step(l, l.state().upload(x), 0.7)
+    o = c.build_oracle(port)
+    ref, ns = o.step(x, 0.7)
+    assert info.spmvs == ns
+    assert np.abs(w.gather() - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+    t1, tq, q = c.series
+    res = api.series(l, l.state().upload(x), t1, tq, int(q), states=True)
+    states, _, nsp = o.series(x, t1, tq, int(q))
+    assert res.info.spmvs == nsp
+    assert np.abs(res.states - states).max() <= 1e-10 * max(1.0, np.abs(states).max())
+
+
+@pytest.mark.parametrize("fmt", ["kron", "auto"])
+@pytest.mark.parametrize("name", ["c1_n64", "c2_n36", "gqsw_multi_rot"])
+def test_term_ring_size_changes_no_bit(name, fmt, monkeypatch):
+    """Running sums are added in term order whatever the ring size, and the
+    bound-settled stop tests take the decisions the exact tests take."""
+    c = Case(name)
+    t1, tq, q = c.series
+    out = {}
+    for pm in ("1", "2", "7", "64"):
+        monkeypatch.setenv("QSWG_PEND_MAX", pm)
+        l = c.build_gpu(api, format=fmt)
+        r = api.series(l, l.state().from_probabilities(c.rho0), t1, tq, int(q), states=True)
+        out[pm] = (r.states, r.info.spmvs)
+        del l
+    base, nsp = out["1"]
+    assert nsp == c.series_spmvs
+    for pm, (st, n) in out.items():
+        assert n == nsp, pm
+        assert np.array_equal(st, base), pm
+
+
+def test_full_size_c2_series_is_hermitian_and_trace_preserving():
+    w = graphs.config("c2")
+    l = api.build_global(w.omega, w.h, w.ops)
+    r = api.series(l, l.state().from_probabilities(w.rho0), w.t1, w.tq, w.steps, final=True)
+    assert r.info.spmvs == 760
+    assert np.abs(r.populations.sum(axis=1) - 1).max() <= 1e-12
+    F = as_matrix(r.final.gather(), w.n)
+    assert np.array_equal(F, F.conj().T)
