@@ -22,7 +22,7 @@ constexpr int kThreads = 256;
 // Resident blocks per SM of `kernel` at kThreads threads (cached per device
 // and kernel: the occupancy query costs microseconds of host time, which
 // would otherwise bound short launches).
-inline int blocks_per_sm(const void* kernel, std::size_t smem = 0) {
+inline int blocks_per_sm(const void* kernel, std::size_t smem = 0, int threads = 256) {
   struct Key {
     int dev;
     const void* k;
@@ -36,7 +36,7 @@ inline int blocks_per_sm(const void* kernel, std::size_t smem = 0) {
   for (int i = 0; i < used; ++i)
     if (keys[i].dev == dev && keys[i].k == kernel && keys[i].smem == smem) return vals[i];
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   if (per_sm < 1) per_sm = 1;
   if (used < 64) {
     keys[used] = {dev, kernel, smem};
