@@ -162,14 +162,17 @@ struct HostOperands {
   }
 
   // Operand entries touched per output element (Kron kernels).
-  double kron_cost(bool factored) const {
+  // `herm`: one GPU, where Hermitian inputs read V_k as conj(W_k') from a
+  // row-major copy of W_k instead of building it.
+  double kron_cost(bool factored, bool herm = false) const {
     const double nn = static_cast<double>(n);
     auto e = [&](const MultiCsr& m) { return static_cast<double>(m.col.size()) / nn; };
     double c = 0.0;
     for (std::size_t k = 0; k < p.size(); ++k) c += e(p[k]) + e(q[k]);
     if (!factored) return c + e(a) + e(b);
     c += e(af) + e(bf);
-    for (std::size_t k = 0; k < r.size(); ++k) c += e(r[k]) + e(sfac[k]) + e(u[k]) + 2.0;  // + V_k pass
+    for (std::size_t k = 0; k < r.size(); ++k)
+      c += e(r[k]) + e(sfac[k]) + (herm ? 1.0 : e(u[k]) + 2.0);  // + V_k pass, or the Wt_k store
     return c;
   }
 };
@@ -259,9 +262,10 @@ struct KronStore {
   // nonzeros; whether the kernels use them is autotuned per operator set at
   // build (ELL wins on lattices and on c3, CSR on c4's 2-hop rows).
   static constexpr double kEllMaxPadding = 2.0;
-  KronStore(const HostOperands& h, cudaStream_t s) : host(h.summed()), ops(host, s) {
+  KronStore(const HostOperands& h, bool single, cudaStream_t s) : host(h.summed()), ops(host, s) {
     // factor the L'L terms when that touches clearly fewer operand entries
-    factored = host.has_factored && host.kron_cost(true) < 0.8 * host.kron_cost(false);
+    // (one GPU: c2 47.2 vs 47.8 ms per series factored, c4 factored either way)
+    factored = host.has_factored && host.kron_cost(true, single) < (single ? 0.9 : 0.8) * host.kron_cost(false);
     if (const char* f = std::getenv("QSWG_KRON_FACTOR")) factored = host.has_factored && f[0] == '1';  // test knob
     a = maybe_ell(factored ? host.af : host.a, s);
     for (const MultiCsr& qk : host.q) q.push_back(maybe_ell(qk, s));
@@ -704,7 +708,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     const std::int64_t j0 = l->block_.row0 / n, j1 = (l->block_.row0 + l->block_.rows) / n;
     l->nnz_local_ = colptr[static_cast<std::size_t>(j1)] - colptr[static_cast<std::size_t>(j0)];
     l->format_ = dev::Format::Kron;
-    l->kron_ = std::make_shared<KronStore>(hops, s);
+    l->kron_ = std::make_shared<KronStore>(hops, world == 1, s);
     for (std::size_t k = 0; k < hops.p.size(); ++k) {
       l->kron_w_.emplace_back(static_cast<std::size_t>(dim));
       QSWG_CHECK(cudaMemsetAsync(l->kron_w_.back().get(), 0, l->kron_w_.back().bytes(), s));
