@@ -307,7 +307,8 @@ def main():
     kernel_name = {"kron": "kron_series_term_kernel", "sell": "sell_series_term_kernel",
                    "csr": "series_term_kernel"}[l.format]
     parts_line = {"prepare_ms": parts["prepare"], "term_ms": parts["term"], "flush_ms": parts["flush"],
-                  "prepare_kernels": "kron_w_kernel" + (" + kron_v_kernel" if l.info.kron_factored else "")
+                  "prepare_kernels": ("kron_w_kernel" + ((" (W_k and its row-major copy; V_k = conj Wt_k)" if world == 1
+                                                          else " + kron_v_kernel") if l.info.kron_factored else ""))
                   if l.format == "kron" else None,
                   "prepare_gbs": prepare_bytes(l) / (parts["prepare"] * 1e-3) / 1e9 if parts["prepare"] > 0 else None,
                   "flush_kernel": "series_flush_kernel (amortised over the term ring)",
