@@ -10,5 +10,5 @@ mkdir -p ../../build_variants
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC "$@" \
   -c cuda/taylor.cu -o /tmp/taylor_$name.o
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static \
-  -o ../../build_variants/libqswg_$name.so build/host/*.o build/capi.o build/cuda/assemble.o build/cuda/norms.o build/cuda/tiny.o \
+  -o ../../build_variants/libqswg_$name.so build/host/*.o build/capi.o $(ls build/cuda/*.o | grep -v taylor) \
   /tmp/taylor_$name.o -ldl -lpthread
