@@ -14,6 +14,7 @@
 #include <array>
 #include <cmath>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -128,6 +129,20 @@ struct Exec {
       }
   }
 
+  // {n_active, flush} of a series control block in one device-to-host read.
+  std::pair<int, int> read_active_flush(const dev::SeriesCtl* ctl) const {
+    constexpr std::size_t lo = offsetof(dev::SeriesCtl, n_active), hi = offsetof(dev::SeriesCtl, flush);
+    static_assert(lo < hi, "n_active precedes flush");
+    unsigned char buf[hi - lo + sizeof(int)];
+    QSWG_CHECK(cudaMemcpyAsync(buf, reinterpret_cast<const unsigned char*>(ctl) + lo, sizeof(buf),
+                               cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
+    int a = 0, f = 0;
+    std::memcpy(&a, buf, sizeof(int));
+    std::memcpy(&f, buf + (hi - lo), sizeof(int));
+    return {a, f};
+  }
+
   template <class T>
   T read(const T* dev_ptr) const {
     T v{};
@@ -178,7 +193,7 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
       if (!ex.single) {
         ex.comm->allreduce_max_u64(&ctl->term_bits, 2, s);  // term_bits, sum_bits
         dev::step_control(ctl, j == 1, static_cast<int>(st), params.tolerance, s);
-        if (ex.read(&ctl->done) || ex.read(&ctl->error)) break;  // expm.cpp:191-194
+        if (ex.read(&ctl->done)) break;  // expm.cpp:191-194 (error sets done)
         if (j < sp.m_star) ex.exchange(term[j % 2]);
       }
     }
@@ -295,8 +310,9 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
         }
         ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
         dev::series_term_control(ctl, static_cast<int>(p), last ? 1 : 0, params.tolerance, s);
-        if (ex.read(&ctl->n_active) == 0) break;
-        if (ex.read(&ctl->flush)) {
+        const auto [n_active, flush] = ex.read_active_flush(ctl);
+        if (n_active == 0) break;
+        if (flush) {
           dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
                             params.tolerance, ctl, false, s);
           ex.comm->allreduce_max_u64(&ctl->sum_bits[0], static_cast<std::size_t>(count), s);
