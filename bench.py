@@ -321,7 +321,7 @@ def main():
         lk = l
         l = None
         ls = build("sell")
-        if ls.padding > 1.03:
+        if ls.padding > 1.3:
             del ls
             ls = build("csr")
         sp = ls.time_series_parts(iters=20, count=d_active)

@@ -25,7 +25,7 @@ for name in a.configs.split(","):
         kw = {"format": "auto"} if fmt == "auto" else {"group": 0, "format": "sell"}
         l = (api.build_local(w.omega, w.h, w.ops[0], **kw) if w.kind == "local"
              else api.build_global(w.omega, w.h, w.ops, **kw))
-        if fmt == "stored" and l.padding > 1.03:
+        if fmt == "stored" and l.padding > 1.3:
             del l
             kw["format"] = "csr"
             l = (api.build_local(w.omega, w.h, w.ops[0], **kw) if w.kind == "local"
