@@ -120,3 +120,19 @@ def test_full_size_c2_series_is_hermitian_and_trace_preserving():
     assert np.abs(r.populations.sum(axis=1) - 1).max() <= 1e-12
     F = as_matrix(r.final.gather(), w.n)
     assert np.array_equal(F, F.conj().T)
+
+
+def test_nccl_communicator_single_rank():
+    """libnccl is resolved with dlopen and a one-rank communicator drives the
+    same series as no communicator (the N > 1 collectives are covered by
+    tests/test_gpu_multirank.py through the in-process communicator)."""
+    c = Case("c2_n36")
+    t1, tq, q = c.series
+    comm = api.Comm.from_unique_id(api.Comm.unique_id(), 0, 1, 0)
+    l = c.build_gpu(api, comm=comm)
+    r = api.series(l, l.state().from_probabilities(c.rho0), t1, tq, int(q), states=True)
+    l0 = c.build_gpu(api)
+    r0 = api.series(l0, l0.state().from_probabilities(c.rho0), t1, tq, int(q), states=True)
+    assert np.array_equal(r.states, r0.states)
+    del l
+    del comm
