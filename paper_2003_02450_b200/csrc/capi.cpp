@@ -574,9 +574,7 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
     QSWG_CHECK(cudaEventCreate(&e0));
     QSWG_CHECK(cudaEventCreate(&e1));
     QSWG_CHECK(cudaEventRecord(e0, s));
-    int64_t emit_launches = 0;
     auto emit = [&](int64_t k, const double2* state) {
-      ++emit_launches;
       qswg::dev::diag_real(state, L.block().row0, rows, n, lm->pops.get() + k * n, s);
       if (states_host)
         QSWG_CHECK(cudaMemcpyAsync(states_host + 2 * rows * k, state, static_cast<std::size_t>(rows) * sizeof(double2),
@@ -585,7 +583,10 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
         QSWG_CHECK(cudaMemcpyAsync(final_state->v.get(), state, static_cast<std::size_t>(rows) * sizeof(double2),
                                    cudaMemcpyDeviceToDevice, s));
     };
-    const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit);
+    // populations only: every emit is a device kernel into lm->pops, so a
+    // repeated identical call may replay a captured graph (expm.hpp: series)
+    const void* graph_key = (states_host || final_state) ? nullptr : lm->pops.get();
+    const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit, graph_key);
     if (L.comm() && L.comm()->world() > 1)  // every diagonal element has exactly one owner
       L.comm()->allreduce_sum_f64(lm->pops.get(), static_cast<std::size_t>((steps + 1) * n), s);
     QSWG_CHECK(cudaEventRecord(e1, s));
@@ -605,7 +606,7 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
       info->remainder = si.remainder;
       info->sub_m_star = si.sub_m_star;
       info->spmvs = si.spmvs;
-      info->launches = si.launches + emit_launches;
+      info->launches = si.launches + si.emits;
       info->device_ms = ms;
     }
   });

@@ -217,20 +217,22 @@ StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorPara
   return {sp.m_star, sp.s, f.spmvs, launches};
 }
 
-SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
-                  const TaylorParameters& params,
-                  const std::function<void(std::int64_t, const double2*)>& emit) {
-  // expm.cpp:216-217
-  if (!(tq > t1)) throw std::invalid_argument("series requires tq > t1");
-  if (steps < 1) throw std::invalid_argument("series requires at least one step");
-  DeviceGuard g(l.device());
-  const Exec ex(l);
+namespace {
+
+// Everything one `series` call enqueues after the Hermiticity check; no host
+// synchronisation on one GPU (capturable).
+SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v, double t1, double tq,
+                          std::int64_t steps, const TaylorParameters& params,
+                          const std::function<void(std::int64_t, const double2*)>& emit_fn) {
   cudaStream_t s = ex.s;
   const std::int64_t q = steps;
   const double h = (tq - t1) / static_cast<double>(q);
   reset_ctls(l, true);
-  l.set_hermitian_input(v);  // Hermitian input: every state stays Hermitian
   SeriesInfo info;
+  auto emit = [&](std::int64_t k, const double2* state) {
+    ++info.emits;
+    emit_fn(k, state);
+  };
 
   // states[0] = step(v, t1) (expm.cpp:225)
   double2* z = ex.local(kZ);
@@ -326,6 +328,75 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
       std::swap(z, sums[static_cast<std::size_t>(count - 1)]);
       if (!ex.single && ex.read(&ctl->error)) break;
     }
+  }
+  return info;
+}
+
+struct SeriesGraph {
+  std::vector<double> key, last;
+  cudaGraphExec_t exec = nullptr;
+  SeriesInfo info;
+  ~SeriesGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+}  // namespace
+
+SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
+                  const TaylorParameters& params,
+                  const std::function<void(std::int64_t, const double2*)>& emit, const void* graph_key) {
+  // expm.cpp:216-217
+  if (!(tq > t1)) throw std::invalid_argument("series requires tq > t1");
+  if (steps < 1) throw std::invalid_argument("series requires at least one step");
+  DeviceGuard g(l.device());
+  const Exec ex(l);
+  cudaStream_t s = ex.s;
+  l.set_hermitian_input(v);  // Hermitian input: every state stays Hermitian
+  static const bool graphs_off = [] {
+    const char* e = std::getenv("QSWG_GRAPH");
+    return e != nullptr && e[0] == '0';
+  }();
+  SeriesInfo info;
+  if (ex.single && graph_key != nullptr && !graphs_off) {
+    Workspace& ws = l.workspace();
+    if (!ws.series_graph) ws.series_graph = std::make_shared<SeriesGraph>();
+    auto* gr = static_cast<SeriesGraph*>(ws.series_graph.get());
+    const std::vector<double> key = {static_cast<double>(reinterpret_cast<std::uintptr_t>(v)), t1, tq,
+                                     static_cast<double>(steps), params.tolerance,
+                                     static_cast<double>(reinterpret_cast<std::uintptr_t>(graph_key)),
+                                     static_cast<double>(l.matrix().kron.herm), static_cast<double>(series_pend_max(ex.dim))};
+    if (gr->exec && gr->key == key) {
+      QSWG_CHECK(cudaGraphLaunch(gr->exec, s));
+      info = gr->info;
+      info.graph = true;
+    } else if (gr->last == key) {  // second identical call: its workspace exists, capture it
+      cudaGraph_t graph = nullptr;
+      QSWG_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        info = enqueue_series(l, ex, v, t1, tq, steps, params, emit);
+      } catch (...) {
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      QSWG_CHECK(cudaStreamEndCapture(s, &graph));
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      QSWG_CHECK(ie);
+      if (gr->exec) cudaGraphExecDestroy(gr->exec);
+      gr->exec = exec;
+      gr->key = key;
+      gr->info = info;
+      QSWG_CHECK(cudaGraphLaunch(exec, s));
+      info.graph = true;
+    } else {
+      info = enqueue_series(l, ex, v, t1, tq, steps, params, emit);
+      gr->last = key;
+    }
+  } else {
+    info = enqueue_series(l, ex, v, t1, tq, steps, params, emit);
   }
   const Flags f = read_flags(l, info.path == 2);
   info.spmvs = f.spmvs;

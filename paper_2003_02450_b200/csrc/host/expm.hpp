@@ -28,6 +28,8 @@ struct SeriesInfo {
   std::int64_t d = 0, n_super = 0, remainder = 0, sub_m_star = 0;
   std::int64_t spmvs = 0;
   std::int64_t launches = 0;  // kernels enqueued (emit() launches excluded)
+  std::int64_t emits = 0;     // emit() calls
+  bool graph = false;         // replayed from a captured CUDA graph
 };
 
 /// out = exp(t L) v.  `out` must not alias `v`.  Throws NumericalError on
@@ -38,9 +40,16 @@ StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorPara
 /// Outputs at t1 + k (tq - t1)/steps, k = 0..steps (expm.cpp:214-325).  Each
 /// output is handed to `emit(k, state)` as a device pointer valid until the
 /// call returns (stream-ordered: enqueue copies on l.stream()).
+///
+/// `graph_key` != nullptr declares that `emit` only enqueues stream-ordered
+/// device work whose targets are identified by graph_key; then a one-GPU call
+/// that repeats the previous call exactly (same v, times, tolerance, graph_key
+/// and Hermitian mode) is captured once into a CUDA graph and replayed by
+/// later identical calls — the same kernels with the same arguments, minus the
+/// per-launch host overhead (QSWG_GRAPH=0 disables).
 SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
                   const TaylorParameters& params,
-                  const std::function<void(std::int64_t, const double2*)>& emit);
+                  const std::function<void(std::int64_t, const double2*)>& emit, const void* graph_key = nullptr);
 
 /// Mean device time (ms) of one fused series-term launch with `count`
 /// active outputs (p > 1 traffic: K read, K write, count sums read+write),

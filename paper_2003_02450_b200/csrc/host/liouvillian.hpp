@@ -38,6 +38,7 @@ struct Workspace {
   std::vector<DeviceBuffer<double2>> vec;
   DeviceBuffer<dev::StepCtl> step_ctl;
   DeviceBuffer<dev::SeriesCtl> series_ctl;
+  std::shared_ptr<void> series_graph;  // expm.cpp: captured launch sequence of a repeated series call
   double2* get(std::size_t idx, std::size_t len) {
     if (vec.size() <= idx) vec.resize(idx + 1);
     if (vec[idx].size() < len) vec[idx].resize(len);
