@@ -23,6 +23,10 @@ namespace detail {
 
 constexpr std::int64_t kExactNormDimLimit = 4096;  // liouvillian.cpp:13
 constexpr std::int64_t kMaxVertices = 46340;       // n^2 must fit int32 columns
+// Auto format: the matrix-free KRON action above this dimension; below it the
+// stored superoperator (c1, dim 4096: SELL 1.57 ms vs KRON 2.55 ms per series —
+// fewer launches per term for a launch-bound system).
+constexpr std::int64_t kKronMinDim = 65536;
 constexpr double kSellMaxPadding = 1.3;  // SELL-32 if stored/nnz <= this (c3: 1.24 -> 0.83 vs 1.06 ms CSR; c4: 1.51 -> CSR wins)
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
@@ -704,7 +708,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   // ---- matrix-free Kronecker action: no superoperator stored ----
   // (the default: fewest bytes and fastest on every BASELINE config; the
   // bitwise reference-order mode needs a stored superoperator)
-  if ((cfg.format == 3 || cfg.format == 0) && cfg.group != 1) {
+  if ((cfg.format == 3 || (cfg.format == 0 && dim > kKronMinDim)) && cfg.group != 1) {
     const std::int64_t j0 = l->block_.row0 / n, j1 = (l->block_.row0 + l->block_.rows) / n;
     l->nnz_local_ = colptr[static_cast<std::size_t>(j1)] - colptr[static_cast<std::size_t>(j0)];
     l->format_ = dev::Format::Kron;
