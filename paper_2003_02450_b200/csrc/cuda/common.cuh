@@ -156,4 +156,34 @@ __device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long lon
                : "memory");
 }
 
+// Programmatic dependent launch: every kernel of the Taylor loop is launched
+// with programmatic stream serialisation.  Each kernel first waits for its
+// predecessor's completion and memory (griddepcontrol.wait; a no-op without a
+// programmatic predecessor); once its main work is done (before the final
+// reductions and the stop test) it lets its dependents' CTAs be scheduled, so
+// their launch overlaps this kernel's tail (triggering at the start was
+// measured slower on c2: the waiting CTAs compete for SM slots).
+__device__ __forceinline__ void pdl_prologue() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), int grid, int block, std::size_t smem, cudaStream_t s,
+                       Args... args) {
+  static const bool off = [] {  // experiment knob: QSWG_PDL=0 launches plainly
+    const char* e = std::getenv("QSWG_PDL");
+    return e != nullptr && e[0] == '0';
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  QSWG_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 }  // namespace qswg::dev

@@ -170,6 +170,7 @@ struct StepTermArgs {
 
 template <int G>
 __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
+  pdl_prologue();
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
   if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
     tmax = umax64(tmax, dbits(cabs2(yv)));
     smax = umax64(smax, dbits(cabs2(sv)));
   });
+  pdl_trigger();
   tmax = block_max_bits(tmax, red);
   smax = block_max_bits(smax, red);
   if (threadIdx.x == 0) {
@@ -337,6 +339,7 @@ __device__ __forceinline__ void series_store(double2* kp, double scale, long lon
 // Grid-wide ||K_p|| and the term control (last block).
 __device__ __forceinline__ void series_term_finish(const SeriesTermArgs& a, unsigned long long tmax,
                                                    unsigned long long* red) {
+  pdl_trigger();  // the main work is done: let the next kernel's CTAs in
   __shared__ int is_last;
   tmax = block_max_bits(tmax, red);
   SeriesCtl* ctl = a.ctl;
@@ -357,6 +360,7 @@ __device__ __forceinline__ void series_term_finish(const SeriesTermArgs& a, unsi
 
 template <int G>
 __global__ void __launch_bounds__(kThreads) series_term_kernel(SeriesTermArgs a, CsrView l) {
+  pdl_prologue();
   if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0;
@@ -461,6 +465,7 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
       }
     }
   }
+  pdl_trigger();
   __syncthreads();
   for (int u = threadIdx.x; u < nm; u += blockDim.x) atomicMax(&ctl->sum_bits[list[u]], smax_sh[u]);
   __syncthreads();
@@ -481,6 +486,7 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
 
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs a) {
+  pdl_prologue();
   if (flush_due(a)) flush_body<kStrict>(a);
 }
 
@@ -548,6 +554,7 @@ __device__ __forceinline__ void slice_loop(const SellView& m, const double2* __r
 
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) sell_spmv_kernel(SellView m, const double2* x, double2* y, double scale) {
+  pdl_prologue();
   slice_loop<kStrict>(m, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
@@ -569,6 +576,7 @@ struct SellStepArgs {
 
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a) {
+  pdl_prologue();
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
   if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
@@ -585,6 +593,7 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
     tmax = umax64(tmax, dbits(cabs2(yv)));
     smax = umax64(smax, dbits(cabs2(sv)));
   });
+  pdl_trigger();
   tmax = block_max_bits(tmax, red);
   smax = block_max_bits(smax, red);
   if (threadIdx.x == 0) {
@@ -604,6 +613,7 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
 
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermArgs a, SellView m) {
+  pdl_prologue();
   if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0;
@@ -897,6 +907,7 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
 template <bool kHerm, bool kFlush>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kernel(KronView m, const double2* __restrict__ x, int k,
                                                                                SeriesFlushArgs fa) {
+  pdl_prologue();
   __shared__ double2 tile[kKT][kKT + 1];
   const unsigned long long xpol = evict_last_policy();
   const long long n = m.n;
@@ -968,12 +979,17 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
     }
   }
   if constexpr (kFlush) {
-    if (flush_due(fa)) flush_body<false>(fa);
+    if (flush_due(fa)) {
+      flush_body<false>(fa);
+      return;
+    }
   }
+  pdl_trigger();
 }
 
 // V_k = X L_k' on the local columns: V_k(i, a) = sum_c conj(L_k(a, c)) X(i, c).
 __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const double2* __restrict__ x, int k) {
+  pdl_prologue();
   const unsigned long long xpol = evict_last_policy();
   const long long n = m.n;
   const KronList& u = m.u[k];
@@ -992,6 +1008,7 @@ __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const doub
 
 template <bool kHerm>
 __global__ void __launch_bounds__(kThreads) kron_spmv_kernel(KronView m, const double2* x, double2* y, double scale) {
+  pdl_prologue();
   kron_tiles<kHerm>(m, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
@@ -1013,6 +1030,7 @@ struct KronStepArgs {
 
 template <bool kHerm>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term_kernel(KronStepArgs a) {
+  pdl_prologue();
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
   if (!a.first_of_stage && *(volatile int*)&ctl->done) return;
@@ -1029,6 +1047,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term
     tmax = umax64(tmax, dbits(cabs2(yv)));
     smax = umax64(smax, dbits(cabs2(sv)));
   });
+  pdl_trigger();
   tmax = block_max_bits(tmax, red);
   smax = block_max_bits(smax, red);
   if (threadIdx.x == 0) {
@@ -1048,6 +1067,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term
 
 template <bool kHerm>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
+  pdl_prologue();
   if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0;
@@ -1111,6 +1131,8 @@ __device__ void series_init_apply(SeriesCtl* ctl, int count, int pend_max, doubl
 }
 
 __global__ void __launch_bounds__(kThreads) step_init_kernel(const double2* v, long long n, StepCtl* ctl, int decide) {
+  pdl_prologue();
+  pdl_trigger();
   norm_body(v, n, &ctl->term_bits, &ctl->arrivals, [ctl, decide](double nv) {
     if (decide) {
       step_init_apply(ctl, nv);
@@ -1122,6 +1144,8 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(const double2* v, l
 
 __global__ void __launch_bounds__(kThreads) series_init_kernel(const double2* z, long long n, int count,
                                                               int pend_max, SeriesCtl* ctl, int decide) {
+  pdl_prologue();
+  pdl_trigger();
   norm_body(z, n, &ctl->term_bits, &ctl->arrivals, [ctl, count, pend_max, decide](double nz) {
     if (decide) {
       series_init_apply(ctl, count, pend_max, nz);
@@ -1133,30 +1157,44 @@ __global__ void __launch_bounds__(kThreads) series_init_kernel(const double2* z,
 
 // Control steps after a cross-GPU allreduce(max) of the maxima (one thread).
 __global__ void step_init_fin_kernel(StepCtl* ctl) {
+  pdl_prologue();
+  pdl_trigger();
   step_init_apply(ctl, bitsd(ctl->term_bits));
 }
 __global__ void series_init_fin_kernel(SeriesCtl* ctl, int count, int pend_max) {
+  pdl_prologue();
+  pdl_trigger();
   series_init_apply(ctl, count, pend_max, bitsd(ctl->term_bits));
 }
 __global__ void step_control_kernel(StepCtl* ctl, int first_of_stage, int stage, double tol) {
+  pdl_prologue();
+  pdl_trigger();
   step_control(ctl, first_of_stage, stage, tol);
 }
 __global__ void __launch_bounds__(kThreads) series_term_control_kernel(SeriesCtl* ctl, int p, int last, double tol) {
+  pdl_prologue();
+  pdl_trigger();
   series_term_control(ctl, p, last, tol);
 }
 __global__ void __launch_bounds__(kThreads) series_flush_control_kernel(SeriesCtl* ctl, int p, double tol) {
+  pdl_prologue();
+  pdl_trigger();
   series_flush_control(ctl, p, tol);
 }
 
 // --------------------------------------------------------------- plain SpMV
 template <int G>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(CsrView l, const double2* x, double2* y, double scale) {
+  pdl_prologue();
+  pdl_trigger();
   tile_loop<G>(l, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
 
 __global__ void diag_kernel(const double2* v, long long row0, long long rows, long long n, double* pops) {
+  pdl_prologue();
+  pdl_trigger();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long g = i * (n + 1) - row0;
@@ -1165,6 +1203,8 @@ __global__ void diag_kernel(const double2* v, long long row0, long long rows, lo
 }
 
 __global__ void probs_kernel(double2* v, long long row0, long long rows, long long n, const double* p) {
+  pdl_prologue();
+  pdl_trigger();
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < rows;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long g = row0 + k;
@@ -1176,6 +1216,8 @@ __global__ void probs_kernel(double2* v, long long row0, long long rows, long lo
 // *flag = 0 when some X(i, j) != conj X(j, i) (i <= j); one thread per
 // upper element, lanes along i (the mirrored reads are strided).
 __global__ void hermitian_check_kernel(const double2* __restrict__ x, long long n, int* flag) {
+  pdl_prologue();
+  pdl_trigger();
   const long long total = n * n;
   bool ok = true;
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < total;
@@ -1189,6 +1231,8 @@ __global__ void hermitian_check_kernel(const double2* __restrict__ x, long long 
 }
 
 __global__ void pattern_hermitian_kernel(double2* v, long long n) {
+  pdl_prologue();
+  pdl_trigger();
   const long long total = n * n;
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < total;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1202,6 +1246,8 @@ __global__ void pattern_hermitian_kernel(double2* v, long long n) {
 }
 
 __global__ void pattern_kernel(double2* v, long long n) {
+  pdl_prologue();
+  pdl_trigger();
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
     const unsigned long long h = (static_cast<unsigned long long>(k) + 1) * 0x9E3779B97F4A7C15ull;
@@ -1251,7 +1297,7 @@ void dispatch_group(int g, long long rows, cudaStream_t s, Args... args) {
 #define QSWG_G(GV)                                                          \
   case GV: {                                                                \
     auto k = KT<GV>::fn;                                                    \
-    k<<<persistent_grid(k, rows), kThreads, 0, s>>>(args...);              \
+    launch_pdl(k, persistent_grid(k, rows), kThreads, 0, s, args...);              \
     break;                                                                  \
   }
     QSWG_G(1)
@@ -1275,32 +1321,32 @@ template <int G> struct SpmvK { static constexpr auto fn = spmv_kernel<G>; };
 int valid_group(int g) { return (g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32) ? g : 0; }
 
 void step_init(const double2* v, std::int64_t n, StepCtl* ctl, bool decide, cudaStream_t s) {
-  step_init_kernel<<<small_grid(n), kThreads, 0, s>>>(v, n, ctl, decide ? 1 : 0);
+  launch_pdl(step_init_kernel, small_grid(n), kThreads, 0, s, v, n, ctl, decide ? 1 : 0);
   QSWG_LAUNCH_CHECK("step_init");
 }
 
 void step_init_fin(StepCtl* ctl, cudaStream_t s) {
-  step_init_fin_kernel<<<1, 1, 0, s>>>(ctl);
+  launch_pdl(step_init_fin_kernel, 1, 1, 0, s, ctl);
   QSWG_LAUNCH_CHECK("step_init_fin");
 }
 
 void step_control(StepCtl* ctl, bool first_of_stage, int stage, double tol, cudaStream_t s) {
-  step_control_kernel<<<1, 1, 0, s>>>(ctl, first_of_stage ? 1 : 0, stage, tol);
+  launch_pdl(step_control_kernel, 1, 1, 0, s, ctl, first_of_stage ? 1 : 0, stage, tol);
   QSWG_LAUNCH_CHECK("step_control");
 }
 
 void series_init_fin(SeriesCtl* ctl, int count, int pend_max, cudaStream_t s) {
-  series_init_fin_kernel<<<1, 1, 0, s>>>(ctl, count, pend_max);
+  launch_pdl(series_init_fin_kernel, 1, 1, 0, s, ctl, count, pend_max);
   QSWG_LAUNCH_CHECK("series_init_fin");
 }
 
 void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s) {
-  series_term_control_kernel<<<1, kThreads, 0, s>>>(ctl, p, last, tol);
+  launch_pdl(series_term_control_kernel, 1, kThreads, 0, s, ctl, p, last, tol);
   QSWG_LAUNCH_CHECK("series_term_control");
 }
 
 void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {
-  series_flush_control_kernel<<<1, kThreads, 0, s>>>(ctl, p, tol);
+  launch_pdl(series_flush_control_kernel, 1, kThreads, 0, s, ctl, p, tol);
   QSWG_LAUNCH_CHECK("series_flush_control");
 }
 
@@ -1310,17 +1356,17 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
     KronStepArgs a{m.kron, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.kron.herm) {
       const auto g = kron_geom(kron_step_term_kernel<true>, m.kron);
-      kron_step_term_kernel<true><<<g.first, kThreads, g.second, s>>>(a);
+      launch_pdl(kron_step_term_kernel<true>, g.first, kThreads, g.second, s, a);
     } else {
       const auto g = kron_geom(kron_step_term_kernel<false>, m.kron);
-      kron_step_term_kernel<false><<<g.first, kThreads, g.second, s>>>(a);
+      launch_pdl(kron_step_term_kernel<false>, g.first, kThreads, g.second, s, a);
     }
   } else if (m.format == Format::Sell) {
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
-      sell_step_term_kernel<true><<<sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s>>>(a);
+      launch_pdl(sell_step_term_kernel<true>, sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s, a);
     } else {
-      sell_step_term_kernel<false><<<sell_grid(sell_step_term_kernel<false>, m.sell), kThreads, 0, s>>>(a);
+      launch_pdl(sell_step_term_kernel<false>, sell_grid(sell_step_term_kernel<false>, m.sell), kThreads, 0, s, a);
     }
   } else {
     StepTermArgs a{m.csr, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
@@ -1332,7 +1378,7 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
 void series_init(const double2* z, std::int64_t n, int count, int pend_max, SeriesCtl* ctl, bool decide,
                  cudaStream_t s) {
   if (count < 1 || count > kMaxSeriesD) throw std::invalid_argument("series super-step size out of range");
-  series_init_kernel<<<small_grid(n), kThreads, 0, s>>>(z, n, count, pend_max, ctl, decide ? 1 : 0);
+  launch_pdl(series_init_kernel, small_grid(n), kThreads, 0, s, z, n, count, pend_max, ctl, decide ? 1 : 0);
   QSWG_LAUNCH_CHECK("series_init");
 }
 
@@ -1342,16 +1388,16 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
   if (m.format == Format::Kron) {
     if (m.kron.herm) {
       const auto g = kron_geom(kron_series_term_kernel<true>, m.kron);
-      kron_series_term_kernel<true><<<g.first, kThreads, g.second, s>>>(a, m.kron);
+      launch_pdl(kron_series_term_kernel<true>, g.first, kThreads, g.second, s, a, m.kron);
     } else {
       const auto g = kron_geom(kron_series_term_kernel<false>, m.kron);
-      kron_series_term_kernel<false><<<g.first, kThreads, g.second, s>>>(a, m.kron);
+      launch_pdl(kron_series_term_kernel<false>, g.first, kThreads, g.second, s, a, m.kron);
     }
   } else if (m.format == Format::Sell) {
     if (m.group == 1) {
-      sell_series_term_kernel<true><<<sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s>>>(a, m.sell);
+      launch_pdl(sell_series_term_kernel<true>, sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s, a, m.sell);
     } else {
-      sell_series_term_kernel<false><<<sell_grid(sell_series_term_kernel<false>, m.sell), kThreads, 0, s>>>(a, m.sell);
+      launch_pdl(sell_series_term_kernel<false>, sell_grid(sell_series_term_kernel<false>, m.sell), kThreads, 0, s, a, m.sell);
     }
   } else {
     dispatch_group<SeriesTermK>(m.group, m.csr.rows, s, a, m.csr);
@@ -1365,9 +1411,9 @@ void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, 
   (void)count;
   const SeriesFlushArgs a{ring, row0, rows, z, sums, p, tol, ctl, decide ? 1 : 0};
   if (strict) {
-    series_flush_kernel<true><<<persistent_grid(series_flush_kernel<true>, rows), kThreads, 0, s>>>(a);
+    launch_pdl(series_flush_kernel<true>, persistent_grid(series_flush_kernel<true>, rows), kThreads, 0, s, a);
   } else {
-    series_flush_kernel<false><<<persistent_grid(series_flush_kernel<false>, rows), kThreads, 0, s>>>(a);
+    launch_pdl(series_flush_kernel<false>, persistent_grid(series_flush_kernel<false>, rows), kThreads, 0, s, a);
   }
   QSWG_LAUNCH_CHECK("series_flush");
 }
@@ -1377,10 +1423,10 @@ template <bool kFlush>
 void launch_w(const DevMatrix& m, const double2* x, int k, const SeriesFlushArgs& fa, cudaStream_t s) {
   if (m.kron.herm) {
     const auto g = kron_geom(kron_w_kernel<true, kFlush>, m.kron);
-    kron_w_kernel<true, kFlush><<<g.first, kThreads, g.second, s>>>(m.kron, x, k, fa);
+    launch_pdl(kron_w_kernel<true, kFlush>, g.first, kThreads, g.second, s, m.kron, x, k, fa);
   } else {
     const auto g = kron_geom(kron_w_kernel<false, kFlush>, m.kron);
-    kron_w_kernel<false, kFlush><<<g.first, kThreads, g.second, s>>>(m.kron, x, k, fa);
+    launch_pdl(kron_w_kernel<false, kFlush>, g.first, kThreads, g.second, s, m.kron, x, k, fa);
   }
 }
 }  // namespace
@@ -1399,7 +1445,7 @@ bool kron_prepare_flush(const DevMatrix& m, const double2* x, const SeriesRing& 
     }
     if (m.kron.factored && !m.kron.herm) {
       const auto gv = kron_geom(kron_v_kernel, m.kron);
-      kron_v_kernel<<<gv.first, kThreads, gv.second, s>>>(m.kron, x, k);
+      launch_pdl(kron_v_kernel, gv.first, kThreads, gv.second, s, m.kron, x, k);
       QSWG_LAUNCH_CHECK("kron_prepare_flush");
     }
   }
@@ -1414,7 +1460,7 @@ void kron_prepare(const DevMatrix& m, const double2* x, cudaStream_t s) {
     QSWG_LAUNCH_CHECK("kron_prepare");
     if (m.kron.factored && !m.kron.herm) {  // Hermitian path: V_k = W_k', read from Wt_k
       const auto gv = kron_geom(kron_v_kernel, m.kron);
-      kron_v_kernel<<<gv.first, kThreads, gv.second, s>>>(m.kron, x, k);
+      launch_pdl(kron_v_kernel, gv.first, kThreads, gv.second, s, m.kron, x, k);
       QSWG_LAUNCH_CHECK("kron_prepare");
     }
   }
@@ -1425,7 +1471,7 @@ bool kron_hermitian_check(const DevMatrix& m, const double2* x, cudaStream_t s) 
   QSWG_CUDA(cudaMemsetAsync(m.kron.herm_flag, 1, sizeof(int), s));  // any non-zero value = Hermitian
   const long long n = m.kron.n;
   const long long want = (n * n + kThreads - 1) / kThreads, cap = sm_count() * 8LL;
-  hermitian_check_kernel<<<static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap), kThreads, 0, s>>>(x, n, m.kron.herm_flag);
+  launch_pdl(hermitian_check_kernel, static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap), kThreads, 0, s, x, n, m.kron.herm_flag);
   QSWG_LAUNCH_CHECK("kron_hermitian_check");
   int flag = 0;
   QSWG_CUDA(cudaMemcpyAsync(&flag, m.kron.herm_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1438,16 +1484,16 @@ void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaSt
     kron_prepare(m, x, s);  // single-GPU product (multi-GPU callers exchange W first)
     if (m.kron.herm) {
       const auto g = kron_geom(kron_spmv_kernel<true>, m.kron);
-      kron_spmv_kernel<true><<<g.first, kThreads, g.second, s>>>(m.kron, x, y, scale);
+      launch_pdl(kron_spmv_kernel<true>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
     } else {
       const auto g = kron_geom(kron_spmv_kernel<false>, m.kron);
-      kron_spmv_kernel<false><<<g.first, kThreads, g.second, s>>>(m.kron, x, y, scale);
+      launch_pdl(kron_spmv_kernel<false>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
     }
   } else if (m.format == Format::Sell) {
     if (m.group == 1) {
-      sell_spmv_kernel<true><<<sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);
+      launch_pdl(sell_spmv_kernel<true>, sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s, m.sell, x, y, scale);
     } else {
-      sell_spmv_kernel<false><<<sell_grid(sell_spmv_kernel<false>, m.sell), kThreads, 0, s>>>(m.sell, x, y, scale);
+      launch_pdl(sell_spmv_kernel<false>, sell_grid(sell_spmv_kernel<false>, m.sell), kThreads, 0, s, m.sell, x, y, scale);
     }
   } else {
     dispatch_group<SpmvK>(m.group, m.csr.rows, s, m.csr, x, y, scale);
@@ -1457,23 +1503,23 @@ void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaSt
 
 void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
                double* pops, cudaStream_t s) {
-  diag_kernel<<<small_grid(n), kThreads, 0, s>>>(v_local, row0, rows, n, pops);
+  launch_pdl(diag_kernel, small_grid(n), kThreads, 0, s, v_local, row0, rows, n, pops);
   QSWG_LAUNCH_CHECK("diag_real");
 }
 
 void fill_pattern(double2* v, std::int64_t n, cudaStream_t s) {
-  pattern_kernel<<<small_grid(n), kThreads, 0, s>>>(v, n);
+  launch_pdl(pattern_kernel, small_grid(n), kThreads, 0, s, v, n);
   QSWG_LAUNCH_CHECK("fill_pattern");
 }
 
 void fill_pattern_hermitian(double2* v, std::int64_t n, cudaStream_t s) {
-  pattern_hermitian_kernel<<<small_grid(n * n), kThreads, 0, s>>>(v, n);
+  launch_pdl(pattern_hermitian_kernel, small_grid(n * n), kThreads, 0, s, v, n);
   QSWG_LAUNCH_CHECK("fill_pattern_hermitian");
 }
 
 void state_from_probabilities(double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
                               const double* p, cudaStream_t s) {
-  probs_kernel<<<small_grid(rows), kThreads, 0, s>>>(v_local, row0, rows, n, p);
+  launch_pdl(probs_kernel, small_grid(rows), kThreads, 0, s, v_local, row0, rows, n, p);
   QSWG_LAUNCH_CHECK("state_from_probabilities");
 }
 
