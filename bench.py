@@ -96,6 +96,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def l2_for(config, fmt):
+    """L2 bytes requested by the SMs per launch of the dominant kernel (ncu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(f"{config}:{fmt}", {}).get("l2_bytes_per_launch")
+    except Exception:
+        return None
+
+
 def traffic_for(config, fmt):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel from the committed ncu --set full capture (profiles/traffic.json)."""
@@ -357,7 +366,12 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_for(w.name, l.format), "kernel": kernel_name,
                      "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell), "bytes_per_launch": term_bytes(l), "ms_per_launch": term_ms,
-                     "peak_source": peak_src, "share_of_step": share, "parts": parts_line},
+                     "peak_source": peak_src, "share_of_step": share, "parts": parts_line,
+                     "l2": ({"bytes_per_launch": l2_for(w.name, l.format),
+                             "achieved_gbs": l2_for(w.name, l.format) / (term_ms * 1e-3) / 1e9,
+                             "note": "gather traffic SM<-L2 (ncu lts__t_sectors_srcunit_tex); the KRON term "
+                                     "kernel is bound by these gathers, not by HBM"}
+                            if l2_for(w.name, l.format) else None)},
         "superop_spmv": superop,
         "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,
                 "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms},
