@@ -38,13 +38,16 @@ enum {
   QSWG_ECUDA = 5,
   QSWG_ENCCL = 6,
   QSWG_ENOMEM = 7,
-  QSWG_EINTERNAL = 9
+  QSWG_EINTERNAL = 9,
+  QSWG_EFORMAT = 10,   /* qsw::FileFormatError (graph.hpp:11-15) */
+  QSWG_EIO = 11        /* qsw::IoError (container.hpp:13-17)      */
 };
 
 typedef struct qswg_sparse qswg_sparse;           /* host canonical CSR, complex128 */
 typedef struct qswg_liouvillian qswg_liouvillian; /* device superoperator (row block) */
 typedef struct qswg_state qswg_state;             /* device vec(rho) (row block)     */
 typedef struct qswg_comm qswg_comm;               /* multi-GPU communicator          */
+typedef struct qswg_container qswg_container;     /* host QSWBOX result container    */
 
 typedef struct { int64_t target; double rate; } qswg_source_arc; /* graph.hpp:17-20 SourceArc */
 typedef struct { int64_t origin; double rate; } qswg_sink_arc;   /* graph.hpp:23-26 SinkArc   */
@@ -172,6 +175,46 @@ int qswg_step(const qswg_liouvillian* l, const qswg_state* v, double t, double t
 int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, double tq, int64_t steps,
                 double tolerance, double* pops_host, double* states_host, qswg_state* final_state,
                 qswg_series_info* info);
+
+/* qswg_series plus the coherence norm of every output state, computed on the
+ * device: coherence_host[(steps+1)] = max_{i != j} |rho_k(i, j)|, what
+ * run() stores as "coherence_norm" from DensityMatrix::max_coherence of each
+ * gathered state (run.cpp:124-137, walk.cpp:32-40).  NULL skips it. */
+int qswg_series_observe(const qswg_liouvillian* l, const qswg_state* v, double t1, double tq, int64_t steps,
+                        double tolerance, double* pops_host, double* coherence_host, double* states_host,
+                        qswg_state* final_state, qswg_series_info* info);
+/* max_{i != j} |rho(i, j)| of one state (DensityMatrix::max_coherence, walk.hpp:25). */
+int qswg_state_coherence(const qswg_state* s, double* out);
+
+/* ---- file formats either side of the path ------ */
+/* WeightedDigraph::load_matrix_market (graph.cpp:54-136) on an in-memory
+ * stream: the adjacency matrix (entry (i, j) = arc j -> i).  Format errors
+ * -> QSWG_EFORMAT; self-loops / non-positive weights -> QSWG_EINVAL. */
+int qswg_matrix_market_parse(const char* text, int64_t len, qswg_sparse** adjacency);
+/* The graph-file loader of run() (run.cpp:14-25): QSWG_EIO when the file
+ * cannot be opened, every other failure QSWG_EFORMAT naming the file. */
+int qswg_matrix_market_load(const char* path, qswg_sparse** adjacency);
+/* WeightedDigraph::save_matrix_market (graph.cpp:138-150). */
+int qswg_matrix_market_save(const qswg_sparse* adjacency, const char* path);
+/* ResultContainer (container.hpp:19-46): metadata text + named float64
+ * arrays (row-major, explicit shape), QSWBOX v1 bytes on disk. */
+int qswg_container_create(qswg_container** out);
+void qswg_container_destroy(qswg_container* c);
+int qswg_container_set_metadata(qswg_container* c, const char* text, int64_t len);
+int qswg_container_get_metadata(const qswg_container* c, char* buf, int64_t cap, int64_t* len);
+/* Inserts or replaces array `name`; data holds prod(shape) doubles. */
+int qswg_container_put_array(qswg_container* c, const char* name, int64_t rank, const int64_t* shape,
+                             const double* data);
+int qswg_container_array_count(const qswg_container* c, int64_t* count);
+/* Arrays are enumerated in name order (the on-disk order). */
+int qswg_container_array_info(const qswg_container* c, int64_t index, char* name, int64_t name_cap,
+                              int64_t* name_len, int64_t* rank, int64_t* shape, int64_t shape_cap);
+int qswg_container_array_data(const qswg_container* c, int64_t index, double* data);
+/* write_container / read_container (container.hpp:48-49). */
+int qswg_container_write(const qswg_container* c, const char* path);
+int qswg_container_read(const char* path, qswg_container** out);
+/* emit_plot_data (container.hpp:51-56) into a text file. */
+int qswg_container_plot_data(const qswg_container* c, const char* quantity, const char* path);
 
 /* ---- multi-GPU (one process per GPU) ------------------------------------ */
 /* Row partition on rho-column boundaries balanced by nnz (the device build

@@ -25,6 +25,7 @@ dp = C.POINTER(C.c_double)
 vp = C.c_void_p
 
 OK, EINVAL, ERANGE, ENUMERICAL, ESTATE, ECUDA, ENCCL, ENOMEM, EINTERNAL = 0, 1, 2, 3, 4, 5, 6, 7, 9
+EFORMAT, EIO = 10, 11
 
 
 class QswgError(RuntimeError):
@@ -52,8 +53,19 @@ class LogicError(QswgError):
     code = ESTATE
 
 
+class FileFormatError(QswgError):
+    """qsw::FileFormatError (graph.hpp:11-15)."""
+    code = EFORMAT
+
+
+class IoError(QswgError, OSError):
+    """qsw::IoError (container.hpp:13-17)."""
+    code = EIO
+
+
 _EXC = {EINVAL: InvalidArgument, ERANGE: OutOfRange, ENUMERICAL: NumericalError,
-        ESTATE: LogicError, ECUDA: CudaError, ENCCL: CudaError, ENOMEM: MemoryError}
+        ESTATE: LogicError, ECUDA: CudaError, ENCCL: CudaError, ENOMEM: MemoryError,
+        EFORMAT: FileFormatError, EIO: IoError}
 
 
 def check(rc: int):
@@ -137,6 +149,23 @@ SIGNATURES = {
     "qswg_step": (C.c_int, [vp, vp, C.c_double, C.c_double, vp, C.POINTER(StepInfo)]),
     "qswg_series": (C.c_int, [vp, vp, C.c_double, C.c_double, i64, C.c_double, dp, dp, vp,
                               C.POINTER(SeriesInfo)]),
+    "qswg_series_observe": (C.c_int, [vp, vp, C.c_double, C.c_double, i64, C.c_double, dp, dp, dp, vp,
+                                      C.POINTER(SeriesInfo)]),
+    "qswg_state_coherence": (C.c_int, [vp, dp]),
+    "qswg_matrix_market_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(vp)]),
+    "qswg_matrix_market_load": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "qswg_matrix_market_save": (C.c_int, [vp, C.c_char_p]),
+    "qswg_container_create": (C.c_int, [C.POINTER(vp)]),
+    "qswg_container_destroy": (None, [vp]),
+    "qswg_container_set_metadata": (C.c_int, [vp, C.c_char_p, i64]),
+    "qswg_container_get_metadata": (C.c_int, [vp, C.c_char_p, i64, i64p]),
+    "qswg_container_put_array": (C.c_int, [vp, C.c_char_p, i64, i64p, dp]),
+    "qswg_container_array_count": (C.c_int, [vp, i64p]),
+    "qswg_container_array_info": (C.c_int, [vp, i64, C.c_char_p, i64, i64p, i64p, i64p, i64]),
+    "qswg_container_array_data": (C.c_int, [vp, i64, dp]),
+    "qswg_container_write": (C.c_int, [vp, C.c_char_p]),
+    "qswg_container_read": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "qswg_container_plot_data": (C.c_int, [vp, C.c_char_p, C.c_char_p]),
     "qswg_plan_rows": (C.c_int, [i64, i64p, C.c_int, i64p]),
     "qswg_plan_halo": (C.c_int, [i64p, i64, i64p, C.c_int, C.c_int, i64p, i64p]),
     "qswg_liouvillian_partition": (C.c_int, [vp, i64p, i64p, i64p]),

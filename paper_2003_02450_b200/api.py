@@ -14,8 +14,8 @@ import dataclasses
 import numpy as np
 
 from . import _lib
-from ._lib import (CudaError, InvalidArgument, LogicError, NumericalError, OutOfRange,  # noqa: F401
-                   QswgError, check, lib)
+from ._lib import (CudaError, FileFormatError, InvalidArgument, IoError, LogicError,  # noqa: F401
+                   NumericalError, OutOfRange, QswgError, check, lib)
 from .graphs import Csr
 
 DOUBLE_TOL = 2.0 ** -53  # expm.hpp:18
@@ -348,6 +348,12 @@ class StateVector:
         check(lib.qswg_state_populations(self._h, _dp(out)))
         return out
 
+    def coherence(self) -> float:
+        """max_{i != j} |rho(i, j)| on the device (DensityMatrix::max_coherence, walk.cpp:32-40)."""
+        out = C.c_double()
+        check(lib.qswg_state_coherence(self._h, C.byref(out)))
+        return out.value
+
 
 # ----------------------------------------------------------------- Taylor
 def build_theta_table(tolerance: float = DOUBLE_TOL) -> np.ndarray:
@@ -379,12 +385,15 @@ class SeriesResult:
     states: np.ndarray | None
     final: StateVector | None
     info: object
+    coherence: np.ndarray | None = None
 
 
 def series(l: Liouvillian, v: StateVector, t1: float, tq: float, steps: int, tolerance: float = DOUBLE_TOL,
-           populations: bool = True, states: bool = False, final: bool = False, pops_out=None) -> SeriesResult:
+           populations: bool = True, states: bool = False, final: bool = False, pops_out=None,
+           coherence: bool = False) -> SeriesResult:
     """States at t1 + k (tq - t1)/steps, k = 0..steps (expm.hpp:60-63).
-    `pops_out` may be a preallocated (e.g. pinned) float64 [(steps+1), n] array."""
+    `pops_out` may be a preallocated (e.g. pinned) float64 [(steps+1), n] array;
+    `coherence` adds max_{i != j} |rho_k(i, j)| per output, computed on the device."""
     if pops_out is not None:
         assert pops_out.dtype == np.float64 and pops_out.size == (steps + 1) * l.n and pops_out.flags.c_contiguous
         pops = pops_out
@@ -392,14 +401,112 @@ def series(l: Liouvillian, v: StateVector, t1: float, tq: float, steps: int, tol
         pops = np.zeros((steps + 1, l.n)) if populations else None
     st = np.zeros((steps + 1, l.rows), np.complex128) if states else None
     fin = StateVector(l) if final else None
+    coh = np.zeros(steps + 1) if coherence and steps >= 1 else None
     info = _lib.SeriesInfo()
-    check(lib.qswg_series(l._h, v._h, t1, tq, steps, tolerance,
-                          _dp(pops) if pops is not None else None,
-                          _dp(st.view(np.float64)) if st is not None else None,
-                          fin._h if fin is not None else None, C.byref(info)))
+    check(lib.qswg_series_observe(l._h, v._h, t1, tq, steps, tolerance,
+                                  _dp(pops) if pops is not None else None,
+                                  _dp(coh) if coh is not None else None,
+                                  _dp(st.view(np.float64)) if st is not None else None,
+                                  fin._h if fin is not None else None, C.byref(info)))
     h = (tq - t1) / steps if steps >= 1 else 0.0
-    times = np.array([t1 + h * k for k in range(steps + 1)])
-    return SeriesResult(times, pops, st, fin, info)
+    times = np.array([t1 + h * float(k) for k in range(steps + 1)])  # expm.cpp:222-223
+    return SeriesResult(times, pops, st, fin, info, coh)
+
+
+# ------------------------------------------------------------ file formats
+def parse_matrix_market(text) -> SparseMatrix:
+    """WeightedDigraph::load_matrix_market on an in-memory stream (graph.cpp:54-136):
+    the adjacency matrix, entry (i, j) = arc j -> i.  FileFormatError for a
+    malformed stream, ValueError for a self-loop or a non-positive weight."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    check(lib.qswg_matrix_market_parse(b, len(b), C.byref(h)))
+    return SparseMatrix(h)
+
+
+def load_matrix_market(path) -> SparseMatrix:
+    """The graph-file loader of run() (run.cpp:14-25): IoError when the file
+    cannot be opened, FileFormatError (naming the file) for anything else."""
+    h = C.c_void_p()
+    check(lib.qswg_matrix_market_load(str(path).encode(), C.byref(h)))
+    return SparseMatrix(h)
+
+
+def save_matrix_market(adjacency, path) -> None:
+    """WeightedDigraph::save_matrix_market (graph.cpp:138-150)."""
+    check(lib.qswg_matrix_market_save(SparseMatrix.of(adjacency)._h, str(path).encode()))
+
+
+class ResultContainer:
+    """qsw::ResultContainer (container.hpp:19-46): `metadata` text plus named
+    float64 arrays; `write`/`read` use the QSWBOX v1 bytes of the reference."""
+
+    def __init__(self, metadata: str = "", arrays=None):
+        self.metadata = metadata
+        self.arrays = dict(arrays or {})
+
+    def _handle(self):
+        h = C.c_void_p()
+        check(lib.qswg_container_create(C.byref(h)))
+        try:
+            m = self.metadata.encode() if isinstance(self.metadata, str) else bytes(self.metadata)
+            check(lib.qswg_container_set_metadata(h, m, len(m)))
+            for name, a in self.arrays.items():
+                a = np.array(a, dtype=np.float64, order="C")  # keeps 0-d arrays 0-d
+                shape = np.asarray(a.shape, np.int64)
+                check(lib.qswg_container_put_array(h, str(name).encode(), a.ndim, _i64p(shape), _dp(a)))
+        except Exception:
+            lib.qswg_container_destroy(h)
+            raise
+        return h
+
+    @staticmethod
+    def _from_handle(h) -> "ResultContainer":
+        n = C.c_int64()
+        check(lib.qswg_container_get_metadata(h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        check(lib.qswg_container_get_metadata(h, buf, n.value, C.byref(n)))
+        out = ResultContainer(buf.raw[: n.value].decode(errors="replace"))
+        check(lib.qswg_container_array_count(h, C.byref(n)))
+        for k in range(n.value):
+            nl, rank = C.c_int64(), C.c_int64()
+            check(lib.qswg_container_array_info(h, k, None, 0, C.byref(nl), C.byref(rank), None, 0))
+            name = C.create_string_buffer(max(nl.value, 1))
+            shape = np.zeros(max(rank.value, 1), np.int64)
+            check(lib.qswg_container_array_info(h, k, name, nl.value, C.byref(nl), C.byref(rank),
+                                                _i64p(shape), rank.value))
+            shp = tuple(int(d) for d in shape[: rank.value])
+            data = np.zeros(int(np.prod(shp)) if shp else 1)
+            check(lib.qswg_container_array_data(h, k, _dp(data)) if data.size else 0)
+            out.arrays[name.raw[: nl.value].decode(errors="replace")] = data.reshape(shp)
+        return out
+
+    def write(self, path) -> None:
+        """write_container (container.hpp:48)."""
+        h = self._handle()
+        try:
+            check(lib.qswg_container_write(h, str(path).encode()))
+        finally:
+            lib.qswg_container_destroy(h)
+
+    @staticmethod
+    def read(path) -> "ResultContainer":
+        """read_container (container.hpp:49): FileFormatError on bad magic,
+        version, checksum or section layout."""
+        h = C.c_void_p()
+        check(lib.qswg_container_read(str(path).encode(), C.byref(h)))
+        try:
+            return ResultContainer._from_handle(h)
+        finally:
+            lib.qswg_container_destroy(h)
+
+    def emit_plot_data(self, quantity: str, path) -> None:
+        """emit_plot_data (container.hpp:51-56): one text row per time."""
+        h = self._handle()
+        try:
+            check(lib.qswg_container_plot_data(h, quantity.encode(), str(path).encode()))
+        finally:
+            lib.qswg_container_destroy(h)
 
 
 # -------------------------------------------------------------- multi-GPU
@@ -550,10 +657,11 @@ class WalkSystem:
         self._result, info = step(self.liouvillian, self._initial, t, tolerance)
         return info
 
-    def series(self, t1, tq, steps, tolerance=DOUBLE_TOL, states=False):
+    def series(self, t1, tq, steps, tolerance=DOUBLE_TOL, states=False, coherence=False):
         if self._initial is None:
             raise LogicError("no initial state: call initial_state first")
-        r = series(self.liouvillian, self._initial, t1, tq, steps, tolerance, True, states, True)
+        r = series(self.liouvillian, self._initial, t1, tq, steps, tolerance, True, states, True,
+                   coherence=coherence)
         self._result = r.final
         if self._vsets is not None:
             r.populations = np.stack([nm_measure(p, self._vsets) for p in r.populations])

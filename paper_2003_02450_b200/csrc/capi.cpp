@@ -5,9 +5,13 @@
 //   CUDA failures -> QSWG_ECUDA, allocation -> QSWG_ENOMEM.
 #include "../../include/qswg.h"
 
+#include <algorithm>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <memory>
 #include <new>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -16,6 +20,7 @@
 #include "host/dist.hpp"
 #include "host/expm.hpp"
 #include "host/graph.hpp"
+#include "host/io.hpp"
 #include "host/liouvillian.hpp"
 #include "host/nm.hpp"
 #include "host/sparse.hpp"
@@ -27,6 +32,10 @@ struct qswg_sparse {
 struct qswg_liouvillian {
   std::unique_ptr<qswg::Liouvillian> l;
   qswg::DeviceBuffer<double> pops;  // (steps + 1) * n populations of the last series
+  qswg::DeviceBuffer<unsigned long long> coh;  // steps + 1 coherence norms (bit patterns)
+};
+struct qswg_container {
+  qswg::ResultContainer c;
 };
 struct qswg_state {
   const qswg_liouvillian* owner;
@@ -58,6 +67,10 @@ int guarded(F&& f) {
     return QSWG_OK;
   } catch (const qswg::NumericalError& e) {
     return fail(QSWG_ENUMERICAL, e.what());
+  } catch (const qswg::FileFormatError& e) {
+    return fail(QSWG_EFORMAT, e.what());
+  } catch (const qswg::IoError& e) {
+    return fail(QSWG_EIO, e.what());
   } catch (const std::out_of_range& e) {
     return fail(QSWG_ERANGE, e.what());
   } catch (const std::invalid_argument& e) {
@@ -510,6 +523,21 @@ int qswg_state_populations(const qswg_state* s, double* out) {
   });
 }
 
+int qswg_state_coherence(const qswg_state* s, double* out) {
+  return guarded([&] {
+    need(s, "state");
+    need(out, "out");
+    const qswg::Liouvillian& L = *s->owner->l;
+    qswg::DeviceGuard g(L.device());
+    qswg::DeviceBuffer<unsigned long long> d(1);
+    QSWG_CHECK(cudaMemsetAsync(d.get(), 0, d.bytes(), L.stream()));
+    qswg::dev::coherence_bits(s->v.get(), L.block().row0, L.block().rows, L.n(), d.get(), L.stream());
+    if (L.comm() && L.comm()->world() > 1) L.comm()->allreduce_max_u64(d.get(), 1, L.stream());
+    QSWG_CHECK(cudaMemcpyAsync(out, d.get(), d.bytes(), cudaMemcpyDeviceToHost, L.stream()));
+    QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+  });
+}
+
 void qswg_state_destroy(qswg_state* s) {
   if (!s) return;
   try {
@@ -556,6 +584,12 @@ int qswg_step(const qswg_liouvillian* l, const qswg_state* v, double t, double t
 int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, double tq, int64_t steps,
                 double tolerance, double* pops_host, double* states_host, qswg_state* final_state,
                 qswg_series_info* info) {
+  return qswg_series_observe(l, v, t1, tq, steps, tolerance, pops_host, nullptr, states_host, final_state, info);
+}
+
+int qswg_series_observe(const qswg_liouvillian* l, const qswg_state* v, double t1, double tq, int64_t steps,
+                        double tolerance, double* pops_host, double* coherence_host, double* states_host,
+                        qswg_state* final_state, qswg_series_info* info) {
   return guarded([&] {
     need(l, "liouvillian");
     check_state(l, v, "v");
@@ -569,6 +603,10 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
     if (steps >= 1) {
       lm->pops.resize(static_cast<std::size_t>((steps + 1) * n));
       QSWG_CHECK(cudaMemsetAsync(lm->pops.get(), 0, lm->pops.bytes(), s));
+      if (coherence_host) {
+        lm->coh.resize(static_cast<std::size_t>(steps + 1));
+        QSWG_CHECK(cudaMemsetAsync(lm->coh.get(), 0, lm->coh.bytes(), s));
+      }
     }
     cudaEvent_t e0, e1;
     QSWG_CHECK(cudaEventCreate(&e0));
@@ -576,6 +614,7 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
     QSWG_CHECK(cudaEventRecord(e0, s));
     auto emit = [&](int64_t k, const double2* state) {
       qswg::dev::diag_real(state, L.block().row0, rows, n, lm->pops.get() + k * n, s);
+      if (coherence_host) qswg::dev::coherence_bits(state, L.block().row0, rows, n, lm->coh.get() + k, s);
       if (states_host)
         QSWG_CHECK(cudaMemcpyAsync(states_host + 2 * rows * k, state, static_cast<std::size_t>(rows) * sizeof(double2),
                                    cudaMemcpyDeviceToHost, s));
@@ -585,13 +624,18 @@ int qswg_series(const qswg_liouvillian* l, const qswg_state* v, double t1, doubl
     };
     // populations only: every emit is a device kernel into lm->pops, so a
     // repeated identical call may replay a captured graph (expm.hpp: series)
-    const void* graph_key = (states_host || final_state) ? nullptr : lm->pops.get();
+    const void* graph_key =
+        (states_host || final_state) ? nullptr : (coherence_host ? static_cast<const void*>(lm->coh.get()) : lm->pops.get());
     const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit, graph_key);
     if (L.comm() && L.comm()->world() > 1)  // every diagonal element has exactly one owner
       L.comm()->allreduce_sum_f64(lm->pops.get(), static_cast<std::size_t>((steps + 1) * n), s);
+    if (coherence_host && L.comm() && L.comm()->world() > 1)
+      L.comm()->allreduce_max_u64(lm->coh.get(), static_cast<std::size_t>(steps + 1), s);
     QSWG_CHECK(cudaEventRecord(e1, s));
     if (pops_host)
       QSWG_CHECK(cudaMemcpyAsync(pops_host, lm->pops.get(), lm->pops.bytes(), cudaMemcpyDeviceToHost, s));
+    if (coherence_host)  // bit patterns of non-negative doubles are the doubles
+      QSWG_CHECK(cudaMemcpyAsync(coherence_host, lm->coh.get(), lm->coh.bytes(), cudaMemcpyDeviceToHost, s));
     QSWG_CHECK(cudaStreamSynchronize(s));
     float ms = 0.f;
     QSWG_CHECK(cudaEventElapsedTime(&ms, e0, e1));
@@ -685,4 +729,147 @@ int qswg_comm_create_local(int world, qswg_comm** outs) {
   });
 }
 
+
+// ------------------------------------------------------------ file formats
+int qswg_matrix_market_parse(const char* text, int64_t len, qswg_sparse** adjacency) {
+  return guarded([&] {
+    need(text, "text");
+    need(adjacency, "adjacency");
+    std::istringstream in(std::string(text, static_cast<std::size_t>(len)));
+    *adjacency = wrap(qswg::load_matrix_market(in));
+  });
+}
+
+int qswg_matrix_market_load(const char* path, qswg_sparse** adjacency) {
+  return guarded([&] {
+    need(path, "path");
+    need(adjacency, "adjacency");
+    *adjacency = wrap(qswg::load_graph_file(path));
+  });
+}
+
+int qswg_matrix_market_save(const qswg_sparse* adjacency, const char* path) {
+  return guarded([&] {
+    need(adjacency, "adjacency");
+    need(path, "path");
+    std::ofstream out(path);
+    if (!out) throw qswg::IoError(std::string("cannot open `") + path + "` for writing");
+    qswg::save_matrix_market(adjacency->m, out);
+    if (!out) throw qswg::IoError(std::string("failed to write `") + path + "`");
+  });
+}
+
+int qswg_container_create(qswg_container** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = new qswg_container();
+  });
+}
+
+void qswg_container_destroy(qswg_container* c) { delete c; }
+
+int qswg_container_set_metadata(qswg_container* c, const char* text, int64_t len) {
+  return guarded([&] {
+    need(c, "container");
+    need(text, "text");
+    c->c.metadata.assign(text, static_cast<std::size_t>(len));
+  });
+}
+
+int qswg_container_get_metadata(const qswg_container* c, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    need(c, "container");
+    if (len) *len = static_cast<int64_t>(c->c.metadata.size());
+    if (buf) std::memcpy(buf, c->c.metadata.data(), std::min<std::size_t>(cap, c->c.metadata.size()));
+  });
+}
+
+int qswg_container_put_array(qswg_container* c, const char* name, int64_t rank, const int64_t* shape,
+                             const double* data) {
+  return guarded([&] {
+    need(c, "container");
+    need(name, "name");
+    if (rank < 0) throw std::invalid_argument("array rank must be non-negative");
+    if (rank > 0) need(shape, "shape");
+    qswg::ArrayBlock a;
+    for (int64_t k = 0; k < rank; ++k) {
+      if (shape[k] < 0) throw std::invalid_argument("array dimensions must be non-negative");
+      a.shape.push_back(static_cast<std::uint64_t>(shape[k]));
+    }
+    const std::uint64_t count = a.element_count();
+    if (count) need(data, "data");
+    a.data.assign(data, data + count);
+    c->c.arrays[name] = std::move(a);
+  });
+}
+
+int qswg_container_array_count(const qswg_container* c, int64_t* count) {
+  return guarded([&] {
+    need(c, "container");
+    need(count, "count");
+    *count = static_cast<int64_t>(c->c.arrays.size());
+  });
+}
+
+namespace {
+const std::pair<const std::string, qswg::ArrayBlock>& nth_array(const qswg_container* c, int64_t index) {
+  if (index < 0 || index >= static_cast<int64_t>(c->c.arrays.size()))
+    throw std::out_of_range("container array index out of range");
+  return *std::next(c->c.arrays.begin(), index);
+}
+}  // namespace
+
+int qswg_container_array_info(const qswg_container* c, int64_t index, char* name, int64_t name_cap,
+                              int64_t* name_len, int64_t* rank, int64_t* shape, int64_t shape_cap) {
+  return guarded([&] {
+    need(c, "container");
+    const auto& [nm, a] = nth_array(c, index);
+    if (name_len) *name_len = static_cast<int64_t>(nm.size());
+    if (name) std::memcpy(name, nm.data(), std::min<std::size_t>(name_cap, nm.size()));
+    if (rank) *rank = static_cast<int64_t>(a.shape.size());
+    if (shape)
+      for (std::size_t k = 0; k < a.shape.size() && static_cast<int64_t>(k) < shape_cap; ++k)
+        shape[k] = static_cast<int64_t>(a.shape[k]);
+  });
+}
+
+int qswg_container_array_data(const qswg_container* c, int64_t index, double* data) {
+  return guarded([&] {
+    need(c, "container");
+    need(data, "data");
+    const auto& a = nth_array(c, index).second;
+    std::memcpy(data, a.data.data(), a.data.size() * sizeof(double));
+  });
+}
+
+int qswg_container_write(const qswg_container* c, const char* path) {
+  return guarded([&] {
+    need(c, "container");
+    need(path, "path");
+    qswg::write_container(c->c, path);
+  });
+}
+
+int qswg_container_read(const char* path, qswg_container** out) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    auto h = std::make_unique<qswg_container>();
+    h->c = qswg::read_container(path);
+    *out = h.release();
+  });
+}
+
+int qswg_container_plot_data(const qswg_container* c, const char* quantity, const char* path) {
+  return guarded([&] {
+    need(c, "container");
+    need(quantity, "quantity");
+    need(path, "path");
+    const std::string text = qswg::plot_data(c->c, quantity);
+    std::ofstream out(path);
+    if (!out) throw qswg::IoError(std::string("cannot open `") + path + "` for writing");
+    out << text;
+    if (!out) throw qswg::IoError("failed to write plot data");
+  });
+}
 }  // extern "C"

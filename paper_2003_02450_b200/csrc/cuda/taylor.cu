@@ -1202,6 +1202,23 @@ __global__ void diag_kernel(const double2* v, long long row0, long long rows, lo
   }
 }
 
+// out[0] = max over the off-diagonal elements of |v| as a bit pattern
+// (DensityMatrix::max_coherence, walk.cpp:32-40; hypot like std::abs).
+__global__ void __launch_bounds__(kThreads) coherence_kernel(const double2* __restrict__ v, long long row0, long long rows,
+                                                             long long n, unsigned long long* out) {
+  pdl_prologue();
+  pdl_trigger();
+  __shared__ unsigned long long red[32];
+  unsigned long long m = 0;
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < rows;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long g = row0 + k;
+    if (g % (n + 1) != 0) m = umax64(m, dbits(cabs2(__ldg(v + k))));  // g = n j + i, i == j <=> g = j (n + 1)
+  }
+  m = block_max_bits(m, red);
+  if (threadIdx.x == 0 && m != 0) atomicMax(out, m);
+}
+
 __global__ void probs_kernel(double2* v, long long row0, long long rows, long long n, const double* p) {
   pdl_prologue();
   pdl_trigger();
@@ -1505,6 +1522,12 @@ void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std
                double* pops, cudaStream_t s) {
   launch_pdl(diag_kernel, small_grid(n), kThreads, 0, s, v_local, row0, rows, n, pops);
   QSWG_LAUNCH_CHECK("diag_real");
+}
+
+void coherence_bits(const double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
+                    unsigned long long* out, cudaStream_t s) {
+  launch_pdl(coherence_kernel, small_grid(rows), kThreads, 0, s, v_local, row0, rows, n, out);
+  QSWG_LAUNCH_CHECK("coherence_bits");
 }
 
 void fill_pattern(double2* v, std::int64_t n, cudaStream_t s) {

@@ -294,6 +294,10 @@ void spmv(const DevMatrix& l, const double2* x, double2* y, double scale, cudaSt
 // pops[i] = Re v[i*(n+1)] for the diagonal elements inside [row0, row0+rows).
 void diag_real(const double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
                double* pops, cudaStream_t s);
+// *out = max(*out, max |v(i, j)| over the local off-diagonal elements) as
+// the uint64 pattern of a non-negative double (max_coherence, walk.cpp:32-40).
+void coherence_bits(const double2* v_local, std::int64_t row0, std::int64_t rows, std::int64_t n,
+                    unsigned long long* out, cudaStream_t s);
 // Deterministic non-zero test pattern (benchmark inputs).
 void fill_pattern(double2* v, std::int64_t n, cudaStream_t s);
 // Deterministic Hermitian n x n test pattern (column-major, n*n entries).
