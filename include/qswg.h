@@ -134,6 +134,11 @@ int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* inf
  * kernels (results agree to rounding; no reference counterpart). */
 int qswg_liouvillian_set_hermitian_mode(qswg_liouvillian* l, int mode);
 /* gather_full() of the local row block (liouvillian.hpp:34): rowptr[rows+1], col[nnz_local], val[2*nnz_local] */
+/* WalkSystem::set_omega (walk.hpp:58, walk.cpp:141-145) on the built operator:
+ * re-mixes the superoperator for a new omega in place on the device (same
+ * handle, same row partition; states of this handle stay valid), with the
+ * 1-norm series recomputed.  EINVAL unless 0 <= omega <= 1. */
+int qswg_liouvillian_set_omega(qswg_liouvillian* l, double omega);
 int qswg_liouvillian_download(const qswg_liouvillian* l, int64_t* rowptr, int64_t* col, double* val);
 void qswg_liouvillian_destroy(qswg_liouvillian* l);
 /* spmv(l, x), liouvillian.hpp:93: y = L x; x: dim complex (host), y: rows complex (host) */

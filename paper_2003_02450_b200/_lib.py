@@ -152,6 +152,7 @@ SIGNATURES = {
     "qswg_series_observe": (C.c_int, [vp, vp, C.c_double, C.c_double, i64, C.c_double, dp, dp, dp, vp,
                                       C.POINTER(SeriesInfo)]),
     "qswg_state_coherence": (C.c_int, [vp, dp]),
+    "qswg_liouvillian_set_omega": (C.c_int, [vp, C.c_double]),
     "qswg_matrix_market_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(vp)]),
     "qswg_matrix_market_load": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
     "qswg_matrix_market_save": (C.c_int, [vp, C.c_char_p]),

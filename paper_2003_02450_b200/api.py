@@ -194,6 +194,9 @@ class Liouvillian:
 
     def __init__(self, handle):
         self._h = handle
+        self._query()
+
+    def _query(self):
         info = _lib.LiouvillianInfo()
         check(lib.qswg_liouvillian_query(self._h, C.byref(info)))
         self.info = info
@@ -250,6 +253,12 @@ class Liouvillian:
         ms = C.c_double()
         check(lib.qswg_time_series_term(self._h, iters, count, C.byref(ms)))
         return ms.value
+
+    def set_omega(self, omega: float) -> None:
+        """Re-mix for a new omega in place on the device (qswg_liouvillian_set_omega);
+        states of this operator stay valid."""
+        check(lib.qswg_liouvillian_set_omega(self._h, float(omega)))
+        self._query()
 
     def set_hermitian_mode(self, on: bool) -> None:
         """KRON on one GPU: allow (default) or forbid the Hermitian tile kernels."""
@@ -645,11 +654,7 @@ class WalkSystem:
         if not (0.0 <= omega <= 1.0):
             raise ValueError("omega must be in [0, 1]")
         self._omega = float(omega)
-        init = self._initial.gather() if self._initial is not None else None
-        self._rebuild()
-        if init is not None:
-            self._initial = StateVector(self.liouvillian).upload(init)
-            self._result = None
+        self.liouvillian.set_omega(omega)  # walk.cpp:141-145; the states stay on the device
 
     def step(self, t, tolerance=DOUBLE_TOL):
         if self._initial is None:

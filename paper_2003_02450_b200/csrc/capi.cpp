@@ -523,6 +523,13 @@ int qswg_state_populations(const qswg_state* s, double* out) {
   });
 }
 
+int qswg_liouvillian_set_omega(qswg_liouvillian* l, double omega) {
+  return guarded([&] {
+    need(l, "liouvillian");
+    l->l->set_omega(omega);
+  });
+}
+
 int qswg_state_coherence(const qswg_state* s, double* out) {
   return guarded([&] {
     need(s, "state");

@@ -341,8 +341,58 @@ void validate_common(double omega, const SparseMatrix& h) {
 class LiouvillianBuilder {
  public:
   static std::unique_ptr<Liouvillian> build(double omega, std::int64_t n, const HostOperands& ops,
-                                            const DeviceConfig& cfg);
+                                            const DeviceConfig& cfg,
+                                            const std::vector<std::int64_t>* fixed_starts = nullptr);
+  // Builds from operands(omega) and keeps the recipe for set_omega.
+  template <class Ops>
+  static std::unique_ptr<Liouvillian> with_rebuild(double omega, std::int64_t n, Ops operands, const DeviceConfig& cfg) {
+    std::unique_ptr<Liouvillian> l = build(omega, n, operands(omega), cfg);
+    l->rebuild_ = [n, operands = std::move(operands), cfg](double w, const std::vector<std::int64_t>* starts) {
+      return build(w, n, operands(w), cfg, starts);
+    };
+    return l;
+  }
 };
+
+void Liouvillian::adopt(Liouvillian& o) {
+  DeviceGuard g(device_);
+  QSWG_CHECK(cudaStreamSynchronize(stream_));
+  std::swap(omega_, o.omega_);
+  std::swap(group_, o.group_);
+  std::swap(block_, o.block_);
+  std::swap(starts_, o.starts_);
+  std::swap(nnz_local_, o.nnz_local_);
+  std::swap(nnz_total_, o.nnz_total_);
+  std::swap(norms_, o.norms_);
+  std::swap(format_, o.format_);
+  std::swap(padding_, o.padding_);
+  std::swap(n_slices_, o.n_slices_);
+  std::swap(slice_ptr_, o.slice_ptr_);
+  std::swap(rowptr_, o.rowptr_);
+  std::swap(col_, o.col_);
+  std::swap(val_, o.val_);
+  std::swap(halo_lo_, o.halo_lo_);
+  std::swap(halo_hi_, o.halo_hi_);
+  std::swap(whalo_lo_, o.whalo_lo_);
+  std::swap(whalo_hi_, o.whalo_hi_);
+  std::swap(vhalo_lo_, o.vhalo_lo_);
+  std::swap(vhalo_hi_, o.vhalo_hi_);
+  std::swap(kron_, o.kron_);
+  std::swap(kron_ell_, o.kron_ell_);
+  std::swap(kron_w_, o.kron_w_);
+  std::swap(kron_v_, o.kron_v_);
+  std::swap(herm_flag_, o.herm_flag_);
+  std::swap(kron_wt_, o.kron_wt_);
+  std::swap(ws_, o.ws_);  // drops captured series graphs and control blocks of the old operator
+  herm_ = 0;
+}
+
+void Liouvillian::set_omega(double omega) {
+  if (!(omega >= 0.0 && omega <= 1.0)) throw std::invalid_argument("omega must be in [0, 1]");
+  if (!rebuild_) throw std::logic_error("this superoperator has no build inputs to re-mix");
+  std::unique_ptr<Liouvillian> fresh = rebuild_(omega, &starts_);
+  adopt(*fresh);
+}
 
 Liouvillian::~Liouvillian() {
   if (stream_) {
@@ -639,7 +689,8 @@ void kron_halos(const HostOperands& h, bool factored, std::int64_t n, const std:
 }  // namespace
 
 std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_t n, const HostOperands& hops,
-                                                       const DeviceConfig& cfg) {
+                                                       const DeviceConfig& cfg,
+                                                       const std::vector<std::int64_t>* fixed_starts) {
   std::unique_ptr<Liouvillian> l(new Liouvillian);
   l->n_ = n;
   l->omega_ = omega;
@@ -656,7 +707,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   DeviceBuffer<std::int64_t> grp;
   const std::vector<std::int64_t> colptr = count_scan(ops.get(), n, grp, s);
   l->nnz_total_ = colptr.back();
-  l->starts_ = partition_rows(colptr, n, world);
+  l->starts_ = fixed_starts ? *fixed_starts : partition_rows(colptr, n, world);
   l->block_ = {l->starts_[static_cast<std::size_t>(rank)],
                l->starts_[static_cast<std::size_t>(rank) + 1] - l->starts_[static_cast<std::size_t>(rank)]};
 
@@ -862,6 +913,7 @@ std::unique_ptr<Liouvillian> build_local(double omega, const SparseMatrix& h, co
   for (const SinkArc& s : sinks)
     if (s.origin < 0 || s.origin >= n_base) throw std::out_of_range("sink origin out of range");
 
+  auto operands = [n, n_base, nsrc, nsnk, h, m_l, sources, sinks](double omega) {
   HostOperands o;
   o.n = n;
   o.omega = omega;
@@ -891,7 +943,9 @@ std::unique_ptr<Liouvillian> build_local(double omega, const SparseMatrix& h, co
   for (std::int64_t k = 0; k < nsnk; ++k)
     te.push_back({n_base + nsrc + k, sinks[static_cast<std::size_t>(k)].origin, Complex{sinks[static_cast<std::size_t>(k)].rate, 0.0}});
   o.t = make_multi(n, te);
-  return LiouvillianBuilder::build(omega, n, o, cfg);
+  return o;
+  };
+  return LiouvillianBuilder::with_rebuild(omega, n, std::move(operands), cfg);
 }
 
 // ----------------------------------------------------------- build_global
@@ -909,6 +963,7 @@ std::unique_ptr<Liouvillian> build_global(double omega, const SparseMatrix& h,
   if (static_cast<int>(lindblads.size()) > dev::kMaxKron)
     throw std::invalid_argument("at most " + std::to_string(dev::kMaxKron) + " Lindblad operators are supported");
 
+  auto operands = [n, h, lindblads, h_rot](double omega) {
   HostOperands o;
   o.n = n;
   o.omega = omega;
@@ -946,7 +1001,9 @@ std::unique_ptr<Liouvillian> build_global(double omega, const SparseMatrix& h,
   o.a = make_multi(n, ae);
   o.b = make_multi(n, be);
   o.t = make_multi(n, {});
-  return LiouvillianBuilder::build(omega, n, o, cfg);
+  return o;
+  };
+  return LiouvillianBuilder::with_rebuild(omega, n, std::move(operands), cfg);
 }
 
 }  // namespace qswg

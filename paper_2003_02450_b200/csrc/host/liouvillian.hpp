@@ -10,6 +10,7 @@
 #pragma once
 
 #include <array>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <vector>
@@ -87,6 +88,12 @@ class Liouvillian {
   void set_hermitian_input(const double2* x) const;
   /// 0: never take the Hermitian kernels; 1 (default): when the input is Hermitian.
   void set_hermitian_mode(int mode) { herm_mode_ = mode ? 1 : 0; }
+  /// Re-mixes the superoperator for a new omega in place (SURVEY.md §8(f)
+  /// item 1; WalkSystem::set_omega, walk.cpp:141-145): the n x n operands
+  /// are re-derived on the host from the inputs kept at build, the device
+  /// reassembles the same handle (format choice, norms, halos) on the same
+  /// row partition, so every state of this handle stays valid.
+  void set_omega(double omega);
   /// y = scale * L x for device vectors: x full-length (dim), y local (rows).
   void multiply(const double2* x, double2* y, double scale) const;
   /// Mean device time (ms) of one term kernel launch over `iters` launches.
@@ -133,6 +140,9 @@ class Liouvillian {
   int herm_mode_ = 1;            // set_hermitian_mode
   std::vector<DeviceBuffer<double2>> kron_wt_;  // factored + one GPU: row-major W_k for the Hermitian path
   mutable Workspace ws_;
+  // build_local / build_global inputs, re-run by set_omega on a fixed partition
+  std::function<std::unique_ptr<Liouvillian>(double, const std::vector<std::int64_t>*)> rebuild_;
+  void adopt(Liouvillian& o);  // take o's operator, keep this handle's stream
 };
 
 /// L-QSW (liouvillian.hpp:65-71, liouvillian.cpp:129-210).
