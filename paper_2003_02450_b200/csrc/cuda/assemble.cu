@@ -11,6 +11,7 @@
 // stay L1/L2 resident.  The same kernel assembles |L^T| (for the 1-norm
 // bound) from transposed operand lists.
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <climits>
 
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(KronOperands o, long lon
 }
 
 __global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, long long row0, long long rows,
-                                                             const long long* slice_ptr, int* col, double2* val) {
+                                                             const long long* slice_ptr, const int* perm, int* col,
+                                                             double2* val) {
   // every lane of every slice, including the lanes past the last row of a
   // partial final slice (pure padding)
   const long long padded_rows = (rows + kSlice - 1) / kSlice * kSlice;
@@ -176,9 +178,10 @@ __global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, lon
     const long long base = slice_ptr[sl] + (lr - sl * kSlice);
     const long long len = (slice_ptr[sl + 1] - slice_ptr[sl]) / kSlice;
     long long k = 0;
+    const long long row = lr < rows ? (perm ? perm[lr] : lr) : rows - 1;
     if (lr < rows) {
       RowMerge m;
-      merge_init(o, row0 + lr, m);
+      merge_init(o, row0 + row, m);
       long long c;
       double2 v;
       while (merge_next(o, m, c, v)) {
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, lon
         ++k;
       }
     }
-    const int pad_col = static_cast<int>(row0 + (lr < rows ? lr : rows - 1));
+    const int pad_col = static_cast<int>(row0 + row);
     for (; k < len; ++k) {  // padding: x[row] * 0
       col[base + k * kSlice] = pad_col;
       val[base + k * kSlice] = make_double2(0.0, 0.0);
@@ -195,14 +198,28 @@ __global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, lon
   }
 }
 
-__global__ void slice_len_kernel(const long long* grp, long long rows, long long n_slices, long long* out) {
+__global__ void slice_len_kernel(const long long* grp, long long rows, const int* perm, long long n_slices,
+                                 long long* out) {
   for (long long sl = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; sl < n_slices;
        sl += static_cast<long long>(gridDim.x) * blockDim.x) {
     long long mx = 0;
-    const long long r1 = min(rows, (sl + 1) * kSlice);
-    for (long long r = sl * kSlice; r < r1; ++r) mx = max(mx, grp[r + 1] - grp[r]);
+    const long long t1 = min(rows, (sl + 1) * kSlice);
+    for (long long t = sl * kSlice; t < t1; ++t) {
+      const long long r = perm ? perm[t] : t;
+      mx = max(mx, grp[r + 1] - grp[r]);
+    }
     out[sl] = mx * kSlice;
   }
+}
+
+__global__ void row_len_kernel(const long long* grp, long long rows, int sigma, int* len, int* idx, int* seg) {
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    len[r] = static_cast<int>(grp[r + 1] - grp[r]);
+    idx[r] = static_cast<int>(r);
+    if (r % sigma == 0) seg[r / sigma] = static_cast<int>(r);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) seg[(rows + sigma - 1) / sigma] = static_cast<int>(rows);
 }
 
 __global__ void rebase_kernel(const long long* src, long long base, long long* dst, long long n) {
@@ -283,21 +300,46 @@ void assemble_fill(const KronOperands& o, std::int64_t row0, std::int64_t rows,
   QSWG_LAUNCH_CHECK("assemble_fill");
 }
 
-void sell_slice_entries(const std::int64_t* grp_local, std::int64_t rows, std::int64_t* slice_entries,
-                        cudaStream_t s) {
+void sell_slice_entries(const std::int64_t* grp_local, std::int64_t rows, const int* perm,
+                        std::int64_t* slice_entries, cudaStream_t s) {
   const long long n_slices = (rows + kSlice - 1) / kSlice;
   if (n_slices <= 0) return;
-  slice_len_kernel<<<grid_for(n_slices), kThreads, 0, s>>>(reinterpret_cast<const long long*>(grp_local), rows,
+  slice_len_kernel<<<grid_for(n_slices), kThreads, 0, s>>>(reinterpret_cast<const long long*>(grp_local), rows, perm,
                                                            n_slices, reinterpret_cast<long long*>(slice_entries));
   QSWG_LAUNCH_CHECK("sell_slice_entries");
 }
 
 void assemble_fill_sell(const KronOperands& o, std::int64_t row0, std::int64_t rows, const std::int64_t* slice_ptr,
-                        int* col, double2* val, cudaStream_t s) {
+                        const int* perm, int* col, double2* val, cudaStream_t s) {
   if (rows <= 0) return;
   fill_sell_kernel<<<grid_for(rows + kSlice), kThreads, 0, s>>>(o, row0, rows, reinterpret_cast<const long long*>(slice_ptr),
-                                                       col, val);
+                                                       perm, col, val);
   QSWG_LAUNCH_CHECK("assemble_fill_sell");
+}
+
+void sell_sort_rows(const std::int64_t* grp_local, std::int64_t rows, int sigma, int* perm, cudaStream_t s) {
+  if (rows <= 0) return;
+  const long long nseg = (rows + sigma - 1) / sigma;
+  int *len = nullptr, *len_out = nullptr, *idx = nullptr, *seg = nullptr;
+  QSWG_CHECK(cudaMallocAsync(&len, sizeof(int) * rows, s));
+  QSWG_CHECK(cudaMallocAsync(&len_out, sizeof(int) * rows, s));
+  QSWG_CHECK(cudaMallocAsync(&idx, sizeof(int) * rows, s));
+  QSWG_CHECK(cudaMallocAsync(&seg, sizeof(int) * (nseg + 1), s));
+  row_len_kernel<<<grid_for(rows), kThreads, 0, s>>>(reinterpret_cast<const long long*>(grp_local), rows, sigma, len,
+                                                     idx, seg);
+  QSWG_LAUNCH_CHECK("row_len");
+  std::size_t bytes = 0;
+  QSWG_CHECK(cub::DeviceSegmentedSort::StableSortPairsDescending(nullptr, bytes, len, len_out, idx, perm,
+                                                                  static_cast<int>(rows), static_cast<int>(nseg), seg,
+                                                                  seg + 1, s));
+  void* tmp = nullptr;
+  QSWG_CHECK(cudaMallocAsync(&tmp, bytes, s));
+  QSWG_CHECK(cub::DeviceSegmentedSort::StableSortPairsDescending(tmp, bytes, len, len_out, idx, perm,
+                                                                  static_cast<int>(rows), static_cast<int>(nseg), seg,
+                                                                  seg + 1, s));
+  for (void* p : {static_cast<void*>(len), static_cast<void*>(len_out), static_cast<void*>(idx),
+                  static_cast<void*>(seg), tmp})
+    QSWG_CHECK(cudaFreeAsync(p, s));
 }
 
 void assemble_fill_abs(const KronOperands& o, std::int64_t row0, std::int64_t rows,

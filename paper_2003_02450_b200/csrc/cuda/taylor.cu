@@ -60,6 +60,10 @@ __device__ __forceinline__ double2 row_dot(const CsrView& l, long long b, long l
       double2 v[U], xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) c[u] = ld_stream(l.col + k + u * G, pol);
+#ifdef QSWG_GATHER_MASK  // experiment: confine the gathers to an L2-sized window
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] &= QSWG_GATHER_MASK;
+#endif
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = ld_stream(l.val + k + u * G, pol);
 #pragma unroll
@@ -73,7 +77,10 @@ __device__ __forceinline__ double2 row_dot(const CsrView& l, long long b, long l
       }
     }
     for (; k < e; k += G) {
-      const int c0 = ld_stream(l.col + k, pol);
+      int c0 = ld_stream(l.col + k, pol);
+#ifdef QSWG_GATHER_MASK
+      c0 &= QSWG_GATHER_MASK;
+#endif
       const double2 v0 = ld_stream(l.val + k, pol);
       const double2 x0 = ld_gather(x + c0, xpol);
       acc.x = fma(v0.x, x0.x, acc.x);
@@ -547,8 +554,9 @@ __device__ __forceinline__ void slice_loop(const SellView& m, const double2* __r
     const long long b = __ldg(m.slice_ptr + sl);
     const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
     const double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
-    const long long row = sl * kSlice + lane;
-    epi(row, acc, row < m.rows);
+    const long long slot = sl * kSlice + lane;
+    const bool valid = slot < m.rows;
+    epi(m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot, acc, valid);
   }
 }
 

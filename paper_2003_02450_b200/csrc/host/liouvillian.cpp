@@ -27,6 +27,18 @@ constexpr std::int64_t kMaxVertices = 46340;       // n^2 must fit int32 columns
 // stored superoperator (c1, dim 4096: SELL 1.57 ms vs KRON 2.55 ms per series —
 // fewer launches per term for a launch-bound system).
 constexpr std::int64_t kKronMinDim = 65536;
+constexpr double kSellSortPadding = 1.02;  // sort rows (SELL-C-sigma) above this consecutive-row padding
+// Sorting window of SELL-C-sigma (QSWG_SELL_SIGMA overrides; 32 disables).
+int sell_sigma_setting() {
+  static const int v = [] {
+    const char* e = std::getenv("QSWG_SELL_SIGMA");
+    // c3 (ER, dim 4.2M) SELL term kernel vs sigma (profiles/r01_superop_spmv.jsonl):
+    // 32: 0.685 of HBM (padding 1.24), 256: 0.64, 4096: 0.71, 16384: 0.77 (padding 1.001)
+    const int x = e ? std::atoi(e) : 16384;
+    return x >= 32 ? x : 32;
+  }();
+  return v;
+}
 constexpr double kSellMaxPadding = 1.3;  // SELL-32 if stored/nnz <= this (c3: 1.24 -> 0.83 vs 1.06 ms CSR; c4: 1.51 -> CSR wins)
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
@@ -368,6 +380,8 @@ void Liouvillian::adopt(Liouvillian& o) {
   std::swap(padding_, o.padding_);
   std::swap(n_slices_, o.n_slices_);
   std::swap(slice_ptr_, o.slice_ptr_);
+  std::swap(perm_, o.perm_);
+  std::swap(sigma_, o.sigma_);
   std::swap(rowptr_, o.rowptr_);
   std::swap(col_, o.col_);
   std::swap(val_, o.val_);
@@ -439,6 +453,7 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
   m.sell.rows = block_.rows;
   m.sell.row0 = block_.row0;
   m.sell.n_slices = n_slices_;
+  m.sell.perm = perm_.size() ? perm_.get() : nullptr;
   if (kron_) {
     const dev::KronOperands& o = kron_->ops.get();
     m.kron.n = static_cast<int>(n_);
@@ -506,13 +521,22 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
       QSWG_CHECK(cudaMemcpy(c32.data(), col_.get(), total * sizeof(int), cudaMemcpyDeviceToHost));
       QSWG_CHECK(cudaMemcpy(v.data(), val_.get(), total * sizeof(double2), cudaMemcpyDeviceToHost));
     }
+    std::vector<int> slot_of(static_cast<std::size_t>(block_.rows));
+    if (perm_.size()) {
+      std::vector<int> perm(static_cast<std::size_t>(block_.rows));
+      QSWG_CHECK(cudaMemcpy(perm.data(), perm_.get(), perm.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      for (std::size_t t = 0; t < perm.size(); ++t) slot_of[static_cast<std::size_t>(perm[t])] = static_cast<int>(t);
+    } else {
+      for (std::size_t t = 0; t < slot_of.size(); ++t) slot_of[t] = static_cast<int>(t);
+    }
     rowptr.assign(static_cast<std::size_t>(block_.rows) + 1, 0);
     col.clear();
     val.clear();
     col.reserve(static_cast<std::size_t>(nnz_local_));
     val.reserve(static_cast<std::size_t>(nnz_local_));
     for (std::int64_t r = 0; r < block_.rows; ++r) {
-      const std::int64_t sl = r / dev::kSlice, lane = r % dev::kSlice;
+      const std::int64_t t = slot_of[static_cast<std::size_t>(r)];
+      const std::int64_t sl = t / dev::kSlice, lane = t % dev::kSlice;
       const std::int64_t len = (sp[static_cast<std::size_t>(sl) + 1] - sp[static_cast<std::size_t>(sl)]) / dev::kSlice;
       for (std::int64_t k = 0; k < len; ++k) {
         const std::size_t e = static_cast<std::size_t>(sp[static_cast<std::size_t>(sl)] + k * dev::kSlice + lane);
@@ -809,16 +833,37 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   std::int64_t sell_entries = 0;
   if (l->n_slices_ > 0) {
     DeviceBuffer<std::int64_t> se(static_cast<std::size_t>(l->n_slices_) + 1);
-    QSWG_CHECK(cudaMemsetAsync(se.get(), 0, se.bytes(), s));
-    dev::sell_slice_entries(grp.get() + l->block_.row0, l->block_.rows, se.get(), s);
     l->slice_ptr_.resize(static_cast<std::size_t>(l->n_slices_) + 1);
     std::size_t tmp_bytes = 0;
     dev::exclusive_scan(se.get(), l->slice_ptr_.get(), l->n_slices_ + 1, nullptr, tmp_bytes, s);
     DeviceBuffer<unsigned char> tmp(tmp_bytes);
-    dev::exclusive_scan(se.get(), l->slice_ptr_.get(), l->n_slices_ + 1, tmp.get(), tmp_bytes, s);
-    QSWG_CHECK(cudaMemcpyAsync(&sell_entries, l->slice_ptr_.get() + l->n_slices_, sizeof(std::int64_t),
-                               cudaMemcpyDeviceToHost, s));
-    QSWG_CHECK(cudaStreamSynchronize(s));
+    const auto entries_for = [&](const int* perm) {
+      QSWG_CHECK(cudaMemsetAsync(se.get(), 0, se.bytes(), s));
+      dev::sell_slice_entries(grp.get() + l->block_.row0, l->block_.rows, perm, se.get(), s);
+      dev::exclusive_scan(se.get(), l->slice_ptr_.get(), l->n_slices_ + 1, tmp.get(), tmp_bytes, s);
+      std::int64_t e = 0;
+      QSWG_CHECK(cudaMemcpyAsync(&e, l->slice_ptr_.get() + l->n_slices_, sizeof(std::int64_t),
+                                 cudaMemcpyDeviceToHost, s));
+      QSWG_CHECK(cudaStreamSynchronize(s));
+      return e;
+    };
+    sell_entries = entries_for(nullptr);
+    // SELL-C-sigma: sort rows by length inside windows of sigma rows when the
+    // consecutive-row slices pad by more than kSellSortPadding
+    const int sigma = sell_sigma_setting();
+    if (sigma > dev::kSlice && l->nnz_local_ > 0 &&
+        static_cast<double>(sell_entries) > kSellSortPadding * static_cast<double>(l->nnz_local_)) {
+      l->perm_.resize(static_cast<std::size_t>(l->block_.rows));
+      dev::sell_sort_rows(grp.get() + l->block_.row0, l->block_.rows, sigma, l->perm_.get(), s);
+      const std::int64_t sorted = entries_for(l->perm_.get());
+      if (sorted < sell_entries) {
+        sell_entries = sorted;
+        l->sigma_ = sigma;
+      } else {
+        l->perm_.reset();
+        sell_entries = entries_for(nullptr);
+      }
+    }
   }
   const double pad = l->nnz_local_ ? static_cast<double>(sell_entries) / static_cast<double>(l->nnz_local_) : 1.0;
   const bool use_sell = l->nnz_local_ > 0 && (cfg.format == 2 || (cfg.format == 0 && pad <= kSellMaxPadding));
@@ -828,11 +873,13 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     l->padding_ = pad;
     l->col_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));
     l->val_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));
-    dev::assemble_fill_sell(ops.get(), l->block_.row0, l->block_.rows, l->slice_ptr_.get(), l->col_.get(),
-                            l->val_.get(), s);
+    dev::assemble_fill_sell(ops.get(), l->block_.row0, l->block_.rows, l->slice_ptr_.get(),
+                            l->perm_.size() ? l->perm_.get() : nullptr, l->col_.get(), l->val_.get(), s);
     QSWG_CHECK(cudaStreamSynchronize(s));
   } else {
     l->slice_ptr_.reset();
+    l->perm_.reset();
+    l->sigma_ = dev::kSlice;
     l->format_ = dev::Format::Csr;
     fill_block(ops.get(), grp, colptr, n, l->block_, l->rowptr_, l->col_, l->val_, l->nnz_local_, s);
   }

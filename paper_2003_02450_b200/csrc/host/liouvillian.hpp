@@ -77,6 +77,8 @@ class Liouvillian {
   dev::Format format() const { return format_; }
   /// Stored entries / nnz (SELL padding; 1.0 for CSR).
   double padding() const { return padding_; }
+  /// SELL sorting window (32: slices of consecutive rows).
+  int sell_sigma() const { return sigma_; }
   bool kron_factored() const;
   bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
 
@@ -127,6 +129,8 @@ class Liouvillian {
   double padding_ = 1.0;
   std::int64_t n_slices_ = 0;
   DeviceBuffer<std::int64_t> slice_ptr_;  // SELL
+  DeviceBuffer<int> perm_;                // SELL-C-sigma slot -> row (empty: identity)
+  int sigma_ = dev::kSlice;
   DeviceBuffer<std::int64_t> rowptr_;     // CSR
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;
