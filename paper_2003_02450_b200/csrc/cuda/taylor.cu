@@ -224,7 +224,14 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
 //   ub_k = (||S_k at the last flush|| + sum of the pending k^q ||K_q||) (1 + 2^-30)
 // is computed with upward rounding: ||S_k|| <= ub_k holds through every
 // rounding of the pending axpys and norms (each at most (1 + 2^-53)), so the
-// settled outcome "continue" is the one the exact test would give.
+// settled outcome "continue" is the one the exact test would give.  Likewise
+// "stop" is settled without S_k when c1_k + c2_k <= tol * lb_k,
+//   lb_k = (||S_k at the last flush|| - pending bound) (1 - 2^-30)
+// (downward rounding; used only while the pending bound is below 2^-20 of
+// ||S_k||, where the 2^-30 slack covers the rounding of <= 64 pending axpys):
+// the output stops at term p exactly as the reference's, and its pending
+// terms join the next flush.  In the stop regime the terms are ~2^-53 ||S_k||,
+// so an output's stop rarely needs a flush of its own.
 __device__ void series_term_control(SeriesCtl* ctl, int p, int last, double tol) {
   static_assert(kMaxSeriesD <= kThreads, "one thread per output");
   __shared__ int pmin_sh;
@@ -245,26 +252,43 @@ __device__ void series_term_control(SeriesCtl* ctl, int p, int last, double tol)
   }
   const int slot = p % ctl->slots;
   const bool act = k < count && ctl->active[k];
-  if (act) atomicMin(&pmin_sh, ctl->p0[k]);
+  const bool pend = k < count && ctl->pending[k];
+  if (act || pend) atomicMin(&pmin_sh, ctl->p0[k]);
   __syncthreads();
   // the next term must not overwrite a pending one
   const bool full = last || p - pmin_sh + 1 >= ctl->pend_max;
   double f = 0.0;
-  bool und = false;
+  bool und = false, stop = false;
   if (act) {
     f = ctl->factor[k];
     ctl->fac_ring[slot][k] = f;
     const double bnd = __dadd_ru(ctl->bound[k], __dmul_ru(f, tn));
     ctl->bound[k] = bnd;
-    const double ub = __dmul_ru(__dadd_ru(ctl->nf_last[k], bnd), 1.0 + 0x1p-30);
-    und = !(ctl->c1[k] + f * tn > tol * ub);  // undecidable (expm.cpp:310, 315)
+    const double nf0 = ctl->nf_last[k];
+    const double ub = __dmul_ru(__dadd_ru(nf0, bnd), 1.0 + 0x1p-30);
+    if (!(ctl->c1[k] + f * tn > tol * ub)) {  // "continue" not settled (expm.cpp:310, 315)
+      const double lb = bnd <= nf0 * 0x1p-20 ? __dmul_rd(__dsub_rd(nf0, bnd), 1.0 - 0x1p-30) : 0.0;
+      stop = __dadd_rn(ctl->c1[k], __dmul_rn(f, tn)) <= __dmul_rd(tol, lb);  // c1 + c2 as expm.cpp:310-315 rounds it
+#ifdef QSWG_NO_SETTLED_STOP  // experiment: every stop through a flush and the exact test
+      stop = false;
+#endif
+      und = !stop;
+    }
   }
+  const bool running = __syncthreads_or(act && !stop);
+  const bool pending_any = __syncthreads_or(pend || stop);
   // One undecidable test flushes every active output: each pending term is
   // then read once per super-step, and a large ring keeps flushes to the
   // outputs' stop events (measured cheaper than flushing the undecidable
-  // outputs alone, which re-reads the shared terms per output).
-  const bool any = __syncthreads_or(und) || full;
-  if (act) {
+  // outputs alone, which re-reads the shared terms per output).  When the
+  // last active output stops, the pending ones are flushed right away.
+  const bool any = __syncthreads_or(und) || full || (!running && pending_any);
+  if (stop) {  // settled stop: done testing, terms p0 .. p pending
+    ctl->active[k] = 0;
+    ctl->pending[k] = 1;
+    ctl->p_end[k] = p;
+    ctl->mark[k] = 0;
+  } else if (act) {
     ctl->mark[k] = any;
     if (!any) {  // every test settled: continue
       ctl->c1[k] = f * tn;
@@ -308,6 +332,10 @@ __device__ void series_flush_control(SeriesCtl* ctl, int p, double tol) {
     ctl->p0[k] = p + 1;
     ctl->fresh[k] = 0;
     ctl->mark[k] = 0;
+  } else if (k < count && ctl->pending[k]) {  // stopped earlier, now summed
+    ctl->pending[k] = 0;
+    ctl->sum_bits[k] = 0;
+    atomicAdd(&stopped, 1);
   }
   __syncthreads();
   if (k == 0) {
@@ -405,8 +433,9 @@ __device__ __forceinline__ bool flush_due(const SeriesFlushArgs& a) {
 template <bool kStrict>
 __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
   SeriesCtl* ctl = a.ctl;
-  __shared__ int list[kMaxSeriesD];   // marked outputs
+  __shared__ int list[kMaxSeriesD];   // marked and pending outputs
   __shared__ int q0[kMaxSeriesD];     // their first pending term
+  __shared__ int q1[kMaxSeriesD];     // and last
   __shared__ int fr[kMaxSeriesD];
   __shared__ unsigned long long smax_sh[kMaxSeriesD];
   __shared__ int nmark;
@@ -414,9 +443,11 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
   if (threadIdx.x == 0) {
     int nm = 0;
     for (int k = 0; k < count; ++k) {
-      if (ctl->active[k] && ctl->mark[k]) {
+      const bool pend = ctl->pending[k];
+      if ((ctl->active[k] && ctl->mark[k]) || pend) {
         list[nm] = k;
         q0[nm] = ctl->p0[k];
+        q1[nm] = pend ? ctl->p_end[k] : p;
         fr[nm] = ctl->fresh[k];
         ++nm;
       }
@@ -452,7 +483,7 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
 #pragma unroll
         for (int v = 0; v < kSeriesRegD; ++v) {
           const int u = u0 + v;
-          if (u < nm && q >= q0[u] && valid) {
+          if (u < nm && q >= q0[u] && q <= q1[u] && valid) {
             const double f = ctl->fac_ring[sl][list[u]];  // block-uniform
             sv[v] = kStrict ? axpy<1>(sv[v], f, kv) : axpy<2>(sv[v], f, kv);
           }
@@ -1130,6 +1161,8 @@ __device__ void series_init_apply(SeriesCtl* ctl, int count, int pend_max, doubl
     ctl->p0[k] = 1;
     ctl->mark[k] = 0;
     ctl->fresh[k] = 1;
+    ctl->pending[k] = 0;
+    ctl->p_end[k] = 0;
   }
   ctl->flush = 0;
   ctl->pend_max = pend_max < 1 ? 1 : (pend_max > kPendMax ? kPendMax : pend_max);

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstddef>
 #include <cstring>
@@ -332,12 +333,35 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
   return info;
 }
 
+// Captured series launch sequences of one Liouvillian, most recent first
+// (a few, so alternating callers, e.g. two input states, keep theirs).
 struct SeriesGraph {
-  std::vector<double> key, last;
-  cudaGraphExec_t exec = nullptr;
-  SeriesInfo info;
+  struct Entry {
+    std::vector<double> key;
+    cudaGraphExec_t exec = nullptr;
+    SeriesInfo info;
+  };
+  static constexpr std::size_t kKeep = 4;
+  std::vector<Entry> entries;
+  std::vector<double> last;
+  Entry* find(const std::vector<double>& key) {
+    for (std::size_t i = 0; i < entries.size(); ++i)
+      if (entries[i].key == key) {
+        std::rotate(entries.begin(), entries.begin() + static_cast<std::ptrdiff_t>(i),
+                    entries.begin() + static_cast<std::ptrdiff_t>(i) + 1);
+        return &entries.front();
+      }
+    return nullptr;
+  }
+  void add(std::vector<double> key, cudaGraphExec_t exec, const SeriesInfo& info) {
+    if (entries.size() == kKeep) {
+      cudaGraphExecDestroy(entries.back().exec);
+      entries.pop_back();
+    }
+    entries.insert(entries.begin(), Entry{std::move(key), exec, info});
+  }
   ~SeriesGraph() {
-    if (exec) cudaGraphExecDestroy(exec);
+    for (Entry& e : entries) cudaGraphExecDestroy(e.exec);
   }
 };
 
@@ -366,11 +390,12 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
                                      static_cast<double>(steps), params.tolerance,
                                      static_cast<double>(reinterpret_cast<std::uintptr_t>(graph_key)),
                                      static_cast<double>(l.matrix().kron.herm), static_cast<double>(series_pend_max(ex.dim))};
-    if (gr->exec && gr->key == key) {
-      QSWG_CHECK(cudaGraphLaunch(gr->exec, s));
-      info = gr->info;
+    if (SeriesGraph::Entry* e = gr->find(key)) {
+      QSWG_CHECK(cudaGraphLaunch(e->exec, s));
+      info = e->info;
       info.graph = true;
     } else if (gr->last == key) {  // second identical call: its workspace exists, capture it
+      if (std::getenv("QSWG_DEBUG_GRAPH")) std::fprintf(stderr, "qswg: capturing a series graph\n");
       cudaGraph_t graph = nullptr;
       QSWG_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       try {
@@ -385,10 +410,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       QSWG_CHECK(ie);
-      if (gr->exec) cudaGraphExecDestroy(gr->exec);
-      gr->exec = exec;
-      gr->key = key;
-      gr->info = info;
+      gr->add(key, exec, info);
       QSWG_CHECK(cudaGraphLaunch(exec, s));
       info.graph = true;
     } else {

@@ -233,6 +233,11 @@ struct SeriesCtl {
   int mark[kMaxSeriesD];        // output k is flushed after this term
   int fresh[kMaxSeriesD];       // output k's first flush starts from Z
   int active[kMaxSeriesD];
+  // Stop settled by the lower bound: the output is done (no more tests) but
+  // its terms p0 .. p_end are still pending; the next flush adds them.
+  // n_active counts active + pending outputs.
+  int pending[kMaxSeriesD];
+  int p_end[kMaxSeriesD];
 };
 
 // Term vectors of a series super-step: term p lives in k[p % slots]
