@@ -47,49 +47,63 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region through NVML in this process (one sample at entry, one at exit and
+    every `period` s in between).  nvidia-smi was used before: its start-up and
+    each of its polls stalled this GPU's work for tens of ms (c1, 7 ms region:
+    1.4 -> 15-21 ms/step), so the in-process NVML queries replace it."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index):
+    def __init__(self, index, period=0.1, enabled=True):
         self.index = index
+        self.enabled = enabled
+        self.period = period
         self.rows = []
-        self.proc = None
+        self.nvml = None
+
+    def _sample(self):
+        n, h = self.nvml, self.h
+        try:
+            sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+            mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+            r = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            return
+        flags = [bool(r & getattr(n, name)) for name in
+                 ("nvmlClocksEventReasonHwSlowdown", "nvmlClocksEventReasonHwThermalSlowdown",
+                  "nvmlClocksEventReasonSwThermalSlowdown", "nvmlClocksEventReasonSwPowerCap")]
+        self.rows.append([str(sm), str(mx), "", "", *["Active" if f else "Not Active" for f in flags]])
+
+    def _loop(self):
+        while not self.stop.wait(self.period):
+            self._sample()
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            try:  # the NVML device behind this CUDA ordinal (CUDA_VISIBLE_DEVICES may remap)
+                import torch
+                pr = torch.cuda.get_device_properties(self.index)
+                bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._sample()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
             self.thread.start()
-            # nvidia-smi's start-up holds the driver for a while: let it reach its
-            # first sample before the timed region begins
-            t0 = time.time()
-            while not self.rows and time.time() - t0 < 3.0:
-                time.sleep(0.02)
-            time.sleep(0.3)
         except Exception:
-            self.proc = None
+            self.nvml = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
+            self._sample()
 
     def summary(self):
         if not self.rows:
@@ -202,6 +216,7 @@ def main():
     ap.add_argument("--group", type=int, default=0)
     ap.add_argument("--format", default="auto", choices=["auto", "kron", "sell", "csr"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="debug: no clock sampling (its NVML queries)")
     ap.add_argument("--no-superop", action="store_true", help="skip the stored-superoperator comparison")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -277,7 +292,7 @@ def main():
     # ---- device-resident timed region ----
     for _ in range(args.warmup):  # (re-)captures this call's series graph
         r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(local_rank, enabled=not args.no_clocks) as clocks:
         barrier()
         ev0.record(stream)
         launches = 0
