@@ -100,3 +100,26 @@ def test_sharded_kron_factored(world, monkeypatch):
     keep = c.z["series_keep"]
     assert np.abs(states[keep] - c.z["series_states"]).max() <= 1e-10
     assert parts[0][2] == c.series_spmvs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("fmt", ["kron", "sell"])
+def test_sharded_coherence_and_set_omega(world, fmt):
+    """Coherence norms (allreduce max over ranks) and populations of a sharded
+    series equal the single-rank run's, before and after an omega re-mix."""
+    c = Case("lqsw_src_snk")
+    t1, tq, q = c.series
+
+    def series_of(l):
+        v = l.state().from_probabilities(c.rho0)
+        r = api.series(l, v, t1, tq, int(q), coherence=True)
+        out = [r.populations.copy(), r.coherence.copy(), v.coherence()]
+        l.set_omega(0.35)
+        r = api.series(l, v, t1, tq, int(q), coherence=True)
+        return out + [r.populations.copy(), r.coherence.copy()]
+
+    single = series_of(c.build_gpu(api, format=fmt))
+    parts = run_ranks(world, lambda r, comm: series_of(c.build_gpu(api, comm=comm, format=fmt)))
+    for p in parts:
+        for got, want in zip(p, single):
+            assert np.abs(np.asarray(got) - np.asarray(want)).max() <= 1e-12
