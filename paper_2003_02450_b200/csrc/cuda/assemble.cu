@@ -130,8 +130,10 @@ __device__ __forceinline__ bool merge_next(const KronOperands& o, RowMerge& m, l
   }
 }
 
+// Entries of each row with column in [c_lo, c_hi) (a column panel; the
+// whole row for [0, LLONG_MAX)).  Columns come out of the merge increasing.
 __global__ void __launch_bounds__(kThreads) count_kernel(KronOperands o, long long row0, long long rows,
-                                                         long long* counts) {
+                                                         long long* counts, long long c_lo, long long c_hi) {
   for (long long lr = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; lr < rows;
        lr += static_cast<long long>(gridDim.x) * blockDim.x) {
     RowMerge m;
@@ -139,7 +141,10 @@ __global__ void __launch_bounds__(kThreads) count_kernel(KronOperands o, long lo
     long long c;
     double2 v;
     long long cnt = 0;
-    while (merge_next(o, m, c, v)) ++cnt;
+    while (merge_next(o, m, c, v)) {
+      if (c >= c_hi) break;
+      cnt += c >= c_lo;
+    }
     counts[lr] = cnt;
   }
 }
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(KronOperands o, long lon
 
 __global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, long long row0, long long rows,
                                                              const long long* slice_ptr, const int* perm, int* col,
-                                                             double2* val) {
+                                                             double2* val, long long c_lo, long long c_hi) {
   // every lane of every slice, including the lanes past the last row of a
   // partial final slice (pure padding)
   const long long padded_rows = (rows + kSlice - 1) / kSlice * kSlice;
@@ -185,6 +190,8 @@ __global__ void __launch_bounds__(kThreads) fill_sell_kernel(KronOperands o, lon
       long long c;
       double2 v;
       while (merge_next(o, m, c, v)) {
+        if (c >= c_hi) break;
+        if (c < c_lo) continue;
         col[base + k * kSlice] = static_cast<int>(c);
         val[base + k * kSlice] = v;
         ++k;
@@ -265,9 +272,9 @@ int grid_for(long long rows) {
 }  // namespace
 
 void assemble_count(const KronOperands& o, std::int64_t row0, std::int64_t rows,
-                    std::int64_t* counts, cudaStream_t s) {
+                    std::int64_t* counts, cudaStream_t s, std::int64_t c_lo, std::int64_t c_hi) {
   if (rows <= 0) return;
-  count_kernel<<<grid_for(rows), kThreads, 0, s>>>(o, row0, rows, reinterpret_cast<long long*>(counts));
+  count_kernel<<<grid_for(rows), kThreads, 0, s>>>(o, row0, rows, reinterpret_cast<long long*>(counts), c_lo, c_hi);
   QSWG_LAUNCH_CHECK("assemble_count");
 }
 
@@ -310,10 +317,11 @@ void sell_slice_entries(const std::int64_t* grp_local, std::int64_t rows, const 
 }
 
 void assemble_fill_sell(const KronOperands& o, std::int64_t row0, std::int64_t rows, const std::int64_t* slice_ptr,
-                        const int* perm, int* col, double2* val, cudaStream_t s) {
+                        const int* perm, int* col, double2* val, cudaStream_t s, std::int64_t c_lo,
+                        std::int64_t c_hi) {
   if (rows <= 0) return;
   fill_sell_kernel<<<grid_for(rows + kSlice), kThreads, 0, s>>>(o, row0, rows, reinterpret_cast<const long long*>(slice_ptr),
-                                                       perm, col, val);
+                                                       perm, col, val, c_lo, c_hi);
   QSWG_LAUNCH_CHECK("assemble_fill_sell");
 }
 

@@ -584,11 +584,48 @@ __device__ __forceinline__ void slice_loop(const SellView& m, const double2* __r
   for (long long sl = warp; sl < m.n_slices; sl += nwarps) {
     const long long b = __ldg(m.slice_ptr + sl);
     const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
-    const double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
+    double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
     const long long slot = sl * kSlice + lane;
     const bool valid = slot < m.rows;
-    epi(m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot, acc, valid);
+    const long long row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
+    if (m.part_in && valid) {  // earlier column panels first, then this one
+      const double2 pp = ld_once(m.part_in + row, pol);
+      acc = make_double2(pp.x + acc.x, pp.y + acc.y);
+    }
+    epi(row, acc, valid);
   }
+}
+
+// Skip test of the partial-panel kernels: the same early exits as the term
+// kernel they precede.
+struct SkipCheck {
+  const SeriesCtl* series = nullptr;
+  const StepCtl* step = nullptr;
+  int first_of_stage = 1;
+};
+__device__ __forceinline__ bool skip_now(const SkipCheck& k) {
+  if (k.series) return series_skip(k.series);
+  if (k.step)
+    return *(volatile const int*)&k.step->error || (!k.first_of_stage && *(volatile const int*)&k.step->done);
+  return false;
+}
+
+// One earlier column panel: part[row] (=|+=) its row sums.
+template <bool kFirst>
+__global__ void __launch_bounds__(kThreads) sell_partial_kernel(SellView m, const double2* x, double2* part,
+                                                                SkipCheck sk) {
+  pdl_prologue();
+  if (skip_now(sk)) return;
+  const unsigned long long once = evict_first_policy();
+  slice_loop<false>(m, x, [&](long long row, double2 acc, bool valid) {
+    if (!valid) return;
+    if constexpr (!kFirst) {
+      const double2 pp = ld_once(part + row, once);
+      acc = make_double2(pp.x + acc.x, pp.y + acc.y);
+    }
+    part[row] = acc;
+  });
+  pdl_trigger();
 }
 
 template <bool kStrict>
@@ -1408,6 +1445,20 @@ void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {
   QSWG_LAUNCH_CHECK("series_flush_control");
 }
 
+// The partial sums of the earlier SELL column panels (no-op for one panel).
+void sell_partials(const DevMatrix& m, const double2* x, const SkipCheck& sk, cudaStream_t s) {
+  for (int q = 0; q < m.n_pre; ++q) {
+    if (q == 0) {
+      launch_pdl(sell_partial_kernel<true>, sell_grid(sell_partial_kernel<true>, m.sell_pre[q]), kThreads, 0, s,
+                 m.sell_pre[q], x, m.part, sk);
+    } else {
+      launch_pdl(sell_partial_kernel<false>, sell_grid(sell_partial_kernel<false>, m.sell_pre[q]), kThreads, 0, s,
+                 m.sell_pre[q], x, m.part, sk);
+    }
+    QSWG_LAUNCH_CHECK("sell_partials");
+  }
+}
+
 void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,
                double scale, bool first_of_stage, int stage, double tol, StepCtl* ctl, bool decide, cudaStream_t s) {
   if (m.format == Format::Kron) {
@@ -1420,6 +1471,7 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
       launch_pdl(kron_step_term_kernel<false>, g.first, kThreads, g.second, s, a);
     }
   } else if (m.format == Format::Sell) {
+    sell_partials(m, x, SkipCheck{nullptr, ctl, first_of_stage ? 1 : 0}, s);
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
       launch_pdl(sell_step_term_kernel<true>, sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s, a);
@@ -1452,6 +1504,7 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
       launch_pdl(kron_series_term_kernel<false>, g.first, kThreads, g.second, s, a, m.kron);
     }
   } else if (m.format == Format::Sell) {
+    sell_partials(m, x, SkipCheck{ctl, nullptr, 1}, s);
     if (m.group == 1) {
       launch_pdl(sell_series_term_kernel<true>, sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s, a, m.sell);
     } else {
@@ -1548,6 +1601,7 @@ void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaSt
       launch_pdl(kron_spmv_kernel<false>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
     }
   } else if (m.format == Format::Sell) {
+    sell_partials(m, x, SkipCheck{}, s);
     if (m.group == 1) {
       launch_pdl(sell_spmv_kernel<true>, sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s, m.sell, x, y, scale);
     } else {

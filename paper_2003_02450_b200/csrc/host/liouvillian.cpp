@@ -32,14 +32,32 @@ constexpr double kSellSortPadding = 1.02;  // sort rows (SELL-C-sigma) above thi
 int sell_sigma_setting() {
   static const int v = [] {
     const char* e = std::getenv("QSWG_SELL_SIGMA");
-    // c3 (ER, dim 4.2M) SELL term kernel vs sigma (profiles/r01_superop_spmv.jsonl):
-    // 32: 0.685 of HBM (padding 1.24), 256: 0.64, 4096: 0.71, 16384: 0.77 (padding 1.001)
-    const int x = e ? std::atoi(e) : 16384;
+    // SELL term kernel vs sigma (profiles/r01_sell_sigma_sweep.jsonl): c3 (ER, dim 4.2M)
+    // 32: 0.685 of HBM (padding 1.24), 256: 0.64, 4096: 0.71, 16384: 0.77, 65536: 0.76;
+    // c4 in 6 column panels 16384: 0.63, 65536: 0.65, 262144: 0.66
+    const int x = e ? std::atoi(e) : 65536;
     return x >= 32 ? x : 32;
   }();
   return v;
 }
-constexpr double kSellMaxPadding = 1.3;  // SELL-32 if stored/nnz <= this (c3: 1.24 -> 0.83 vs 1.06 ms CSR; c4: 1.51 -> CSR wins)
+constexpr double kSellMaxPadding = 1.3;
+// Column panels of a SELL superoperator on one GPU: when the gathered vector
+// is larger than kPanelMinX and the rows are irregular (sorted: gathers go
+// everywhere, c4), split the columns so each panel's slice of x (about
+// kPanelX) stays in L2 while the panel's entries stream.  QSWG_SELL_PANELS
+// forces a count (tests); lattices and the bitwise mode keep one pass.
+constexpr double kPanelMinX = 96e6, kPanelX = 40e6;
+int sell_panel_count(int world, int group, std::int64_t n, bool sorted) {
+  if (world != 1 || group == 1) return 1;
+  int p = 1;
+  if (const char* e = std::getenv("QSWG_SELL_PANELS")) {
+    p = std::atoi(e);
+  } else if (sorted) {
+    const double xb = 16.0 * static_cast<double>(n) * static_cast<double>(n);
+    if (xb > kPanelMinX) p = static_cast<int>(std::ceil(xb / kPanelX));
+  }
+  return static_cast<int>(std::clamp<std::int64_t>(p, 1, std::min<std::int64_t>(dev::kMaxSellPanels, n)));
+}  // SELL-32 if stored/nnz <= this (c3: 1.24 -> 0.83 vs 1.06 ms CSR; c4: 1.51 -> CSR wins)
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
 
@@ -382,6 +400,9 @@ void Liouvillian::adopt(Liouvillian& o) {
   std::swap(slice_ptr_, o.slice_ptr_);
   std::swap(perm_, o.perm_);
   std::swap(sigma_, o.sigma_);
+  std::swap(pre_, o.pre_);
+  std::swap(part_, o.part_);
+  std::swap(main_c_lo_, o.main_c_lo_);
   std::swap(rowptr_, o.rowptr_);
   std::swap(col_, o.col_);
   std::swap(val_, o.val_);
@@ -454,6 +475,19 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
   m.sell.row0 = block_.row0;
   m.sell.n_slices = n_slices_;
   m.sell.perm = perm_.size() ? perm_.get() : nullptr;
+  if (!pre_.empty()) {  // column panels
+    m.n_pre = static_cast<int>(pre_.size());
+    for (std::size_t q = 0; q < pre_.size(); ++q) {
+      dev::SellView& v = m.sell_pre[q];
+      v = m.sell;
+      v.slice_ptr = pre_[q].slice_ptr.get();
+      v.col = pre_[q].col.get();
+      v.val = pre_[q].val.get();
+      v.perm = pre_[q].perm.size() ? pre_[q].perm.get() : nullptr;
+    }
+    m.part = part_.get();
+    m.sell.part_in = part_.get();
+  }
   if (kron_) {
     const dev::KronOperands& o = kron_->ops.get();
     m.kron.n = static_cast<int>(n_);
@@ -511,40 +545,58 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
   }
   if (format_ == dev::Format::Sell) {
     // de-pad: a row's genuine entries precede its padding (val == 0 exactly;
-    // canonical entries are never zero)
-    std::vector<std::int64_t> sp(static_cast<std::size_t>(n_slices_) + 1);
-    QSWG_CHECK(cudaMemcpy(sp.data(), slice_ptr_.get(), sp.size() * sizeof(std::int64_t), cudaMemcpyDeviceToHost));
-    const std::size_t total = static_cast<std::size_t>(sp.back());
-    std::vector<int> c32(total);
-    std::vector<Complex> v(total);
-    if (total) {
-      QSWG_CHECK(cudaMemcpy(c32.data(), col_.get(), total * sizeof(int), cudaMemcpyDeviceToHost));
-      QSWG_CHECK(cudaMemcpy(v.data(), val_.get(), total * sizeof(double2), cudaMemcpyDeviceToHost));
+    // canonical entries are never zero); column panels hold increasing
+    // column ranges, so a row is its panels' pieces in panel order
+    struct View {
+      const std::int64_t* sp;
+      const int* perm;
+      const int* col;
+      const double2* val;
+    };
+    std::vector<View> views;
+    for (const SellPanel& pn : pre_)
+      views.push_back({pn.slice_ptr.get(), pn.perm.size() ? pn.perm.get() : nullptr, pn.col.get(), pn.val.get()});
+    views.push_back({slice_ptr_.get(), perm_.size() ? perm_.get() : nullptr, col_.get(), val_.get()});
+    const std::size_t rows = static_cast<std::size_t>(block_.rows);
+    std::vector<std::vector<int>> rc(rows);
+    std::vector<std::vector<Complex>> rv(rows);
+    for (const View& w : views) {
+      std::vector<std::int64_t> sp(static_cast<std::size_t>(n_slices_) + 1);
+      QSWG_CHECK(cudaMemcpy(sp.data(), w.sp, sp.size() * sizeof(std::int64_t), cudaMemcpyDeviceToHost));
+      const std::size_t total = static_cast<std::size_t>(sp.back());
+      std::vector<int> c32(total);
+      std::vector<Complex> v(total);
+      if (total) {
+        QSWG_CHECK(cudaMemcpy(c32.data(), w.col, total * sizeof(int), cudaMemcpyDeviceToHost));
+        QSWG_CHECK(cudaMemcpy(v.data(), w.val, total * sizeof(double2), cudaMemcpyDeviceToHost));
+      }
+      std::vector<int> perm(rows);
+      if (w.perm) {
+        QSWG_CHECK(cudaMemcpy(perm.data(), w.perm, rows * sizeof(int), cudaMemcpyDeviceToHost));
+      } else {
+        for (std::size_t t = 0; t < rows; ++t) perm[t] = static_cast<int>(t);
+      }
+      for (std::size_t t = 0; t < rows; ++t) {  // slot t holds row perm[t]
+        const std::size_t r = static_cast<std::size_t>(perm[t]);
+        const std::size_t sl = t / dev::kSlice, lane = t % dev::kSlice;
+        const std::int64_t len = (sp[sl + 1] - sp[sl]) / dev::kSlice;
+        for (std::int64_t k = 0; k < len; ++k) {
+          const std::size_t e = static_cast<std::size_t>(sp[sl] + k * dev::kSlice) + lane;
+          if (v[e] == Complex{}) break;
+          rc[r].push_back(c32[e]);
+          rv[r].push_back(v[e]);
+        }
+      }
     }
-    std::vector<int> slot_of(static_cast<std::size_t>(block_.rows));
-    if (perm_.size()) {
-      std::vector<int> perm(static_cast<std::size_t>(block_.rows));
-      QSWG_CHECK(cudaMemcpy(perm.data(), perm_.get(), perm.size() * sizeof(int), cudaMemcpyDeviceToHost));
-      for (std::size_t t = 0; t < perm.size(); ++t) slot_of[static_cast<std::size_t>(perm[t])] = static_cast<int>(t);
-    } else {
-      for (std::size_t t = 0; t < slot_of.size(); ++t) slot_of[t] = static_cast<int>(t);
-    }
-    rowptr.assign(static_cast<std::size_t>(block_.rows) + 1, 0);
+    rowptr.assign(rows + 1, 0);
     col.clear();
     val.clear();
     col.reserve(static_cast<std::size_t>(nnz_local_));
     val.reserve(static_cast<std::size_t>(nnz_local_));
-    for (std::int64_t r = 0; r < block_.rows; ++r) {
-      const std::int64_t t = slot_of[static_cast<std::size_t>(r)];
-      const std::int64_t sl = t / dev::kSlice, lane = t % dev::kSlice;
-      const std::int64_t len = (sp[static_cast<std::size_t>(sl) + 1] - sp[static_cast<std::size_t>(sl)]) / dev::kSlice;
-      for (std::int64_t k = 0; k < len; ++k) {
-        const std::size_t e = static_cast<std::size_t>(sp[static_cast<std::size_t>(sl)] + k * dev::kSlice + lane);
-        if (v[e] == Complex{}) break;
-        col.push_back(c32[e]);
-        val.push_back(v[e]);
-      }
-      rowptr[static_cast<std::size_t>(r) + 1] = static_cast<std::int64_t>(col.size());
+    for (std::size_t r = 0; r < rows; ++r) {
+      col.insert(col.end(), rc[r].begin(), rc[r].end());
+      val.insert(val.end(), rv[r].begin(), rv[r].end());
+      rowptr[r + 1] = static_cast<std::int64_t>(col.size());
     }
     return;
   }
@@ -868,7 +920,57 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   const double pad = l->nnz_local_ ? static_cast<double>(sell_entries) / static_cast<double>(l->nnz_local_) : 1.0;
   const bool use_sell = l->nnz_local_ > 0 && (cfg.format == 2 || (cfg.format == 0 && pad <= kSellMaxPadding));
   if (cfg.format == 3) throw std::invalid_argument("the Kron format has no bitwise (group = 1) mode");
-  if (use_sell) {
+  const int panels = use_sell ? sell_panel_count(world, cfg.group, n, l->perm_.size() > 0) : 1;
+  if (use_sell && panels > 1) {
+    // ---- column panels: x slices that stay in L2 while their entries stream ----
+    l->format_ = dev::Format::Sell;
+    const std::int64_t rows = l->block_.rows;
+    DeviceBuffer<std::int64_t> cnt(static_cast<std::size_t>(rows) + 1), g(static_cast<std::size_t>(rows) + 1);
+    DeviceBuffer<std::int64_t> se(static_cast<std::size_t>(l->n_slices_) + 1);
+    std::size_t tmp_bytes = 0;
+    dev::exclusive_scan(cnt.get(), g.get(), std::max(rows + 1, l->n_slices_ + 1), nullptr, tmp_bytes, s);
+    DeviceBuffer<unsigned char> tmp(tmp_bytes);
+    std::int64_t stored = 0;
+    l->pre_.clear();
+    for (int q = 0; q < panels; ++q) {
+      SellPanel pn;
+      pn.c_lo = n * (static_cast<std::int64_t>(q) * n / panels);
+      pn.c_hi = n * (static_cast<std::int64_t>(q + 1) * n / panels);
+      QSWG_CHECK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+      dev::assemble_count(ops.get(), l->block_.row0, rows, cnt.get(), s, pn.c_lo, pn.c_hi);
+      dev::exclusive_scan(cnt.get(), g.get(), rows + 1, tmp.get(), tmp_bytes, s);
+      if (l->sigma_ > dev::kSlice) {
+        pn.perm.resize(static_cast<std::size_t>(rows));
+        dev::sell_sort_rows(g.get(), rows, l->sigma_, pn.perm.get(), s);
+      }
+      QSWG_CHECK(cudaMemsetAsync(se.get(), 0, se.bytes(), s));
+      dev::sell_slice_entries(g.get(), rows, pn.perm.size() ? pn.perm.get() : nullptr, se.get(), s);
+      pn.slice_ptr.resize(static_cast<std::size_t>(l->n_slices_) + 1);
+      dev::exclusive_scan(se.get(), pn.slice_ptr.get(), l->n_slices_ + 1, tmp.get(), tmp_bytes, s);
+      std::int64_t e = 0;
+      QSWG_CHECK(cudaMemcpyAsync(&e, pn.slice_ptr.get() + l->n_slices_, sizeof(std::int64_t), cudaMemcpyDeviceToHost, s));
+      QSWG_CHECK(cudaStreamSynchronize(s));
+      stored += e;
+      pn.col.resize(static_cast<std::size_t>(std::max<std::int64_t>(e, 1)));
+      pn.val.resize(static_cast<std::size_t>(std::max<std::int64_t>(e, 1)));
+      dev::assemble_fill_sell(ops.get(), l->block_.row0, rows, pn.slice_ptr.get(),
+                              pn.perm.size() ? pn.perm.get() : nullptr, pn.col.get(), pn.val.get(), s, pn.c_lo,
+                              pn.c_hi);
+      QSWG_CHECK(cudaStreamSynchronize(s));
+      if (q + 1 < panels) {
+        l->pre_.push_back(std::move(pn));
+      } else {  // the last panel lives in the main arrays (its kernel runs the epilogue)
+        l->slice_ptr_ = std::move(pn.slice_ptr);
+        l->perm_ = std::move(pn.perm);
+        l->col_ = std::move(pn.col);
+        l->val_ = std::move(pn.val);
+        l->main_c_lo_ = pn.c_lo;
+      }
+    }
+    l->part_.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)));
+    l->padding_ = static_cast<double>(stored) / static_cast<double>(l->nnz_local_);
+    sell_entries = stored;
+  } else if (use_sell) {
     l->format_ = dev::Format::Sell;
     l->padding_ = pad;
     l->col_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));

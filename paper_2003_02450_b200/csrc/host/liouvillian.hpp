@@ -47,6 +47,15 @@ struct Workspace {
   }
 };
 
+// One SELL column panel (liouvillian.cpp: column panels).
+struct SellPanel {
+  DeviceBuffer<std::int64_t> slice_ptr;
+  DeviceBuffer<int> perm;  // empty: identity
+  DeviceBuffer<int> col;
+  DeviceBuffer<double2> val;
+  std::int64_t c_lo = 0, c_hi = 0;  // global column range
+};
+
 struct RowBlock {
   std::int64_t row0 = 0;  // first global row owned
   std::int64_t rows = 0;  // rows owned
@@ -79,6 +88,8 @@ class Liouvillian {
   double padding() const { return padding_; }
   /// SELL sorting window (32: slices of consecutive rows).
   int sell_sigma() const { return sigma_; }
+  /// SELL column panels (1: the whole row in one pass).
+  int sell_panels() const { return static_cast<int>(pre_.size()) + 1; }
   bool kron_factored() const;
   bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
 
@@ -131,6 +142,9 @@ class Liouvillian {
   DeviceBuffer<std::int64_t> slice_ptr_;  // SELL
   DeviceBuffer<int> perm_;                // SELL-C-sigma slot -> row (empty: identity)
   int sigma_ = dev::kSlice;
+  std::vector<SellPanel> pre_;            // SELL column panels before the main arrays (one GPU)
+  DeviceBuffer<double2> part_;            // their row sums
+  std::int64_t main_c_lo_ = 0;            // column range of the main SELL arrays
   DeviceBuffer<std::int64_t> rowptr_;     // CSR
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;

@@ -67,6 +67,9 @@ struct SellView {
   const int* col = nullptr;
   const double2* val = nullptr;
   const int* perm = nullptr;  // slot -> local row; nullptr = identity
+  // Column panels: the row sums of the earlier panels, added to this
+  // panel's sum (nullptr: a single panel).
+  const double2* part_in = nullptr;
   std::int64_t rows = 0;
   std::int64_t row0 = 0;
   std::int64_t n_slices = 0;
@@ -130,12 +133,19 @@ struct KronView {
 // The device superoperator block as the Taylor kernels see it.  group: CSR
 // lanes per row (2..32); group == 1 selects the bitwise reference-order mode
 // for either format.
+// SELL split into column panels (one GPU, x beyond L2): the earlier panels
+// accumulate row sums in `part`; the last one (DevMatrix::sell) adds them.
+inline constexpr int kMaxSellPanels = 16;
+
 struct DevMatrix {
   Format format = Format::Csr;
   int group = 8;
   CsrView csr;
   SellView sell;
   KronView kron;
+  int n_pre = 0;                           // SELL column panels before `sell`
+  SellView sell_pre[kMaxSellPanels - 1];
+  double2* part = nullptr;                 // their row sums (local rows)
   std::int64_t rows() const {
     return format == Format::Csr ? csr.rows : format == Format::Sell ? sell.rows : kron.rows;
   }
@@ -150,8 +160,10 @@ struct RealCsrView {
 };
 
 // ---- assembly (cuda/assemble.cu) -------------------------------------------
+// Entries per row; with [c_lo, c_hi) only those of that column panel.
 void assemble_count(const KronOperands& o, std::int64_t row0, std::int64_t rows,
-                    std::int64_t* counts, cudaStream_t s);
+                    std::int64_t* counts, cudaStream_t s, std::int64_t c_lo = 0,
+                    std::int64_t c_hi = INT64_MAX);
 // counts (rows + 1 entries, last one ignored) -> exclusive prefix sum.
 void exclusive_scan(const std::int64_t* counts, std::int64_t* rowptr, std::int64_t n,
                     void* tmp, std::size_t& tmp_bytes, cudaStream_t s);
@@ -166,7 +178,8 @@ void assemble_fill(const KronOperands& o, std::int64_t row0, std::int64_t rows,
 void sell_slice_entries(const std::int64_t* grp_local, std::int64_t rows, const int* perm,
                         std::int64_t* slice_entries, cudaStream_t s);
 void assemble_fill_sell(const KronOperands& o, std::int64_t row0, std::int64_t rows,
-                        const std::int64_t* slice_ptr, const int* perm, int* col, double2* val, cudaStream_t s);
+                        const std::int64_t* slice_ptr, const int* perm, int* col, double2* val, cudaStream_t s,
+                        std::int64_t c_lo = 0, std::int64_t c_hi = INT64_MAX);
 // perm[0..rows): inside each window of sigma rows, the rows by descending
 // length (grp_local[r+1] - grp_local[r]), equal lengths in row order.
 void sell_sort_rows(const std::int64_t* grp_local, std::int64_t rows, int sigma, int* perm, cudaStream_t s);
