@@ -742,6 +742,7 @@ int qswg_matrix_market_parse(const char* text, int64_t len, qswg_sparse** adjace
   return guarded([&] {
     need(text, "text");
     need(adjacency, "adjacency");
+    if (len < 0) throw std::invalid_argument("text length must be non-negative");
     std::istringstream in(std::string(text, static_cast<std::size_t>(len)));
     *adjacency = wrap(qswg::load_matrix_market(in));
   });
@@ -779,6 +780,7 @@ int qswg_container_set_metadata(qswg_container* c, const char* text, int64_t len
   return guarded([&] {
     need(c, "container");
     need(text, "text");
+    if (len < 0) throw std::invalid_argument("metadata length must be non-negative");
     c->c.metadata.assign(text, static_cast<std::size_t>(len));
   });
 }
@@ -787,7 +789,8 @@ int qswg_container_get_metadata(const qswg_container* c, char* buf, int64_t cap,
   return guarded([&] {
     need(c, "container");
     if (len) *len = static_cast<int64_t>(c->c.metadata.size());
-    if (buf) std::memcpy(buf, c->c.metadata.data(), std::min<std::size_t>(cap, c->c.metadata.size()));
+    if (buf && cap > 0)
+      std::memcpy(buf, c->c.metadata.data(), std::min(static_cast<std::size_t>(cap), c->c.metadata.size()));
   });
 }
 
@@ -832,7 +835,7 @@ int qswg_container_array_info(const qswg_container* c, int64_t index, char* name
     need(c, "container");
     const auto& [nm, a] = nth_array(c, index);
     if (name_len) *name_len = static_cast<int64_t>(nm.size());
-    if (name) std::memcpy(name, nm.data(), std::min<std::size_t>(name_cap, nm.size()));
+    if (name && name_cap > 0) std::memcpy(name, nm.data(), std::min(static_cast<std::size_t>(name_cap), nm.size()));
     if (rank) *rank = static_cast<int64_t>(a.shape.size());
     if (shape)
       for (std::size_t k = 0; k < a.shape.size() && static_cast<int64_t>(k) < shape_cap; ++k)
