@@ -415,6 +415,7 @@ struct SeriesFlushArgs {
   double tol;
   SeriesCtl* ctl;
   int decide;
+  int herm_n = 0;  // > 0: Hermitian tile flush over an n x n state (one GPU)
 };
 
 // Batched running-sum update of the marked outputs (kernels.hpp:
@@ -428,85 +429,48 @@ __device__ __forceinline__ bool flush_due(const SeriesFlushArgs& a) {
   return *(volatile const int*)&a.ctl->flush && !series_skip(a.ctl);
 }
 
-// The flush work of one block (every thread calls it; the last block to
-// arrive runs the exact stop tests).
-template <bool kStrict>
-__device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
-  SeriesCtl* ctl = a.ctl;
-  __shared__ int list[kMaxSeriesD];   // marked and pending outputs
-  __shared__ int q0[kMaxSeriesD];     // their first pending term
-  __shared__ int q1[kMaxSeriesD];     // and last
-  __shared__ int fr[kMaxSeriesD];
-  __shared__ unsigned long long smax_sh[kMaxSeriesD];
-  __shared__ int nmark;
-  const int count = ctl->count, slots = ctl->slots, p = a.p;
+// The outputs a flush updates (marked active and stopped-pending ones), with
+// their pending-term ranges; built by thread 0, block-shared.
+struct FlushList {
+  int list[kMaxSeriesD];
+  int q0[kMaxSeriesD];  // first pending term
+  int q1[kMaxSeriesD];  // last pending term
+  int fr[kMaxSeriesD];  // first flush: starts from Z
+  unsigned long long smax[kMaxSeriesD];
+  int nm;
+};
+
+__device__ __forceinline__ void flush_prepare(const SeriesFlushArgs& a, FlushList& L) {
+  const SeriesCtl* ctl = a.ctl;
   if (threadIdx.x == 0) {
     int nm = 0;
-    for (int k = 0; k < count; ++k) {
+    for (int k = 0; k < ctl->count; ++k) {
       const bool pend = ctl->pending[k];
       if ((ctl->active[k] && ctl->mark[k]) || pend) {
-        list[nm] = k;
-        q0[nm] = ctl->p0[k];
-        q1[nm] = pend ? ctl->p_end[k] : p;
-        fr[nm] = ctl->fresh[k];
+        L.list[nm] = k;
+        L.q0[nm] = ctl->p0[k];
+        L.q1[nm] = pend ? ctl->p_end[k] : a.p;
+        L.fr[nm] = ctl->fresh[k];
         ++nm;
       }
     }
-    nmark = nm;
+    L.nm = nm;
   }
   __syncthreads();
-  const int nm = nmark;
-  for (int u = threadIdx.x; u < nm; u += blockDim.x) smax_sh[u] = 0;
+  for (int u = threadIdx.x; u < L.nm; u += blockDim.x) L.smax[u] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const unsigned long long once = evict_first_policy();
-  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.rows; base += stride) {
-    const long long row = base + threadIdx.x;
-    const bool valid = row < a.rows;
-#pragma unroll 1
-    for (int u0 = 0; u0 < nm; u0 += kSeriesRegD) {
-      double2 sv[kSeriesRegD];
-      int lo = p + 1;
-#pragma unroll
-      for (int v = 0; v < kSeriesRegD; ++v) {
-        const int u = u0 + v;
-        if (u < nm) {
-          lo = q0[u] < lo ? q0[u] : lo;
-          if (valid) sv[v] = ld_once((fr[u] ? a.z : a.sums.s[list[u]]) + row, once);
-        }
-      }
-#pragma unroll 1
-      for (int q = lo; q <= p; ++q) {  // sum += k^q K_q (expm.cpp:300-305)
-        const int sl = q % slots;
-        const double2 kv = valid ? __ldg(a.ring.k[sl] + a.row0 + row) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int v = 0; v < kSeriesRegD; ++v) {
-          const int u = u0 + v;
-          if (u < nm && q >= q0[u] && q <= q1[u] && valid) {
-            const double f = ctl->fac_ring[sl][list[u]];  // block-uniform
-            sv[v] = kStrict ? axpy<1>(sv[v], f, kv) : axpy<2>(sv[v], f, kv);
-          }
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < kSeriesRegD; ++v) {
-        const int u = u0 + v;
-        if (u >= nm) break;  // block-uniform
-        unsigned long long mk = 0;
-        if (valid) {
-          st_hint(a.sums.s[list[u]] + row, sv[v], once);
-          mk = dbits(cabs2(sv[v]));
-        }
-        mk = warp_max_bits(mk);
-        if (lane == 0 && mk) atomicMax(&smax_sh[u], mk);
-      }
-    }
-  }
+}
+
+// Norms into the control block; the last block to arrive runs the exact
+// stop tests (kCoop: the caller does, after a grid barrier).
+template <bool kCoop>
+__device__ __forceinline__ void flush_finish(const SeriesFlushArgs& a, FlushList& L) {
+  SeriesCtl* ctl = a.ctl;
   pdl_trigger();
   __syncthreads();
-  for (int u = threadIdx.x; u < nm; u += blockDim.x) atomicMax(&ctl->sum_bits[list[u]], smax_sh[u]);
+  for (int u = threadIdx.x; u < L.nm; u += blockDim.x) atomicMax(&ctl->sum_bits[L.list[u]], L.smax[u]);
   __syncthreads();
+  if constexpr (kCoop) return;
   __shared__ int is_last;
   if (threadIdx.x == 0) {
     __threadfence();
@@ -516,16 +480,150 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
   __syncthreads();
   if (!is_last) return;
   if (a.decide) {
-    series_flush_control(ctl, p, a.tol);
+    series_flush_control(ctl, a.p, a.tol);
   } else if (threadIdx.x == 0) {
     ctl->arrivals = 0;
   }
 }
 
+// Sum updates of one element row (local index) for the outputs u0 .. u0 +
+// kSeriesRegD of the list: sv[v] = S (or Z) + sum over its pending terms of
+// k^q K_q, oldest first.
+template <bool kStrict>
+__device__ __forceinline__ void flush_element(const SeriesFlushArgs& a, const FlushList& L, int u0, long long row,
+                                              bool valid, unsigned long long once, double2* sv) {
+  const SeriesCtl* ctl = a.ctl;
+  const int slots = ctl->slots, p = a.p, nm = L.nm;
+  int lo = p + 1;
+#pragma unroll
+  for (int v = 0; v < kSeriesRegD; ++v) {
+    const int u = u0 + v;
+    sv[v] = make_double2(0.0, 0.0);
+    if (u < nm) {
+      lo = L.q0[u] < lo ? L.q0[u] : lo;
+      if (valid) sv[v] = ld_once((L.fr[u] ? a.z : a.sums.s[L.list[u]]) + row, once);
+    }
+  }
+#pragma unroll 1
+  for (int q = lo; q <= p; ++q) {  // sum += k^q K_q (expm.cpp:300-305)
+    const int sl = q % slots;
+    const double2 kv = valid ? __ldg(a.ring.k[sl] + a.row0 + row) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int v = 0; v < kSeriesRegD; ++v) {
+      const int u = u0 + v;
+      if (u < nm && q >= L.q0[u] && q <= L.q1[u] && valid) {
+        const double f = ctl->fac_ring[sl][L.list[u]];  // block-uniform
+        sv[v] = kStrict ? axpy<1>(sv[v], f, kv) : axpy<2>(sv[v], f, kv);
+      }
+    }
+  }
+}
+
+// The flush work of one block over all local rows (every thread calls it).
+template <bool kStrict, bool kCoop = false>
+__device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
+  __shared__ FlushList L;
+  flush_prepare(a, L);
+  const int nm = L.nm, lane = threadIdx.x & 31;
+  const unsigned long long once = evict_first_policy();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.rows; base += stride) {
+    const long long row = base + threadIdx.x;
+    const bool valid = row < a.rows;
+#pragma unroll 1
+    for (int u0 = 0; u0 < nm; u0 += kSeriesRegD) {
+      double2 sv[kSeriesRegD];
+      flush_element<kStrict>(a, L, u0, row, valid, once, sv);
+#pragma unroll
+      for (int v = 0; v < kSeriesRegD; ++v) {
+        const int u = u0 + v;
+        if (u >= nm) break;  // block-uniform
+        unsigned long long mk = 0;
+        if (valid) {
+          st_hint(a.sums.s[L.list[u]] + row, sv[v], once);
+          mk = dbits(cabs2(sv[v]));
+        }
+        mk = warp_max_bits(mk);
+        if (lane == 0 && mk) atomicMax(&L.smax[u], mk);
+      }
+    }
+  }
+  flush_finish<kCoop>(a, L);
+}
+
+// Hermitian flush (KRON Hermitian path, one GPU: every pending term and sum is
+// exactly Hermitian, a.herm_n = n): only the upper elements i <= j are
+// computed, in 32 x 8 sub-tiles of the upper 32 x 32 tiles, and each is
+// written twice, S(j, i) = conj S(i, j), through a shared-memory transpose.
+// The mirrored element is bit-identical to what the element-wise flush
+// computes (conj is exact and the axpys are symmetric in the sign of the
+// imaginary parts), so the pending terms and sums are read for half the
+// elements only.
+__device__ __forceinline__ void flush_body_herm(const SeriesFlushArgs& a) {
+  __shared__ FlushList L;
+  __shared__ double2 tr[kSeriesRegD][8][33];
+  flush_prepare(a, L);
+  const int nm = L.nm, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n = a.herm_n, nt = (n + 31) / 32;
+  const long long ntiles = static_cast<long long>(nt) * (nt + 1) / 2;
+  const unsigned long long once = evict_first_policy();
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
+    while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
+    while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
+    const int I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
+#pragma unroll 1
+    for (int sub = 0; sub < 4; ++sub) {
+      const int i = I * 32 + lane, j = J * 32 + sub * 8 + w;
+      const bool upper = i < n && j < n && i <= j;
+      const long long row = static_cast<long long>(j) * n + i;
+      // mirror target of this thread after the transpose: row i2 of the
+      // sub-tile's columns, column j2 (8 consecutive j per 8 threads)
+      const int i2 = I * 32 + (threadIdx.x >> 3), j2 = J * 32 + sub * 8 + (threadIdx.x & 7);
+      const bool mirror = i2 < n && j2 < n && i2 < j2;
+#pragma unroll 1
+      for (int u0 = 0; u0 < nm; u0 += kSeriesRegD) {
+        double2 sv[kSeriesRegD];
+        flush_element<false>(a, L, u0, row, upper, once, sv);
+#pragma unroll
+        for (int v = 0; v < kSeriesRegD; ++v) {
+          const int u = u0 + v;
+          if (u >= nm) break;  // block-uniform
+          unsigned long long mk = 0;
+          if (upper) {
+            st_hint(a.sums.s[L.list[u]] + row, sv[v], once);
+            mk = dbits(cabs2(sv[v]));
+          }
+          mk = warp_max_bits(mk);
+          if (lane == 0 && mk) atomicMax(&L.smax[u], mk);
+          tr[v][w][lane] = sv[v];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < kSeriesRegD; ++v) {
+          const int u = u0 + v;
+          if (u >= nm) break;
+          if (mirror) {  // element (j2, i2) = conj of the computed (i2, j2)
+            const double2 m = tr[v][threadIdx.x & 7][threadIdx.x >> 3];
+            st_hint(a.sums.s[L.list[u]] + static_cast<long long>(i2) * n + j2, make_double2(m.x, -m.y), once);
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  flush_finish<false>(a, L);
+}
+
 template <bool kStrict>
 __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs a) {
   pdl_prologue();
-  if (flush_due(a)) flush_body<kStrict>(a);
+  if (!flush_due(a)) return;
+  if (a.herm_n > 0) {
+    flush_body_herm(a);
+  } else {
+    flush_body<kStrict>(a);
+  }
 }
 
 // ------------------------------------------------------------- SELL path
@@ -1056,7 +1154,11 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
   }
   if constexpr (kFlush) {
     if (flush_due(fa)) {
-      flush_body<false>(fa);
+      if (fa.herm_n > 0) {
+        flush_body_herm(fa);
+      } else {
+        flush_body<false>(fa);
+      }
       return;
     }
   }
@@ -1517,10 +1619,9 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
 }
 
 void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, const double2* z,
-                  const SeriesSums& sums, int count, int p, bool strict, double tol, SeriesCtl* ctl,
+                  const SeriesSums& sums, int herm_n, int p, bool strict, double tol, SeriesCtl* ctl,
                   bool decide, cudaStream_t s) {
-  (void)count;
-  const SeriesFlushArgs a{ring, row0, rows, z, sums, p, tol, ctl, decide ? 1 : 0};
+  const SeriesFlushArgs a{ring, row0, rows, z, sums, p, tol, ctl, decide ? 1 : 0, strict ? 0 : herm_n};
   if (strict) {
     launch_pdl(series_flush_kernel<true>, persistent_grid(series_flush_kernel<true>, rows), kThreads, 0, s, a);
   } else {
@@ -1546,7 +1647,7 @@ bool kron_prepare_flush(const DevMatrix& m, const double2* x, const SeriesRing& 
                         std::int64_t rows, const double2* z, const SeriesSums& sums, int p, double tol,
                         SeriesCtl* ctl, cudaStream_t s) {
   if (m.format != Format::Kron || m.kron.nk == 0) return false;
-  const SeriesFlushArgs fa{ring, row0, rows, z, sums, p, tol, ctl, 1};
+  const SeriesFlushArgs fa{ring, row0, rows, z, sums, p, tol, ctl, 1, m.kron.herm ? m.kron.n : 0};
   launch_w<true>(m, x, 0, fa, s);
   QSWG_LAUNCH_CHECK("kron_prepare_flush");
   for (int k = 0; k < m.kron.nk; ++k) {

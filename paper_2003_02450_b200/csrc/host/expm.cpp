@@ -279,6 +279,8 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
     std::vector<double2*> sums(static_cast<std::size_t>(d));
     for (std::int64_t k = 0; k < d; ++k) sums[static_cast<std::size_t>(k)] = ex.local(kSums + static_cast<std::size_t>(k));
     const bool strict = mat.group == 1;
+    // KRON Hermitian path (one GPU): every term and sum is exactly Hermitian
+    const int herm_n = (ex.single && mat.format == dev::Format::Kron && mat.kron.herm) ? static_cast<int>(l.n()) : 0;
     // One GPU, Kron with Lindblad terms: the flush after term p runs in the
     // launch that prepares W for term p + 1.
     const bool fused = ex.single && mat.format == dev::Format::Kron && mat.kron.nk > 0;
@@ -307,7 +309,7 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
           if (!(fused && !last &&
                 dev::kron_prepare_flush(mat, ring.k[p % ring.slots], ring, ex.row0, ex.rows, z, ss,
                                         static_cast<int>(p), params.tolerance, ctl, s)))
-            dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
+            dev::series_flush(ring, ex.row0, ex.rows, z, ss, herm_n, static_cast<int>(p), strict,
                               params.tolerance, ctl, true, s);
           continue;
         }
@@ -316,7 +318,7 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
         const auto [n_active, flush] = ex.read_active_flush(ctl);
         if (n_active == 0) break;
         if (flush) {
-          dev::series_flush(ring, ex.row0, ex.rows, z, ss, static_cast<int>(count), static_cast<int>(p), strict,
+          dev::series_flush(ring, ex.row0, ex.rows, z, ss, herm_n, static_cast<int>(p), strict,
                             params.tolerance, ctl, false, s);
           ex.comm->allreduce_max_u64(&ctl->sum_bits[0], static_cast<std::size_t>(count), s);
           dev::series_flush_control(ctl, static_cast<int>(p), params.tolerance, s);
@@ -474,7 +476,9 @@ std::array<double, 4> time_series_parts(const Liouvillian& l, int iters, int cou
     mark(1);
     dev::series_term(mat, x, ring.k[(i + 1) % ring.slots] + ex.row0, i + 1, false, scale, -1.0, ctl, true, s);
     mark(2);
-    dev::series_flush(ring, ex.row0, ex.rows, z, ss, count, i + 1, mat.group == 1, -1.0, ctl, true, s);
+    dev::series_flush(ring, ex.row0, ex.rows, z, ss,
+                      (ex.single && mat.format == dev::Format::Kron && mat.kron.herm) ? static_cast<int>(l.n()) : 0,
+                      i + 1, mat.group == 1, -1.0, ctl, true, s);
     mark(3);
   }
   QSWG_CHECK(cudaEventSynchronize(ev.back()));

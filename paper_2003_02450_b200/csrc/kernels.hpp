@@ -298,8 +298,10 @@ void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream
 // When ctl->flush: for every marked output k, S_k = (fresh_k ? Z : S_k) +
 // sum over its pending terms q of k^q K_q, in term order (expm.cpp:300-305),
 // then its exact stop test of term p (expm.cpp:306-316).  No-op otherwise.
+// herm_n > 0 (KRON Hermitian path on one GPU, n x n states): the Hermitian
+// tile flush, which reads the upper elements only and mirrors them.
 void series_flush(const SeriesRing& ring, std::int64_t row0, std::int64_t rows, const double2* z,
-                  const SeriesSums& sums, int count, int p, bool strict, double tol, SeriesCtl* ctl,
+                  const SeriesSums& sums, int herm_n, int p, bool strict, double tol, SeriesCtl* ctl,
                   bool decide, cudaStream_t s);
 void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s);
 // Kron format: W_k = Q_k X on the local columns (call before every product
