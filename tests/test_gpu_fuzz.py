@@ -1,0 +1,126 @@
+"""Randomised parity sweep: small random walks (odd sizes, n = 1, empty graphs,
+omega at 0 and 1, sources/sinks, several complex Lindblad operators, a rotating
+Hamiltonian, probability and dense initial states, non-Hermitian inputs) in
+every format and both arithmetic modes, against the pinned C oracle.
+
+Bar: rho at every output <= 1e-10 elementwise (the north-star tolerance);
+identical SpMV counts in the bitwise mode (group = 1), which reproduces the
+reference's arithmetic; step agrees the same way."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, rho0_vec
+
+pytestmark = pytest.mark.gpu
+api = pytest.importorskip("paper_2003_02450_b200.api")
+from paper_2003_02450_b200.graphs import Csr  # noqa: E402
+
+RHO_TOL = 1e-10
+MODES = [("kron", 0), ("sell", 0), ("csr", 0), ("sell", 1), ("csr", 1)]
+
+
+@pytest.fixture(scope="module")
+def port():
+    return Oracle("port")
+
+
+def random_digraph(rng, n, density):
+    r, c, v = [], [], []
+    for i in range(n):
+        for j in range(n):
+            if i != j and rng.random() < density:
+                r.append(i)
+                c.append(j)
+                v.append(float(0.05 + 2 * rng.random()))
+    return Csr.from_coo(n, n, r, c, v)
+
+
+def random_complex(rng, n, density):
+    mask = rng.random((n, n)) < density
+    r, c = np.nonzero(mask)
+    v = rng.standard_normal(len(r)) + 1j * rng.standard_normal(len(r))
+    return Csr.from_coo(n, n, r, c, v * 0.5)
+
+
+def random_hermitian(rng, n, density):
+    a = random_complex(rng, n, density)
+    d = np.zeros((n, n), complex)
+    for i in range(n):
+        for k in range(a.indptr[i], a.indptr[i + 1]):
+            d[i, a.indices[k]] += a.data[k]
+    d = d + d.conj().T
+    r, c = np.nonzero(d)
+    return Csr.from_coo(n, n, r, c, d[r, c])
+
+
+def instance(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([1, 2, 3, 5, 17, 31, 32, 33, 40, 47]))
+    density = float(rng.choice([0.0, 0.05, 0.2, 0.6]))
+    omega = float(rng.choice([0.0, 1.0, round(float(rng.random()), 3)]))
+    g = random_digraph(rng, n, density)
+    gu = api.symmetrize(g)
+    inst = {"n": n, "omega": omega}
+    if seed % 2 == 0:  # L-QSW, with sources and sinks on some seeds
+        n_src = int(rng.integers(0, 3)) if n > 1 else 0
+        n_snk = int(rng.integers(0, 3)) if n > 1 else 0
+        src = [(int(rng.integers(0, n)), float(0.1 + rng.random())) for _ in range(n_src)]
+        snk = [(int(rng.integers(0, n)), float(0.1 + rng.random())) for _ in range(n_snk)]
+        total = n + n_src + n_snk
+        h = api.generator_matrix(1.0, gu).to_csr()
+        ml = api.local_lindblad(api.markov_chain_matrix(g)).to_csr() if density > 0 else Csr.from_coo(n, n, [], [], [])
+        pad = lambda m: Csr(total, total, np.concatenate([m.indptr, np.full(total - m.rows, m.indptr[-1])]),  # noqa: E731
+                            m.indices, m.data)
+        inst.update(kind="local", h=pad(h), ml=pad(ml), src=src, snk=snk, N=total)
+    else:  # G-QSW with 1-2 complex Lindblad operators, sometimes a rotating Hamiltonian
+        h = api.generator_matrix(float(0.5 + rng.random()), gu).to_csr()
+        ls = [random_complex(rng, n, 0.3) for _ in range(int(rng.integers(1, 3)))]
+        hrot = random_hermitian(rng, n, 0.2) if rng.random() < 0.4 else None
+        inst.update(kind="global", h=h, ls=ls, hrot=hrot, N=n)
+    N = inst["N"]
+    if rng.random() < 0.5:
+        p = rng.random(N)
+        inst["v0"] = rho0_vec(N, p / p.sum())
+    else:  # dense density matrix (Hermitian, unit trace), or a non-Hermitian vector
+        a = rng.standard_normal((N, N)) + 1j * rng.standard_normal((N, N))
+        rho = a @ a.conj().T
+        rho /= np.trace(rho).real
+        if rng.random() < 0.3:
+            rho = rho + 0.01 * (rng.standard_normal((N, N)) + 1j * rng.standard_normal((N, N)))
+        inst["v0"] = np.ascontiguousarray(rho.T).reshape(-1)  # column-major vec
+    t1 = float(rng.random())
+    inst["times"] = (t1, t1 + float(0.3 + 3 * rng.random()), int(rng.integers(1, 8)))
+    return inst
+
+
+def build_oracle(port, inst):
+    if inst["kind"] == "local":
+        return port.build_local(inst["omega"], inst["h"], inst["ml"], inst["src"], inst["snk"])
+    return port.build_global(inst["omega"], inst["h"], inst["ls"], inst["hrot"])
+
+
+def build_gpu(inst, fmt, group):
+    if inst["kind"] == "local":
+        return api.build_local(inst["omega"], inst["h"], inst["ml"], inst["src"], inst["snk"], group=group, format=fmt)
+    return api.build_global(inst["omega"], inst["h"], inst["ls"], inst["hrot"], group=group, format=fmt)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_walk_parity(port, seed):
+    inst = instance(seed)
+    t1, tq, q = inst["times"]
+    o = build_oracle(port, inst)
+    so, po, n_ref = o.series(inst["v0"], t1, tq, q)
+    want, n_step = o.step(inst["v0"], tq)
+    for fmt, group in MODES:
+        l = build_gpu(inst, fmt, group)
+        np.testing.assert_allclose(l.one_norms(), o.norms, rtol=1e-12, atol=1e-300)
+        r = api.series(l, l.state().upload(inst["v0"]), t1, tq, q, states=True)
+        err = float(np.abs(r.states - so).max())
+        assert err <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, group, err)
+        if group == 1:
+            assert int(r.info.spmvs) == n_ref, (seed, fmt, r.info.spmvs, n_ref)
+        got, info = api.step(l, l.state().upload(inst["v0"]), tq)
+        assert np.abs(got.gather() - want).max() <= RHO_TOL * max(1.0, float(np.abs(want).max())), (seed, fmt)
+        if group == 1:
+            assert int(info.spmvs) == n_step
