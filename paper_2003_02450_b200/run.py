@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import dataclasses
 import os
+import re
 import time
 
 import numpy as np
@@ -31,6 +32,7 @@ class ConfigError(RuntimeError):
 
 
 _KINDS = ("local", "global", "nm_global")
+_NUMBER = re.compile(r"[+-]?(\d+\.?\d*|\.\d+)([eE][+-]?\d+)?")
 
 
 def _g(x: float) -> str:
@@ -135,10 +137,12 @@ def load_probability_file(path) -> np.ndarray:
         raise api.IoError(f"cannot open initial state file `{path}`") from None
     p = []
     for tok in text.split():
-        try:
-            p.append(float(tok))
-        except ValueError:
+        m = _NUMBER.match(tok)  # what `in >> x` accepts: no inf/nan words
+        if m is None:
             break  # `in >> x` stops at the first token that is not a number
+        p.append(float(m.group(0)))
+        if m.end() != len(tok):
+            break  # a number followed by junk: the stream fails on the junk
     if not p:
         raise api.FileFormatError(f"initial state file `{path}` is empty")
     return np.asarray(p)
