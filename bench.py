@@ -391,8 +391,11 @@ def main():
                      "peak_source": peak_src, "share_of_step": share, "parts": parts_line,
                      "l2": ({"bytes_per_launch": l2_for(w.name, l.format),
                              "achieved_gbs": l2_for(w.name, l.format) / (term_ms * 1e-3) / 1e9,
-                             "note": "gather traffic SM<-L2 (ncu lts__t_sectors_srcunit_tex); the KRON term "
-                                     "kernel is bound by these gathers, not by HBM"}
+                             "note": "gather traffic SM<-L2 (ncu lts__t_sectors_srcunit_tex). The KRON term "
+                                     "kernel is bound by neither HBM nor L2: with every gather folded into L1 "
+                                     "it is only 7% faster (profiles/r01_kron_gather_fold.jsonl); it is bound "
+                                     "by its dependent operand-index -> gather -> FMA chains (ncu: 21 cycles "
+                                     "per issued instruction, 28.5 warps/SM, DESIGN.md section 3)"}
                             if l2_for(w.name, l.format) else None)},
         "superop_spmv": superop,
         "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,
