@@ -40,15 +40,16 @@ int sell_sigma_setting() {
   }();
   return v;
 }
-constexpr double kSellMaxPadding = 1.3;
-// Column panels of a SELL superoperator on one GPU: when the gathered vector
-// is larger than kPanelMinX and the rows are irregular (sorted: gathers go
-// everywhere, c4), split the columns so each panel's slice of x (about
-// kPanelX) stays in L2 while the panel's entries stream.  QSWG_SELL_PANELS
-// forces a count (tests); lattices and the bitwise mode keep one pass.
+constexpr double kSellMaxPadding = 1.3;  // SELL if stored/nnz <= this (else CSR)
+// Column panels of a SELL superoperator: when the gathered vector (the
+// full-length x, also on every rank of a row-partitioned run) is larger than
+// kPanelMinX and the rows are irregular (sorted: gathers go everywhere, c4),
+// split the columns so each panel's slice of x (about kPanelX) stays in L2
+// while the panel's entries stream.  QSWG_SELL_PANELS forces a count
+// (tests); lattices and the bitwise mode keep one pass.
 constexpr double kPanelMinX = 96e6, kPanelX = 40e6;
-int sell_panel_count(int world, int group, std::int64_t n, bool sorted) {
-  if (world != 1 || group == 1) return 1;
+int sell_panel_count(int group, std::int64_t n, bool sorted) {
+  if (group == 1) return 1;
   int p = 1;
   if (const char* e = std::getenv("QSWG_SELL_PANELS")) {
     p = std::atoi(e);
@@ -57,7 +58,7 @@ int sell_panel_count(int world, int group, std::int64_t n, bool sorted) {
     if (xb > kPanelMinX) p = static_cast<int>(std::ceil(xb / kPanelX));
   }
   return static_cast<int>(std::clamp<std::int64_t>(p, 1, std::min<std::int64_t>(dev::kMaxSellPanels, n)));
-}  // SELL-32 if stored/nnz <= this (c3: 1.24 -> 0.83 vs 1.06 ms CSR; c4: 1.51 -> CSR wins)
+}
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
 
@@ -920,7 +921,8 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   const double pad = l->nnz_local_ ? static_cast<double>(sell_entries) / static_cast<double>(l->nnz_local_) : 1.0;
   const bool use_sell = l->nnz_local_ > 0 && (cfg.format == 2 || (cfg.format == 0 && pad <= kSellMaxPadding));
   if (cfg.format == 3) throw std::invalid_argument("the Kron format has no bitwise (group = 1) mode");
-  const int panels = use_sell ? sell_panel_count(world, cfg.group, n, l->perm_.size() > 0) : 1;
+  const int panels = use_sell ? sell_panel_count(cfg.group, n, l->perm_.size() > 0) : 1;
+  std::int64_t main_entries = 0;
   if (use_sell && panels > 1) {
     // ---- column panels: x slices that stay in L2 while their entries stream ----
     l->format_ = dev::Format::Sell;
@@ -951,6 +953,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       QSWG_CHECK(cudaMemcpyAsync(&e, pn.slice_ptr.get() + l->n_slices_, sizeof(std::int64_t), cudaMemcpyDeviceToHost, s));
       QSWG_CHECK(cudaStreamSynchronize(s));
       stored += e;
+      pn.entries = e;
       pn.col.resize(static_cast<std::size_t>(std::max<std::int64_t>(e, 1)));
       pn.val.resize(static_cast<std::size_t>(std::max<std::int64_t>(e, 1)));
       dev::assemble_fill_sell(ops.get(), l->block_.row0, rows, pn.slice_ptr.get(),
@@ -965,11 +968,12 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
         l->col_ = std::move(pn.col);
         l->val_ = std::move(pn.val);
         l->main_c_lo_ = pn.c_lo;
+        main_entries = e;
       }
     }
     l->part_.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)));
     l->padding_ = static_cast<double>(stored) / static_cast<double>(l->nnz_local_);
-    sell_entries = stored;
+    sell_entries = main_entries;  // the halo hull below walks the earlier panels separately
   } else if (use_sell) {
     l->format_ = dev::Format::Sell;
     l->padding_ = pad;
@@ -1003,6 +1007,8 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     std::int64_t* mine = table.get() + 2 * world * rank;
     QSWG_CHECK(cudaMemcpyAsync(mine, init.data(), init.size() * sizeof(std::int64_t), cudaMemcpyHostToDevice, s));
     dev::halo_hulls(l->col_.get(), stored, dstarts.get(), world, rank, mine, mine + world, s);
+    for (const SellPanel& pn : l->pre_)  // column panels: every panel's columns
+      dev::halo_hulls(pn.col.get(), pn.entries, dstarts.get(), world, rank, mine, mine + world, s);
     std::vector<std::int64_t> tstarts(static_cast<std::size_t>(world) + 1);
     for (int w = 0; w <= world; ++w) tstarts[static_cast<std::size_t>(w)] = 2 * world * w;
     cfg.comm->allgather_rows(table.get(), tstarts, sizeof(std::int64_t), s);

@@ -54,6 +54,7 @@ struct SellPanel {
   DeviceBuffer<int> col;
   DeviceBuffer<double2> val;
   std::int64_t c_lo = 0, c_hi = 0;  // global column range
+  std::int64_t entries = 0;          // stored entries (padding included)
 };
 
 struct RowBlock {
