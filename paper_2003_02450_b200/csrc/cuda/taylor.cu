@@ -1549,7 +1549,7 @@ void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {
 
 // The partial sums of the earlier SELL column panels (no-op for one panel).
 void sell_partials(const DevMatrix& m, const double2* x, const SkipCheck& sk, cudaStream_t s) {
-  for (int q = 0; q < m.n_pre; ++q) {
+  for (int q = m.pre_done; q < m.n_pre; ++q) {
     if (q == 0) {
       launch_pdl(sell_partial_kernel<true>, sell_grid(sell_partial_kernel<true>, m.sell_pre[q]), kThreads, 0, s,
                  m.sell_pre[q], x, m.part, sk);
@@ -1559,6 +1559,15 @@ void sell_partials(const DevMatrix& m, const double2* x, const SkipCheck& sk, cu
     }
     QSWG_LAUNCH_CHECK("sell_partials");
   }
+}
+
+void sell_local_panel(const DevMatrix& m, const double2* x, const SeriesCtl* series, const StepCtl* step,
+                      int first_of_stage, cudaStream_t s) {
+  if (m.format != Format::Sell || !m.local_first || m.n_pre < 1) return;
+  DevMatrix one = m;
+  one.n_pre = 1;
+  one.pre_done = 0;
+  sell_partials(one, x, SkipCheck{series, step, first_of_stage}, s);
 }
 
 void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,

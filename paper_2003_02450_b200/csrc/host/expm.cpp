@@ -107,6 +107,28 @@ struct Exec {
     if (!single) comm->exchange_ranges(full_vec, l.halo_lo(), l.halo_hi(), sizeof(double2), s);
   }
 
+  // Halo exchange of the next product's input; with an own-column SELL panel
+  // (row-partitioned stored superoperator) that panel's partial sums run on
+  // the library stream while the exchange runs on a side stream.  Returns
+  // true when the panel was launched (the product then runs with pre_done).
+  bool exchange_overlap(double2* full_vec, const dev::DevMatrix& m, const dev::SeriesCtl* series,
+                        const dev::StepCtl* step, int first_of_stage) const {
+    if (single) return false;
+    if (m.format != dev::Format::Sell || !m.local_first) {
+      exchange(full_vec);
+      return false;
+    }
+    cudaEvent_t ev[2];
+    cudaStream_t side = l.side_stream(ev);
+    QSWG_CHECK(cudaEventRecord(ev[0], s));  // the input's own rows are final
+    QSWG_CHECK(cudaStreamWaitEvent(side, ev[0], 0));
+    dev::sell_local_panel(m, full_vec, series, step, first_of_stage, s);
+    comm->exchange_ranges(full_vec, l.halo_lo(), l.halo_hi(), sizeof(double2), side);
+    QSWG_CHECK(cudaEventRecord(ev[1], side));
+    QSWG_CHECK(cudaStreamWaitEvent(s, ev[1], 0));
+    return true;
+  }
+
   // SpMV input from a local state: on one GPU the state itself; otherwise
   // its rows copied into a full-length buffer whose halo is then exchanged.
   const double2* spmv_input(const double2* local_vec, std::size_t slot) const {
@@ -184,18 +206,22 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
     const double2* x_stage = st == 0 ? v : sums[(st - 1) % 2];
     const double2* x_stage_full = ex.spmv_input(x_stage, kXStage);
     double2* acc = sums[st % 2];
+    bool pre = false;  // the own-column panel of this product already ran (overlapped exchange)
     for (std::int64_t j = 1; j <= sp.m_star; ++j) {
       const double2* x = j == 1 ? x_stage_full : term[(j - 1) % 2];
       double2* y = term[j % 2] + ex.row0;
       const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
       ex.prepare(mat, x);
-      dev::step_term(mat, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1, static_cast<int>(st),
+      dev::DevMatrix mj = mat;
+      mj.pre_done = pre ? 1 : 0;
+      dev::step_term(mj, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1, static_cast<int>(st),
                      params.tolerance, ctl, ex.single, s);
+      pre = false;
       if (!ex.single) {
         ex.comm->allreduce_max_u64(&ctl->term_bits, 2, s);  // term_bits, sum_bits
         dev::step_control(ctl, j == 1, static_cast<int>(st), params.tolerance, s);
         if (ex.read(&ctl->done)) break;  // expm.cpp:191-194 (error sets done)
-        if (j < sp.m_star) ex.exchange(term[j % 2]);
+        if (j < sp.m_star) pre = ex.exchange_overlap(term[j % 2], mat, nullptr, ctl, 0);
       }
     }
     if (!ex.single && ex.read(&ctl->error)) break;
@@ -298,12 +324,16 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
       dev::SeriesSums ss{};
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
       const double2* z_full = ex.spmv_input(z, kZFull);
+      bool pre = false;  // the own-column panel of this term already ran (overlapped exchange)
       for (std::int64_t p = 1; p <= m_star; ++p) {
         const double2* x = p == 1 ? z_full : ring.k[(p - 1) % ring.slots];
         double2* kp = ring.k[p % ring.slots] + ex.row0;
         const bool last = p == m_star;
         if (!fused || p == 1) ex.prepare(mat, x);
-        dev::series_term(mat, x, kp, static_cast<int>(p), last, h / static_cast<double>(p), params.tolerance, ctl,
+        dev::DevMatrix mp = mat;
+        mp.pre_done = pre ? 1 : 0;
+        pre = false;
+        dev::series_term(mp, x, kp, static_cast<int>(p), last, h / static_cast<double>(p), params.tolerance, ctl,
                          ex.single, s);
         if (ex.single) {
           if (!(fused && !last &&
@@ -324,7 +354,7 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
           dev::series_flush_control(ctl, static_cast<int>(p), params.tolerance, s);
           if (ex.read(&ctl->n_active) == 0) break;
         }
-        if (p < m_star) ex.exchange(ring.k[p % ring.slots]);
+        if (p < m_star) pre = ex.exchange_overlap(ring.k[p % ring.slots], mat, ctl, nullptr, 1);
       }
       for (std::int64_t k = 1; k <= count; ++k) emit(super * d + k, sums[static_cast<std::size_t>(k - 1)]);
       // the next super-step starts from states[(super + 1) d] = the last output

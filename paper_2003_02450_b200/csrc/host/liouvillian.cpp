@@ -404,6 +404,7 @@ void Liouvillian::adopt(Liouvillian& o) {
   std::swap(pre_, o.pre_);
   std::swap(part_, o.part_);
   std::swap(main_c_lo_, o.main_c_lo_);
+  std::swap(local_first_, o.local_first_);
   std::swap(rowptr_, o.rowptr_);
   std::swap(col_, o.col_);
   std::swap(val_, o.val_);
@@ -438,8 +439,26 @@ Liouvillian::~Liouvillian() {
     col_.reset();
     val_.reset();
     ws_ = Workspace{};
+    if (side_) {
+      cudaStreamSynchronize(side_);
+      cudaStreamDestroy(side_);
+      cudaEventDestroy(ev_[0]);
+      cudaEventDestroy(ev_[1]);
+    }
     cudaStreamDestroy(stream_);
   }
+}
+
+cudaStream_t Liouvillian::side_stream(cudaEvent_t* ev) const {
+  if (!side_) {
+    DeviceGuard g(device_);
+    QSWG_CHECK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    QSWG_CHECK(cudaEventCreateWithFlags(&ev_[0], cudaEventDisableTiming));
+    QSWG_CHECK(cudaEventCreateWithFlags(&ev_[1], cudaEventDisableTiming));
+  }
+  ev[0] = ev_[0];
+  ev[1] = ev_[1];
+  return side_;
 }
 
 dev::CsrView Liouvillian::view() const {
@@ -488,6 +507,7 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     }
     m.part = part_.get();
     m.sell.part_in = part_.get();
+    m.local_first = local_first_ ? 1 : 0;
   }
   if (kron_) {
     const dev::KronOperands& o = kron_->ops.get();
@@ -554,10 +574,13 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
       const int* col;
       const double2* val;
     };
-    std::vector<View> views;
+    std::vector<std::pair<std::int64_t, View>> pv;  // (first column, panel), walked in column order
     for (const SellPanel& pn : pre_)
-      views.push_back({pn.slice_ptr.get(), pn.perm.size() ? pn.perm.get() : nullptr, pn.col.get(), pn.val.get()});
-    views.push_back({slice_ptr_.get(), perm_.size() ? perm_.get() : nullptr, col_.get(), val_.get()});
+      pv.push_back({pn.c_lo, {pn.slice_ptr.get(), pn.perm.size() ? pn.perm.get() : nullptr, pn.col.get(), pn.val.get()}});
+    pv.push_back({main_c_lo_, {slice_ptr_.get(), perm_.size() ? perm_.get() : nullptr, col_.get(), val_.get()}});
+    std::stable_sort(pv.begin(), pv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<View> views;
+    for (const auto& e : pv) views.push_back(e.second);
     const std::size_t rows = static_cast<std::size_t>(block_.rows);
     std::vector<std::vector<int>> rc(rows);
     std::vector<std::vector<Complex>> rv(rows);
@@ -921,8 +944,30 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   const double pad = l->nnz_local_ ? static_cast<double>(sell_entries) / static_cast<double>(l->nnz_local_) : 1.0;
   const bool use_sell = l->nnz_local_ > 0 && (cfg.format == 2 || (cfg.format == 0 && pad <= kSellMaxPadding));
   if (cfg.format == 3) throw std::invalid_argument("the Kron format has no bitwise (group = 1) mode");
-  const int panels = use_sell ? sell_panel_count(cfg.group, n, l->perm_.size() > 0) : 1;
+  // Column ranges of the panels.  One GPU: equal ranges when x outgrows L2
+  // (sell_panel_count).  Row-partitioned (stored, non-bitwise): this rank's own
+  // columns first — that panel needs no halo, so its partial sums run while the
+  // halo of the next input is exchanged (Exec::exchange_overlap) — then the
+  // columns before and after, in chunks of about kPanelX when x is large.
+  std::vector<std::pair<std::int64_t, std::int64_t>> ranges;
+  bool local_first = false;
+  if (use_sell && world > 1 && cfg.group != 1) {
+    const std::int64_t lo = l->block_.row0, hi = l->block_.row0 + l->block_.rows;
+    const int per = std::max(1, sell_panel_count(cfg.group, n, l->perm_.size() > 0));
+    const std::int64_t chunk = std::max<std::int64_t>(n, (dim + per - 1) / per / n * n);  // whole rho columns
+    ranges.push_back({lo, hi});
+    for (std::int64_t c = 0; c < lo; c += chunk) ranges.push_back({c, std::min(lo, c + chunk)});
+    for (std::int64_t c = hi; c < dim; c += chunk) ranges.push_back({c, std::min(dim, c + chunk)});
+    local_first = true;
+  } else if (use_sell) {
+    const int panels = sell_panel_count(cfg.group, n, l->perm_.size() > 0);
+    for (int q = 0; panels > 1 && q < panels; ++q)
+      ranges.push_back({n * (static_cast<std::int64_t>(q) * n / panels), n * (static_cast<std::int64_t>(q + 1) * n / panels)});
+  }
+  const int panels = ranges.size() > 1 ? static_cast<int>(ranges.size()) : 1;
+  if (panels > dev::kMaxSellPanels) throw std::logic_error("too many SELL column panels");
   std::int64_t main_entries = 0;
+  l->local_first_ = local_first && panels > 1;
   if (use_sell && panels > 1) {
     // ---- column panels: x slices that stay in L2 while their entries stream ----
     l->format_ = dev::Format::Sell;
@@ -936,8 +981,8 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     l->pre_.clear();
     for (int q = 0; q < panels; ++q) {
       SellPanel pn;
-      pn.c_lo = n * (static_cast<std::int64_t>(q) * n / panels);
-      pn.c_hi = n * (static_cast<std::int64_t>(q + 1) * n / panels);
+      pn.c_lo = ranges[static_cast<std::size_t>(q)].first;
+      pn.c_hi = ranges[static_cast<std::size_t>(q)].second;
       QSWG_CHECK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
       dev::assemble_count(ops.get(), l->block_.row0, rows, cnt.get(), s, pn.c_lo, pn.c_hi);
       dev::exclusive_scan(cnt.get(), g.get(), rows + 1, tmp.get(), tmp_bytes, s);

@@ -91,6 +91,9 @@ class Liouvillian {
   int sell_sigma() const { return sigma_; }
   /// SELL column panels (1: the whole row in one pass).
   int sell_panels() const { return static_cast<int>(pre_.size()) + 1; }
+  /// Second stream (and two events) for halo exchanges overlapped with the
+  /// own-column panel of a row-partitioned stored superoperator.
+  cudaStream_t side_stream(cudaEvent_t* ev) const;
   bool kron_factored() const;
   bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
 
@@ -146,6 +149,9 @@ class Liouvillian {
   std::vector<SellPanel> pre_;            // SELL column panels before the main arrays (one GPU)
   DeviceBuffer<double2> part_;            // their row sums
   std::int64_t main_c_lo_ = 0;            // column range of the main SELL arrays
+  bool local_first_ = false;              // panel 0 = this rank's own columns (overlap with the halo exchange)
+  mutable cudaStream_t side_ = nullptr;   // halo exchanges overlapped with the local panel
+  mutable cudaEvent_t ev_[2] = {nullptr, nullptr};
   DeviceBuffer<std::int64_t> rowptr_;     // CSR
   DeviceBuffer<int> col_;
   DeviceBuffer<double2> val_;
