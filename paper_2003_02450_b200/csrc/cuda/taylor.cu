@@ -1563,11 +1563,11 @@ void sell_partials(const DevMatrix& m, const double2* x, const SkipCheck& sk, cu
 
 void sell_local_panel(const DevMatrix& m, const double2* x, const SeriesCtl* series, const StepCtl* step,
                       int first_of_stage, cudaStream_t s) {
-  if (m.format != Format::Sell || !m.local_first || m.n_pre < 1) return;
-  DevMatrix one = m;
-  one.n_pre = 1;
-  one.pre_done = 0;
-  sell_partials(one, x, SkipCheck{series, step, first_of_stage}, s);
+  if (m.format != Format::Sell || m.local_first < 1 || m.n_pre < 1) return;
+  DevMatrix own = m;
+  own.n_pre = m.local_first < m.n_pre ? m.local_first : m.n_pre;
+  own.pre_done = 0;
+  sell_partials(own, x, SkipCheck{series, step, first_of_stage}, s);
 }
 
 void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* sum_in, double2* sum_out,

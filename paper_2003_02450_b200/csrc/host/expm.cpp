@@ -110,13 +110,13 @@ struct Exec {
   // Halo exchange of the next product's input; with an own-column SELL panel
   // (row-partitioned stored superoperator) that panel's partial sums run on
   // the library stream while the exchange runs on a side stream.  Returns
-  // true when the panel was launched (the product then runs with pre_done).
-  bool exchange_overlap(double2* full_vec, const dev::DevMatrix& m, const dev::SeriesCtl* series,
-                        const dev::StepCtl* step, int first_of_stage) const {
-    if (single) return false;
-    if (m.format != dev::Format::Sell || !m.local_first) {
+  // the number of panels launched (the product then runs with pre_done = it).
+  int exchange_overlap(double2* full_vec, const dev::DevMatrix& m, const dev::SeriesCtl* series,
+                       const dev::StepCtl* step, int first_of_stage) const {
+    if (single) return 0;
+    if (m.format != dev::Format::Sell || m.local_first < 1) {
       exchange(full_vec);
-      return false;
+      return 0;
     }
     cudaEvent_t ev[2];
     cudaStream_t side = l.side_stream(ev);
@@ -126,7 +126,7 @@ struct Exec {
     comm->exchange_ranges(full_vec, l.halo_lo(), l.halo_hi(), sizeof(double2), side);
     QSWG_CHECK(cudaEventRecord(ev[1], side));
     QSWG_CHECK(cudaStreamWaitEvent(s, ev[1], 0));
-    return true;
+    return std::min(m.local_first, m.n_pre);
   }
 
   // SpMV input from a local state: on one GPU the state itself; otherwise
@@ -206,17 +206,17 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
     const double2* x_stage = st == 0 ? v : sums[(st - 1) % 2];
     const double2* x_stage_full = ex.spmv_input(x_stage, kXStage);
     double2* acc = sums[st % 2];
-    bool pre = false;  // the own-column panel of this product already ran (overlapped exchange)
+    int pre = 0;  // own-column panels of this product already summed (overlapped exchange)
     for (std::int64_t j = 1; j <= sp.m_star; ++j) {
       const double2* x = j == 1 ? x_stage_full : term[(j - 1) % 2];
       double2* y = term[j % 2] + ex.row0;
       const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
       ex.prepare(mat, x);
       dev::DevMatrix mj = mat;
-      mj.pre_done = pre ? 1 : 0;
+      mj.pre_done = pre;
       dev::step_term(mj, x, y, j == 1 ? x_stage : acc, acc, scale, j == 1, static_cast<int>(st),
                      params.tolerance, ctl, ex.single, s);
-      pre = false;
+      pre = 0;
       if (!ex.single) {
         ex.comm->allreduce_max_u64(&ctl->term_bits, 2, s);  // term_bits, sum_bits
         dev::step_control(ctl, j == 1, static_cast<int>(st), params.tolerance, s);
@@ -324,15 +324,15 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
       dev::SeriesSums ss{};
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
       const double2* z_full = ex.spmv_input(z, kZFull);
-      bool pre = false;  // the own-column panel of this term already ran (overlapped exchange)
+      int pre = 0;  // own-column panels of this term already summed (overlapped exchange)
       for (std::int64_t p = 1; p <= m_star; ++p) {
         const double2* x = p == 1 ? z_full : ring.k[(p - 1) % ring.slots];
         double2* kp = ring.k[p % ring.slots] + ex.row0;
         const bool last = p == m_star;
         if (!fused || p == 1) ex.prepare(mat, x);
         dev::DevMatrix mp = mat;
-        mp.pre_done = pre ? 1 : 0;
-        pre = false;
+        mp.pre_done = pre;
+        pre = 0;
         dev::series_term(mp, x, kp, static_cast<int>(p), last, h / static_cast<double>(p), params.tolerance, ctl,
                          ex.single, s);
         if (ex.single) {

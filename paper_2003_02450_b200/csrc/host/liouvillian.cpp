@@ -507,7 +507,7 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     }
     m.part = part_.get();
     m.sell.part_in = part_.get();
-    m.local_first = local_first_ ? 1 : 0;
+    m.local_first = local_first_;
   }
   if (kron_) {
     const dev::KronOperands& o = kron_->ops.get();
@@ -950,15 +950,15 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   // halo of the next input is exchanged (Exec::exchange_overlap) — then the
   // columns before and after, in chunks of about kPanelX when x is large.
   std::vector<std::pair<std::int64_t, std::int64_t>> ranges;
-  bool local_first = false;
+  int local_first = 0;  // leading panels that cover this rank's own columns
   if (use_sell && world > 1 && cfg.group != 1) {
     const std::int64_t lo = l->block_.row0, hi = l->block_.row0 + l->block_.rows;
     const int per = std::max(1, sell_panel_count(cfg.group, n, l->perm_.size() > 0));
     const std::int64_t chunk = std::max<std::int64_t>(n, (dim + per - 1) / per / n * n);  // whole rho columns
-    ranges.push_back({lo, hi});
+    for (std::int64_t c = lo; c < hi; c += chunk) ranges.push_back({c, std::min(hi, c + chunk)});
+    local_first = static_cast<int>(ranges.size());
     for (std::int64_t c = 0; c < lo; c += chunk) ranges.push_back({c, std::min(lo, c + chunk)});
     for (std::int64_t c = hi; c < dim; c += chunk) ranges.push_back({c, std::min(dim, c + chunk)});
-    local_first = true;
   } else if (use_sell) {
     const int panels = sell_panel_count(cfg.group, n, l->perm_.size() > 0);
     for (int q = 0; panels > 1 && q < panels; ++q)
@@ -967,7 +967,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   const int panels = ranges.size() > 1 ? static_cast<int>(ranges.size()) : 1;
   if (panels > dev::kMaxSellPanels) throw std::logic_error("too many SELL column panels");
   std::int64_t main_entries = 0;
-  l->local_first_ = local_first && panels > 1;
+  l->local_first_ = panels > 1 ? std::min(local_first, panels - 1) : 0;
   if (use_sell && panels > 1) {
     // ---- column panels: x slices that stay in L2 while their entries stream ----
     l->format_ = dev::Format::Sell;

@@ -149,7 +149,7 @@ class Liouvillian {
   std::vector<SellPanel> pre_;            // SELL column panels before the main arrays (one GPU)
   DeviceBuffer<double2> part_;            // their row sums
   std::int64_t main_c_lo_ = 0;            // column range of the main SELL arrays
-  bool local_first_ = false;              // panel 0 = this rank's own columns (overlap with the halo exchange)
+  int local_first_ = 0;                   // leading panels = this rank's own columns (overlap the halo exchange)
   mutable cudaStream_t side_ = nullptr;   // halo exchanges overlapped with the local panel
   mutable cudaEvent_t ev_[2] = {nullptr, nullptr};
   DeviceBuffer<std::int64_t> rowptr_;     // CSR

@@ -146,7 +146,7 @@ struct DevMatrix {
   int n_pre = 0;                           // SELL column panels before `sell`
   SellView sell_pre[kMaxSellPanels - 1];
   double2* part = nullptr;                 // their row sums (local rows)
-  int local_first = 0;                     // sell_pre[0] = this rank's own columns (no halo needed)
+  int local_first = 0;                     // sell_pre[0 .. local_first) = this rank's own columns (no halo)
   int pre_done = 0;                        // panels already summed for this product (sell_local_panel)
   std::int64_t rows() const {
     return format == Format::Csr ? csr.rows : format == Format::Sell ? sell.rows : kron.rows;
@@ -266,9 +266,9 @@ struct SeriesSums {
   double2* s[kMaxSeriesD];
 };
 
-// Multi-GPU overlap: the partial sums of panel 0 (this rank's own columns,
-// DevMatrix::local_first) of the next product with x, launched while x's halo
-// is exchanged; the product then runs with pre_done = 1.  The skip test is the
+// Multi-GPU overlap: the partial sums of the own-column panels
+// (DevMatrix::local_first of them) of the next product with x, launched while
+// x's halo is exchanged; the product then runs with pre_done = local_first.  The skip test is the
 // term kernel's: series control (series != nullptr) or step control.
 void sell_local_panel(const DevMatrix& m, const double2* x, const SeriesCtl* series, const StepCtl* step,
                       int first_of_stage, cudaStream_t s);
