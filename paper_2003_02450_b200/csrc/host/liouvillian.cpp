@@ -954,18 +954,21 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   if (use_sell && world > 1 && cfg.group != 1) {
     const std::int64_t lo = l->block_.row0, hi = l->block_.row0 + l->block_.rows;
     const int per = std::max(1, sell_panel_count(cfg.group, n, l->perm_.size() > 0));
-    const std::int64_t chunk = std::max<std::int64_t>(n, (dim + per - 1) / per / n * n);  // whole rho columns
-    for (std::int64_t c = lo; c < hi; c += chunk) ranges.push_back({c, std::min(hi, c + chunk)});
-    local_first = static_cast<int>(ranges.size());
-    for (std::int64_t c = 0; c < lo; c += chunk) ranges.push_back({c, std::min(lo, c + chunk)});
-    for (std::int64_t c = hi; c < dim; c += chunk) ranges.push_back({c, std::min(dim, c + chunk)});
+    std::int64_t chunk = std::max<std::int64_t>(n, (dim + per - 1) / per / n * n);  // whole rho columns
+    do {  // (coarser chunks if the three runs would exceed the panel limit)
+      ranges.clear();
+      for (std::int64_t c = lo; c < hi; c += chunk) ranges.push_back({c, std::min(hi, c + chunk)});
+      local_first = static_cast<int>(ranges.size());
+      for (std::int64_t c = 0; c < lo; c += chunk) ranges.push_back({c, std::min(lo, c + chunk)});
+      for (std::int64_t c = hi; c < dim; c += chunk) ranges.push_back({c, std::min(dim, c + chunk)});
+      chunk *= 2;
+    } while (static_cast<int>(ranges.size()) > dev::kMaxSellPanels);
   } else if (use_sell) {
     const int panels = sell_panel_count(cfg.group, n, l->perm_.size() > 0);
     for (int q = 0; panels > 1 && q < panels; ++q)
       ranges.push_back({n * (static_cast<std::int64_t>(q) * n / panels), n * (static_cast<std::int64_t>(q + 1) * n / panels)});
   }
   const int panels = ranges.size() > 1 ? static_cast<int>(ranges.size()) : 1;
-  if (panels > dev::kMaxSellPanels) throw std::logic_error("too many SELL column panels");
   std::int64_t main_entries = 0;
   l->local_first_ = panels > 1 ? std::min(local_first, panels - 1) : 0;
   if (use_sell && panels > 1) {
