@@ -806,7 +806,8 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
 // Matrix-free action (kernels.hpp: KronView), in 32 x 32 tiles of X.
 // Per element the terms are summed in the order
 //   A, R_1 .. R_nk (row-indexed operands),  B, P_1, S_1, .., P_nk, S_nk,
-//   T, decay (column-indexed operands and the diagonal terms),
+//   (A_ii + B_jj), T, decay (column-indexed operands and the diagonal terms;
+//   A and B are stored without their diagonals),
 // in every path, so the Hermitian path reproduces the general one bit for bit.
 //
 // General path: lane = rho row i, warp w = rho columns j0 + 4w .. j0 + 4w + 3.
@@ -928,6 +929,15 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
         const double2* vi = m.v[k] + i;
         uniform_rows(m.s[k], j, acc, [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
       }
+    }
+  }
+  if (m.da) {  // the diagonals of A and B: (A_ii + B_jj) X(i, j), one gather
+    const double2 dai = __ldg(m.da + i);
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const double2 dbj = __ldg(m.db + j[r]);
+      const double2 c = make_double2(dai.x + dbj.x, dai.y + dbj.y);
+      if (c.x != 0.0 || c.y != 0.0) cfma(acc[r], c, ld_gather(x + static_cast<long long>(j[r]) * n + i, xpol));
     }
   }
 #pragma unroll
@@ -1105,8 +1115,11 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
         if (q.ptr)
           uniform_row(q, i, acc[r], [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
         if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<long long>(iv) * n + au, acc[r], xpol);
+#ifndef QSWG_W_NO_COLMAJOR  // experiment (wrong results): cost of the column-major copy
         tile[kKR * w + r][lane] = acc[r];
+#endif
       }
+#ifndef QSWG_W_NO_COLMAJOR
       __syncthreads();
       const int iu = I * kKT + lane;
 #pragma unroll
@@ -1115,6 +1128,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
         if (iu < g.n && at < g.n) st_hint(m.w[k] + static_cast<long long>(at) * n + iu, tile[lane][kKR * w + r], xpol);
       }
       __syncthreads();
+#endif
     } else {
       const int iu = I * kKT + lane;
       const bool vi = iu < m.n;

@@ -292,6 +292,29 @@ EllHost to_ell(const MultiCsr& m) {
 }
 
 // Device copy of the summed operands kept by a Kron-format Liouvillian.
+// Splits the diagonal off a (summed) operand list: d[i] = m(i, i), 0 if absent.
+MultiCsr strip_diagonal(const MultiCsr& m, std::vector<double2>& d) {
+  MultiCsr o;
+  o.n = m.n;
+  d.assign(static_cast<std::size_t>(m.n), make_double2(0.0, 0.0));
+  if (m.ptr.empty()) return o;
+  o.ptr.assign(static_cast<std::size_t>(m.n) + 1, 0);
+  for (std::int64_t i = 0; i < m.n; ++i) {
+    for (int k = m.ptr[static_cast<std::size_t>(i)]; k < m.ptr[static_cast<std::size_t>(i) + 1]; ++k) {
+      const auto uk = static_cast<std::size_t>(k);
+      if (m.col[uk] == i) {
+        d[static_cast<std::size_t>(i)].x += m.val[uk].x;
+        d[static_cast<std::size_t>(i)].y += m.val[uk].y;
+      } else {
+        o.col.push_back(m.col[uk]);
+        o.val.push_back(m.val[uk]);
+      }
+    }
+    o.ptr[static_cast<std::size_t>(i) + 1] = static_cast<int>(o.col.size());
+  }
+  return o;
+}
+
 struct KronStore {
   // Sliced ELL copies unless they store more than kEllMaxPadding x the
   // nonzeros; whether the kernels use them is autotuned per operator set at
@@ -302,7 +325,35 @@ struct KronStore {
     // (one GPU: c2 47.2 vs 47.8 ms per series factored, c4 factored either way)
     factored = host.has_factored && host.kron_cost(true, single) < (single ? 0.9 : 0.8) * host.kron_cost(false);
     if (const char* f = std::getenv("QSWG_KRON_FACTOR")) factored = host.has_factored && f[0] == '1';  // test knob
-    a = maybe_ell(factored ? host.af : host.a, s);
+    // The diagonals of A and B both multiply X(i, j): on G-QSW operators the
+    // kernels apply them as one coefficient (A_ii + B_jj) with one gather (c2:
+    // 22 -> 20 gathers per element, exactly zero on regular graphs, then
+    // skipped; term 35.4 -> 33.9 us, series 39.8 -> 39.2 ms).  L-QSW keeps them
+    // in the lists: its decay term gathers X(i, j) already, and the split
+    // measured slower there (c5 17.17 -> 17.36 s, c3 0.88 -> 0.89 s).
+    // QSWG_KRON_DIAG=0/1 forces either form (experiment knob).
+    const MultiCsr& a0 = factored ? host.af : host.a;
+    const MultiCsr& b0 = factored ? host.bf : host.b;
+    const char* dk = std::getenv("QSWG_KRON_DIAG");
+    const bool split = dk ? dk[0] == '1' : host.d_loc.empty();
+    if (!split) {
+      a_list = upload_list(a0, s);
+      b_list = upload_list(b0, s);
+      a = maybe_ell(a0, s);
+    } else {
+      std::vector<double2> dah, dbh;
+      const MultiCsr a1 = strip_diagonal(a0, dah), b1 = strip_diagonal(b0, dbh);
+      a_list = upload_list(a1, s);
+      b_list = upload_list(b1, s);
+      a = maybe_ell(a1, s);
+      bool any = false;
+      for (std::size_t i = 0; i < dah.size(); ++i)
+        any = any || dah[i].x != 0.0 || dah[i].y != 0.0 || dbh[i].x != 0.0 || dbh[i].y != 0.0;
+      if (any) {
+        da = up(dah, s);
+        db = up(dbh, s);
+      }
+    }
     for (const MultiCsr& qk : host.q) q.push_back(maybe_ell(qk, s));
     if (factored) {
       af = upload_list(host.af, s);
@@ -317,7 +368,10 @@ struct KronStore {
   }
   HostOperands host;
   DeviceOperands ops;  // CSR lists (B, P, T; and A, Q for on-demand assembly)
-  dev::KronEll a;
+  dev::KronEll a;               // A without its diagonal, sliced ELL (or empty)
+  dev::KronList a_list, b_list;  // A and B without their diagonals, CSR
+  const double2* da = nullptr;   // diag(A), diag(B) (nullptr when both vanish)
+  const double2* db = nullptr;
   std::vector<dev::KronEll> q;
   bool factored = false;
   dev::KronList af, bf;
@@ -515,8 +569,10 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.rows = block_.rows;
     m.kron.row0 = block_.row0;
     m.kron.a_ell = kron_ell_ ? kron_->a : dev::KronEll{};
-    m.kron.a = kron_->factored ? kron_->af : o.a;
-    m.kron.b = kron_->factored ? kron_->bf : o.b;
+    m.kron.a = kron_->a_list;
+    m.kron.b = kron_->b_list;
+    m.kron.da = kron_->da;
+    m.kron.db = kron_->db;
     m.kron.factored = kron_->factored ? 1 : 0;
     m.kron.t = o.t;
     m.kron.nk = o.nk;

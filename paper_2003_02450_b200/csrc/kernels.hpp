@@ -104,6 +104,10 @@ struct KronView {
   KronList a;
   KronList b;     // B (x) I, indexed by the rho column j (warp-uniform)
   KronList t;     // transfer onto the diagonal (rows i == j)
+  // a and b hold no diagonal entries: (A_ii + B_jj) X(i, j) is one term
+  // (nullptr: both diagonals vanish)
+  const double2* da = nullptr;
+  const double2* db = nullptr;
   int nk = 0;
   KronList p[kMaxKron];      // indexed by j (warp-uniform)
   KronEll q_ell[kMaxKron];   // W_k = Q_k X, indexed by i
