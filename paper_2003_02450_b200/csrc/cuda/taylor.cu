@@ -805,9 +805,9 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
 
 // Matrix-free action (kernels.hpp: KronView), in 32 x 32 tiles of X.
 // Per element the terms are summed in the order
-//   A, R_1 .. R_nk (row-indexed operands),  B, P_1, S_1, .., P_nk, S_nk,
+//   A, R_1 .. R_nk (row-indexed operands),  P_1 .. P_nk, B, S_1 .. S_nk,
 //   (A_ii + B_jj), T, decay (column-indexed operands and the diagonal terms;
-//   A and B are stored without their diagonals),
+//   A and B of G-QSW are stored without their diagonals),
 // in every path, so the Hermitian path reproduces the general one bit for bit.
 //
 // General path: lane = rho row i, warp w = rho columns j0 + 4w .. j0 + 4w + 3.
@@ -905,6 +905,21 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
       uniform_rows(m.r[k], i, acc, [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
     }
   }
+  if (m.p_rows) {  // P_k(j, a) W_k(i, a), lane = j: padding-free ELL rows of P_k, rows i of Wt_k
+    const int sl = j >> 5, ln = j & 31;
+    for (int k = 0; k < m.nk; ++k) {
+      const KronEll& pe = m.p_ell[k];
+      const double2* wt = m.wt[k];
+      const int b = __ldg(pe.sptr + sl), len = (__ldg(pe.sptr + sl + 1) - b) >> 5;
+#pragma unroll 2
+      for (int e = 0; e < len; ++e) {
+        const int a = __ldg(pe.col + b + 32 * e + ln);
+        const double2 v = __ldg(pe.val + b + 32 * e + ln);
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(wt + static_cast<long long>(i[r]) * n + a, xpol));
+      }
+    }
+  }
 }
 
 // Column-indexed part and diagonal terms at (i, j[r]), lane = row i.
@@ -914,13 +929,17 @@ template <bool kHerm>
 __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __restrict__ x, int i, const int* j,
                                           double2* acc, unsigned long long xpol) {
   const long long n = m.n;
+  if (!(kHerm && m.p_rows)) {  // (the Hermitian tiles applied P_k in the transposed section)
+    for (int k = 0; k < m.nk; ++k) {
+      const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
+      uniform_rows(m.p[k], j, acc, [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
+    }
+  }
   if (m.b.ptr) {  // B (x) I: coalesced columns c of X
     const double2* xi = x + i;
     uniform_rows(m.b, j, acc, [&](int c) { return ld_gather(xi + static_cast<long long>(c) * n, xpol); });
   }
   for (int k = 0; k < m.nk; ++k) {
-    const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
-    uniform_rows(m.p[k], j, acc, [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
     if (m.factored) {  // -w/2 (X L') L: columns of V_k
       if constexpr (kHerm) {
         const double2* vi = m.wt[k] + i;
@@ -1115,20 +1134,18 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
         if (q.ptr)
           uniform_row(q, i, acc[r], [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
         if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<long long>(iv) * n + au, acc[r], xpol);
-#ifndef QSWG_W_NO_COLMAJOR  // experiment (wrong results): cost of the column-major copy
         tile[kKR * w + r][lane] = acc[r];
-#endif
       }
-#ifndef QSWG_W_NO_COLMAJOR
-      __syncthreads();
-      const int iu = I * kKT + lane;
+      if (!m.p_rows) {  // the column-major W_k (read by P_k in the normal orientation)
+        __syncthreads();
+        const int iu = I * kKT + lane;
 #pragma unroll
-      for (int r = 0; r < kKR; ++r) {
-        const int at = J * kKT + kKR * w + r;
-        if (iu < g.n && at < g.n) st_hint(m.w[k] + static_cast<long long>(at) * n + iu, tile[lane][kKR * w + r], xpol);
+        for (int r = 0; r < kKR; ++r) {
+          const int at = J * kKT + kKR * w + r;
+          if (iu < g.n && at < g.n) st_hint(m.w[k] + static_cast<long long>(at) * n + iu, tile[lane][kKR * w + r], xpol);
+        }
+        __syncthreads();
       }
-      __syncthreads();
-#endif
     } else {
       const int iu = I * kKT + lane;
       const bool vi = iu < m.n;

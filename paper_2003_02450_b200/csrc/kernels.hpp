@@ -132,6 +132,11 @@ struct KronView {
   int* herm_flag = nullptr;
   int herm = 0;
   double2* wt[kMaxKron] = {};  // factored + Hermitian: row-major copies of W_k
+  // p_rows (factored, one GPU, padding-free P_k ELL): the Hermitian tiles
+  // apply P_k in the transposed section, P_k(j, a) W_k(i, a) = P_k(j, a)
+  // Wt_k[n i + a], lane = j, so the column-major W_k is never read (nor written).
+  int p_rows = 0;
+  KronEll p_ell[kMaxKron];
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
