@@ -920,6 +920,18 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
       }
     }
   }
+  if (m.b_rows) {  // B(j, c) X(i, c) = B(j, c) conj x[n i + c], lane = j: padding-free ELL rows of B
+    const int sl = j >> 5, ln = j & 31;
+    const KronEll& be = m.b_ell;
+    const int b = __ldg(be.sptr + sl), len = (__ldg(be.sptr + sl + 1) - b) >> 5;
+#pragma unroll 2
+    for (int e = 0; e < len; ++e) {
+      const int c = __ldg(be.col + b + 32 * e + ln);
+      const double2 v = __ldg(be.val + b + 32 * e + ln);
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) cfma(acc[r], v, conj2(ld_gather(x + static_cast<long long>(i[r]) * n + c, xpol)));
+    }
+  }
 }
 
 // Column-indexed part and diagonal terms at (i, j[r]), lane = row i.
@@ -935,7 +947,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
       uniform_rows(m.p[k], j, acc, [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
     }
   }
-  if (m.b.ptr) {  // B (x) I: coalesced columns c of X
+  if (m.b.ptr && !(kHerm && m.b_rows)) {  // B (x) I: coalesced columns c of X
     const double2* xi = x + i;
     uniform_rows(m.b, j, acc, [&](int c) { return ld_gather(xi + static_cast<long long>(c) * n, xpol); });
   }

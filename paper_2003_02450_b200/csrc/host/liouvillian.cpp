@@ -340,11 +340,13 @@ struct KronStore {
       a_list = upload_list(a0, s);
       b_list = upload_list(b0, s);
       a = maybe_ell(a0, s);
+      b_host = b0;
     } else {
       std::vector<double2> dah, dbh;
       const MultiCsr a1 = strip_diagonal(a0, dah), b1 = strip_diagonal(b0, dbh);
       a_list = upload_list(a1, s);
       b_list = upload_list(b1, s);
+      b_host = b1;
       a = maybe_ell(a1, s);
       bool any = false;
       for (std::size_t i = 0; i < dah.size(); ++i)
@@ -367,6 +369,16 @@ struct KronStore {
       p_ell.push_back(exact ? upload_ell(e, s) : dev::KronEll{});
     }
     if (const char* pr = std::getenv("QSWG_KRON_PROWS")) p_rows = p_rows && pr[0] == '1';  // experiment knob
+    // B likewise (lane = j, X(i, c) read as conj X(c, i) = conj x[n i + c]):
+    // one operand load feeds the four rows of a thread.
+    if (single && !b_host.col.empty()) {
+      const EllHost e = to_ell(b_host);
+      if (e.col.size() == b_host.col.size()) {
+        b_ell = upload_ell(e, s);
+        b_rows = true;
+      }
+    }
+    if (const char* br = std::getenv("QSWG_KRON_BROWS")) b_rows = b_rows && br[0] == '1';  // experiment knob
     if (factored) {
       af = upload_list(host.af, s);
       bf = upload_list(host.bf, s);
@@ -387,6 +399,9 @@ struct KronStore {
   std::vector<dev::KronEll> q;
   std::vector<dev::KronEll> p_ell;  // padding-free ELL copies of P_k (or empty)
   bool p_rows = false;              // Hermitian tiles apply P_k transposed (from Wt_k)
+  MultiCsr b_host;                  // B as the kernels apply it
+  dev::KronEll b_ell;               // padding-free ELL copy of B (or empty)
+  bool b_rows = false;              // Hermitian tiles apply B transposed
   bool factored = false;
   dev::KronList af, bf;
   std::vector<dev::KronList> r, sfac, u;
@@ -604,6 +619,8 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
       if (kron_->p_rows) m.kron.p_ell[k] = kron_->p_ell[static_cast<std::size_t>(k)];
     }
     m.kron.p_rows = kron_->p_rows ? 1 : 0;
+    m.kron.b_rows = kron_->b_rows ? 1 : 0;
+    m.kron.b_ell = kron_->b_rows ? kron_->b_ell : dev::KronEll{};
     m.kron.d_loc = o.d_loc;
     m.kron.d_ss = o.d_ss;
     m.kron.omega = o.omega;

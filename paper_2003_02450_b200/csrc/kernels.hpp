@@ -137,6 +137,10 @@ struct KronView {
   // Wt_k[n i + a], lane = j, so the column-major W_k is never read (nor written).
   int p_rows = 0;
   KronEll p_ell[kMaxKron];
+  // b_rows (one GPU, padding-free B ELL): B applied there too, lane = j,
+  // B(j, c) X(i, c) = B(j, c) conj x[n i + c].
+  int b_rows = 0;
+  KronEll b_ell;
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
