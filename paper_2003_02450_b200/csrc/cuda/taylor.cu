@@ -898,7 +898,8 @@ __device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows,
 __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
                                                   int j, double2* acc, unsigned long long xpol) {
   const long long n = m.n;
-  if (m.a.ptr) uniform_rows(m.a, i, acc, [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
+  if (m.a.ptr)
+    uniform_rows(m.a, i, acc, [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
   if (m.factored) {
     for (int k = 0; k < m.nk; ++k) {
       const double2* wt = m.wt[k];
