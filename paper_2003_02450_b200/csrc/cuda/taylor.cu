@@ -1250,8 +1250,15 @@ struct KronStepArgs {
   int decide;
 };
 
+// The step term's epilogue (running sum in and out, two norms) needs more
+// registers than the series term's: 3 blocks per SM (<= 80 registers) there
+// (c3, whose series is 50 sequential steps: 865 -> 825 ms), 4 for the series
+// term (c2 at 3 blocks: 35.2 -> 40.1 ms).
+#ifndef QSWG_KRON_STEP_MIN_BLOCKS
+#define QSWG_KRON_STEP_MIN_BLOCKS 3
+#endif
 template <bool kHerm>
-__global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_step_term_kernel(KronStepArgs a) {
+__global__ void __launch_bounds__(kThreads, QSWG_KRON_STEP_MIN_BLOCKS) kron_step_term_kernel(KronStepArgs a) {
   pdl_prologue();
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
