@@ -325,17 +325,15 @@ struct KronStore {
     // (one GPU: c2 47.2 vs 47.8 ms per series factored, c4 factored either way)
     factored = host.has_factored && host.kron_cost(true, single) < (single ? 0.9 : 0.8) * host.kron_cost(false);
     if (const char* f = std::getenv("QSWG_KRON_FACTOR")) factored = host.has_factored && f[0] == '1';  // test knob
-    // The diagonals of A and B both multiply X(i, j): on G-QSW operators the
-    // kernels apply them as one coefficient (A_ii + B_jj) with one gather (c2:
-    // 22 -> 20 gathers per element, exactly zero on regular graphs, then
-    // skipped; term 35.4 -> 33.9 us, series 39.8 -> 39.2 ms).  L-QSW keeps them
-    // in the lists: its decay term gathers X(i, j) already, and the split
-    // measured slower there (c5 17.17 -> 17.36 s, c3 0.88 -> 0.89 s).
-    // QSWG_KRON_DIAG=0/1 forces either form (experiment knob).
+    // The diagonals of A and B both multiply X(i, j): the kernels apply them as
+    // one coefficient (A_ii + B_jj) with one gather (c2: 22 -> 20 gathers per
+    // element, exactly zero on regular graphs, then skipped; term 35.4 -> 33.9
+    // us; with B transposed also c3 827 -> 812 ms, c5 term 2.93 -> 2.88 ms).
+    // QSWG_KRON_DIAG=0 keeps them in the lists (experiment knob).
     const MultiCsr& a0 = factored ? host.af : host.a;
     const MultiCsr& b0 = factored ? host.bf : host.b;
     const char* dk = std::getenv("QSWG_KRON_DIAG");
-    const bool split = dk ? dk[0] == '1' : host.d_loc.empty();
+    const bool split = !(dk && dk[0] == '0');
     if (!split) {
       a_list = upload_list(a0, s);
       b_list = upload_list(b0, s);
