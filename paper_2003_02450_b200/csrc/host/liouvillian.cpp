@@ -259,6 +259,19 @@ struct EllHost {
   std::vector<double2> val;
 };
 
+// Every real row of every 32-row slice equally long: the sliced ELL holds no
+// padding a kernel reads (the phantom lanes past n in the last slice are never
+// addressed: columns are clamped to n - 1).
+bool uniform_slices(const MultiCsr& m) {
+  if (m.col.empty()) return false;
+  for (std::int64_t s0 = 0; s0 < m.n; s0 += 32) {
+    const int len0 = m.ptr[static_cast<std::size_t>(s0) + 1] - m.ptr[static_cast<std::size_t>(s0)];
+    for (std::int64_t i = s0; i < std::min<std::int64_t>(m.n, s0 + 32); ++i)
+      if (m.ptr[static_cast<std::size_t>(i) + 1] - m.ptr[static_cast<std::size_t>(i)] != len0) return false;
+  }
+  return true;
+}
+
 EllHost to_ell(const MultiCsr& m) {
   EllHost e;
   const std::int64_t ns = (m.n + 31) / 32;
@@ -361,20 +374,18 @@ struct KronStore {
     // is not written at all (c2: W kernel 17.0 -> 14.9 us).
     p_rows = factored && single && !host.p.empty();
     for (const MultiCsr& pk : host.p) {
-      const EllHost e = to_ell(pk);
-      const bool exact = !pk.col.empty() && e.col.size() == pk.col.size();
+      const bool exact = uniform_slices(pk);
       p_rows = p_rows && exact;
-      p_ell.push_back(exact ? upload_ell(e, s) : dev::KronEll{});
+      p_ell.push_back(exact ? upload_ell(to_ell(pk), s) : dev::KronEll{});
     }
     if (const char* pr = std::getenv("QSWG_KRON_PROWS")) p_rows = p_rows && pr[0] == '1';  // experiment knob
     // B likewise (lane = j, X(i, c) read as conj X(c, i) = conj x[n i + c]):
     // one operand load feeds the four rows of a thread.
-    if (single && !b_host.col.empty()) {
-      const EllHost e = to_ell(b_host);
-      if (e.col.size() == b_host.col.size()) {
-        b_ell = upload_ell(e, s);
-        b_rows = true;
-      }
+    // (only after P in the per-element order A, R, P, B: B joins the transposed
+    // section when P is there too or there is no P)
+    if (single && (p_rows || host.p.empty()) && uniform_slices(b_host)) {
+      b_ell = upload_ell(to_ell(b_host), s);
+      b_rows = true;
     }
     if (const char* br = std::getenv("QSWG_KRON_BROWS")) b_rows = b_rows && br[0] == '1';  // experiment knob
     if (factored) {

@@ -124,3 +124,44 @@ def test_random_walk_parity(port, seed):
         assert np.abs(got.gather() - want).max() <= RHO_TOL * max(1.0, float(np.abs(want).max())), (seed, fmt)
         if group == 1:
             assert int(info.spmvs) == n_step
+
+
+LATTICES = [("cycle", 37), ("cycle", 64), ("cycle", 100), ("torus2d", 5), ("torus2d", 6), ("torus2d", 9),
+            ("torus3d", 3), ("torus3d", 4)]
+
+
+@pytest.mark.parametrize("kind", ["local", "global"])
+@pytest.mark.parametrize("lattice,size", LATTICES)
+def test_regular_lattice_kron_paths(port, lattice, size, kind):
+    """Regular graphs take the Hermitian tiles' transposed P / B paths (uniform
+    ELL slices, also with a partial last slice) and the merged A/B diagonal:
+    series against the oracle, and the Hermitian kernels against the general
+    ones bit for bit on the upper triangle."""
+    from paper_2003_02450_b200 import graphs
+    g = {"cycle": graphs.cycle_graph, "torus2d": graphs.torus2d, "torus3d": graphs.torus3d}[lattice](size)
+    n = g.rows
+    rng = np.random.default_rng(n * 7 + (kind == "global"))
+    omega = float(0.2 + 0.6 * rng.random())
+    h = api.generator_matrix(1.0, g).to_csr()
+    if kind == "local":
+        ml = api.local_lindblad(api.markov_chain_matrix(g)).to_csr()
+        o = port.build_local(omega, h, ml)
+        l = api.build_local(omega, h, ml, format="kron")
+    else:
+        lm = api.markov_chain_matrix(g).to_csr()
+        o = port.build_global(omega, h, [lm])
+        l = api.build_global(omega, h, [lm], format="kron")
+    p = rng.random(n)
+    v0 = rho0_vec(n, p / p.sum())
+    so, _, n_ref = o.series(v0, 0.0, 2.0, 4)
+    r = api.series(l, l.state().upload(v0), 0.0, 2.0, 4, states=True)
+    assert np.abs(r.states - so).max() <= RHO_TOL
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    x = np.ascontiguousarray((a + a.conj().T).T).reshape(-1)  # Hermitian input, column-major vec
+    y_h = l.spmv(x)
+    l.set_hermitian_mode(False)
+    y_g = l.spmv(x)
+    Yh, Yg = y_h.reshape(n, n, order="F"), y_g.reshape(n, n, order="F")
+    iu = np.triu_indices(n, 1)
+    assert np.array_equal(Yh[iu], Yg[iu])
+    assert np.array_equal(Yh, Yh.conj().T)
