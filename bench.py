@@ -321,15 +321,16 @@ def main():
         (20 B/nnz + 8 B/row) or, matrix-free, the W_k (and V_k) work vectors
         read once."""
         vec = 16 * lv.dim + 16 * lv.rows
-        if lv.format == "kron":
-            return vec + 16 * n_lind * lv.dim * (2 if lv.info.kron_factored else 1)
+        if lv.format == "kron":  # W_k and/or its row-major copy, as the kernels read them
+            return vec + 16 * n_lind * lv.dim * int(lv.info.kron_term_vectors)
         return vec + 20 * int(lv.info.nnz_local) + 8 * (lv.rows + 1)
 
     def prepare_bytes(lv):
-        """Kron prepare kernels: x read, W_k (V_k) written."""
+        """Kron prepare kernels: x read once per Lindblad term, W_k and/or its
+        row-major copy written."""
         if lv.format != "kron":
             return 0
-        return n_lind * (2 if lv.info.kron_factored else 1) * 32 * lv.dim
+        return n_lind * (1 + int(lv.info.kron_term_vectors)) * 16 * lv.dim
 
     parts = l.time_series_parts(iters=20, count=d_active)
     term_ms = parts["term"]

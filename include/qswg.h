@@ -74,6 +74,8 @@ typedef struct {
   double padding; /* stored entries / nnz_local */
   int kron_factored; /* KRON: G-QSW L'L terms applied in factored form */
   int kron_ell;      /* KRON: row-indexed operands read in sliced ELL */
+  int kron_term_vectors; /* KRON: n^2 work vectors per Lindblad term the (Hermitian-path) term
+                            kernel reads and the prepare kernel writes (roofline bytes) */
 } qswg_liouvillian_info;
 
 typedef struct { int64_t m_star, s, spmvs, launches; } qswg_step_info;

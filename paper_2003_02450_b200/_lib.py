@@ -91,7 +91,8 @@ class LiouvillianInfo(C.Structure):
     _fields_ = [("n", i64), ("dim", i64), ("nnz", i64), ("nnz_local", i64), ("row0", i64), ("rows", i64),
                 ("omega", C.c_double), ("one_norms", C.c_double * 9),
                 ("group", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("format", C.c_int), ("padding", C.c_double), ("kron_factored", C.c_int), ("kron_ell", C.c_int)]
+                ("format", C.c_int), ("padding", C.c_double), ("kron_factored", C.c_int), ("kron_ell", C.c_int),
+                ("kron_term_vectors", C.c_int)]
 
 
 class StepInfo(C.Structure):

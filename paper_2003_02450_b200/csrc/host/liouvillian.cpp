@@ -574,6 +574,14 @@ void fill_block(const dev::KronOperands& ops, const DeviceBuffer<std::int64_t>& 
 }  // namespace
 
 bool Liouvillian::kron_factored() const { return kron_ != nullptr && kron_->factored; }
+// Factored: Wt_k only when P_k is applied transposed (one GPU), else W_k and
+// Wt_k (one GPU) or W_k and V_k (row-partitioned); unfactored: W_k.
+int Liouvillian::kron_term_vectors() const {
+  if (!kron_) return 0;
+  if (!kron_->factored) return 1;
+  return kron_->p_rows && (comm_ == nullptr || comm_->world() == 1) ? 1 : 2;
+}
+int Liouvillian::kron_prepare_vectors() const { return kron_term_vectors(); }
 
 dev::DevMatrix Liouvillian::matrix(int group_override) const {
   dev::DevMatrix m;

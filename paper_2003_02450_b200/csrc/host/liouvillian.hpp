@@ -95,6 +95,11 @@ class Liouvillian {
   /// own-column panel of a row-partitioned stored superoperator.
   cudaStream_t side_stream(cudaEvent_t* ev) const;
   bool kron_factored() const;
+  /// Per Lindblad term, the n^2-vectors the Hermitian-path (one GPU) Kron
+  /// kernels touch: read by the term kernel (W_k, Wt_k) and written by the
+  /// prepare kernel (roofline byte counts).
+  int kron_term_vectors() const;
+  int kron_prepare_vectors() const;
   bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
 
   /// Local row block downloaded as CSR with global columns (parity / debug).
