@@ -903,8 +903,27 @@ __device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows,
 __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
                                                   int j, double2* acc, unsigned long long xpol) {
   const long long n = m.n;
-  if (m.a.ptr)
+  if (m.a_len > 0) {
+    // rows i[r] = I*32 + 4w + r: lanes 4w .. 4w+3 of ELL slice I (clamped edge rows read
+    // that slice's padding lanes, whose results are discarded)
+    const KronEll& ae = m.a_ellu;
+    const int lane = threadIdx.x & 31, sl = i[0] >> 5, l0 = (threadIdx.x >> 5) * kKR;
+    const int base = __ldg(ae.sptr + sl);
+    const int len = m.a_len;
+    const int kt = lane >> 2, rt = lane & 3;
+    const int mycol = kt < len ? __ldg(ae.col + base + 32 * kt + l0 + rt) : 0;
+#pragma unroll 2
+    for (int k = 0; k < len; ++k) {
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const int c = __shfl_sync(0xffffffffu, mycol, kKR * k + r);
+        const double2 v = __ldg(ae.val + base + 32 * k + l0 + r);
+        cfma(acc[r], v, conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)));
+      }
+    }
+  } else if (m.a.ptr) {
     uniform_rows(m.a, i, acc, [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
+  }
   if (m.factored) {
     for (int k = 0; k < m.nk; ++k) {
       const double2* wt = m.wt[k];

@@ -351,12 +351,14 @@ struct KronStore {
       a_list = upload_list(a0, s);
       b_list = upload_list(b0, s);
       a = maybe_ell(a0, s);
+      a_host = a0;
       b_host = b0;
     } else {
       std::vector<double2> dah, dbh;
       const MultiCsr a1 = strip_diagonal(a0, dah), b1 = strip_diagonal(b0, dbh);
       a_list = upload_list(a1, s);
       b_list = upload_list(b1, s);
+      a_host = a1;
       b_host = b1;
       a = maybe_ell(a1, s);
       bool any = false;
@@ -383,6 +385,15 @@ struct KronStore {
     // one operand load feeds the four rows of a thread.
     // (only after P in the per-element order A, R, P, B: B joins the transposed
     // section when P is there too or there is no P)
+    // A (transposed, rows i warp-uniform): with uniform ELL slices of at most 8
+    // entries, the four rows of a thread are consecutive lanes of one slice,
+    // so a warp fetches all their column indices in one load and hands them
+    // out by shuffle (the index -> gather chain starts without an L1 round trip).
+    if (const char* ash = std::getenv("QSWG_KRON_ASHFL"); single && !(ash && ash[0] == '0') &&
+        uniform_slices(a_host) && a_host.ptr[1] - a_host.ptr[0] <= 8) {
+      a_ellu = upload_ell(to_ell(a_host), s);
+      a_len = a_host.ptr[1] - a_host.ptr[0];
+    }
     if (single && (p_rows || host.p.empty()) && uniform_slices(b_host)) {
       b_ell = upload_ell(to_ell(b_host), s);
       b_rows = true;
@@ -408,7 +419,9 @@ struct KronStore {
   std::vector<dev::KronEll> q;
   std::vector<dev::KronEll> p_ell;  // padding-free ELL copies of P_k (or empty)
   bool p_rows = false;              // Hermitian tiles apply P_k transposed (from Wt_k)
-  MultiCsr b_host;                  // B as the kernels apply it
+  MultiCsr a_host, b_host;          // A and B as the kernels apply them
+  dev::KronEll a_ellu;              // uniform-slice ELL copy of A (or empty)
+  int a_len = 0;                    // its row length (<= 8) when the shuffle path is on
   dev::KronEll b_ell;               // padding-free ELL copy of B (or empty)
   bool b_rows = false;              // Hermitian tiles apply B transposed
   bool factored = false;
@@ -637,6 +650,8 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     }
     m.kron.p_rows = kron_->p_rows ? 1 : 0;
     m.kron.b_rows = kron_->b_rows ? 1 : 0;
+    m.kron.a_len = kron_->a_len;
+    m.kron.a_ellu = kron_->a_ellu;
     m.kron.b_ell = kron_->b_rows ? kron_->b_ell : dev::KronEll{};
     m.kron.d_loc = o.d_loc;
     m.kron.d_ss = o.d_ss;

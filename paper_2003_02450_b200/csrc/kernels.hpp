@@ -141,6 +141,11 @@ struct KronView {
   // B(j, c) X(i, c) = B(j, c) conj x[n i + c].
   int b_rows = 0;
   KronEll b_ell;
+  // a_len > 0 (one GPU, uniform A slices of a_len <= 8 entries): the
+  // transposed A part fetches its four rows' column indices with one warp load
+  // and shuffles them out.
+  int a_len = 0;
+  KronEll a_ellu;
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
