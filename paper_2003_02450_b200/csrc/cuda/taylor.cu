@@ -897,37 +897,51 @@ __device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows,
   for (int r = 0; r < kKR; ++r) uniform_row(l, rows[r], acc[r], g);
 }
 
+// acc[r] += sum_k E(row0 + r, k) g(col) over the kKR consecutive rows row0 ..
+// row0 + 3 (row0 = 32 slice + l0) of a uniform-slice ELL operand of len <= 8
+// entries per row: one warp load fetches all their column indices, which are
+// shuffled out, so the index -> gather chain skips an L1 round trip.  The
+// entries of each row are added in their stored order.
+template <class G>
+__device__ __forceinline__ void shfl_rows(const KronEll& e, int len, int slice, int l0, double2* acc, G&& g) {
+  const int lane = threadIdx.x & 31;
+  const int base = __ldg(e.sptr + slice);
+  const int kt = lane >> 2, rt = lane & 3;
+  const int mycol = kt < len ? __ldg(e.col + base + 32 * kt + l0 + rt) : 0;
+#pragma unroll 2
+  for (int k = 0; k < len; ++k) {
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const int c = __shfl_sync(0xffffffffu, mycol, kKR * k + r);
+      cfma(acc[r], __ldg(e.val + base + 32 * k + l0 + r), g(c));
+    }
+  }
+}
+
 // Row-indexed part, transposed (Hermitian path): acc[r] at (i[r], j), warp-
 // uniform rows i[r], lane = column j: A from conj X(j, c), R_k from the
 // row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).
 __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
                                                   int j, double2* acc, unsigned long long xpol) {
   const long long n = m.n;
+  // rows i[r] = I*32 + 4w + r: lanes 4w .. 4w+3 of ELL slice I (clamped edge rows read
+  // that slice's padding lanes, whose results are discarded)
+  const int sl = i[0] >> 5, l0 = (threadIdx.x >> 5) * kKR;
   if (m.a_len > 0) {
-    // rows i[r] = I*32 + 4w + r: lanes 4w .. 4w+3 of ELL slice I (clamped edge rows read
-    // that slice's padding lanes, whose results are discarded)
-    const KronEll& ae = m.a_ellu;
-    const int lane = threadIdx.x & 31, sl = i[0] >> 5, l0 = (threadIdx.x >> 5) * kKR;
-    const int base = __ldg(ae.sptr + sl);
-    const int len = m.a_len;
-    const int kt = lane >> 2, rt = lane & 3;
-    const int mycol = kt < len ? __ldg(ae.col + base + 32 * kt + l0 + rt) : 0;
-#pragma unroll 2
-    for (int k = 0; k < len; ++k) {
-#pragma unroll
-      for (int r = 0; r < kKR; ++r) {
-        const int c = __shfl_sync(0xffffffffu, mycol, kKR * k + r);
-        const double2 v = __ldg(ae.val + base + 32 * k + l0 + r);
-        cfma(acc[r], v, conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)));
-      }
-    }
+    shfl_rows(m.a_ellu, m.a_len, sl, l0, acc,
+              [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
   } else if (m.a.ptr) {
     uniform_rows(m.a, i, acc, [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
   }
   if (m.factored) {
     for (int k = 0; k < m.nk; ++k) {
       const double2* wt = m.wt[k];
-      uniform_rows(m.r[k], i, acc, [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
+      if (m.r_len[k] > 0) {
+        shfl_rows(m.r_ellu[k], m.r_len[k], sl, l0, acc,
+                  [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
+      } else {
+        uniform_rows(m.r[k], i, acc, [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
+      }
     }
   }
   if (m.p_rows) {  // P_k(j, a) W_k(i, a), lane = j: padding-free ELL rows of P_k, rows i of Wt_k
@@ -980,7 +994,12 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
     if (m.factored) {  // -w/2 (X L') L: columns of V_k
       if constexpr (kHerm) {
         const double2* vi = m.wt[k] + i;
-        uniform_rows(m.s[k], j, acc, [&](int c) { return conj2(ld_gather(vi + static_cast<long long>(c) * n, xpol)); });
+        if (m.s_len[k] > 0) {  // rows j[r] = J*32 + 4w + r: lanes 4w .. 4w+3 of slice J
+          shfl_rows(m.s_ellu[k], m.s_len[k], j[0] >> 5, (threadIdx.x >> 5) * kKR, acc,
+                    [&](int c) { return conj2(ld_gather(vi + static_cast<long long>(c) * n, xpol)); });
+        } else {
+          uniform_rows(m.s[k], j, acc, [&](int c) { return conj2(ld_gather(vi + static_cast<long long>(c) * n, xpol)); });
+        }
       } else {
         const double2* vi = m.v[k] + i;
         uniform_rows(m.s[k], j, acc, [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
@@ -1164,11 +1183,16 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
     if constexpr (kHerm) {
       const int au = J * kKT + lane;  // column a (single GPU: c0 = 0)
       const int a = au < g.n ? au : g.n - 1;
+      if (m.q_len[k] > 0) {  // rows I*32 + 4w + r: lanes 4w .. 4w+3 of slice I
+        const int iv0 = I * kKT + kKR * w;
+        shfl_rows(m.q_ellu[k], m.q_len[k], (iv0 < g.n ? iv0 : g.n - 1) >> 5, kKR * w, acc,
+                  [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
+      }
 #pragma unroll
       for (int r = 0; r < kKR; ++r) {
         const int iv = I * kKT + kKR * w + r;
         const int i = iv < g.n ? iv : g.n - 1;
-        if (q.ptr)
+        if (q.ptr && m.q_len[k] == 0)
           uniform_row(q, i, acc[r], [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
         if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<long long>(iv) * n + au, acc[r], xpol);
         tile[kKR * w + r][lane] = acc[r];

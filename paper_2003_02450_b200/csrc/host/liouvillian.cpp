@@ -389,10 +389,32 @@ struct KronStore {
     // entries, the four rows of a thread are consecutive lanes of one slice,
     // so a warp fetches all their column indices in one load and hands them
     // out by shuffle (the index -> gather chain starts without an L1 round trip).
-    if (const char* ash = std::getenv("QSWG_KRON_ASHFL"); single && !(ash && ash[0] == '0') &&
-        uniform_slices(a_host) && a_host.ptr[1] - a_host.ptr[0] <= 8) {
+    const char* ash = std::getenv("QSWG_KRON_ASHFL");  // experiment knob: 0 = no shuffled operand rows
+    if (single && !(ash && ash[0] == '0') && uniform_slices(a_host) && a_host.ptr[1] - a_host.ptr[0] <= 8) {
       a_ellu = upload_ell(to_ell(a_host), s);
       a_len = a_host.ptr[1] - a_host.ptr[0];
+    }
+    for (std::size_t k = 0; k < host.q.size(); ++k) {  // Q_k, and R_k / S_k when factored
+      const auto shfl = [&](const MultiCsr& m, dev::KronEll& e, int& len) {
+        if (!single || (ash && ash[0] == '0') || !uniform_slices(m) || m.ptr[1] - m.ptr[0] > 8) return;
+        e = upload_ell(to_ell(m), s);
+        len = m.ptr[1] - m.ptr[0];
+      };
+      dev::KronEll e;
+      int len = 0;
+      shfl(host.q[k], e, len);
+      q_ellu.push_back(e);
+      q_len.push_back(len);
+      dev::KronEll er, es;
+      int lr = 0, ls = 0;
+      if (factored) {
+        shfl(host.r[k], er, lr);
+        shfl(host.sfac[k], es, ls);
+      }
+      r_ellu.push_back(er);
+      r_len.push_back(lr);
+      s_ellu.push_back(es);
+      s_len.push_back(ls);
     }
     if (single && (p_rows || host.p.empty()) && uniform_slices(b_host)) {
       b_ell = upload_ell(to_ell(b_host), s);
@@ -422,6 +444,8 @@ struct KronStore {
   MultiCsr a_host, b_host;          // A and B as the kernels apply them
   dev::KronEll a_ellu;              // uniform-slice ELL copy of A (or empty)
   int a_len = 0;                    // its row length (<= 8) when the shuffle path is on
+  std::vector<dev::KronEll> q_ellu, r_ellu, s_ellu;  // the same for Q_k, R_k, S_k
+  std::vector<int> q_len, r_len, s_len;
   dev::KronEll b_ell;               // padding-free ELL copy of B (or empty)
   bool b_rows = false;              // Hermitian tiles apply B transposed
   bool factored = false;
@@ -652,6 +676,14 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.b_rows = kron_->b_rows ? 1 : 0;
     m.kron.a_len = kron_->a_len;
     m.kron.a_ellu = kron_->a_ellu;
+    for (std::size_t k = 0; k < kron_->q_len.size(); ++k) {
+      m.kron.q_len[k] = kron_->q_len[k];
+      m.kron.q_ellu[k] = kron_->q_ellu[k];
+      m.kron.r_len[k] = kron_->r_len[k];
+      m.kron.r_ellu[k] = kron_->r_ellu[k];
+      m.kron.s_len[k] = kron_->s_len[k];
+      m.kron.s_ellu[k] = kron_->s_ellu[k];
+    }
     m.kron.b_ell = kron_->b_rows ? kron_->b_ell : dev::KronEll{};
     m.kron.d_loc = o.d_loc;
     m.kron.d_ss = o.d_ss;

@@ -146,6 +146,10 @@ struct KronView {
   // and shuffles them out.
   int a_len = 0;
   KronEll a_ellu;
+  // The same for R_k and S_k (factored) and Q_k (Hermitian W kernel): uniform
+  // ELL slices of r_len / s_len / q_len <= 8 entries (0: the CSR rows).
+  int r_len[kMaxKron] = {}, s_len[kMaxKron] = {}, q_len[kMaxKron] = {};
+  KronEll r_ellu[kMaxKron], s_ellu[kMaxKron], q_ellu[kMaxKron];
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
