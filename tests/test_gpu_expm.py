@@ -214,6 +214,11 @@ def test_regular_graph_coherence_death():  # acceptance_main.cpp:293-308
     rho = w.gather_result()
     off = rho - np.diag(np.diag(rho))
     assert np.abs(off).max() <= 1e-8
+    # the device coherence norm (run()'s "coherence_norm") tells the same story
+    r = w.series(0.0, 100.0, 10, coherence=True)
+    assert r.coherence[0] == 0.0 and r.coherence[-1] <= 1e-8
+    assert np.all(np.diff(r.coherence[1:]) < 0)  # coherences die out monotonically here
+    assert abs(r.coherence[-1] - np.abs(off).max()) <= 1e-12
 
 
 def test_dense_initial_state_and_set_omega():  # walk.hpp:57-66, walk.cpp:141-145
