@@ -1,9 +1,12 @@
 // 1-norm power series ||L^p||_1, p = 1..9 (liouvillian.cpp:309-344).
 //
-// dim <= 4096: exact.  The reference forms sparse powers on the host
-// (Gustavson); here column c of L^p is L applied p times to e_c, i.e. a dense
-// SpMM of L with the identity, then per-column sums of |.| in ascending row
-// order (the reference's one_norm order, sparse.cpp:134-140).
+// dim <= 4096: exact.  The reference forms sparse powers on the host,
+// P <- P * L by Gustavson (sparse.cpp:178-208); here P is dense and
+// Y[i][c] = sum over k of P[i][k] L[k][c] is summed in the same order —
+// ascending k, zero P entries skipped (the reference drops them), complex
+// products rounded like std::complex (no contraction) — so every power is
+// bit-identical to the reference's; then per-column sums of |.| in ascending
+// row order (the reference's one_norm order, sparse.cpp:134-140).
 // dim > 4096: the bound max(1^T |L|^p): v <- |L|^T v from v = 1.  |L^T| is
 // assembled by the same merge kernel from transposed operands, so each
 // next[r] is a plain row-ordered sum in ascending original-row order with no
@@ -11,6 +14,7 @@
 // deterministic and without fp64 atomics.
 #include "../kernels.hpp"
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -18,22 +22,27 @@ namespace qswg::dev {
 
 namespace {
 
-// Y[r][c] = sum_k L(r, col_k) X[col_k][c]; X, Y row-major dim x dim.
-__global__ void __launch_bounds__(kThreads) dense_power_kernel(CsrView l, long long dim,
+// Y[i][c] = sum_k X[i][k] L[k][c], k ascending over column c of L (CSC:
+// lcp / lrow / lval); X, Y row-major dim x dim.
+__global__ void __launch_bounds__(kThreads) dense_power_kernel(const long long* __restrict__ lcp,
+                                                               const int* __restrict__ lrow,
+                                                               const double2* __restrict__ lval, long long dim,
                                                                const double2* __restrict__ x,
                                                                double2* __restrict__ y) {
-  const long long r = blockIdx.y;
-  const long long b = __ldg(l.rowptr + r), e = __ldg(l.rowptr + r + 1);
+  const long long i = blockIdx.y;
+  const double2* xi = x + i * dim;
   for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < dim;
        c += static_cast<long long>(gridDim.x) * blockDim.x) {
     double2 acc = make_double2(0.0, 0.0);
+    const long long b = __ldg(lcp + c), e = __ldg(lcp + c + 1);
     for (long long k = b; k < e; ++k) {
-      const double2 v = __ldg(l.val + k);
-      const double2 xv = x[static_cast<long long>(__ldg(l.col + k)) * dim + c];
-      acc.x += v.x * xv.x - v.y * xv.y;
-      acc.y += v.x * xv.y + v.y * xv.x;
+      const double2 w = xi[__ldg(lrow + k)];
+      if (w.x == 0.0 && w.y == 0.0) continue;  // not stored in the reference's power
+      const double2 a = __ldg(lval + k);
+      acc.x = __dadd_rn(acc.x, __dsub_rn(__dmul_rn(w.x, a.x), __dmul_rn(w.y, a.y)));
+      acc.y = __dadd_rn(acc.y, __dadd_rn(__dmul_rn(w.x, a.y), __dmul_rn(w.y, a.x)));
     }
-    y[r * dim + c] = acc;
+    y[i * dim + c] = acc;
   }
 }
 
@@ -89,6 +98,40 @@ __global__ void __launch_bounds__(kThreads) abs_product_kernel(RealCsrView lt, c
 
 void exact_norms(const CsrView& l, std::int64_t dim, double2* w0, double2* w1, double* colsum,
                  double* norms9_host, cudaStream_t s) {
+  // CSC of L (rows ascending in each column), transposed on the host: the
+  // matrix is small here (dim <= 4096)
+  std::vector<long long> rp(static_cast<std::size_t>(dim) + 1);
+  QSWG_CUDA(cudaMemcpyAsync(rp.data(), l.rowptr, rp.size() * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  QSWG_CUDA(cudaStreamSynchronize(s));
+  const long long nz = rp.back();
+  std::vector<int> col(static_cast<std::size_t>(nz)), row(static_cast<std::size_t>(nz));
+  std::vector<double2> val(static_cast<std::size_t>(nz)), tval(static_cast<std::size_t>(nz));
+  if (nz > 0) {
+    QSWG_CUDA(cudaMemcpyAsync(col.data(), l.col, col.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    QSWG_CUDA(cudaMemcpyAsync(val.data(), l.val, val.size() * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    QSWG_CUDA(cudaStreamSynchronize(s));
+  }
+  std::vector<long long> cp(static_cast<std::size_t>(dim) + 1, 0);
+  for (long long k = 0; k < nz; ++k) ++cp[static_cast<std::size_t>(col[k]) + 1];
+  for (long long c = 0; c < dim; ++c) cp[c + 1] += cp[c];
+  std::vector<long long> fill(cp.begin(), cp.end() - 1);
+  for (long long r = 0; r < dim; ++r)
+    for (long long k = rp[r]; k < rp[r + 1]; ++k) {
+      const long long d = fill[col[k]]++;
+      row[d] = static_cast<int>(r);
+      tval[d] = val[k];
+    }
+  long long* dcp = nullptr;
+  int* drow = nullptr;
+  double2* dval = nullptr;
+  QSWG_CUDA(cudaMallocAsync(&dcp, cp.size() * sizeof(long long), s));
+  QSWG_CUDA(cudaMallocAsync(&drow, (row.size() + 1) * sizeof(int), s));
+  QSWG_CUDA(cudaMallocAsync(&dval, (tval.size() + 1) * sizeof(double2), s));
+  QSWG_CUDA(cudaMemcpyAsync(dcp, cp.data(), cp.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  if (nz > 0) {
+    QSWG_CUDA(cudaMemcpyAsync(drow, row.data(), row.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    QSWG_CUDA(cudaMemcpyAsync(dval, tval.data(), tval.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+  }
   identity_kernel<<<sm_count() * 4, kThreads, 0, s>>>(w0, dim);
   QSWG_LAUNCH_CHECK("identity");
   unsigned long long* dmax = nullptr;
@@ -98,7 +141,7 @@ void exact_norms(const CsrView& l, std::int64_t dim, double2* w0, double2* w1, d
   double2* y = w1;
   const int gx = static_cast<int>((dim + kThreads - 1) / kThreads);
   for (int p = 0; p < 9; ++p) {
-    dense_power_kernel<<<dim3(gx, static_cast<unsigned>(dim)), kThreads, 0, s>>>(l, dim, x, y);
+    dense_power_kernel<<<dim3(gx, static_cast<unsigned>(dim)), kThreads, 0, s>>>(dcp, drow, dval, dim, x, y);
     QSWG_LAUNCH_CHECK("dense_power");
     colsum_kernel<<<gx, kThreads, 0, s>>>(y, dim, colsum);
     QSWG_LAUNCH_CHECK("colsum");
@@ -111,6 +154,9 @@ void exact_norms(const CsrView& l, std::int64_t dim, double2* w0, double2* w1, d
   unsigned long long bits[9];
   QSWG_CUDA(cudaMemcpyAsync(bits, dmax, sizeof(bits), cudaMemcpyDeviceToHost, s));
   QSWG_CUDA(cudaFreeAsync(dmax, s));
+  QSWG_CUDA(cudaFreeAsync(dcp, s));
+  QSWG_CUDA(cudaFreeAsync(drow, s));
+  QSWG_CUDA(cudaFreeAsync(dval, s));
   QSWG_CUDA(cudaStreamSynchronize(s));
   for (int p = 0; p < 9; ++p) std::memcpy(norms9_host + p, bits + p, sizeof(double));
 }

@@ -5,7 +5,14 @@ every format and both arithmetic modes, against the pinned C oracle.
 
 Bar: rho at every output <= 1e-10 elementwise (the north-star tolerance);
 identical SpMV counts in the bitwise mode (group = 1), which reproduces the
-reference's arithmetic; step agrees the same way."""
+reference's arithmetic, whenever the assembled superoperator is bit-identical
+to the oracle's; step agrees the same way.  With several Lindblad operators
+the duplicate contributions of an entry are summed in the device merge's
+stream order, the reference's in its triplet sort's (unstable) order, so such
+entries can differ in the last bit and a stop test that sits on the knife edge
+c1 + c2 = tol * ||F|| may then take one term more or less (seen on seed 33 of
+an 84-seed sweep: 343 vs 342 step terms, states equal to 1.4e-16); there the
+counts must agree to within one term per stage / output."""
 import numpy as np
 import pytest
 
@@ -105,25 +112,27 @@ def build_gpu(inst, fmt, group):
     return api.build_global(inst["omega"], inst["h"], inst["ls"], inst["hrot"], group=group, format=fmt)
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", list(range(24)) + [33])
 def test_random_walk_parity(port, seed):
     inst = instance(seed)
     t1, tq, q = inst["times"]
     o = build_oracle(port, inst)
     so, po, n_ref = o.series(inst["v0"], t1, tq, q)
     want, n_step = o.step(inst["v0"], tq)
+    L_ref = o.csr()
     for fmt, group in MODES:
         l = build_gpu(inst, fmt, group)
         np.testing.assert_allclose(l.one_norms(), o.norms, rtol=1e-12, atol=1e-300)
         r = api.series(l, l.state().upload(inst["v0"]), t1, tq, q, states=True)
         err = float(np.abs(r.states - so).max())
         assert err <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, group, err)
-        if group == 1:
-            assert int(r.info.spmvs) == n_ref, (seed, fmt, r.info.spmvs, n_ref)
         got, info = api.step(l, l.state().upload(inst["v0"]), tq)
         assert np.abs(got.gather() - want).max() <= RHO_TOL * max(1.0, float(np.abs(want).max())), (seed, fmt)
         if group == 1:
-            assert int(info.spmvs) == n_step
+            same_L = bool(np.array_equal(l.gather_full().data, L_ref.data))
+            slack_series, slack_step = (0, 0) if same_L else (q, int(info.s))
+            assert abs(int(r.info.spmvs) - n_ref) <= slack_series, (seed, fmt, r.info.spmvs, n_ref, same_L)
+            assert abs(int(info.spmvs) - n_step) <= slack_step, (seed, fmt, info.spmvs, n_step, same_L)
 
 
 LATTICES = [("cycle", 37), ("cycle", 64), ("cycle", 100), ("torus2d", 5), ("torus2d", 6), ("torus2d", 9),
