@@ -174,3 +174,33 @@ def test_regular_lattice_kron_paths(port, lattice, size, kind):
     iu = np.triu_indices(n, 1)
     assert np.array_equal(Yh[iu], Yg[iu])
     assert np.array_equal(Yh, Yh.conj().T)
+
+
+def _build_sharded(inst, fmt, comm):
+    if inst["kind"] == "local":
+        return api.build_local(inst["omega"], inst["h"], inst["ml"], inst["src"], inst["snk"], format=fmt, comm=comm)
+    return api.build_global(inst["omega"], inst["h"], inst["ls"], inst["hrot"], format=fmt, comm=comm)
+
+
+SHARD_SEEDS = [s for s in range(40) if instance(s)["N"] >= 8][:10]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fmt", ["kron", "sell"])
+@pytest.mark.parametrize("seed", SHARD_SEEDS)
+def test_random_walk_sharded(port, seed, fmt, world):
+    """The random walks on row-partitioned in-process ranks (halo exchanges,
+    distributed norms and stop tests) against the C oracle."""
+    from test_gpu_multirank import run_ranks
+    inst = instance(seed)
+    t1, tq, q = inst["times"]
+    so, _, _ = build_oracle(port, inst).series(inst["v0"], t1, tq, q)
+
+    def rank_fn(r, comm):
+        l = _build_sharded(inst, fmt, comm)
+        res = api.series(l, l.state().upload(inst["v0"]), t1, tq, q, states=True)
+        return l.row0, res.states
+
+    parts = sorted(run_ranks(world, rank_fn), key=lambda p: p[0])
+    states = np.concatenate([p[1] for p in parts], axis=1)
+    assert np.abs(states - so).max() <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, world)
