@@ -76,6 +76,8 @@ typedef struct {
   int kron_ell;      /* KRON: row-indexed operands read in sliced ELL */
   int kron_term_vectors; /* KRON: n^2 work vectors per Lindblad term the (Hermitian-path) term
                             kernel reads and the prepare kernel writes (roofline bytes) */
+  int sell_panels;    /* SELL: column panels of the stored superoperator (1 = one pass; 0 other formats) */
+  int kron_hermitian; /* KRON: the last product / step / series ran the Hermitian tile kernels */
 } qswg_liouvillian_info;
 
 typedef struct { int64_t m_star, s, spmvs, launches; } qswg_step_info;

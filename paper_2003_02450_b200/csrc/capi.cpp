@@ -363,6 +363,8 @@ int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* inf
     info->kron_factored = L.kron_factored() ? 1 : 0;
     info->kron_ell = L.kron_ell() ? 1 : 0;
     info->kron_term_vectors = L.kron_term_vectors();
+    info->sell_panels = L.format() == qswg::dev::Format::Sell ? L.sell_panels() : 0;
+    info->kron_hermitian = L.matrix().kron.herm;
   });
 }
 
@@ -632,8 +634,12 @@ int qswg_series_observe(const qswg_liouvillian* l, const qswg_state* v, double t
     };
     // populations only: every emit is a device kernel into lm->pops, so a
     // repeated identical call may replay a captured graph (expm.hpp: series)
-    const void* graph_key =
-        (states_host || final_state) ? nullptr : (coherence_host ? static_cast<const void*>(lm->coh.get()) : lm->pops.get());
+    // (both targets are in the key: either buffer may be reallocated between calls)
+    std::vector<const void*> graph_key;
+    if (!states_host && !final_state) {
+      graph_key.push_back(lm->pops.get());
+      if (coherence_host) graph_key.push_back(lm->coh.get());
+    }
     const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit, graph_key);
     if (L.comm() && L.comm()->world() > 1)  // every diagonal element has exactly one owner
       L.comm()->allreduce_sum_f64(lm->pops.get(), static_cast<std::size_t>((steps + 1) * n), s);

@@ -401,7 +401,8 @@ struct SeriesGraph {
 
 SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
                   const TaylorParameters& params,
-                  const std::function<void(std::int64_t, const double2*)>& emit, const void* graph_key) {
+                  const std::function<void(std::int64_t, const double2*)>& emit,
+                  const std::vector<const void*>& graph_key) {
   // expm.cpp:216-217
   if (!(tq > t1)) throw std::invalid_argument("series requires tq > t1");
   if (steps < 1) throw std::invalid_argument("series requires at least one step");
@@ -414,14 +415,14 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
     return e != nullptr && e[0] == '0';
   }();
   SeriesInfo info;
-  if (ex.single && graph_key != nullptr && !graphs_off) {
+  if (ex.single && !graph_key.empty() && !graphs_off) {
     Workspace& ws = l.workspace();
     if (!ws.series_graph) ws.series_graph = std::make_shared<SeriesGraph>();
     auto* gr = static_cast<SeriesGraph*>(ws.series_graph.get());
-    const std::vector<double> key = {static_cast<double>(reinterpret_cast<std::uintptr_t>(v)), t1, tq,
-                                     static_cast<double>(steps), params.tolerance,
-                                     static_cast<double>(reinterpret_cast<std::uintptr_t>(graph_key)),
-                                     static_cast<double>(l.matrix().kron.herm), static_cast<double>(series_pend_max(ex.dim))};
+    std::vector<double> key = {static_cast<double>(reinterpret_cast<std::uintptr_t>(v)), t1, tq,
+                               static_cast<double>(steps), params.tolerance,
+                               static_cast<double>(l.matrix().kron.herm), static_cast<double>(series_pend_max(ex.dim))};
+    for (const void* b : graph_key) key.push_back(static_cast<double>(reinterpret_cast<std::uintptr_t>(b)));
     if (SeriesGraph::Entry* e = gr->find(key)) {
       QSWG_CHECK(cudaGraphLaunch(e->exec, s));
       info = e->info;

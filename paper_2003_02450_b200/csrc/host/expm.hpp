@@ -9,6 +9,7 @@
 
 #include <array>
 #include <functional>
+#include <vector>
 
 #include "liouvillian.hpp"
 #include "taylor.hpp"
@@ -41,15 +42,16 @@ StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorPara
 /// output is handed to `emit(k, state)` as a device pointer valid until the
 /// call returns (stream-ordered: enqueue copies on l.stream()).
 ///
-/// `graph_key` != nullptr declares that `emit` only enqueues stream-ordered
-/// device work whose targets are identified by graph_key; then a one-GPU call
-/// that repeats the previous call exactly (same v, times, tolerance, graph_key
-/// and Hermitian mode) is captured once into a CUDA graph and replayed by
+/// A non-empty `graph_key` declares that `emit` only enqueues stream-ordered
+/// device work whose targets are exactly the buffers listed in graph_key; then
+/// a one-GPU call that repeats the previous call exactly (same v, times,
+/// tolerance, graph_key buffers and Hermitian mode) is captured once into a CUDA graph and replayed by
 /// later identical calls — the same kernels with the same arguments, minus the
 /// per-launch host overhead (QSWG_GRAPH=0 disables).
 SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
                   const TaylorParameters& params,
-                  const std::function<void(std::int64_t, const double2*)>& emit, const void* graph_key = nullptr);
+                  const std::function<void(std::int64_t, const double2*)>& emit,
+                  const std::vector<const void*>& graph_key = {});
 
 /// Mean device time (ms) of one fused series-term launch with `count`
 /// active outputs (p > 1 traffic: K read, K write, count sums read+write),
