@@ -34,6 +34,15 @@ constexpr int kTile = kThreads;  // rows per block tile
 
 __device__ __forceinline__ double cabs2(double2 v) { return hypot(v.x, v.y); }
 
+// m = max(m, bits of |v|) with |v| = hypot as std::abs (expm.cpp:167, 182-183),
+// evaluated only when it can raise the maximum: hypot(x, y) <= |x| + |y|
+// (and CUDA's hypot is within 2 ulp), so an element with
+// (|x| + |y|)(1 + 2^-48) <= max cannot change it.  NaN/Inf fail the test and
+// reach hypot, so non-finite values are still flagged.
+__device__ __forceinline__ void max_abs_bits(unsigned long long& m, double2 v) {
+  if (!((fabs(v.x) + fabs(v.y)) * (1.0 + 0x1p-48) <= bitsd(m))) m = umax64(m, dbits(cabs2(v)));
+}
+
 // Sum of one row, computed by the G lanes of a group; every lane returns the
 // full sum.  G == 1 is the bitwise "reference order" mode: one thread per
 // row, columns in CSR order, every product and sum rounded separately (no
@@ -192,8 +201,8 @@ __global__ void __launch_bounds__(kThreads) step_term_kernel(StepTermArgs a) {
     st_hint(a.y + row, yv, keep);  // next term's SpMV input
     const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
     st_hint(a.sum_out + row, sv, once);
-    tmax = umax64(tmax, dbits(cabs2(yv)));
-    smax = umax64(smax, dbits(cabs2(sv)));
+    max_abs_bits(tmax, yv);
+    max_abs_bits(smax, sv);
   });
   pdl_trigger();
   tmax = block_max_bits(tmax, red);
@@ -368,7 +377,7 @@ __device__ __forceinline__ void series_store(double2* kp, double scale, long lon
   if (!valid) return;
   const double2 kv = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   st_hint(kp + row, kv, keep);
-  tmax = umax64(tmax, dbits(cabs2(kv)));
+  max_abs_bits(tmax, kv);
 }
 
 // Grid-wide ||K_p|| and the term control (last block).
@@ -769,8 +778,8 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
     st_hint(a.y + row, yv, keep);
     const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
     st_hint(a.sum_out + row, sv, once);
-    tmax = umax64(tmax, dbits(cabs2(yv)));
-    smax = umax64(smax, dbits(cabs2(sv)));
+    max_abs_bits(tmax, yv);
+    max_abs_bits(smax, sv);
   });
   pdl_trigger();
   tmax = block_max_bits(tmax, red);
@@ -838,63 +847,122 @@ __device__ __forceinline__ void cfma(double2& acc, double2 v, double2 xv) {
 }
 __device__ __forceinline__ double2 conj2(double2 v) { return make_double2(v.x, -v.y); }
 
+// Operand value classes (KronView::vk_*).  Every operand of the BASELINE
+// configs is purely real (R_k, P_k, S_k, Q_k, T) or purely imaginary (A, B
+// and their diagonals: the coherent -i(1-w)H parts): those multiply with 2
+// FMAs instead of 4 and load 8 bytes instead of 16.  The products dropped are
+// exact zeros, so every class gives the complex formula's values.
+template <int K>
+__device__ __forceinline__ double2 ldv(const double2* p) {
+  if constexpr (K == kValReal) {
+    return make_double2(__ldg(&p->x), 0.0);
+  } else if constexpr (K == kValImag) {
+    return make_double2(0.0, __ldg(&p->y));
+  } else {
+    return __ldg(p);
+  }
+}
+template <int K>
+__device__ __forceinline__ void cfmak(double2& acc, double2 v, double2 xv) {
+  if constexpr (K == kValReal) {
+    acc.x = fma(v.x, xv.x, acc.x);
+    acc.y = fma(v.x, xv.y, acc.y);
+  } else if constexpr (K == kValImag) {
+    acc.x = fma(-v.y, xv.y, acc.x);
+    acc.y = fma(v.y, xv.x, acc.y);
+  } else {
+    cfma(acc, v, xv);
+  }
+}
+template <int K>
+using ValK = std::integral_constant<int, K>;
+// f(ValK<class>{}) for the runtime (warp-uniform) class k.
+template <class F>
+__device__ __forceinline__ void by_kind(int k, F&& f) {
+  if (k == kValReal) {
+    f(ValK<kValReal>{});
+  } else if (k == kValImag) {
+    f(ValK<kValImag>{});
+  } else {
+    f(ValK<kValComplex>{});
+  }
+}
+
+// Element offsets are 32-bit (dim <= 46340^2 < 2^31): base + unsigned offset
+// is one wide multiply-add instead of 64-bit index arithmetic per gather.
+__device__ __forceinline__ double2 gat(const double2* base, unsigned off, unsigned long long pol) {
+  return ld_gather(base + off, pol);
+}
+
 // Row-indexed part at (i, j[r]), lane = row i: A then R_k.
 __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2* __restrict__ x, int i,
                                                const int* j, double2* acc, unsigned long long xpol) {
-  const long long n = m.n;
+  const unsigned n = static_cast<unsigned>(m.n);
+  unsigned jn[kKR];
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) jn[r] = static_cast<unsigned>(j[r]) * n;
   if (m.a_ell.sptr) {  // I (x) A: columns j of X, operand rows in sliced ELL
     const int sl = i >> 5, lane = i & 31;
     const int b = __ldg(m.a_ell.sptr + sl), len = (__ldg(m.a_ell.sptr + sl + 1) - b) >> 5;
     const int* cp = m.a_ell.col + b + lane;
     const double2* vp = m.a_ell.val + b + lane;
+    by_kind(m.vk_a, [&](auto kc) {
+      constexpr int K = decltype(kc)::value;
 #pragma unroll 2
-    for (int e = 0; e < len; ++e) {
-      const int c = __ldg(cp + 32 * e);
-      const double2 v = __ldg(vp + 32 * e);
+      for (int e = 0; e < len; ++e) {
+        const unsigned c = static_cast<unsigned>(__ldg(cp + 32 * e));
+        const double2 v = ldv<K>(vp + 32 * e);
 #pragma unroll
-      for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + j[r] * n + c, xpol));
-    }
+        for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, jn[r] + c, xpol));
+      }
+    });
   } else if (m.a.ptr) {
-    const int e1 = __ldg(m.a.ptr + i + 1);
+    const int e0 = __ldg(m.a.ptr + i), e1 = __ldg(m.a.ptr + i + 1);
+    by_kind(m.vk_a, [&](auto kc) {
+      constexpr int K = decltype(kc)::value;
 #pragma unroll 2
-    for (int e = __ldg(m.a.ptr + i); e < e1; ++e) {
-      const int c = __ldg(m.a.col + e);
-      const double2 v = __ldg(m.a.val + e);
+      for (int e = e0; e < e1; ++e) {
+        const unsigned c = static_cast<unsigned>(__ldg(m.a.col + e));
+        const double2 v = ldv<K>(m.a.val + e);
 #pragma unroll
-      for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + j[r] * n + c, xpol));
-    }
+        for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, jn[r] + c, xpol));
+      }
+    });
   }
   if (m.factored) {
     for (int k = 0; k < m.nk; ++k) {  // -w/2 L'(L X): columns j of W_k
       const KronList& rk = m.r[k];
-      const int r1 = __ldg(rk.ptr + i + 1);
+      const int e0 = __ldg(rk.ptr + i), e1 = __ldg(rk.ptr + i + 1);
       const double2* wk = m.w[k];
+      by_kind(m.vk_r[k], [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
 #pragma unroll 2
-      for (int e = __ldg(rk.ptr + i); e < r1; ++e) {
-        const int c = __ldg(rk.col + e);
-        const double2 v = __ldg(rk.val + e);
+        for (int e = e0; e < e1; ++e) {
+          const unsigned c = static_cast<unsigned>(__ldg(rk.col + e));
+          const double2 v = ldv<K>(rk.val + e);
 #pragma unroll
-        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(wk + j[r] * n + c, xpol));
-      }
+          for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(wk, jn[r] + c, xpol));
+        }
+      });
     }
   }
 }
 
 // acc += sum over operand row `row` of val * g(col) (warp-uniform row).
-template <class G>
+template <int K, class G>
 __device__ __forceinline__ void uniform_row(const KronList& l, int row, double2& acc, G&& g) {
   const int e1 = __ldg(l.ptr + row + 1);
 #pragma unroll 4
-  for (int e = __ldg(l.ptr + row); e < e1; ++e) cfma(acc, __ldg(l.val + e), g(__ldg(l.col + e)));
+  for (int e = __ldg(l.ptr + row); e < e1; ++e) cfmak<K>(acc, ldv<K>(l.val + e), g(static_cast<unsigned>(__ldg(l.col + e))));
 }
 
 // acc[r] += sum over operand row rows[r] of val * g(col) for r < kKR, one
 // row after the other.  (Walking the kKR rows in lockstep was measured
 // slower on c2-c4.)
-template <class G>
+template <int K, class G>
 __device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows, double2* acc, G&& g) {
 #pragma unroll
-  for (int r = 0; r < kKR; ++r) uniform_row(l, rows[r], acc[r], g);
+  for (int r = 0; r < kKR; ++r) uniform_row<K>(l, rows[r], acc[r], g);
 }
 
 // acc[r] += sum_k E(row0 + r, k) g(col) over the kKR consecutive rows row0 ..
@@ -902,7 +970,7 @@ __device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows,
 // entries per row: one warp load fetches all their column indices, which are
 // shuffled out, so the index -> gather chain skips an L1 round trip.  The
 // entries of each row are added in their stored order.
-template <class G>
+template <int K, class G>
 __device__ __forceinline__ void shfl_rows(const KronEll& e, int len, int slice, int l0, double2* acc, G&& g) {
   const int lane = threadIdx.x & 31;
   const int base = __ldg(e.sptr + slice);
@@ -912,8 +980,8 @@ __device__ __forceinline__ void shfl_rows(const KronEll& e, int len, int slice, 
   for (int k = 0; k < len; ++k) {
 #pragma unroll
     for (int r = 0; r < kKR; ++r) {
-      const int c = __shfl_sync(0xffffffffu, mycol, kKR * k + r);
-      cfma(acc[r], __ldg(e.val + base + 32 * k + l0 + r), g(c));
+      const unsigned c = static_cast<unsigned>(__shfl_sync(0xffffffffu, mycol, kKR * k + r));
+      cfmak<K>(acc[r], ldv<K>(e.val + base + 32 * k + l0 + r), g(c));
     }
   }
 }
@@ -923,53 +991,69 @@ __device__ __forceinline__ void shfl_rows(const KronEll& e, int len, int slice, 
 // row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).
 __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
                                                   int j, double2* acc, unsigned long long xpol) {
-  const long long n = m.n;
+  const unsigned n = static_cast<unsigned>(m.n);
+  const double2* xj = x + j;
   // rows i[r] = I*32 + 4w + r: lanes 4w .. 4w+3 of ELL slice I (clamped edge rows read
   // that slice's padding lanes, whose results are discarded)
   const int sl = i[0] >> 5, l0 = (threadIdx.x >> 5) * kKR;
-  if (m.a_len > 0) {
-    shfl_rows(m.a_ellu, m.a_len, sl, l0, acc,
-              [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
-  } else if (m.a.ptr) {
-    uniform_rows(m.a, i, acc, [&](int c) { return conj2(ld_gather(x + static_cast<long long>(c) * n + j, xpol)); });
-  }
+  by_kind(m.vk_a, [&](auto kc) {
+    constexpr int K = decltype(kc)::value;
+    const auto g = [&](unsigned c) { return conj2(gat(xj, c * n, xpol)); };
+    if (m.a_len > 0) {
+      shfl_rows<K>(m.a_ellu, m.a_len, sl, l0, acc, g);
+    } else if (m.a.ptr) {
+      uniform_rows<K>(m.a, i, acc, g);
+    }
+  });
   if (m.factored) {
     for (int k = 0; k < m.nk; ++k) {
-      const double2* wt = m.wt[k];
-      if (m.r_len[k] > 0) {
-        shfl_rows(m.r_ellu[k], m.r_len[k], sl, l0, acc,
-                  [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
-      } else {
-        uniform_rows(m.r[k], i, acc, [&](int c) { return ld_gather(wt + static_cast<long long>(c) * n + j, xpol); });
-      }
+      const double2* wtj = m.wt[k] + j;
+      by_kind(m.vk_r[k], [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        const auto g = [&](unsigned c) { return gat(wtj, c * n, xpol); };
+        if (m.r_len[k] > 0) {
+          shfl_rows<K>(m.r_ellu[k], m.r_len[k], sl, l0, acc, g);
+        } else {
+          uniform_rows<K>(m.r[k], i, acc, g);
+        }
+      });
     }
   }
+  unsigned in_[kKR];
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) in_[r] = static_cast<unsigned>(i[r]) * n;
   if (m.p_rows) {  // P_k(j, a) W_k(i, a), lane = j: padding-free ELL rows of P_k, rows i of Wt_k
-    const int sl = j >> 5, ln = j & 31;
+    const int sj = j >> 5, ln = j & 31;
     for (int k = 0; k < m.nk; ++k) {
       const KronEll& pe = m.p_ell[k];
       const double2* wt = m.wt[k];
-      const int b = __ldg(pe.sptr + sl), len = (__ldg(pe.sptr + sl + 1) - b) >> 5;
+      const int b = __ldg(pe.sptr + sj), len = (__ldg(pe.sptr + sj + 1) - b) >> 5;
+      by_kind(m.vk_p[k], [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
 #pragma unroll 2
-      for (int e = 0; e < len; ++e) {
-        const int a = __ldg(pe.col + b + 32 * e + ln);
-        const double2 v = __ldg(pe.val + b + 32 * e + ln);
+        for (int e = 0; e < len; ++e) {
+          const unsigned a = static_cast<unsigned>(__ldg(pe.col + b + 32 * e + ln));
+          const double2 v = ldv<K>(pe.val + b + 32 * e + ln);
 #pragma unroll
-        for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(wt + static_cast<long long>(i[r]) * n + a, xpol));
-      }
+          for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(wt, in_[r] + a, xpol));
+        }
+      });
     }
   }
   if (m.b_rows) {  // B(j, c) X(i, c) = B(j, c) conj x[n i + c], lane = j: padding-free ELL rows of B
-    const int sl = j >> 5, ln = j & 31;
+    const int sj = j >> 5, ln = j & 31;
     const KronEll& be = m.b_ell;
-    const int b = __ldg(be.sptr + sl), len = (__ldg(be.sptr + sl + 1) - b) >> 5;
+    const int b = __ldg(be.sptr + sj), len = (__ldg(be.sptr + sj + 1) - b) >> 5;
+    by_kind(m.vk_b, [&](auto kc) {
+      constexpr int K = decltype(kc)::value;
 #pragma unroll 2
-    for (int e = 0; e < len; ++e) {
-      const int c = __ldg(be.col + b + 32 * e + ln);
-      const double2 v = __ldg(be.val + b + 32 * e + ln);
+      for (int e = 0; e < len; ++e) {
+        const unsigned c = static_cast<unsigned>(__ldg(be.col + b + 32 * e + ln));
+        const double2 v = ldv<K>(be.val + b + 32 * e + ln);
 #pragma unroll
-      for (int r = 0; r < kKR; ++r) cfma(acc[r], v, conj2(ld_gather(x + static_cast<long long>(i[r]) * n + c, xpol)));
-    }
+        for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, conj2(gat(x, in_[r] + c, xpol)));
+      }
+    });
   }
 }
 
@@ -979,48 +1063,68 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
 template <bool kHerm>
 __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __restrict__ x, int i, const int* j,
                                           double2* acc, unsigned long long xpol) {
-  const long long n = m.n;
+  const unsigned n = static_cast<unsigned>(m.n);
   if (!(kHerm && m.p_rows)) {  // (the Hermitian tiles applied P_k in the transposed section)
     for (int k = 0; k < m.nk; ++k) {
       const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
-      uniform_rows(m.p[k], j, acc, [&](int c) { return ld_gather(wi + static_cast<long long>(c) * n, xpol); });
+      by_kind(m.vk_p[k], [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        uniform_rows<K>(m.p[k], j, acc, [&](unsigned c) { return gat(wi, c * n, xpol); });
+      });
     }
   }
   if (m.b.ptr && !(kHerm && m.b_rows)) {  // B (x) I: coalesced columns c of X
     const double2* xi = x + i;
-    uniform_rows(m.b, j, acc, [&](int c) { return ld_gather(xi + static_cast<long long>(c) * n, xpol); });
+    by_kind(m.vk_b, [&](auto kc) {
+      constexpr int K = decltype(kc)::value;
+      uniform_rows<K>(m.b, j, acc, [&](unsigned c) { return gat(xi, c * n, xpol); });
+    });
   }
-  for (int k = 0; k < m.nk; ++k) {
-    if (m.factored) {  // -w/2 (X L') L: columns of V_k
-      if constexpr (kHerm) {
-        const double2* vi = m.wt[k] + i;
-        if (m.s_len[k] > 0) {  // rows j[r] = J*32 + 4w + r: lanes 4w .. 4w+3 of slice J
-          shfl_rows(m.s_ellu[k], m.s_len[k], j[0] >> 5, (threadIdx.x >> 5) * kKR, acc,
-                    [&](int c) { return conj2(ld_gather(vi + static_cast<long long>(c) * n, xpol)); });
+  if (m.factored) {
+    for (int k = 0; k < m.nk; ++k) {  // -w/2 (X L') L: columns of V_k
+      by_kind(m.vk_s[k], [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        if constexpr (kHerm) {
+          const double2* vi = m.wt[k] + i;
+          const auto g = [&](unsigned c) { return conj2(gat(vi, c * n, xpol)); };
+          if (m.s_len[k] > 0) {  // rows j[r] = J*32 + 4w + r: lanes 4w .. 4w+3 of slice J
+            shfl_rows<K>(m.s_ellu[k], m.s_len[k], j[0] >> 5, (threadIdx.x >> 5) * kKR, acc, g);
+          } else {
+            uniform_rows<K>(m.s[k], j, acc, g);
+          }
         } else {
-          uniform_rows(m.s[k], j, acc, [&](int c) { return conj2(ld_gather(vi + static_cast<long long>(c) * n, xpol)); });
+          const double2* vi = m.v[k] + i;
+          uniform_rows<K>(m.s[k], j, acc, [&](unsigned c) { return gat(vi, c * n, xpol); });
         }
-      } else {
-        const double2* vi = m.v[k] + i;
-        uniform_rows(m.s[k], j, acc, [&](int c) { return ld_gather(vi + static_cast<long long>(c) * n, xpol); });
-      }
+      });
     }
   }
+  unsigned jn[kKR];
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) jn[r] = static_cast<unsigned>(j[r]) * n + static_cast<unsigned>(i);
   if (m.da) {  // the diagonals of A and B: (A_ii + B_jj) X(i, j), one gather
     const double2 dai = __ldg(m.da + i);
+    by_kind(m.vk_d, [&](auto kc) {
+      constexpr int K = decltype(kc)::value;
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const double2 dbj = __ldg(m.db + j[r]);
+        const double2 c = make_double2(dai.x + dbj.x, dai.y + dbj.y);
+        if (c.x != 0.0 || c.y != 0.0) cfmak<K>(acc[r], c, gat(x, jn[r], xpol));
+      }
+    });
+  }
+  if (m.t.ptr) {
 #pragma unroll
     for (int r = 0; r < kKR; ++r) {
-      const double2 dbj = __ldg(m.db + j[r]);
-      const double2 c = make_double2(dai.x + dbj.x, dai.y + dbj.y);
-      if (c.x != 0.0 || c.y != 0.0) cfma(acc[r], c, ld_gather(x + static_cast<long long>(j[r]) * n + i, xpol));
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < kKR; ++r) {
-    if (m.t.ptr && i == j[r]) {  // transfer onto the diagonal
-      const int e1 = __ldg(m.t.ptr + i + 1);
-      for (int e = __ldg(m.t.ptr + i); e < e1; ++e)
-        cfma(acc[r], __ldg(m.t.val + e), ld_gather(x + static_cast<long long>(__ldg(m.t.col + e)) * (n + 1), xpol));
+      if (i == j[r]) {  // transfer onto the diagonal
+        const int e1 = __ldg(m.t.ptr + i + 1);
+        by_kind(m.vk_t, [&](auto kc) {
+          constexpr int K = decltype(kc)::value;
+          for (int e = __ldg(m.t.ptr + i); e < e1; ++e)
+            cfmak<K>(acc[r], ldv<K>(m.t.val + e), gat(x, static_cast<unsigned>(__ldg(m.t.col + e)) * (n + 1), xpol));
+        });
+      }
     }
   }
   if (m.d_loc) {  // -0.5 (w (dl_i + dl_j) + ds_i + ds_j) X(i, j)
@@ -1031,7 +1135,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
           0.5, __dadd_rn(__dadd_rn(__dmul_rn(m.omega, __dadd_rn(dli, __ldg(m.d_loc + j[r]))), dsi),
                          __ldg(m.d_ss + j[r])));
       if (d != 0.0) {
-        const double2 xg = ld_gather(x + j[r] * n + i, xpol);
+        const double2 xg = gat(x, jn[r], xpol);
         acc[r].x = fma(-d, xg.x, acc[r].x);
         acc[r].y = fma(-d, xg.y, acc[r].y);
       }
@@ -1070,10 +1174,11 @@ __device__ __forceinline__ void tile_coords(const TileGrid& g, bool herm, long l
 }
 
 // Writes one computed tile (acc[r] at row I*32 + lane, column J*32 + 4w + r)
-// through epi(local_row, value, valid): directly and, in Hermitian mode,
-// conjugated into tile (J, I) through a shared-memory transpose (coalesced
-// both ways); diagonal tiles keep their upper triangle, a real diagonal and
-// its mirror.  Every thread of the block calls it.
+// through epi(local_row, value, valid, mirror): directly and, in Hermitian
+// mode, conjugated into tile (J, I) through a shared-memory transpose
+// (coalesced both ways; mirror = true: the conjugate of an element already
+// emitted, same magnitude); diagonal tiles keep their upper triangle, a real
+// diagonal and its mirror.  Every thread of the block calls it.
 template <bool kHerm, class Epi>
 __device__ __forceinline__ void kron_tile_emit(const TileGrid& g, int I, int J, const double2* acc,
                                                double2 (*tile)[kKT + 1], Epi&& epi) {
@@ -1087,7 +1192,8 @@ __device__ __forceinline__ void kron_tile_emit(const TileGrid& g, int I, int J, 
     const int jl = J * kKT + jt;
     double2 y = acc[r];
     if (diag && lane == jt) y.y = 0.0;
-    epi(static_cast<long long>(jl) * n + iu, y, iu < n && jl < g.nc && (!diag || lane <= jt));
+    epi(static_cast<unsigned>(jl) * static_cast<unsigned>(n) + static_cast<unsigned>(iu), y,
+        iu < n && jl < g.nc && (!diag || lane <= jt), false);
     if (kHerm) tile[jt][lane] = acc[r];
   }
   if (kHerm) {
@@ -1099,15 +1205,16 @@ __device__ __forceinline__ void kron_tile_emit(const TileGrid& g, int I, int J, 
       const int it = kKR * w + r;
       const double2 v = tile[lane][it];
       const int icol = I * kKT + it;
-      epi(static_cast<long long>(icol) * n + jrow, conj2(v), jrow < n && icol < n && (!diag || lane > it));
+      epi(static_cast<unsigned>(icol) * static_cast<unsigned>(n) + static_cast<unsigned>(jrow), conj2(v),
+          jrow < n && icol < n && (!diag || lane > it), true);
     }
     __syncthreads();
   }
 }
 
-// Persistent loop over the tiles; epi(local_row, value, valid) runs on every
-// thread for every element (valid is false outside the matrix and for the
-// elements a Hermitian tile takes from its mirror).
+// Persistent loop over the tiles; epi(local_row, value, valid, mirror) runs on
+// every thread for every element (valid is false outside the matrix and for
+// the elements a Hermitian tile takes from its mirror).
 template <bool kHerm, class Epi>
 __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
   __shared__ double2 tile[kKT][kKT + 1];
@@ -1169,11 +1276,12 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
   pdl_prologue();
   __shared__ double2 tile[kKT][kKT + 1];
   const unsigned long long xpol = evict_last_policy();
-  const long long n = m.n;
+  const unsigned n = static_cast<unsigned>(m.n);
   const TileGrid g = tile_grid(m, false);
   const KronEll& qe = m.q_ell[k];
   const KronList& q = m.q[k];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int vk = m.vk_q[k];
   for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     int I, J;
     tile_coords(g, false, t, I, J);
@@ -1182,19 +1290,26 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
     for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
     if constexpr (kHerm) {
       const int au = J * kKT + lane;  // column a (single GPU: c0 = 0)
-      const int a = au < g.n ? au : g.n - 1;
+      const double2* xa = x + (au < g.n ? au : g.n - 1);
+      const auto gx = [&](unsigned b) { return conj2(gat(xa, b * n, xpol)); };
       if (m.q_len[k] > 0) {  // rows I*32 + 4w + r: lanes 4w .. 4w+3 of slice I
         const int iv0 = I * kKT + kKR * w;
-        shfl_rows(m.q_ellu[k], m.q_len[k], (iv0 < g.n ? iv0 : g.n - 1) >> 5, kKR * w, acc,
-                  [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
+        by_kind(vk, [&](auto kc) {
+          shfl_rows<decltype(kc)::value>(m.q_ellu[k], m.q_len[k], (iv0 < g.n ? iv0 : g.n - 1) >> 5, kKR * w, acc, gx);
+        });
+      } else if (q.ptr) {
+        int ir[kKR];
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) {
+          const int iv = I * kKT + kKR * w + r;
+          ir[r] = iv < g.n ? iv : g.n - 1;
+        }
+        by_kind(vk, [&](auto kc) { uniform_rows<decltype(kc)::value>(q, ir, acc, gx); });
       }
 #pragma unroll
       for (int r = 0; r < kKR; ++r) {
         const int iv = I * kKT + kKR * w + r;
-        const int i = iv < g.n ? iv : g.n - 1;
-        if (q.ptr && m.q_len[k] == 0)
-          uniform_row(q, i, acc[r], [&](int b) { return conj2(ld_gather(x + static_cast<long long>(b) * n + a, xpol)); });
-        if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<long long>(iv) * n + au, acc[r], xpol);
+        if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<unsigned>(iv) * n + static_cast<unsigned>(au), acc[r], xpol);
         tile[kKR * w + r][lane] = acc[r];
       }
       if (!m.p_rows) {  // the column-major W_k (read by P_k in the normal orientation)
@@ -1203,7 +1318,8 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
 #pragma unroll
         for (int r = 0; r < kKR; ++r) {
           const int at = J * kKT + kKR * w + r;
-          if (iu < g.n && at < g.n) st_hint(m.w[k] + static_cast<long long>(at) * n + iu, tile[lane][kKR * w + r], xpol);
+          if (iu < g.n && at < g.n)
+            st_hint(m.w[k] + static_cast<unsigned>(at) * n + static_cast<unsigned>(iu), tile[lane][kKR * w + r], xpol);
         }
         __syncthreads();
       }
@@ -1211,37 +1327,40 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
       const int iu = I * kKT + lane;
       const bool vi = iu < m.n;
       const int i = vi ? iu : m.n - 1;
-      long long col[kKR];
+      unsigned col[kKR];
       bool vj[kKR];
 #pragma unroll
       for (int r = 0; r < kKR; ++r) {
         const int jl = J * kKT + kKR * w + r;
         vj[r] = jl < g.nc;
-        col[r] = (g.c0 + (vj[r] ? jl : g.nc - 1)) * n;
+        col[r] = static_cast<unsigned>(g.c0 + (vj[r] ? jl : g.nc - 1)) * n;
       }
-      if (qe.sptr) {
-        const int sl = i >> 5, ln = i & 31;
-        const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
+      by_kind(vk, [&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        if (qe.sptr) {
+          const int sl = i >> 5, ln = i & 31;
+          const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
 #pragma unroll 2
-        for (int e = 0; e < len; ++e) {
-          const int c = __ldg(qe.col + b + 32 * e + ln);
-          const double2 v = __ldg(qe.val + b + 32 * e + ln);
+          for (int e = 0; e < len; ++e) {
+            const unsigned c = static_cast<unsigned>(__ldg(qe.col + b + 32 * e + ln));
+            const double2 v = ldv<K>(qe.val + b + 32 * e + ln);
 #pragma unroll
-          for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
-        }
-      } else if (q.ptr) {
-        const int e1 = __ldg(q.ptr + i + 1);
+            for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, col[r] + c, xpol));
+          }
+        } else if (q.ptr) {
+          const int e1 = __ldg(q.ptr + i + 1);
 #pragma unroll 2
-        for (int e = __ldg(q.ptr + i); e < e1; ++e) {
-          const int c = __ldg(q.col + e);
-          const double2 v = __ldg(q.val + e);
+          for (int e = __ldg(q.ptr + i); e < e1; ++e) {
+            const unsigned c = static_cast<unsigned>(__ldg(q.col + e));
+            const double2 v = ldv<K>(q.val + e);
 #pragma unroll
-          for (int r = 0; r < kKR; ++r) cfma(acc[r], v, ld_gather(x + col[r] + c, xpol));
+            for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, col[r] + c, xpol));
+          }
         }
-      }
+      });
 #pragma unroll
       for (int r = 0; r < kKR; ++r)
-        if (vi && vj[r]) st_hint(m.w[k] + col[r] + i, acc[r], xpol);
+        if (vi && vj[r]) st_hint(m.w[k] + col[r] + static_cast<unsigned>(i), acc[r], xpol);
     }
   }
   if constexpr (kFlush) {
@@ -1268,10 +1387,10 @@ __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const doub
     const long long g = m.row0 + r;
     const long long a = g / n, i = g - a * n;
     double2 acc = make_double2(0.0, 0.0);
-    const int e1 = __ldg(u.ptr + a + 1);
-#pragma unroll 4
-    for (int e = __ldg(u.ptr + a); e < e1; ++e)
-      cfma(acc, __ldg(u.val + e), ld_gather(x + static_cast<long long>(__ldg(u.col + e)) * n + i, xpol));
+    by_kind(m.vk_u[k], [&](auto kc) {
+      uniform_row<decltype(kc)::value>(u, static_cast<int>(a), acc,
+                                       [&](unsigned c) { return gat(x + i, c * static_cast<unsigned>(n), xpol); });
+    });
     st_hint(m.v[k] + g, acc, xpol);
   }
 }
@@ -1279,7 +1398,7 @@ __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const doub
 template <bool kHerm>
 __global__ void __launch_bounds__(kThreads) kron_spmv_kernel(KronView m, const double2* x, double2* y, double scale) {
   pdl_prologue();
-  kron_tiles<kHerm>(m, x, [&](long long row, double2 acc, bool valid) {
+  kron_tiles<kHerm>(m, x, [&](unsigned row, double2 acc, bool valid, bool) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
@@ -1314,15 +1433,17 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_STEP_MIN_BLOCKS) kron_step
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0, smax = 0;
   const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  kron_tiles<kHerm>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+  kron_tiles<kHerm>(a.m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
     if (!valid) return;
     const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
     const double2 sv0 = ld_once(a.sum_in + row, once);
     st_hint(a.y + row, yv, keep);
     const double2 sv = make_double2(sv0.x + yv.x, sv0.y + yv.y);  // expm.cpp:181
     st_hint(a.sum_out + row, sv, once);
-    tmax = umax64(tmax, dbits(cabs2(yv)));
-    smax = umax64(smax, dbits(cabs2(sv)));
+    if (!mirror) {  // a mirrored element is the conjugate of one already counted (Hermitian sums)
+      max_abs_bits(tmax, yv);
+      max_abs_bits(smax, sv);
+    }
   });
   pdl_trigger();
   tmax = block_max_bits(tmax, red);
@@ -1351,7 +1472,10 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_te
   const unsigned long long keep = evict_last_policy();
   double2* const kp = a.kp;
   const double scale = a.scale;
-  kron_tiles<kHerm>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  kron_tiles<kHerm>(m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
+    series_store(kp, scale, row, acc, valid && !mirror, keep, tmax);
+    if (valid && mirror) st_hint(kp + row, make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y)), keep);
+  });
   series_term_finish(a, tmax, red);
 }
 
@@ -1364,7 +1488,7 @@ __device__ __forceinline__ void norm_body(const double2* __restrict__ v, long lo
   unsigned long long m = 0;
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<long long>(gridDim.x) * blockDim.x)
-    m = umax64(m, dbits(cabs2(v[k])));
+    max_abs_bits(m, v[k]);
   m = block_max_bits(m, red);
   if (threadIdx.x == 0) {
     atomicMax(bits, m);

@@ -328,6 +328,16 @@ MultiCsr strip_diagonal(const MultiCsr& m, std::vector<double2>& d) {
   return o;
 }
 
+// kernels.hpp: value classes.  A list with no entries is "real" (no term).
+int value_class(const std::vector<double2>& v) {
+  bool re = true, im = true;
+  for (const double2& x : v) {
+    re = re && x.y == 0.0;
+    im = im && x.x == 0.0;
+  }
+  return re ? dev::kValReal : im ? dev::kValImag : dev::kValComplex;
+}
+
 struct KronStore {
   // Sliced ELL copies unless they store more than kEllMaxPadding x the
   // nonzeros; whether the kernels use them is autotuned per operator set at
@@ -361,12 +371,20 @@ struct KronStore {
       a_host = a1;
       b_host = b1;
       a = maybe_ell(a1, s);
-      bool any = false;
-      for (std::size_t i = 0; i < dah.size(); ++i)
-        any = any || dah[i].x != 0.0 || dah[i].y != 0.0 || dbh[i].x != 0.0 || dbh[i].y != 0.0;
-      if (any) {
+      // the merged coefficient A_ii + B_jj, as the kernels round it, vanishes for
+      // every (i, j) exactly when diag(A) and diag(B) are constants a, b with
+      // a + b == 0 (regular graphs: the coherent H_ii and -H_jj cancel); then
+      // no term at all
+      bool zero = true;
+      for (std::size_t i = 0; i < dah.size() && zero; ++i)
+        zero = dah[i].x + dbh[0].x == 0.0 && dah[i].y + dbh[0].y == 0.0 && dah[0].x + dbh[i].x == 0.0 &&
+               dah[0].y + dbh[i].y == 0.0;
+      if (!zero) {
         da = up(dah, s);
         db = up(dbh, s);
+        std::vector<double2> both(dah);
+        both.insert(both.end(), dbh.begin(), dbh.end());
+        vk_d = value_class(both);
       }
     }
     for (const MultiCsr& qk : host.q) q.push_back(maybe_ell(qk, s));
@@ -421,6 +439,20 @@ struct KronStore {
       b_rows = true;
     }
     if (const char* br = std::getenv("QSWG_KRON_BROWS")) b_rows = b_rows && br[0] == '1';  // experiment knob
+    vk_a = value_class(a_host.val);
+    vk_b = value_class(b_host.val);
+    vk_t = value_class(host.t.val);
+    for (std::size_t k = 0; k < host.p.size(); ++k) {
+      vk_p.push_back(value_class(host.p[k].val));
+      vk_q.push_back(value_class(host.q[k].val));
+      vk_r.push_back(factored ? value_class(host.r[k].val) : dev::kValComplex);
+      vk_s.push_back(factored ? value_class(host.sfac[k].val) : dev::kValComplex);
+      vk_u.push_back(factored ? value_class(host.u[k].val) : dev::kValComplex);
+    }
+    if (const char* vk = std::getenv("QSWG_KRON_VALCLASS"); vk && vk[0] == '0') {  // experiment knob: all complex
+      vk_a = vk_b = vk_t = vk_d = dev::kValComplex;
+      for (auto* v : {&vk_p, &vk_q, &vk_r, &vk_s, &vk_u}) std::fill(v->begin(), v->end(), dev::kValComplex);
+    }
     if (factored) {
       af = upload_list(host.af, s);
       bf = upload_list(host.bf, s);
@@ -449,6 +481,8 @@ struct KronStore {
   dev::KronEll b_ell;               // padding-free ELL copy of B (or empty)
   bool b_rows = false;              // Hermitian tiles apply B transposed
   bool factored = false;
+  int vk_a = dev::kValComplex, vk_b = dev::kValComplex, vk_t = dev::kValComplex, vk_d = dev::kValComplex;
+  std::vector<int> vk_p, vk_q, vk_r, vk_s, vk_u;  // kernels.hpp: value classes
   dev::KronList af, bf;
   std::vector<dev::KronList> r, sfac, u;
 
@@ -671,6 +705,17 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
       }
       m.kron.w[k] = kron_w_[static_cast<std::size_t>(k)].get();
       if (kron_->p_rows) m.kron.p_ell[k] = kron_->p_ell[static_cast<std::size_t>(k)];
+    }
+    m.kron.vk_a = kron_->vk_a;
+    m.kron.vk_b = kron_->vk_b;
+    m.kron.vk_t = kron_->vk_t;
+    m.kron.vk_d = kron_->vk_d;
+    for (std::size_t k = 0; k < kron_->vk_p.size(); ++k) {
+      m.kron.vk_p[k] = kron_->vk_p[k];
+      m.kron.vk_q[k] = kron_->vk_q[k];
+      m.kron.vk_r[k] = kron_->vk_r[k];
+      m.kron.vk_s[k] = kron_->vk_s[k];
+      m.kron.vk_u[k] = kron_->vk_u[k];
     }
     m.kron.p_rows = kron_->p_rows ? 1 : 0;
     m.kron.b_rows = kron_->b_rows ? 1 : 0;

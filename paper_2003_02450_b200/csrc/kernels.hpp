@@ -94,6 +94,11 @@ struct KronEll {
   const double2* val = nullptr;
 };
 
+// Value class of an operand (KronView::vk_*): every stored value purely real,
+// purely imaginary, or general complex.  The kernels multiply the first two
+// with half the FMAs; the products they drop are exact zeros.
+inline constexpr int kValComplex = 0, kValReal = 1, kValImag = 2;
+
 struct KronView {
   int n = 0;
   std::int64_t rows = 0;  // local rows [row0, row0 + rows), multiples of n
@@ -150,6 +155,10 @@ struct KronView {
   // ELL slices of r_len / s_len / q_len <= 8 entries (0: the CSR rows).
   int r_len[kMaxKron] = {}, s_len[kMaxKron] = {}, q_len[kMaxKron] = {};
   KronEll r_ellu[kMaxKron], s_ellu[kMaxKron], q_ellu[kMaxKron];
+  // value classes: A, B, T, the merged diagonal (da, db), and per Lindblad
+  // term P_k, Q_k, R_k, S_k, U_k
+  int vk_a = kValComplex, vk_b = kValComplex, vk_t = kValComplex, vk_d = kValComplex;
+  int vk_p[kMaxKron] = {}, vk_q[kMaxKron] = {}, vk_r[kMaxKron] = {}, vk_s[kMaxKron] = {}, vk_u[kMaxKron] = {};
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
