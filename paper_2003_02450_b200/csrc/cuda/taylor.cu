@@ -851,16 +851,25 @@ __device__ __forceinline__ double2 conj2(double2 v) { return make_double2(v.x, -
 // configs is purely real (R_k, P_k, S_k, Q_k, T) or purely imaginary (A, B
 // and their diagonals: the coherent -i(1-w)H parts): those multiply with 2
 // FMAs instead of 4 and load 8 bytes instead of 16.  The products dropped are
-// exact zeros, so every class gives the complex formula's values.
-template <int K>
-__device__ __forceinline__ double2 ldv(const double2* p) {
-  if constexpr (K == kValReal) {
+// exact zeros, so every class gives the complex formula's values.  With
+// kValConst every entry holds the same value (unweighted lattices, the
+// coherent part of any unweighted graph), taken from the kernel parameters
+// instead of being loaded.
+template <int K, bool C>
+__device__ __forceinline__ double2 opv(const double2* p, double2 cv) {
+  if constexpr (C) {
+    return cv;
+  } else if constexpr (K == kValReal) {
     return make_double2(__ldg(&p->x), 0.0);
   } else if constexpr (K == kValImag) {
     return make_double2(0.0, __ldg(&p->y));
   } else {
     return __ldg(p);
   }
+}
+template <int K>
+__device__ __forceinline__ double2 ldv(const double2* p) {
+  return opv<K, false>(p, double2{});
 }
 template <int K>
 __device__ __forceinline__ void cfmak(double2& acc, double2 v, double2 xv) {
@@ -876,25 +885,54 @@ __device__ __forceinline__ void cfmak(double2& acc, double2 v, double2 xv) {
 }
 template <int K>
 using ValK = std::integral_constant<int, K>;
-// f(ValK<class>{}) for the runtime (warp-uniform) class k.
+template <bool C>
+using ConstK = std::integral_constant<bool, C>;
+// f(ValK<class>{}, ConstK<constant>{}) for the runtime (warp-uniform) code k.
 template <class F>
 __device__ __forceinline__ void by_kind(int k, F&& f) {
-  if (k == kValReal) {
-    f(ValK<kValReal>{});
-  } else if (k == kValImag) {
-    f(ValK<kValImag>{});
-  } else {
-    f(ValK<kValComplex>{});
+  const bool c = (k & kValConst) != 0;
+  switch (k & 3) {
+    case kValReal:
+      if (c) {
+        f(ValK<kValReal>{}, ConstK<true>{});
+      } else {
+        f(ValK<kValReal>{}, ConstK<false>{});
+      }
+      break;
+    case kValImag:
+      if (c) {
+        f(ValK<kValImag>{}, ConstK<true>{});
+      } else {
+        f(ValK<kValImag>{}, ConstK<false>{});
+      }
+      break;
+    default:
+      f(ValK<kValComplex>{}, ConstK<false>{});
   }
 }
+#define QSWG_KC(kc, cc)                     \
+  constexpr int K = decltype(kc)::value;    \
+  constexpr bool C = decltype(cc)::value;   \
+  (void)0
 
 // Element offsets are 32-bit (dim <= 46340^2 < 2^31): base + unsigned offset
-// is one wide multiply-add instead of 64-bit index arithmetic per gather.
+// is one wide multiply-add.  Column lists the gathers scale by n hold c * n
+// already (kernels.hpp: KronView).
 __device__ __forceinline__ double2 gat(const double2* base, unsigned off, unsigned long long pol) {
-  return ld_gather(base + off, pol);
+  (void)pol;  // plain read-only load (common.cuh: ld_gather)
+  double2 r;
+  // one IMAD.WIDE.U32 for the address: written out, so the compiler does not
+  // re-associate base + off into 64-bit index arithmetic
+  asm("{\n\t.reg .b64 qa;\n\tmad.wide.u32 qa, %2, 16, %3;\n\tld.global.nc.v2.f64 {%0, %1}, [qa];\n\t}"
+      : "=d"(r.x), "=d"(r.y)
+      : "r"(off), "l"(base));
+  return r;
 }
 
-// Row-indexed part at (i, j[r]), lane = row i: A then R_k.
+// Row-indexed part at (i, j[r]), lane = row i: A then R_k (general path).
+// kF: the factored G-QSW dissipator is present (1) or not (0); the kernels
+// are instantiated per case (KronView::factored).
+template <int kF>
 __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2* __restrict__ x, int i,
                                                const int* j, double2* acc, unsigned long long xpol) {
   const unsigned n = static_cast<unsigned>(m.n);
@@ -906,40 +944,40 @@ __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2*
     const int b = __ldg(m.a_ell.sptr + sl), len = (__ldg(m.a_ell.sptr + sl + 1) - b) >> 5;
     const int* cp = m.a_ell.col + b + lane;
     const double2* vp = m.a_ell.val + b + lane;
-    by_kind(m.vk_a, [&](auto kc) {
-      constexpr int K = decltype(kc)::value;
+    by_kind(m.vk_a, [&](auto kc, auto cc) {
+      QSWG_KC(kc, cc);
 #pragma unroll 2
       for (int e = 0; e < len; ++e) {
         const unsigned c = static_cast<unsigned>(__ldg(cp + 32 * e));
-        const double2 v = ldv<K>(vp + 32 * e);
+        const double2 v = opv<K, C>(vp + 32 * e, m.cv_a);
 #pragma unroll
         for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, jn[r] + c, xpol));
       }
     });
   } else if (m.a.ptr) {
     const int e0 = __ldg(m.a.ptr + i), e1 = __ldg(m.a.ptr + i + 1);
-    by_kind(m.vk_a, [&](auto kc) {
-      constexpr int K = decltype(kc)::value;
+    by_kind(m.vk_a, [&](auto kc, auto cc) {
+      QSWG_KC(kc, cc);
 #pragma unroll 2
       for (int e = e0; e < e1; ++e) {
         const unsigned c = static_cast<unsigned>(__ldg(m.a.col + e));
-        const double2 v = ldv<K>(m.a.val + e);
+        const double2 v = opv<K, C>(m.a.val + e, m.cv_a);
 #pragma unroll
         for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, jn[r] + c, xpol));
       }
     });
   }
-  if (m.factored) {
+  if constexpr (kF == 1) {
     for (int k = 0; k < m.nk; ++k) {  // -w/2 L'(L X): columns j of W_k
       const KronList& rk = m.r[k];
       const int e0 = __ldg(rk.ptr + i), e1 = __ldg(rk.ptr + i + 1);
       const double2* wk = m.w[k];
-      by_kind(m.vk_r[k], [&](auto kc) {
-        constexpr int K = decltype(kc)::value;
+      by_kind(m.vk_r[k], [&](auto kc, auto cc) {
+        QSWG_KC(kc, cc);
 #pragma unroll 2
         for (int e = e0; e < e1; ++e) {
           const unsigned c = static_cast<unsigned>(__ldg(rk.col + e));
-          const double2 v = ldv<K>(rk.val + e);
+          const double2 v = opv<K, C>(rk.val + e, m.cv_r[k]);
 #pragma unroll
           for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(wk, jn[r] + c, xpol));
         }
@@ -949,20 +987,25 @@ __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2*
 }
 
 // acc += sum over operand row `row` of val * g(col) (warp-uniform row).
-template <int K, class G>
-__device__ __forceinline__ void uniform_row(const KronList& l, int row, double2& acc, G&& g) {
+#ifndef QSWG_ROW_UNROLL
+#define QSWG_ROW_UNROLL 4
+#endif
+constexpr int kRowUnroll = QSWG_ROW_UNROLL;
+template <int K, bool C, class G>
+__device__ __forceinline__ void uniform_row(const KronList& l, double2 cv, int row, double2& acc, G&& g) {
   const int e1 = __ldg(l.ptr + row + 1);
-#pragma unroll 4
-  for (int e = __ldg(l.ptr + row); e < e1; ++e) cfmak<K>(acc, ldv<K>(l.val + e), g(static_cast<unsigned>(__ldg(l.col + e))));
+#pragma unroll kRowUnroll
+  for (int e = __ldg(l.ptr + row); e < e1; ++e)
+    cfmak<K>(acc, opv<K, C>(l.val + e, cv), g(static_cast<unsigned>(__ldg(l.col + e))));
 }
 
 // acc[r] += sum over operand row rows[r] of val * g(col) for r < kKR, one
 // row after the other.  (Walking the kKR rows in lockstep was measured
 // slower on c2-c4.)
-template <int K, class G>
-__device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows, double2* acc, G&& g) {
+template <int K, bool C, class G>
+__device__ __forceinline__ void uniform_rows(const KronList& l, double2 cv, const int* rows, double2* acc, G&& g) {
 #pragma unroll
-  for (int r = 0; r < kKR; ++r) uniform_row<K>(l, rows[r], acc[r], g);
+  for (int r = 0; r < kKR; ++r) uniform_row<K, C>(l, cv, rows[r], acc[r], g);
 }
 
 // acc[r] += sum_k E(row0 + r, k) g(col) over the kKR consecutive rows row0 ..
@@ -970,25 +1013,40 @@ __device__ __forceinline__ void uniform_rows(const KronList& l, const int* rows,
 // entries per row: one warp load fetches all their column indices, which are
 // shuffled out, so the index -> gather chain skips an L1 round trip.  The
 // entries of each row are added in their stored order.
-template <int K, class G>
-__device__ __forceinline__ void shfl_rows(const KronEll& e, int len, int slice, int l0, double2* acc, G&& g) {
+template <int K, bool C, int L, class G>
+__device__ __forceinline__ void shfl_rows_len(const KronEll& e, double2 cv, int len, int base, int mycol, int l0,
+                                              double2* acc, G&& g) {
+  // L > 0: the row length as a constant (fully unrolled, constant shuffle lanes)
+  const int n_e = L > 0 ? L : len;
+#pragma unroll(L > 0 ? L : 2)
+  for (int k = 0; k < n_e; ++k) {
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const unsigned c = static_cast<unsigned>(__shfl_sync(0xffffffffu, mycol, kKR * k + r));
+      cfmak<K>(acc[r], opv<K, C>(e.val + base + 32 * k + l0 + r, cv), g(c));
+    }
+  }
+}
+template <int K, bool C, class G>
+__device__ __forceinline__ void shfl_rows(const KronEll& e, double2 cv, int len, int slice, int l0, double2* acc,
+                                          G&& g) {
   const int lane = threadIdx.x & 31;
   const int base = __ldg(e.sptr + slice);
   const int kt = lane >> 2, rt = lane & 3;
   const int mycol = kt < len ? __ldg(e.col + base + 32 * kt + l0 + rt) : 0;
-#pragma unroll 2
-  for (int k = 0; k < len; ++k) {
-#pragma unroll
-    for (int r = 0; r < kKR; ++r) {
-      const unsigned c = static_cast<unsigned>(__shfl_sync(0xffffffffu, mycol, kKR * k + r));
-      cfmak<K>(acc[r], ldv<K>(e.val + base + 32 * k + l0 + r), g(c));
-    }
+  if (len == 4) {  // square lattices (c2)
+    shfl_rows_len<K, C, 4>(e, cv, len, base, mycol, l0, acc, g);
+  } else if (len == 6) {  // cubic lattices (c5)
+    shfl_rows_len<K, C, 6>(e, cv, len, base, mycol, l0, acc, g);
+  } else {
+    shfl_rows_len<K, C, 0>(e, cv, len, base, mycol, l0, acc, g);
   }
 }
 
 // Row-indexed part, transposed (Hermitian path): acc[r] at (i[r], j), warp-
 // uniform rows i[r], lane = column j: A from conj X(j, c), R_k from the
-// row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).
+// row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).  Column lists pre-scaled.
+template <int kF>
 __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const double2* __restrict__ x, const int* i,
                                                   int j, double2* acc, unsigned long long xpol) {
   const unsigned n = static_cast<unsigned>(m.n);
@@ -996,46 +1054,45 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
   // rows i[r] = I*32 + 4w + r: lanes 4w .. 4w+3 of ELL slice I (clamped edge rows read
   // that slice's padding lanes, whose results are discarded)
   const int sl = i[0] >> 5, l0 = (threadIdx.x >> 5) * kKR;
-  by_kind(m.vk_a, [&](auto kc) {
-    constexpr int K = decltype(kc)::value;
-    const auto g = [&](unsigned c) { return conj2(gat(xj, c * n, xpol)); };
+  by_kind(m.vk_a, [&](auto kc, auto cc) {
+    QSWG_KC(kc, cc);
+    const auto g = [&](unsigned cn) { return conj2(gat(xj, cn, xpol)); };
     if (m.a_len > 0) {
-      shfl_rows<K>(m.a_ellu, m.a_len, sl, l0, acc, g);
-    } else if (m.a.ptr) {
-      uniform_rows<K>(m.a, i, acc, g);
+      shfl_rows<K, C>(m.a_ellu, m.cv_a, m.a_len, sl, l0, acc, g);
+    } else if (m.a_sc.ptr) {
+      uniform_rows<K, C>(m.a_sc, m.cv_a, i, acc, g);
     }
   });
-  if (m.factored) {
+  if constexpr (kF == 1) {
     for (int k = 0; k < m.nk; ++k) {
       const double2* wtj = m.wt[k] + j;
-      by_kind(m.vk_r[k], [&](auto kc) {
-        constexpr int K = decltype(kc)::value;
-        const auto g = [&](unsigned c) { return gat(wtj, c * n, xpol); };
+      by_kind(m.vk_r[k], [&](auto kc, auto cc) {
+        QSWG_KC(kc, cc);
+        const auto g = [&](unsigned cn) { return gat(wtj, cn, xpol); };
         if (m.r_len[k] > 0) {
-          shfl_rows<K>(m.r_ellu[k], m.r_len[k], sl, l0, acc, g);
+          shfl_rows<K, C>(m.r_ellu[k], m.cv_r[k], m.r_len[k], sl, l0, acc, g);
         } else {
-          uniform_rows<K>(m.r[k], i, acc, g);
+          uniform_rows<K, C>(m.r_sc[k], m.cv_r[k], i, acc, g);
         }
       });
     }
   }
-  unsigned in_[kKR];
-#pragma unroll
-  for (int r = 0; r < kKR; ++r) in_[r] = static_cast<unsigned>(i[r]) * n;
   if (m.p_rows) {  // P_k(j, a) W_k(i, a), lane = j: padding-free ELL rows of P_k, rows i of Wt_k
     const int sj = j >> 5, ln = j & 31;
     for (int k = 0; k < m.nk; ++k) {
       const KronEll& pe = m.p_ell[k];
-      const double2* wt = m.wt[k];
+      const double2* wr[kKR];
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) wr[r] = m.wt[k] + static_cast<unsigned>(i[r]) * n;
       const int b = __ldg(pe.sptr + sj), len = (__ldg(pe.sptr + sj + 1) - b) >> 5;
-      by_kind(m.vk_p[k], [&](auto kc) {
-        constexpr int K = decltype(kc)::value;
+      by_kind(m.vk_p[k], [&](auto kc, auto cc) {
+        QSWG_KC(kc, cc);
 #pragma unroll 2
         for (int e = 0; e < len; ++e) {
           const unsigned a = static_cast<unsigned>(__ldg(pe.col + b + 32 * e + ln));
-          const double2 v = ldv<K>(pe.val + b + 32 * e + ln);
+          const double2 v = opv<K, C>(pe.val + b + 32 * e + ln, m.cv_p[k]);
 #pragma unroll
-          for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(wt, in_[r] + a, xpol));
+          for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(wr[r], a, xpol));
         }
       });
     }
@@ -1043,15 +1100,18 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
   if (m.b_rows) {  // B(j, c) X(i, c) = B(j, c) conj x[n i + c], lane = j: padding-free ELL rows of B
     const int sj = j >> 5, ln = j & 31;
     const KronEll& be = m.b_ell;
+    const double2* xr[kKR];
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) xr[r] = x + static_cast<unsigned>(i[r]) * n;
     const int b = __ldg(be.sptr + sj), len = (__ldg(be.sptr + sj + 1) - b) >> 5;
-    by_kind(m.vk_b, [&](auto kc) {
-      constexpr int K = decltype(kc)::value;
+    by_kind(m.vk_b, [&](auto kc, auto cc) {
+      QSWG_KC(kc, cc);
 #pragma unroll 2
       for (int e = 0; e < len; ++e) {
         const unsigned c = static_cast<unsigned>(__ldg(be.col + b + 32 * e + ln));
-        const double2 v = ldv<K>(be.val + b + 32 * e + ln);
+        const double2 v = opv<K, C>(be.val + b + 32 * e + ln, m.cv_b);
 #pragma unroll
-        for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, conj2(gat(x, in_[r] + c, xpol)));
+        for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, conj2(gat(xr[r], c, xpol)));
       }
     });
   }
@@ -1059,58 +1119,58 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
 
 // Column-indexed part and diagonal terms at (i, j[r]), lane = row i.
 // kHerm: V_k = X L_k' = W_k' for Hermitian X, so V_k(i, a) = conj Wt_k[n a + i]
-// and no V_k is built.
-template <bool kHerm>
+// and no V_k is built.  (B, P_k, S_k lists and the S_k uniform ELL hold c * n.)
+template <bool kHerm, int kF>
 __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __restrict__ x, int i, const int* j,
                                           double2* acc, unsigned long long xpol) {
   const unsigned n = static_cast<unsigned>(m.n);
   if (!(kHerm && m.p_rows)) {  // (the Hermitian tiles applied P_k in the transposed section)
     for (int k = 0; k < m.nk; ++k) {
       const double2* wi = m.w[k] + i;  // P_k (x) Q_k = P_k applied to the columns of W_k = Q_k X
-      by_kind(m.vk_p[k], [&](auto kc) {
-        constexpr int K = decltype(kc)::value;
-        uniform_rows<K>(m.p[k], j, acc, [&](unsigned c) { return gat(wi, c * n, xpol); });
+      by_kind(m.vk_p[k], [&](auto kc, auto cc) {
+        QSWG_KC(kc, cc);
+        uniform_rows<K, C>(m.p[k], m.cv_p[k], j, acc, [&](unsigned cn) { return gat(wi, cn, xpol); });
       });
     }
   }
   if (m.b.ptr && !(kHerm && m.b_rows)) {  // B (x) I: coalesced columns c of X
     const double2* xi = x + i;
-    by_kind(m.vk_b, [&](auto kc) {
-      constexpr int K = decltype(kc)::value;
-      uniform_rows<K>(m.b, j, acc, [&](unsigned c) { return gat(xi, c * n, xpol); });
+    by_kind(m.vk_b, [&](auto kc, auto cc) {
+      QSWG_KC(kc, cc);
+      uniform_rows<K, C>(m.b, m.cv_b, j, acc, [&](unsigned cn) { return gat(xi, cn, xpol); });
     });
   }
-  if (m.factored) {
+  if constexpr (kF == 1) {
     for (int k = 0; k < m.nk; ++k) {  // -w/2 (X L') L: columns of V_k
-      by_kind(m.vk_s[k], [&](auto kc) {
-        constexpr int K = decltype(kc)::value;
+      by_kind(m.vk_s[k], [&](auto kc, auto cc) {
+        QSWG_KC(kc, cc);
         if constexpr (kHerm) {
           const double2* vi = m.wt[k] + i;
-          const auto g = [&](unsigned c) { return conj2(gat(vi, c * n, xpol)); };
+          const auto g = [&](unsigned cn) { return conj2(gat(vi, cn, xpol)); };
           if (m.s_len[k] > 0) {  // rows j[r] = J*32 + 4w + r: lanes 4w .. 4w+3 of slice J
-            shfl_rows<K>(m.s_ellu[k], m.s_len[k], j[0] >> 5, (threadIdx.x >> 5) * kKR, acc, g);
+            shfl_rows<K, C>(m.s_ellu[k], m.cv_s[k], m.s_len[k], j[0] >> 5, (threadIdx.x >> 5) * kKR, acc, g);
           } else {
-            uniform_rows<K>(m.s[k], j, acc, g);
+            uniform_rows<K, C>(m.s[k], m.cv_s[k], j, acc, g);
           }
         } else {
           const double2* vi = m.v[k] + i;
-          uniform_rows<K>(m.s[k], j, acc, [&](unsigned c) { return gat(vi, c * n, xpol); });
+          uniform_rows<K, C>(m.s[k], m.cv_s[k], j, acc, [&](unsigned cn) { return gat(vi, cn, xpol); });
         }
       });
     }
   }
-  unsigned jn[kKR];
+  const double2* xij[kKR];
 #pragma unroll
-  for (int r = 0; r < kKR; ++r) jn[r] = static_cast<unsigned>(j[r]) * n + static_cast<unsigned>(i);
+  for (int r = 0; r < kKR; ++r) xij[r] = x + (static_cast<unsigned>(j[r]) * n + static_cast<unsigned>(i));
   if (m.da) {  // the diagonals of A and B: (A_ii + B_jj) X(i, j), one gather
     const double2 dai = __ldg(m.da + i);
-    by_kind(m.vk_d, [&](auto kc) {
+    by_kind(m.vk_d & 3, [&](auto kc, auto) {
       constexpr int K = decltype(kc)::value;
 #pragma unroll
       for (int r = 0; r < kKR; ++r) {
         const double2 dbj = __ldg(m.db + j[r]);
         const double2 c = make_double2(dai.x + dbj.x, dai.y + dbj.y);
-        if (c.x != 0.0 || c.y != 0.0) cfmak<K>(acc[r], c, gat(x, jn[r], xpol));
+        if (c.x != 0.0 || c.y != 0.0) cfmak<K>(acc[r], c, ld_gather(xij[r], xpol));
       }
     });
   }
@@ -1119,7 +1179,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
     for (int r = 0; r < kKR; ++r) {
       if (i == j[r]) {  // transfer onto the diagonal
         const int e1 = __ldg(m.t.ptr + i + 1);
-        by_kind(m.vk_t, [&](auto kc) {
+        by_kind(m.vk_t & 3, [&](auto kc, auto) {
           constexpr int K = decltype(kc)::value;
           for (int e = __ldg(m.t.ptr + i); e < e1; ++e)
             cfmak<K>(acc[r], ldv<K>(m.t.val + e), gat(x, static_cast<unsigned>(__ldg(m.t.col + e)) * (n + 1), xpol));
@@ -1135,7 +1195,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
           0.5, __dadd_rn(__dadd_rn(__dmul_rn(m.omega, __dadd_rn(dli, __ldg(m.d_loc + j[r]))), dsi),
                          __ldg(m.d_ss + j[r])));
       if (d != 0.0) {
-        const double2 xg = gat(x, jn[r], xpol);
+        const double2 xg = ld_gather(xij[r], xpol);
         acc[r].x = fma(-d, xg.x, acc[r].x);
         acc[r].y = fma(-d, xg.y, acc[r].y);
       }
@@ -1143,30 +1203,26 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
   }
 }
 
-// Tile enumeration: J-major (blocks launched together share the columns J).
-// Hermitian mode enumerates the upper tiles I <= J only.
+// Tile enumeration (grid constants precomputed on the host, KronView::tg):
+// J-major over all tiles (blocks launched together share the columns J), or
+// in Hermitian mode the upper tiles I <= J in the order of the host table
+// tg.herm_tiles.
 struct TileGrid {
-  int n, nc, nti, ntj;
-  long long c0, ntiles;
+  int n, nc, nti;
+  int c0;
+  long long ntiles;
 };
 
 __device__ __forceinline__ TileGrid tile_grid(const KronView& m, bool herm) {
-  TileGrid g;
-  g.n = m.n;
-  g.nc = static_cast<int>(m.rows / m.n);
-  g.c0 = m.row0 / m.n;
-  g.nti = (g.n + kKT - 1) / kKT;
-  g.ntj = (g.nc + kKT - 1) / kKT;
-  g.ntiles = herm ? static_cast<long long>(g.nti) * (g.nti + 1) / 2 : static_cast<long long>(g.nti) * g.ntj;
-  return g;
+  return TileGrid{m.n, m.tg.nc, m.tg.nti, m.tg.c0, herm ? m.tg.ntiles_herm : m.tg.ntiles};
 }
 
-__device__ __forceinline__ void tile_coords(const TileGrid& g, bool herm, long long t, int& I, int& J) {
+__device__ __forceinline__ void tile_coords(const KronView& m, const TileGrid& g, bool herm, long long t, int& I,
+                                            int& J) {
   if (herm) {
-    J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
-    while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
-    while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
-    I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
+    const int2 ij = __ldg(m.tg.herm_tiles + t);
+    I = ij.x;
+    J = ij.y;
   } else {
     J = static_cast<int>(t / g.nti);
     I = static_cast<int>(t - static_cast<long long>(J) * g.nti);
@@ -1183,30 +1239,30 @@ template <bool kHerm, class Epi>
 __device__ __forceinline__ void kron_tile_emit(const TileGrid& g, int I, int J, const double2* acc,
                                                double2 (*tile)[kKT + 1], Epi&& epi) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int n = g.n;
+  const unsigned n = static_cast<unsigned>(g.n);
   const int iu = I * kKT + lane;
   const bool diag = kHerm && I == J;
+  const unsigned row0 = static_cast<unsigned>(J * kKT + kKR * w) * n + static_cast<unsigned>(iu);
 #pragma unroll
   for (int r = 0; r < kKR; ++r) {
     const int jt = kKR * w + r;  // column within the tile
     const int jl = J * kKT + jt;
     double2 y = acc[r];
     if (diag && lane == jt) y.y = 0.0;
-    epi(static_cast<unsigned>(jl) * static_cast<unsigned>(n) + static_cast<unsigned>(iu), y,
-        iu < n && jl < g.nc && (!diag || lane <= jt), false);
+    epi(row0 + static_cast<unsigned>(r) * n, y, iu < g.n && jl < g.nc && (!diag || lane <= jt), false);
     if (kHerm) tile[jt][lane] = acc[r];
   }
   if (kHerm) {
     __syncthreads();
     // mirror: element (row J*32 + lane, column I*32 + it) = conj Y(I*32 + it, J*32 + lane)
     const int jrow = J * kKT + lane;
+    const unsigned mrow0 = static_cast<unsigned>(I * kKT + kKR * w) * n + static_cast<unsigned>(jrow);
 #pragma unroll
     for (int r = 0; r < kKR; ++r) {
       const int it = kKR * w + r;
       const double2 v = tile[lane][it];
       const int icol = I * kKT + it;
-      epi(static_cast<unsigned>(icol) * static_cast<unsigned>(n) + static_cast<unsigned>(jrow), conj2(v),
-          jrow < n && icol < n && (!diag || lane > it), true);
+      epi(mrow0 + static_cast<unsigned>(r) * n, conj2(v), jrow < g.n && icol < g.n && (!diag || lane > it), true);
     }
     __syncthreads();
   }
@@ -1215,7 +1271,7 @@ __device__ __forceinline__ void kron_tile_emit(const TileGrid& g, int I, int J, 
 // Persistent loop over the tiles; epi(local_row, value, valid, mirror) runs on
 // every thread for every element (valid is false outside the matrix and for
 // the elements a Hermitian tile takes from its mirror).
-template <bool kHerm, class Epi>
+template <bool kHerm, int kF, class Epi>
 __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
   __shared__ double2 tile[kKT][kKT + 1];
   const unsigned long long xpol = evict_last_policy();
@@ -1223,14 +1279,14 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     int I, J;
-    tile_coords(g, kHerm, t, I, J);
+    tile_coords(m, g, kHerm, t, I, J);
     const int iu = I * kKT + lane;
     const int i = iu < g.n ? iu : g.n - 1;
     int jg[kKR];
 #pragma unroll
     for (int r = 0; r < kKR; ++r) {
       const int jl = J * kKT + kKR * w + r;
-      jg[r] = static_cast<int>(g.c0) + (jl < g.nc ? jl : g.nc - 1);
+      jg[r] = g.c0 + (jl < g.nc ? jl : g.nc - 1);
     }
     double2 acc[kKR];
     if constexpr (kHerm) {
@@ -1242,7 +1298,7 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
         acc[r] = make_double2(0.0, 0.0);
       }
       const int ju = J * kKT + lane;
-      kron_rows_uniform(m, x, ir, ju < g.n ? ju : g.n - 1, acc, xpol);
+      kron_rows_uniform<kF>(m, x, ir, ju < g.n ? ju : g.n - 1, acc, xpol);
 #pragma unroll
       for (int r = 0; r < kKR; ++r) tile[kKR * w + r][lane] = acc[r];  // [row][column] of the tile
       __syncthreads();
@@ -1252,9 +1308,9 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
     } else {
 #pragma unroll
       for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
-      kron_rows_lane(m, x, i, jg, acc, xpol);
+      kron_rows_lane<kF>(m, x, i, jg, acc, xpol);
     }
-    kron_cols<kHerm>(m, x, i, jg, acc, xpol);
+    kron_cols<kHerm, kF>(m, x, i, jg, acc, xpol);
     kron_tile_emit<kHerm>(g, I, J, acc, tile, epi);
   }
 }
@@ -1282,44 +1338,50 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
   const KronList& q = m.q[k];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int vk = m.vk_q[k];
+  const double2 cv = m.cv_q[k];
   for (long long t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     int I, J;
-    tile_coords(g, false, t, I, J);
+    tile_coords(m, g, false, t, I, J);
     double2 acc[kKR];
 #pragma unroll
     for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
     if constexpr (kHerm) {
       const int au = J * kKT + lane;  // column a (single GPU: c0 = 0)
       const double2* xa = x + (au < g.n ? au : g.n - 1);
-      const auto gx = [&](unsigned b) { return conj2(gat(xa, b * n, xpol)); };
+      const auto gx = [&](unsigned bn) { return conj2(gat(xa, bn, xpol)); };  // q_ellu / q_sc hold b * n
       if (m.q_len[k] > 0) {  // rows I*32 + 4w + r: lanes 4w .. 4w+3 of slice I
         const int iv0 = I * kKT + kKR * w;
-        by_kind(vk, [&](auto kc) {
-          shfl_rows<decltype(kc)::value>(m.q_ellu[k], m.q_len[k], (iv0 < g.n ? iv0 : g.n - 1) >> 5, kKR * w, acc, gx);
+        by_kind(vk, [&](auto kc, auto cc) {
+          QSWG_KC(kc, cc);
+          shfl_rows<K, C>(m.q_ellu[k], cv, m.q_len[k], (iv0 < g.n ? iv0 : g.n - 1) >> 5, kKR * w, acc, gx);
         });
-      } else if (q.ptr) {
+      } else if (m.q_sc[k].ptr) {
         int ir[kKR];
 #pragma unroll
         for (int r = 0; r < kKR; ++r) {
           const int iv = I * kKT + kKR * w + r;
           ir[r] = iv < g.n ? iv : g.n - 1;
         }
-        by_kind(vk, [&](auto kc) { uniform_rows<decltype(kc)::value>(q, ir, acc, gx); });
+        by_kind(vk, [&](auto kc, auto cc) {
+          QSWG_KC(kc, cc);
+          uniform_rows<K, C>(m.q_sc[k], cv, ir, acc, gx);
+        });
       }
+      const unsigned wrow = static_cast<unsigned>(I * kKT + kKR * w) * n + static_cast<unsigned>(au);
 #pragma unroll
       for (int r = 0; r < kKR; ++r) {
         const int iv = I * kKT + kKR * w + r;
-        if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + static_cast<unsigned>(iv) * n + static_cast<unsigned>(au), acc[r], xpol);
+        if (m.wt[k] && iv < g.n && au < g.n) st_hint(m.wt[k] + (wrow + static_cast<unsigned>(r) * n), acc[r], xpol);
         tile[kKR * w + r][lane] = acc[r];
       }
       if (!m.p_rows) {  // the column-major W_k (read by P_k in the normal orientation)
         __syncthreads();
         const int iu = I * kKT + lane;
+        const unsigned wcol = static_cast<unsigned>(J * kKT + kKR * w) * n + static_cast<unsigned>(iu);
 #pragma unroll
         for (int r = 0; r < kKR; ++r) {
           const int at = J * kKT + kKR * w + r;
-          if (iu < g.n && at < g.n)
-            st_hint(m.w[k] + static_cast<unsigned>(at) * n + static_cast<unsigned>(iu), tile[lane][kKR * w + r], xpol);
+          if (iu < g.n && at < g.n) st_hint(m.w[k] + (wcol + static_cast<unsigned>(r) * n), tile[lane][kKR * w + r], xpol);
         }
         __syncthreads();
       }
@@ -1335,15 +1397,15 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
         vj[r] = jl < g.nc;
         col[r] = static_cast<unsigned>(g.c0 + (vj[r] ? jl : g.nc - 1)) * n;
       }
-      by_kind(vk, [&](auto kc) {
-        constexpr int K = decltype(kc)::value;
+      by_kind(vk, [&](auto kc, auto cc) {
+        QSWG_KC(kc, cc);
         if (qe.sptr) {
           const int sl = i >> 5, ln = i & 31;
           const int b = __ldg(qe.sptr + sl), len = (__ldg(qe.sptr + sl + 1) - b) >> 5;
 #pragma unroll 2
           for (int e = 0; e < len; ++e) {
             const unsigned c = static_cast<unsigned>(__ldg(qe.col + b + 32 * e + ln));
-            const double2 v = ldv<K>(qe.val + b + 32 * e + ln);
+            const double2 v = opv<K, C>(qe.val + b + 32 * e + ln, cv);
 #pragma unroll
             for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, col[r] + c, xpol));
           }
@@ -1352,7 +1414,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
 #pragma unroll 2
           for (int e = __ldg(q.ptr + i); e < e1; ++e) {
             const unsigned c = static_cast<unsigned>(__ldg(q.col + e));
-            const double2 v = ldv<K>(q.val + e);
+            const double2 v = opv<K, C>(q.val + e, cv);
 #pragma unroll
             for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, gat(x, col[r] + c, xpol));
           }
@@ -1360,7 +1422,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
       });
 #pragma unroll
       for (int r = 0; r < kKR; ++r)
-        if (vi && vj[r]) st_hint(m.w[k] + col[r] + static_cast<unsigned>(i), acc[r], xpol);
+        if (vi && vj[r]) st_hint(m.w[k] + (col[r] + static_cast<unsigned>(i)), acc[r], xpol);
     }
   }
   if constexpr (kFlush) {
@@ -1376,7 +1438,8 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
   pdl_trigger();
 }
 
-// V_k = X L_k' on the local columns: V_k(i, a) = sum_c conj(L_k(a, c)) X(i, c).
+// V_k = X L_k' on the local columns: V_k(i, a) = sum_c conj(L_k(a, c)) X(i, c)
+// (U_k lists hold c * n).
 __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const double2* __restrict__ x, int k) {
   pdl_prologue();
   const unsigned long long xpol = evict_last_policy();
@@ -1387,18 +1450,19 @@ __global__ void __launch_bounds__(kThreads) kron_v_kernel(KronView m, const doub
     const long long g = m.row0 + r;
     const long long a = g / n, i = g - a * n;
     double2 acc = make_double2(0.0, 0.0);
-    by_kind(m.vk_u[k], [&](auto kc) {
-      uniform_row<decltype(kc)::value>(u, static_cast<int>(a), acc,
-                                       [&](unsigned c) { return gat(x + i, c * static_cast<unsigned>(n), xpol); });
+    const double2* xi = x + i;
+    by_kind(m.vk_u[k] & 3, [&](auto kc, auto) {
+      uniform_row<decltype(kc)::value, false>(u, double2{}, static_cast<int>(a), acc,
+                                              [&](unsigned cn) { return gat(xi, cn, xpol); });
     });
     st_hint(m.v[k] + g, acc, xpol);
   }
 }
 
-template <bool kHerm>
+template <bool kHerm, int kF>
 __global__ void __launch_bounds__(kThreads) kron_spmv_kernel(KronView m, const double2* x, double2* y, double scale) {
   pdl_prologue();
-  kron_tiles<kHerm>(m, x, [&](unsigned row, double2 acc, bool valid, bool) {
+  kron_tiles<kHerm, kF>(m, x, [&](unsigned row, double2 acc, bool valid, bool) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
@@ -1424,7 +1488,7 @@ struct KronStepArgs {
 #ifndef QSWG_KRON_STEP_MIN_BLOCKS
 #define QSWG_KRON_STEP_MIN_BLOCKS 3
 #endif
-template <bool kHerm>
+template <bool kHerm, int kF>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_STEP_MIN_BLOCKS) kron_step_term_kernel(KronStepArgs a) {
   pdl_prologue();
   StepCtl* ctl = a.ctl;
@@ -1433,7 +1497,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_STEP_MIN_BLOCKS) kron_step
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0, smax = 0;
   const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  kron_tiles<kHerm>(a.m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
+  kron_tiles<kHerm, kF>(a.m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
     if (!valid) return;
     const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
     const double2 sv0 = ld_once(a.sum_in + row, once);
@@ -1463,7 +1527,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_STEP_MIN_BLOCKS) kron_step
   }
 }
 
-template <bool kHerm>
+template <bool kHerm, int kF>
 __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_term_kernel(SeriesTermArgs a, KronView m) {
   pdl_prologue();
   if (series_skip(a.ctl)) return;
@@ -1472,7 +1536,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_te
   const unsigned long long keep = evict_last_policy();
   double2* const kp = a.kp;
   const double scale = a.scale;
-  kron_tiles<kHerm>(m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
+  kron_tiles<kHerm, kF>(m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
     series_store(kp, scale, row, acc, valid && !mirror, keep, tmax);
     if (valid && mirror) st_hint(kp + row, make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y)), keep);
   });
@@ -1697,11 +1761,10 @@ int sell_grid(K kernel, const SellView& m) {
 
 // Persistent launch geometry of a Kron kernel (no dynamic shared memory).
 template <class K>
-std::pair<int, std::size_t> kron_geom(K kernel, const KronView& m) {
+std::pair<int, std::size_t> kron_geom(K kernel, const KronView& m, bool herm = false) {
   const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel));
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
-  const long long nti = (m.n + kKT - 1) / kKT, ntj = (m.rows / (m.n > 0 ? m.n : 1) + kKT - 1) / kKT;
-  long long want = nti * ntj;
+  long long want = herm ? m.tg.ntiles_herm : m.tg.ntiles;
   if (want < 1) want = 1;
   return {static_cast<int>(want < cap ? want : cap), std::size_t{0}};
 }
@@ -1798,11 +1861,21 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
   if (m.format == Format::Kron) {
     KronStepArgs a{m.kron, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.kron.herm) {
-      const auto g = kron_geom(kron_step_term_kernel<true>, m.kron);
-      launch_pdl(kron_step_term_kernel<true>, g.first, kThreads, g.second, s, a);
+      if (m.kron.factored) {
+        const auto g = kron_geom(kron_step_term_kernel<true, 1>, m.kron, true);
+        launch_pdl(kron_step_term_kernel<true, 1>, g.first, kThreads, g.second, s, a);
+      } else {
+        const auto g = kron_geom(kron_step_term_kernel<true, 0>, m.kron, true);
+        launch_pdl(kron_step_term_kernel<true, 0>, g.first, kThreads, g.second, s, a);
+      }
     } else {
-      const auto g = kron_geom(kron_step_term_kernel<false>, m.kron);
-      launch_pdl(kron_step_term_kernel<false>, g.first, kThreads, g.second, s, a);
+      if (m.kron.factored) {
+        const auto g = kron_geom(kron_step_term_kernel<false, 1>, m.kron);
+        launch_pdl(kron_step_term_kernel<false, 1>, g.first, kThreads, g.second, s, a);
+      } else {
+        const auto g = kron_geom(kron_step_term_kernel<false, 0>, m.kron);
+        launch_pdl(kron_step_term_kernel<false, 0>, g.first, kThreads, g.second, s, a);
+      }
     }
   } else if (m.format == Format::Sell) {
     sell_partials(m, x, SkipCheck{nullptr, ctl, first_of_stage ? 1 : 0}, s);
@@ -1831,11 +1904,21 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
   const SeriesTermArgs a{x, kp, p, last ? 1 : 0, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Kron) {
     if (m.kron.herm) {
-      const auto g = kron_geom(kron_series_term_kernel<true>, m.kron);
-      launch_pdl(kron_series_term_kernel<true>, g.first, kThreads, g.second, s, a, m.kron);
+      if (m.kron.factored) {
+        const auto g = kron_geom(kron_series_term_kernel<true, 1>, m.kron, true);
+        launch_pdl(kron_series_term_kernel<true, 1>, g.first, kThreads, g.second, s, a, m.kron);
+      } else {
+        const auto g = kron_geom(kron_series_term_kernel<true, 0>, m.kron, true);
+        launch_pdl(kron_series_term_kernel<true, 0>, g.first, kThreads, g.second, s, a, m.kron);
+      }
     } else {
-      const auto g = kron_geom(kron_series_term_kernel<false>, m.kron);
-      launch_pdl(kron_series_term_kernel<false>, g.first, kThreads, g.second, s, a, m.kron);
+      if (m.kron.factored) {
+        const auto g = kron_geom(kron_series_term_kernel<false, 1>, m.kron);
+        launch_pdl(kron_series_term_kernel<false, 1>, g.first, kThreads, g.second, s, a, m.kron);
+      } else {
+        const auto g = kron_geom(kron_series_term_kernel<false, 0>, m.kron);
+        launch_pdl(kron_series_term_kernel<false, 0>, g.first, kThreads, g.second, s, a, m.kron);
+      }
     }
   } else if (m.format == Format::Sell) {
     sell_partials(m, x, SkipCheck{ctl, nullptr, 1}, s);
@@ -1927,11 +2010,21 @@ void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaSt
   if (m.format == Format::Kron) {
     kron_prepare(m, x, s);  // single-GPU product (multi-GPU callers exchange W first)
     if (m.kron.herm) {
-      const auto g = kron_geom(kron_spmv_kernel<true>, m.kron);
-      launch_pdl(kron_spmv_kernel<true>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
+      if (m.kron.factored) {
+        const auto g = kron_geom(kron_spmv_kernel<true, 1>, m.kron, true);
+        launch_pdl(kron_spmv_kernel<true, 1>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
+      } else {
+        const auto g = kron_geom(kron_spmv_kernel<true, 0>, m.kron, true);
+        launch_pdl(kron_spmv_kernel<true, 0>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
+      }
     } else {
-      const auto g = kron_geom(kron_spmv_kernel<false>, m.kron);
-      launch_pdl(kron_spmv_kernel<false>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
+      if (m.kron.factored) {
+        const auto g = kron_geom(kron_spmv_kernel<false, 1>, m.kron);
+        launch_pdl(kron_spmv_kernel<false, 1>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
+      } else {
+        const auto g = kron_geom(kron_spmv_kernel<false, 0>, m.kron);
+        launch_pdl(kron_spmv_kernel<false, 0>, g.first, kThreads, g.second, s, m.kron, x, y, scale);
+      }
     }
   } else if (m.format == Format::Sell) {
     sell_partials(m, x, SkipCheck{}, s);

@@ -329,13 +329,28 @@ MultiCsr strip_diagonal(const MultiCsr& m, std::vector<double2>& d) {
 }
 
 // kernels.hpp: value classes.  A list with no entries is "real" (no term).
-int value_class(const std::vector<double2>& v) {
-  bool re = true, im = true;
+// With `cv`, kValConst is added when every entry equals one value (*cv).
+int value_class(const std::vector<double2>& v, double2* cv = nullptr) {
+  bool re = true, im = true, same = !v.empty();
   for (const double2& x : v) {
     re = re && x.y == 0.0;
     im = im && x.x == 0.0;
+    same = same && x.x == v[0].x && x.y == v[0].y;
   }
-  return re ? dev::kValReal : im ? dev::kValImag : dev::kValComplex;
+  int k = re ? dev::kValReal : im ? dev::kValImag : dev::kValComplex;
+  if (cv && same && k != dev::kValComplex) {
+    *cv = v[0];
+    k |= dev::kValConst;
+  }
+  return k;
+}
+
+// Column offsets pre-multiplied by n (kernels.hpp: KronView), for the lists
+// the kernels gather as base + c n: c n < n^2 = dim < 2^31.
+MultiCsr scaled(const MultiCsr& m) {
+  MultiCsr o = m;
+  for (int& c : o.col) c *= static_cast<int>(m.n);
+  return o;
 }
 
 struct KronStore {
@@ -359,7 +374,8 @@ struct KronStore {
     const bool split = !(dk && dk[0] == '0');
     if (!split) {
       a_list = upload_list(a0, s);
-      b_list = upload_list(b0, s);
+      a_sc = upload_list(scaled(a0), s);
+      b_list = upload_list(scaled(b0), s);
       a = maybe_ell(a0, s);
       a_host = a0;
       b_host = b0;
@@ -367,7 +383,8 @@ struct KronStore {
       std::vector<double2> dah, dbh;
       const MultiCsr a1 = strip_diagonal(a0, dah), b1 = strip_diagonal(b0, dbh);
       a_list = upload_list(a1, s);
-      b_list = upload_list(b1, s);
+      a_sc = upload_list(scaled(a1), s);
+      b_list = upload_list(scaled(b1), s);
       a_host = a1;
       b_host = b1;
       a = maybe_ell(a1, s);
@@ -409,13 +426,13 @@ struct KronStore {
     // out by shuffle (the index -> gather chain starts without an L1 round trip).
     const char* ash = std::getenv("QSWG_KRON_ASHFL");  // experiment knob: 0 = no shuffled operand rows
     if (single && !(ash && ash[0] == '0') && uniform_slices(a_host) && a_host.ptr[1] - a_host.ptr[0] <= 8) {
-      a_ellu = upload_ell(to_ell(a_host), s);
+      a_ellu = upload_ell(to_ell(scaled(a_host)), s);
       a_len = a_host.ptr[1] - a_host.ptr[0];
     }
     for (std::size_t k = 0; k < host.q.size(); ++k) {  // Q_k, and R_k / S_k when factored
       const auto shfl = [&](const MultiCsr& m, dev::KronEll& e, int& len) {
         if (!single || (ash && ash[0] == '0') || !uniform_slices(m) || m.ptr[1] - m.ptr[0] > 8) return;
-        e = upload_ell(to_ell(m), s);
+        e = upload_ell(to_ell(scaled(m)), s);
         len = m.ptr[1] - m.ptr[0];
       };
       dev::KronEll e;
@@ -439,27 +456,49 @@ struct KronStore {
       b_rows = true;
     }
     if (const char* br = std::getenv("QSWG_KRON_BROWS")) b_rows = b_rows && br[0] == '1';  // experiment knob
-    vk_a = value_class(a_host.val);
-    vk_b = value_class(b_host.val);
+    vk_a = value_class(a_host.val, &cv_a);
+    vk_b = value_class(b_host.val, &cv_b);
     vk_t = value_class(host.t.val);
     for (std::size_t k = 0; k < host.p.size(); ++k) {
-      vk_p.push_back(value_class(host.p[k].val));
-      vk_q.push_back(value_class(host.q[k].val));
-      vk_r.push_back(factored ? value_class(host.r[k].val) : dev::kValComplex);
-      vk_s.push_back(factored ? value_class(host.sfac[k].val) : dev::kValComplex);
+      double2 c{};
+      vk_p.push_back(value_class(host.p[k].val, &c));
+      cv_p.push_back(c);
+      vk_q.push_back(value_class(host.q[k].val, &c));
+      cv_q.push_back(c);
+      vk_r.push_back(factored ? value_class(host.r[k].val, &c) : dev::kValComplex);
+      cv_r.push_back(c);
+      vk_s.push_back(factored ? value_class(host.sfac[k].val, &c) : dev::kValComplex);
+      cv_s.push_back(c);
       vk_u.push_back(factored ? value_class(host.u[k].val) : dev::kValComplex);
+      p_sc.push_back(upload_list(scaled(host.p[k]), s));
+      q_sc.push_back(upload_list(scaled(host.q[k]), s));
     }
     if (const char* vk = std::getenv("QSWG_KRON_VALCLASS"); vk && vk[0] == '0') {  // experiment knob: all complex
       vk_a = vk_b = vk_t = vk_d = dev::kValComplex;
       for (auto* v : {&vk_p, &vk_q, &vk_r, &vk_s, &vk_u}) std::fill(v->begin(), v->end(), dev::kValComplex);
+    } else if (vk && vk[0] == '1') {  // experiment knob: classes without the constant-value loads
+      vk_a &= 3;
+      vk_b &= 3;
+      for (auto* v : {&vk_p, &vk_q, &vk_r, &vk_s, &vk_u})
+        for (int& x : *v) x &= 3;
+    }
+    if (single) {  // the upper 32 x 32 tiles, J-major (kernels.hpp: KronTiles)
+      const int nti = static_cast<int>((host.n + 31) / 32);
+      std::vector<int2> tl;
+      tl.reserve(static_cast<std::size_t>(nti) * (nti + 1) / 2);
+      for (int J = 0; J < nti; ++J)
+        for (int I = 0; I <= J; ++I) tl.push_back(make_int2(I, J));
+      herm_tiles.resize(tl.size());
+      QSWG_CHECK(cudaMemcpyAsync(herm_tiles.get(), tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
     }
     if (factored) {
       af = upload_list(host.af, s);
       bf = upload_list(host.bf, s);
       for (std::size_t k = 0; k < host.r.size(); ++k) {
         r.push_back(upload_list(host.r[k], s));
-        sfac.push_back(upload_list(host.sfac[k], s));
-        u.push_back(upload_list(host.u[k], s));
+        r_sc.push_back(upload_list(scaled(host.r[k]), s));
+        sfac.push_back(upload_list(scaled(host.sfac[k]), s));
+        u.push_back(upload_list(scaled(host.u[k]), s));
       }
     }
     QSWG_CHECK(cudaStreamSynchronize(s));
@@ -483,6 +522,11 @@ struct KronStore {
   bool factored = false;
   int vk_a = dev::kValComplex, vk_b = dev::kValComplex, vk_t = dev::kValComplex, vk_d = dev::kValComplex;
   std::vector<int> vk_p, vk_q, vk_r, vk_s, vk_u;  // kernels.hpp: value classes
+  double2 cv_a{}, cv_b{};
+  std::vector<double2> cv_p, cv_q, cv_r, cv_s;
+  DeviceBuffer<int2> herm_tiles;               // one GPU: upper tiles in launch order
+  dev::KronList a_sc;                          // A (as a_list) with columns scaled by n
+  std::vector<dev::KronList> p_sc, q_sc, r_sc;  // P_k, Q_k, R_k with columns scaled by n
   dev::KronList af, bf;
   std::vector<dev::KronList> r, sfac, u;
 
@@ -694,7 +738,6 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.t = o.t;
     m.kron.nk = o.nk;
     for (int k = 0; k < o.nk; ++k) {
-      m.kron.p[k] = o.p[k];
       m.kron.q_ell[k] = kron_ell_ ? kron_->q[static_cast<std::size_t>(k)] : dev::KronEll{};
       m.kron.q[k] = o.q[k];
       if (kron_->factored) {
@@ -705,6 +748,28 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
       }
       m.kron.w[k] = kron_w_[static_cast<std::size_t>(k)].get();
       if (kron_->p_rows) m.kron.p_ell[k] = kron_->p_ell[static_cast<std::size_t>(k)];
+    }
+    m.kron.cv_a = kron_->cv_a;
+    m.kron.cv_b = kron_->cv_b;
+    m.kron.a_sc = kron_->a_sc;
+    for (std::size_t k = 0; k < kron_->cv_p.size(); ++k) {
+      m.kron.cv_p[k] = kron_->cv_p[k];
+      m.kron.cv_q[k] = kron_->cv_q[k];
+      m.kron.cv_r[k] = kron_->cv_r[k];
+      m.kron.cv_s[k] = kron_->cv_s[k];
+      m.kron.p[k] = kron_->p_sc[k];
+      m.kron.q_sc[k] = kron_->q_sc[k];
+      if (kron_->factored) m.kron.r_sc[k] = kron_->r_sc[k];
+    }
+    {
+      dev::KronTiles& tg = m.kron.tg;
+      tg.nc = static_cast<int>(block_.rows / n_);
+      tg.c0 = static_cast<int>(block_.row0 / n_);
+      tg.nti = static_cast<int>((n_ + 31) / 32);
+      tg.ntj = (tg.nc + 31) / 32;
+      tg.ntiles = static_cast<long long>(tg.nti) * tg.ntj;
+      tg.ntiles_herm = static_cast<long long>(tg.nti) * (tg.nti + 1) / 2;
+      tg.herm_tiles = kron_->herm_tiles.get();
     }
     m.kron.vk_a = kron_->vk_a;
     m.kron.vk_b = kron_->vk_b;

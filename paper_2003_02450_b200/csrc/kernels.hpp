@@ -97,7 +97,17 @@ struct KronEll {
 // Value class of an operand (KronView::vk_*): every stored value purely real,
 // purely imaginary, or general complex.  The kernels multiply the first two
 // with half the FMAs; the products they drop are exact zeros.
-inline constexpr int kValComplex = 0, kValReal = 1, kValImag = 2;
+// kValConst (or-ed in): every entry of the operand equals KronView::cv_*.
+inline constexpr int kValComplex = 0, kValReal = 1, kValImag = 2, kValConst = 4;
+
+// Tile grid of the KRON kernels (32 x 32 tiles of X over the local columns),
+// precomputed on the host: herm_tiles lists the upper tiles (I, J), I <= J,
+// in launch order (one GPU).
+struct KronTiles {
+  int nc = 0, c0 = 0, nti = 0, ntj = 0;
+  long long ntiles = 0, ntiles_herm = 0;
+  const int2* herm_tiles = nullptr;
+};
 
 struct KronView {
   int n = 0;
@@ -159,6 +169,12 @@ struct KronView {
   // term P_k, Q_k, R_k, S_k, U_k
   int vk_a = kValComplex, vk_b = kValComplex, vk_t = kValComplex, vk_d = kValComplex;
   int vk_p[kMaxKron] = {}, vk_q[kMaxKron] = {}, vk_r[kMaxKron] = {}, vk_s[kMaxKron] = {}, vk_u[kMaxKron] = {};
+  double2 cv_a{}, cv_b{}, cv_p[kMaxKron] = {}, cv_q[kMaxKron] = {}, cv_r[kMaxKron] = {}, cv_s[kMaxKron] = {};
+  // Column offsets: the lists gathered as base + c * n hold c * n already —
+  // b, p, s, u, every *_ellu and the Hermitian-path copies a_sc, r_sc, q_sc
+  // (a, r, q, a_ell, q_ell, p_ell, b_ell and t hold plain columns).
+  KronList a_sc, r_sc[kMaxKron], q_sc[kMaxKron];
+  KronTiles tg;
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
