@@ -137,15 +137,26 @@ def traffic_for(config, fmt):
         return None
 
 
-def workload_desc(w, extra=None):
-    d = {"workload": f"{w.name}: {'L-QSW' if w.kind == 'local' else 'G-QSW'} n={w.n} omega={w.omega} "
-                     f"t=[{w.t1},{w.tq}] outputs={w.steps + 1}",
-         "dim": w.dim, "outputs": w.steps + 1, "omega": w.omega, "kind": w.kind, "seed": w.seed,
-         "l2_policy": "no flush: one step (a whole series) streams far more than the 126 MB L2 "
-                      "(term ring, running sums, stored superoperator), so no input survives in L2 "
-                      "from one step to the next"}
-    d.update(extra or {})
-    return d
+def workload_desc(w):
+    """The workload, identical in both arms (implementation details go to
+    `impl_config`)."""
+    return {"workload": f"{w.name}: {'L-QSW' if w.kind == 'local' else 'G-QSW'} n={w.n} omega={w.omega} "
+                        f"t=[{w.t1},{w.tq}] outputs={w.steps + 1}",
+            "dim": w.dim, "outputs": w.steps + 1, "omega": w.omega, "kind": w.kind, "seed": w.seed,
+            "l2_policy": "no flush: one step (a whole series) streams far more than the 126 MB L2 "
+                         "(term ring, running sums, stored superoperator), so no input survives in L2 "
+                         "from one step to the next"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ------------------------------------------------------------ reference arm
@@ -173,10 +184,12 @@ def run_reference(args, w, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
             "data": "synthetic (seeded, BASELINE.json config)",
-            "config": workload_desc(w, {"parallelism": f"{cores} host threads (reference WorkerPool)",
-                                        "build_norms_s": build_s, "spmvs_per_step": spmvs,
-                                        "library": os.path.relpath(o.path, ROOT)}),
+            "config": workload_desc(w),
+            "impl_config": {"parallelism": f"{cores} host threads (reference WorkerPool)",
+                            "build_norms_s": build_s, "spmvs_per_step": spmvs,
+                            "library": os.path.relpath(o.path, ROOT)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "cpu_model": cpu_model(),
                              "sample": f"full {w.name} series ({w.steps + 1} outputs) per step, "
                                        f"n_workers={cores}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -199,7 +212,7 @@ def cpu_baseline(w):
     t0 = time.perf_counter()
     _, _, nsp = h.series(rho0_vec(w.n, w.rho0), w.t1, w.tq, w.steps, states=False, pops=True)
     sec = time.perf_counter() - t0
-    return {"value": w.steps / sec, "unit": UNIT, "cores": cores, "kind": kind,
+    return {"value": w.steps / sec, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
             "sample": f"one full {w.name} series ({w.steps + 1} outputs, {nsp} SpMVs) in {sec:.2f} s; "
                       f"library {os.path.relpath(o.path, ROOT)}"}
 
@@ -218,6 +231,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="debug: no clock sampling (its NVML queries)")
     ap.add_argument("--no-superop", action="store_true", help="skip the stored-superoperator comparison")
+    ap.add_argument("--configs", default="c3,c4,c5",
+                    help="other BASELINE configs measured on one GPU after the headline ('' to skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -261,25 +276,35 @@ def main():
     v = l.state().from_probabilities(w.rho0)
 
     # ---- end to end through the public API, host buffers ----
-    # (measured before the device-resident region: the nvidia-smi clock sampler's
-    # start/stop around that region perturbs the GPU for a while)
+    # (measured before the device-resident region: the clock sampler's start
+    # and stop around that region perturb the GPU for a while).  Host buffers
+    # are page-locked by the library (qswg_host_alloc), so every step's H2D of
+    # vec(rho(0)) and D2H of the populations are direct DMA transfers.
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    vec_host = torch.zeros(2 * l.rows, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    vec_host = api.pinned_empty(l.rows, np.complex128)
+    vec_host[:] = 0
     diag = np.arange(w.n) * (w.n + 1) - l.row0
     own = (diag >= 0) & (diag < l.rows)
     vec_host[diag[own]] = w.rho0[own]
-    full_vec = vec_host if world == 1 else None
-    pops_host = torch.zeros((w.steps + 1) * w.n, dtype=torch.float64, pin_memory=True).numpy().reshape(w.steps + 1, w.n)
+    pops_host = api.pinned_empty((w.steps + 1, w.n), np.float64)
     e2e_state = l.state()
+    impl_rows = l.rows
     for _ in range(args.warmup):  # the second identical call captures the series graph: keep it out of the timing
         e2e_state.upload_local(vec_host)
         api.series(l, e2e_state, w.t1, w.tq, w.steps, pops_out=pops_host)
     barrier()
+    host_parts = {"upload_ms": [], "series_call_ms": [], "series_device_ms": []}
     ev0.record(stream)
     for _ in range(args.steps):
-        e2e_state.upload_local(vec_host)                                   # H2D of vec(rho(0))
-        api.series(l, e2e_state, w.t1, w.tq, w.steps, pops_out=pops_host)  # + D2H populations
+        h0 = time.perf_counter()
+        e2e_state.upload_local(vec_host)                                        # H2D of vec(rho(0))
+        h1 = time.perf_counter()
+        r_e2e = api.series(l, e2e_state, w.t1, w.tq, w.steps, pops_out=pops_host)  # + D2H populations
+        h2 = time.perf_counter()
+        host_parts["upload_ms"].append(1e3 * (h1 - h0))
+        host_parts["series_call_ms"].append(1e3 * (h2 - h1))
+        host_parts["series_device_ms"].append(float(r_e2e.info.device_ms))
     ev1.record(stream)
     barrier()
     e2e_ms = ev0.elapsed_time(ev1) / args.steps
@@ -287,7 +312,10 @@ def main():
         t = torch.tensor([e2e_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    del full_vec
+    e2e_parts = {k: float(np.median(v)) for k, v in host_parts.items()}
+    e2e_parts["note"] = ("host wall time per call (median): upload = H2D + the one-time Hermiticity check of the "
+                         "uploaded state (one synchronisation); series call = enqueue/graph replay + D2H of the "
+                         "populations + one synchronisation; series_device_ms = CUDA events around the series")
 
     # ---- device-resident timed region ----
     for _ in range(args.warmup):  # (re-)captures this call's series graph
@@ -314,27 +342,9 @@ def main():
     d_active = int(info.d) if info.path == 2 else 1
     peak, peak_src = load_peaks()
     n_lind = len(w.ops) if w.kind == "global" else 0
-
-    def term_bytes(lv):
-        """Algorithmic HBM bytes of one term-kernel launch: the
-        input x read once, K_p written once, plus the stored superoperator
-        (20 B/nnz + 8 B/row) or, matrix-free, the W_k (and V_k) work vectors
-        read once."""
-        vec = 16 * lv.dim + 16 * lv.rows
-        if lv.format == "kron":  # W_k and/or its row-major copy, as the kernels read them
-            return vec + 16 * n_lind * lv.dim * int(lv.info.kron_term_vectors)
-        return vec + 20 * int(lv.info.nnz_local) + 8 * (lv.rows + 1)
-
-    def prepare_bytes(lv):
-        """Kron prepare kernels: x read once per Lindblad term, W_k and/or its
-        row-major copy written."""
-        if lv.format != "kron":
-            return 0
-        return n_lind * (1 + int(lv.info.kron_term_vectors)) * 16 * lv.dim
-
     parts = l.time_series_parts(iters=20, count=d_active)
     term_ms = parts["term"]
-    achieved = term_bytes(l) / (term_ms * 1e-3) / 1e9
+    achieved = term_bytes(l, n_lind) / (term_ms * 1e-3) / 1e9
     share = info.spmvs * term_ms / ms_per_step
     kernel_name = {"kron": "kron_series_term_kernel", "sell": "sell_series_term_kernel",
                    "csr": "series_term_kernel"}[l.format]
@@ -342,9 +352,32 @@ def main():
                   "prepare_kernels": ("kron_w_kernel" + ((" (W_k and its row-major copy; V_k = conj Wt_k)" if world == 1
                                                           else " + kron_v_kernel") if l.info.kron_factored else ""))
                   if l.format == "kron" else None,
-                  "prepare_gbs": prepare_bytes(l) / (parts["prepare"] * 1e-3) / 1e9 if parts["prepare"] > 0 else None,
+                  "prepare_gbs": prepare_bytes(l, n_lind) / (parts["prepare"] * 1e-3) / 1e9 if parts["prepare"] > 0 else None,
                   "flush_kernel": "series_flush_kernel (amortised over the term ring)",
                   "count": d_active}
+    impl_config = {
+        "parallelism": f"row-block x{world}" if world > 1 else "1 GPU", "nnz": int(l.nnz),
+        "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell),
+        "build_norms_s": build_s, "one_norms": l.one_norms().tolist(), "group": int(l.group),
+        "plan": {"path": int(info.path), "span": [int(info.span_m_star), int(info.span_s)],
+                 "d": int(info.d), "n_super": int(info.n_super), "remainder": int(info.remainder),
+                 "sub_m_star": int(info.sub_m_star)},
+        "spmvs_per_step": int(info.spmvs)}
+    roofline = {"bound": "l2" if l.format == "kron" else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic_for(w.name, l.format), "kernel": kernel_name,
+                "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell),
+                "bytes_per_launch": term_bytes(l, n_lind), "ms_per_launch": term_ms,
+                "peak_source": peak_src, "share_of_step": share, "parts": parts_line}
+    if l.format == "kron":
+        l2b = l2_for(w.name, l.format)
+        roofline["bound_note"] = (
+            "matrix-free (KRON) term: its algorithmic HBM bytes (x read, K_p written, W_k read) are small; "
+            "the bound is the SM<-L2 traffic of its ~20 operand-weighted 512-byte segment gathers per element "
+            "and the dependent index -> gather -> FMA chains (DESIGN.md section 3); achieved/frac are reported "
+            "against HBM as the contract asks.  The stored-superoperator kernel (superop_spmv) is the HBM-bound one.")
+        if l2b:
+            roofline["l2"] = {"bytes_per_launch": l2b, "achieved_gbs": l2b / (term_ms * 1e-3) / 1e9,
+                              "source": "ncu lts__t_sectors_srcunit_tex (profiles/traffic.json)"}
 
     # ---- the stored-superoperator SpMV (BASELINE's "superop SpMV HBM GB/s") ----
     superop = None
@@ -361,7 +394,7 @@ def main():
         vs = ls.state().from_probabilities(w.rho0)
         api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)  # warm-up
         rs = api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)
-        sb = term_bytes(ls)
+        sb = term_bytes(ls, n_lind)
         superop = {"format": ls.format, "kernel": "sell_series_term_kernel" if ls.format == "sell" else
                    "series_term_kernel", "bytes_per_launch": sb, "ms_per_launch": s_ms,
                    "achieved_gbs": sb / (s_ms * 1e-3) / 1e9, "frac": sb / (s_ms * 1e-3) / 1e9 / peak,
@@ -371,6 +404,13 @@ def main():
         del ls, vs
         l = lk
 
+    # ---- the other BASELINE configs on one GPU (assembly excluded) ----
+    configs = None
+    if world == 1 and args.configs:
+        del l
+        l = None
+        configs = [config_block(name, peak) for name in args.configs.split(",") if name]
+
     if rank != 0:
         return 0
     line = {
@@ -378,29 +418,14 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "complex128",
         "data": "synthetic (seeded graph of BASELINE.json config; no public dataset exists for this path)",
-        "config": workload_desc(w, {
-            "parallelism": f"row-block x{world}" if world > 1 else "1 GPU", "nnz": int(l.nnz),
-            "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell),
-            "build_norms_s": build_s, "one_norms": l.one_norms().tolist(), "group": int(l.group),
-            "plan": {"path": int(info.path), "span": [int(info.span_m_star), int(info.span_s)],
-                     "d": int(info.d), "n_super": int(info.n_super), "remainder": int(info.remainder),
-                     "sub_m_star": int(info.sub_m_star)},
-            "spmvs_per_step": int(info.spmvs)}),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_for(w.name, l.format), "kernel": kernel_name,
-                     "format": l.format, "kron_factored": bool(l.info.kron_factored), "kron_ell": bool(l.info.kron_ell), "bytes_per_launch": term_bytes(l), "ms_per_launch": term_ms,
-                     "peak_source": peak_src, "share_of_step": share, "parts": parts_line,
-                     "l2": ({"bytes_per_launch": l2_for(w.name, l.format),
-                             "achieved_gbs": l2_for(w.name, l.format) / (term_ms * 1e-3) / 1e9,
-                             "note": "gather traffic SM<-L2 (ncu lts__t_sectors_srcunit_tex). The KRON term "
-                                     "kernel is bound by neither HBM nor L2: with every gather folded into L1 "
-                                     "it is only 7% faster (profiles/r01_kron_gather_fold.jsonl); it is bound "
-                                     "by its dependent operand-index -> gather -> FMA chains (ncu: 21 cycles "
-                                     "per issued instruction, 28.5 warps/SM, DESIGN.md section 3)"}
-                            if l2_for(w.name, l.format) else None)},
+        "config": workload_desc(w),
+        "impl_config": impl_config,
+        "roofline": roofline,
         "superop_spmv": superop,
-        "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * l.dim,
-                "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms},
+        "configs": configs,
+        "e2e": {"value": w.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 16 * int(impl_rows),
+                "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms, "h2d_pinned": True,
+                "parts": e2e_parts},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
@@ -408,6 +433,80 @@ def main():
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def term_bytes(lv, n_lind):
+    """Algorithmic HBM bytes of one term-kernel launch: the
+    input x read once, K_p written once, plus the stored superoperator
+    (20 B/nnz + 8 B/row) or, matrix-free, the W_k (and V_k) work vectors
+    read once."""
+    vec = 16 * lv.dim + 16 * lv.rows
+    if lv.format == "kron":  # W_k and/or its row-major copy, as the kernels read them
+        return vec + 16 * n_lind * lv.dim * int(lv.info.kron_term_vectors)
+    return vec + 20 * int(lv.info.nnz_local) + 8 * (lv.rows + 1)
+
+
+def prepare_bytes(lv, n_lind):
+    """Kron prepare kernels: x read once per Lindblad term, W_k and/or its
+    row-major copy written."""
+    if lv.format != "kron":
+        return 0
+    return n_lind * (1 + int(lv.info.kron_term_vectors)) * 16 * lv.dim
+
+
+def config_block(name, peak):
+    """One BASELINE config on one GPU: the default (matrix-free) series with
+    assembly excluded — series time, SpMVs, plan, the dominant kernel's
+    algorithmic bytes and fraction — and the stored-superoperator SpMV
+    (SELL-C-sigma, column panels where x exceeds L2) with its HBM fraction."""
+    from paper_2003_02450_b200 import api, graphs
+    w = graphs.config(name)
+    n_lind = len(w.ops) if w.kind == "global" else 0
+
+    def build(fmt):
+        if w.kind == "local":
+            return api.build_local(w.omega, w.h, w.ops[0], format=fmt)
+        return api.build_global(w.omega, w.h, w.ops, format=fmt)
+
+    out = {"config": name, "workload": workload_desc(w)["workload"], "dim": int(w.dim)}
+    t0 = time.perf_counter()
+    l = build("auto")
+    out["build_s"] = time.perf_counter() - t0
+    out["nnz"] = int(l.nnz)
+    out["format"] = l.format
+    v = l.state().from_probabilities(w.rho0)
+    # warm-up: allocates the workspace (term ring, sums) with a short series of the same plan shape
+    api.series(l, v, w.t1, w.t1 + (w.tq - w.t1) / w.steps * 2, 2, populations=False)
+    reps = 1 if w.dim > 100_000_000 else 2  # c5: one 14 s series
+    best = None
+    for _ in range(reps):
+        r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
+        best = r.info.device_ms if best is None else min(best, r.info.device_ms)
+    info = r.info
+    out.update({"series_ms": float(best), "output_steps_per_s": w.steps / (best / 1e3), "spmvs": int(info.spmvs),
+                "plan": [int(info.path), int(info.span_m_star), int(info.span_s), int(info.d), int(info.sub_m_star)],
+                "trace_err": float(abs(r.populations[-1].sum() - 1)) if r.populations is not None else None})
+    d_active = int(info.d) if info.path == 2 else 1
+    parts = l.time_series_parts(iters=10 if w.dim > 100_000_000 else 20, count=d_active)
+    tb = term_bytes(l, n_lind)
+    out["dominant"] = {"kernel": "kron_series_term_kernel" if l.format == "kron" else "sell_series_term_kernel",
+                       "bytes_per_launch": tb, "ms_per_launch": parts["term"],
+                       "achieved_gbs": tb / (parts["term"] * 1e-3) / 1e9,
+                       "frac": tb / (parts["term"] * 1e-3) / 1e9 / peak,
+                       "bound": "l2" if l.format == "kron" else "hbm",
+                       "prepare_ms": parts["prepare"], "flush_ms": parts["flush"],
+                       "note": ("path 1 (c3): its series runs kron_step_term_kernel, the same tiles plus "
+                                "the running-sum epilogue" if info.path == 1 else None)}
+    del l, v
+    ls = build("sell")
+    sp = ls.time_series_parts(iters=5 if w.dim > 10_000_000 else 20, count=d_active)
+    sb = term_bytes(ls, n_lind)
+    out["superop_spmv"] = {"format": ls.format, "panels": int(ls.info.sell_panels), "padding": float(ls.padding),
+                           "bytes_per_launch": sb, "ms_per_launch": sp["term"],
+                           "achieved_gbs": sb / (sp["term"] * 1e-3) / 1e9,
+                           "frac": sb / (sp["term"] * 1e-3) / 1e9 / peak}
+    del ls
+    return out
 
 
 if __name__ == "__main__":

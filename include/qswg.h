@@ -92,6 +92,11 @@ typedef struct {
 const char* qswg_last_error(void);
 int qswg_version(int* major, int* minor);
 int qswg_device_count(int* count);
+/* Page-locked host buffers (cudaHostAlloc / cudaFreeHost): uploads from and
+ * population reads into them are DMA transfers without a staging copy.  No
+ * reference counterpart (host vectors are std::vector there). */
+int qswg_host_alloc(int64_t bytes, void** out);
+void qswg_host_free(void* p);
 
 /* ---- host sparse matrices (sparse.hpp:29-84) ---------------------------- */
 /* SparseMatrix::from_triplets (sparse.hpp:35-37): sort, sum duplicates, drop zeros. */
@@ -159,7 +164,10 @@ int qswg_liouvillian_stream(const qswg_liouvillian* l, void** stream);
 
 /* ---- states (state.hpp:13-27, walk.hpp:57-66) --------------------------- */
 int qswg_state_create(const qswg_liouvillian* l, qswg_state** out);
-/* StateVector::scatter(full) — uploads this rank's rows of a full host vec(rho) */
+/* StateVector::scatter(full) — uploads this rank's rows of a full host vec(rho).
+ * On one GPU (matrix-free format) the state's exact Hermiticity is checked on
+ * the device here, once, so later step/series calls on it do not synchronise
+ * for it. */
 int qswg_state_upload(qswg_state* s, const double* vec);
 /* WalkSystem::initial_state(probabilities) (walk.cpp:101-126), built on the device */
 int qswg_state_from_probabilities(qswg_state* s, const double* p, int64_t n);

@@ -110,6 +110,8 @@ SIGNATURES = {
     "qswg_last_error": (C.c_char_p, []),
     "qswg_version": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "qswg_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "qswg_host_alloc": (C.c_int, [i64, C.POINTER(vp)]),
+    "qswg_host_free": (None, [vp]),
     "qswg_sparse_from_triplets": (C.c_int, [i64, i64, i64, i64p, i64p, dp, C.POINTER(vp)]),
     "qswg_sparse_from_csr": (C.c_int, [i64, i64, i64p, i64p, dp, C.POINTER(vp)]),
     "qswg_sparse_shape": (C.c_int, [vp, i64p, i64p, i64p]),

@@ -37,6 +37,32 @@ def _cplx(a, n=None):
     return a
 
 
+class _Pinned:
+    """Owner of one qswg_host_alloc block (freed with the last array view)."""
+
+    def __init__(self, nbytes):
+        self.ptr = C.c_void_p()
+        check(lib.qswg_host_alloc(int(nbytes), C.byref(self.ptr)))
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) is not None and self.ptr.value:
+            lib.qswg_host_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (qswg_host_alloc): uploads from
+    it and population reads into it are direct DMA transfers.  The block is
+    freed when the last view of the array goes away."""
+    dt = np.dtype(dtype)
+    shape = tuple(int(d) for d in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+    owner = _Pinned(max(int(np.prod(shape)) * dt.itemsize, 1))
+    owner.__array_interface__ = {"shape": shape, "typestr": dt.str, "data": (owner.ptr.value, False),
+                                 "version": 3}
+    return np.asarray(owner)  # .base is the owner
+
+
 # --------------------------------------------------------------- sparse
 class SparseMatrix:
     """Host canonical CSR (sparse.hpp:29-84) owned by the C library."""

@@ -40,6 +40,10 @@ struct qswg_container {
 struct qswg_state {
   const qswg_liouvillian* owner;
   qswg::DeviceBuffer<double2> v;  // local rows
+  // exact Hermiticity of the matrix held (1 / 0), -1 unknown: checked once at
+  // upload, known for states built from probabilities and for outputs of the
+  // Hermitian kernels, so step/series need no check (and no synchronisation)
+  int herm = -1;
 };
 
 namespace qswg {
@@ -134,6 +138,19 @@ int qswg_version(int* major, int* minor) {
     *major = QSWG_VERSION_MAJOR;
     *minor = QSWG_VERSION_MINOR;
   });
+}
+
+int qswg_host_alloc(int64_t bytes, void** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (bytes < 0) throw std::invalid_argument("bytes must be non-negative");
+    *out = nullptr;
+    if (bytes > 0) QSWG_CHECK(cudaHostAlloc(out, static_cast<std::size_t>(bytes), cudaHostAllocPortable));
+  });
+}
+
+void qswg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int qswg_device_count(int* count) {
@@ -473,6 +490,7 @@ int qswg_state_upload(qswg_state* s, const double* vec) {
     QSWG_CHECK(cudaMemcpyAsync(s->v.get(), vec + 2 * L.block().row0,
                                static_cast<std::size_t>(L.block().rows) * sizeof(double2),
                                cudaMemcpyHostToDevice, L.stream()));
+    s->herm = L.hermitian_state(s->v.get());  // (synchronises; -1 where no kernel uses it)
     QSWG_CHECK(cudaStreamSynchronize(L.stream()));
   });
 }
@@ -496,6 +514,7 @@ int qswg_state_from_probabilities(qswg_state* s, const double* p, int64_t n) {
     QSWG_CHECK(cudaMemcpyAsync(dp.get(), p, dp.bytes(), cudaMemcpyHostToDevice, L.stream()));
     qswg::dev::state_from_probabilities(s->v.get(), L.block().row0, L.block().rows, L.n(), dp.get(), L.stream());
     QSWG_CHECK(cudaStreamSynchronize(L.stream()));
+    s->herm = 1;  // a real diagonal matrix
   });
 }
 
@@ -586,7 +605,8 @@ int qswg_step(const qswg_liouvillian* l, const qswg_state* v, double t, double t
     check_state(l, out, "out");
     if (out == v) throw std::invalid_argument("step output must not alias its input");
     const auto& params = qswg::build_theta_table(tolerance);
-    const qswg::StepInfo si = qswg::step(*l->l, v->v.get(), t, params, out->v.get());
+    const qswg::StepInfo si = qswg::step(*l->l, v->v.get(), t, params, out->v.get(), v->herm);
+    const_cast<qswg_state*>(out)->herm = l->l->hermitian_mode() ? 1 : -1;  // mirrored tiles: exactly Hermitian
     if (info) *info = {si.m_star, si.s, si.spmvs, si.launches};
   });
 }
@@ -640,17 +660,20 @@ int qswg_series_observe(const qswg_liouvillian* l, const qswg_state* v, double t
       graph_key.push_back(lm->pops.get());
       if (coherence_host) graph_key.push_back(lm->coh.get());
     }
-    const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit, graph_key);
-    if (L.comm() && L.comm()->world() > 1)  // every diagonal element has exactly one owner
-      L.comm()->allreduce_sum_f64(lm->pops.get(), static_cast<std::size_t>((steps + 1) * n), s);
-    if (coherence_host && L.comm() && L.comm()->world() > 1)
-      L.comm()->allreduce_max_u64(lm->coh.get(), static_cast<std::size_t>(steps + 1), s);
-    QSWG_CHECK(cudaEventRecord(e1, s));
-    if (pops_host)
-      QSWG_CHECK(cudaMemcpyAsync(pops_host, lm->pops.get(), lm->pops.bytes(), cudaMemcpyDeviceToHost, s));
-    if (coherence_host)  // bit patterns of non-negative doubles are the doubles
-      QSWG_CHECK(cudaMemcpyAsync(coherence_host, lm->coh.get(), lm->coh.bytes(), cudaMemcpyDeviceToHost, s));
-    QSWG_CHECK(cudaStreamSynchronize(s));
+    // the outputs' reads are enqueued before the call's one synchronisation
+    const auto reads = [&] {
+      if (L.comm() && L.comm()->world() > 1)  // every diagonal element has exactly one owner
+        L.comm()->allreduce_sum_f64(lm->pops.get(), static_cast<std::size_t>((steps + 1) * n), s);
+      if (coherence_host && L.comm() && L.comm()->world() > 1)
+        L.comm()->allreduce_max_u64(lm->coh.get(), static_cast<std::size_t>(steps + 1), s);
+      QSWG_CHECK(cudaEventRecord(e1, s));
+      if (pops_host)
+        QSWG_CHECK(cudaMemcpyAsync(pops_host, lm->pops.get(), lm->pops.bytes(), cudaMemcpyDeviceToHost, s));
+      if (coherence_host)  // bit patterns of non-negative doubles are the doubles
+        QSWG_CHECK(cudaMemcpyAsync(coherence_host, lm->coh.get(), lm->coh.bytes(), cudaMemcpyDeviceToHost, s));
+    };
+    const qswg::SeriesInfo si = qswg::series(L, v->v.get(), t1, tq, steps, params, emit, graph_key, v->herm, reads);
+    if (final_state) final_state->herm = L.hermitian_mode() ? 1 : -1;
     float ms = 0.f;
     QSWG_CHECK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);

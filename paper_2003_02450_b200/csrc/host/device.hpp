@@ -65,6 +65,24 @@ class DeviceBuffer {
   std::size_t n_ = 0;
 };
 
+// Page-locked host memory (cudaHostAlloc): stream-ordered copies into it stay
+// asynchronous, so several small reads share one synchronisation.
+template <class T>
+class PinnedBuffer {
+ public:
+  PinnedBuffer() = default;
+  explicit PinnedBuffer(std::size_t n) { QSWG_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&p_), n * sizeof(T), 0)); }
+  ~PinnedBuffer() {
+    if (p_) cudaFreeHost(p_);
+  }
+  PinnedBuffer(const PinnedBuffer&) = delete;
+  PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  T* get() const { return p_; }
+
+ private:
+  T* p_ = nullptr;
+};
+
 // Makes `device` current for the scope and restores the previous device.
 class DeviceGuard {
  public:

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstddef>
 #include <cstring>
+#include <functional>
 #include <utility>
 #include <vector>
 
@@ -66,17 +67,23 @@ struct Flags {
   std::int64_t spmvs = 0;
 };
 
-Flags read_flags(const Liouvillian& l, bool with_series) {
-  int se[2] = {0, 0}, re[2] = {0, 0};
+// The error flags and SpMV counters of the call, read into pinned memory
+// (asynchronous copies) after the caller's own reads, one synchronisation.
+Flags read_flags(const Liouvillian& l, bool with_series, const std::function<void()>& before_sync = {}) {
+  Workspace& ws = l.workspace();
+  if (!ws.flags) ws.flags = std::make_shared<PinnedBuffer<int>>(4);
+  int* h = ws.flags->get();
+  h[0] = h[1] = h[2] = h[3] = 0;
   cudaStream_t s = l.stream();
-  QSWG_CHECK(cudaMemcpyAsync(&se[0], &step_ctl(l)->error, sizeof(int), cudaMemcpyDeviceToHost, s));
-  QSWG_CHECK(cudaMemcpyAsync(&se[1], &step_ctl(l)->spmvs, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (before_sync) before_sync();
+  static_assert(offsetof(dev::StepCtl, spmvs) == offsetof(dev::StepCtl, error) + sizeof(int), "error, spmvs adjacent");
+  QSWG_CHECK(cudaMemcpyAsync(h, &step_ctl(l)->error, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   if (with_series) {
-    QSWG_CHECK(cudaMemcpyAsync(&re[0], &series_ctl(l)->error, sizeof(int), cudaMemcpyDeviceToHost, s));
-    QSWG_CHECK(cudaMemcpyAsync(&re[1], &series_ctl(l)->spmvs, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaMemcpyAsync(h + 2, &series_ctl(l)->error, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaMemcpyAsync(h + 3, &series_ctl(l)->spmvs, sizeof(int), cudaMemcpyDeviceToHost, s));
   }
   QSWG_CHECK(cudaStreamSynchronize(s));
-  return {se[0] | re[0], static_cast<std::int64_t>(se[1]) + re[1]};
+  return {h[0] | h[2], static_cast<std::int64_t>(h[1]) + h[3]};
 }
 
 void reset_ctls(const Liouvillian& l, bool with_series) {
@@ -232,11 +239,11 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
 }  // namespace
 
 StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorParameters& params,
-              double2* out) {
+              double2* out, int herm_known) {
   DeviceGuard g(l.device());
   const Exec ex(l);
   reset_ctls(l, false);
-  l.set_hermitian_input(v);  // Hermitian input: the iterates stay Hermitian
+  l.set_hermitian_input(v, herm_known);  // Hermitian input: the iterates stay Hermitian
   std::int64_t launches = 0;
   const StepParameters sp = enqueue_step(ex, v, t, params, out, launches);
   const Flags f = read_flags(l, false);
@@ -402,14 +409,15 @@ struct SeriesGraph {
 SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
                   const TaylorParameters& params,
                   const std::function<void(std::int64_t, const double2*)>& emit,
-                  const std::vector<const void*>& graph_key) {
+                  const std::vector<const void*>& graph_key, int herm_known,
+                  const std::function<void()>& before_sync) {
   // expm.cpp:216-217
   if (!(tq > t1)) throw std::invalid_argument("series requires tq > t1");
   if (steps < 1) throw std::invalid_argument("series requires at least one step");
   DeviceGuard g(l.device());
   const Exec ex(l);
   cudaStream_t s = ex.s;
-  l.set_hermitian_input(v);  // Hermitian input: every state stays Hermitian
+  l.set_hermitian_input(v, herm_known);  // Hermitian input: every state stays Hermitian
   static const bool graphs_off = [] {
     const char* e = std::getenv("QSWG_GRAPH");
     return e != nullptr && e[0] == '0';
@@ -453,7 +461,7 @@ SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, 
   } else {
     info = enqueue_series(l, ex, v, t1, tq, steps, params, emit);
   }
-  const Flags f = read_flags(l, info.path == 2);
+  const Flags f = read_flags(l, info.path == 2, before_sync);
   info.spmvs = f.spmvs;
   if (f.error) throw NumericalError("non-finite values encountered in series evolution");
   return info;

@@ -36,7 +36,7 @@ struct SeriesInfo {
 /// out = exp(t L) v.  `out` must not alias `v`.  Throws NumericalError on
 /// non-finite values (expm.cpp:191-193).
 StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorParameters& params,
-              double2* out);
+              double2* out, int herm_known = -1);
 
 /// Outputs at t1 + k (tq - t1)/steps, k = 0..steps (expm.cpp:214-325).  Each
 /// output is handed to `emit(k, state)` as a device pointer valid until the
@@ -48,10 +48,14 @@ StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorPara
 /// tolerance, graph_key buffers and Hermitian mode) is captured once into a CUDA graph and replayed by
 /// later identical calls — the same kernels with the same arguments, minus the
 /// per-launch host overhead (QSWG_GRAPH=0 disables).
+/// herm_known: as Liouvillian::set_hermitian_input.  before_sync: enqueues
+/// the caller's stream-ordered reads (D2H of the outputs) before the one
+/// synchronisation of the call.
 SeriesInfo series(const Liouvillian& l, const double2* v, double t1, double tq, std::int64_t steps,
                   const TaylorParameters& params,
                   const std::function<void(std::int64_t, const double2*)>& emit,
-                  const std::vector<const void*>& graph_key = {});
+                  const std::vector<const void*>& graph_key = {}, int herm_known = -1,
+                  const std::function<void()>& before_sync = {});
 
 /// Mean device time (ms) of one fused series-term launch with `count`
 /// active outputs (p > 1 traffic: K read, K write, count sums read+write),

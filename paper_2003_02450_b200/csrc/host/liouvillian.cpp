@@ -906,13 +906,23 @@ void Liouvillian::multiply(const double2* x, double2* y, double scale) const {
   dev::spmv(matrix(), x, y, scale, stream_);
 }
 
-void Liouvillian::set_hermitian_input(const double2* x) const {
+int Liouvillian::hermitian_state(const double2* x) const {
+  if (format_ != dev::Format::Kron || !herm_flag_.get()) return -1;
+  DeviceGuard g(device_);
+  return dev::kron_hermitian_check(matrix(), x, stream_) ? 1 : 0;
+}
+
+void Liouvillian::set_hermitian_input(const double2* x, int known) const {
   DeviceGuard g(device_);
   static const bool off = [] {
     const char* e = std::getenv("QSWG_KRON_HERM");  // experiment knob: 0 = always the general kernels
     return e != nullptr && e[0] == '0';
   }();
-  herm_ = !off && herm_mode_ && dev::kron_hermitian_check(matrix(), x, stream_) ? 1 : 0;
+  if (off || !herm_mode_ || format_ != dev::Format::Kron || !herm_flag_.get()) {
+    herm_ = 0;
+    return;
+  }
+  herm_ = (known >= 0 ? known != 0 : dev::kron_hermitian_check(matrix(), x, stream_)) ? 1 : 0;
 }
 
 double Liouvillian::time_spmv(int iters, int group) const {

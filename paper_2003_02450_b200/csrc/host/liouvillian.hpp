@@ -40,6 +40,7 @@ struct Workspace {
   DeviceBuffer<dev::StepCtl> step_ctl;
   DeviceBuffer<dev::SeriesCtl> series_ctl;
   std::shared_ptr<void> series_graph;  // expm.cpp: captured launch sequence of a repeated series call
+  std::shared_ptr<PinnedBuffer<int>> flags;  // expm.cpp: error / SpMV counters read back once per call
   double2* get(std::size_t idx, std::size_t len) {
     if (vec.size() <= idx) vec.resize(idx + 1);
     if (vec[idx].size() < len) vec[idx].resize(len);
@@ -106,8 +107,17 @@ class Liouvillian {
   void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
                 std::vector<Complex>& val) const;
   /// Kron on one GPU: selects the Hermitian kernels for the products that
-  /// follow when x (full-length) is exactly Hermitian (synchronises).
-  void set_hermitian_input(const double2* x) const;
+  /// follow when x (full-length) is exactly Hermitian.  known >= 0: the
+  /// caller already knows (a state checked at upload, built from
+  /// probabilities, or produced by the Hermitian kernels): no check, no
+  /// synchronisation; -1: check on the device (synchronises).
+  void set_hermitian_input(const double2* x, int known = -1) const;
+  /// 1 if x is exactly Hermitian, 0 if not, -1 when no kernel here uses it
+  /// (not the one-GPU Kron format); synchronises when it checks.
+  int hermitian_state(const double2* x) const;
+  /// Whether the products since the last set_hermitian_input ran the
+  /// Hermitian kernels (their outputs are then exactly Hermitian).
+  bool hermitian_mode() const { return herm_ != 0; }
   /// 0: never take the Hermitian kernels; 1 (default): when the input is Hermitian.
   void set_hermitian_mode(int mode) { herm_mode_ = mode ? 1 : 0; }
   /// Re-mixes the superoperator for a new omega in place (SURVEY.md §8(f)
