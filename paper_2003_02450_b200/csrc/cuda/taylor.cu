@@ -944,7 +944,8 @@ __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2*
     const int b = __ldg(m.a_ell.sptr + sl), len = (__ldg(m.a_ell.sptr + sl + 1) - b) >> 5;
     const int* cp = m.a_ell.col + b + lane;
     const double2* vp = m.a_ell.val + b + lane;
-    by_kind(m.vk_a, [&](auto kc, auto cc) {
+    // (padded slices: the padding's zero values must be loaded, not the constant)
+    by_kind(m.vk_a & 3, [&](auto kc, auto cc) {
       QSWG_KC(kc, cc);
 #pragma unroll 2
       for (int e = 0; e < len; ++e) {
@@ -970,6 +971,7 @@ __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2*
   if constexpr (kF == 1) {
     for (int k = 0; k < m.nk; ++k) {  // -w/2 L'(L X): columns j of W_k
       const KronList& rk = m.r[k];
+      if (rk.ptr == nullptr) continue;
       const int e0 = __ldg(rk.ptr + i), e1 = __ldg(rk.ptr + i + 1);
       const double2* wk = m.w[k];
       by_kind(m.vk_r[k], [&](auto kc, auto cc) {
@@ -993,6 +995,7 @@ __device__ __forceinline__ void kron_rows_lane(const KronView& m, const double2*
 constexpr int kRowUnroll = QSWG_ROW_UNROLL;
 template <int K, bool C, class G>
 __device__ __forceinline__ void uniform_row(const KronList& l, double2 cv, int row, double2& acc, G&& g) {
+  if (l.ptr == nullptr) return;
   const int e1 = __ldg(l.ptr + row + 1);
 #pragma unroll kRowUnroll
   for (int e = __ldg(l.ptr + row); e < e1; ++e)
@@ -1004,6 +1007,7 @@ __device__ __forceinline__ void uniform_row(const KronList& l, double2 cv, int r
 // slower on c2-c4.)
 template <int K, bool C, class G>
 __device__ __forceinline__ void uniform_rows(const KronList& l, double2 cv, const int* rows, double2* acc, G&& g) {
+  if (l.ptr == nullptr) return;  // an operand without entries (e.g. a zero Lindblad operator)
 #pragma unroll
   for (int r = 0; r < kKR; ++r) uniform_row<K, C>(l, cv, rows[r], acc[r], g);
 }
@@ -1397,7 +1401,7 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
         vj[r] = jl < g.nc;
         col[r] = static_cast<unsigned>(g.c0 + (vj[r] ? jl : g.nc - 1)) * n;
       }
-      by_kind(vk, [&](auto kc, auto cc) {
+      by_kind(qe.sptr ? vk & 3 : vk, [&](auto kc, auto cc) {  // (padded ELL: load the zeros)
         QSWG_KC(kc, cc);
         if (qe.sptr) {
           const int sl = i >> 5, ln = i & 31;

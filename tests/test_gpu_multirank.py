@@ -123,3 +123,30 @@ def test_sharded_coherence_and_set_omega(world, fmt):
     for p in parts:
         for got, want in zip(p, single):
             assert np.abs(np.asarray(got) - np.asarray(want)).max() <= 1e-12
+
+
+@pytest.mark.parametrize("factor", ["1", "0"])
+@pytest.mark.parametrize("size", [64, 96])
+def test_sharded_kron_er_matches_single(size, factor, monkeypatch):
+    """The c4 family (ER G-QSW) at n = 64 / 96 on two row-partitioned ranks —
+    the general KRON kernels with padded sliced-ELL operand rows, factored and
+    not — against the one-GPU run (Hermitian tiles)."""
+    from paper_2003_02450_b200 import graphs
+    monkeypatch.setenv("QSWG_KRON_FACTOR", factor)
+    w = graphs.config("c4", size=size)
+
+    def build(**kw):
+        return api.build_global(w.omega, w.h, w.ops, format="kron", **kw)
+
+    l1 = build()
+    r1 = api.series(l1, l1.state().from_probabilities(w.rho0), w.t1, w.tq, w.steps, states=True)
+
+    def rank_fn(r, comm):
+        l = build(comm=comm)
+        res = api.series(l, l.state().from_probabilities(w.rho0), w.t1, w.tq, w.steps, states=True)
+        return l.row0, res.states, int(res.info.spmvs)
+
+    parts = sorted(run_ranks(2, rank_fn), key=lambda p: p[0])
+    states = np.concatenate([p[1] for p in parts], axis=1)
+    assert np.abs(states - r1.states).max() <= 1e-13
+    assert parts[0][2] == int(r1.info.spmvs)
