@@ -1064,6 +1064,14 @@ void kron_halos(const HostOperands& h, bool factored, std::int64_t n, const std:
 std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_t n, const HostOperands& hops,
                                                        const DeviceConfig& cfg,
                                                        const std::vector<std::int64_t>* fixed_starts) {
+  {  // after the reference's argument validation (build_local / build_global), before any device work
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      throw CudaError("no CUDA device available (qswg has no CPU fallback)");
+    }
+    if (cfg.device < 0 || cfg.device >= count) throw std::invalid_argument("CUDA device ordinal out of range");
+  }
   std::unique_ptr<Liouvillian> l(new Liouvillian);
   l->n_ = n;
   l->omega_ = omega;
