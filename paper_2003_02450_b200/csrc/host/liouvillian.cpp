@@ -162,6 +162,11 @@ struct HostOperands {
   std::vector<MultiCsr> p, q;
   std::vector<double> d_loc, d_ss;  // empty -> no decay term
   double omega = 0.0;
+  // Every Hermitian X maps to a Hermitian L(X): true for the Lindblad form
+  // whenever H (and H_rot) are exactly Hermitian.  The reference accepts H
+  // within a tolerance and never checks H_rot (liouvillian.cpp:217-229), so
+  // the Hermitian tile kernels are enabled only when this holds exactly.
+  bool herm_preserving = true;
   // Factored dissipator of G-QSW for the matrix-free path: A = af, B = bf
   // (no L'L terms) and per Lindblad operator R_k = -w/2 L_k' (gathers in the
   // columns of W_k = L_k X), S_k = -w/2 L_k^T (streams the columns of
@@ -181,6 +186,7 @@ struct HostOperands {
     o.d_loc = d_loc;
     o.d_ss = d_ss;
     o.omega = omega;
+    o.herm_preserving = herm_preserving;
     return o;
   }
 
@@ -1153,7 +1159,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
         QSWG_CHECK(cudaMemsetAsync(l->kron_v_.back().get(), 0, l->kron_v_.back().bytes(), s));
       }
     }
-    if (world == 1) {
+    if (world == 1 && hops.herm_preserving) {
       l->herm_flag_.resize(1);
       QSWG_CHECK(cudaMemsetAsync(l->herm_flag_.get(), 0, sizeof(int), s));
       if (l->kron_->factored)
@@ -1397,9 +1403,11 @@ std::unique_ptr<Liouvillian> build_local(double omega, const SparseMatrix& h, co
   for (const SinkArc& s : sinks)
     if (s.origin < 0 || s.origin >= n_base) throw std::out_of_range("sink origin out of range");
 
-  auto operands = [n, n_base, nsrc, nsnk, h, m_l, sources, sinks](double omega) {
+  const bool exact_herm = h.is_hermitian(0.0);
+  auto operands = [n, n_base, nsrc, nsnk, h, m_l, sources, sinks, exact_herm](double omega) {
   HostOperands o;
   o.n = n;
+  o.herm_preserving = exact_herm;
   o.omega = omega;
   const Complex coh{0.0, -(1.0 - omega)};
   const SparseMatrix ht = h.transpose();
@@ -1447,10 +1455,12 @@ std::unique_ptr<Liouvillian> build_global(double omega, const SparseMatrix& h,
   if (static_cast<int>(lindblads.size()) > dev::kMaxKron)
     throw std::invalid_argument("at most " + std::to_string(dev::kMaxKron) + " Lindblad operators are supported");
 
-  auto operands = [n, h, lindblads, h_rot](double omega) {
+  const bool exact_herm = h.is_hermitian(0.0) && (!h_rot || h_rot->is_hermitian(0.0));
+  auto operands = [n, h, lindblads, h_rot, exact_herm](double omega) {
   HostOperands o;
   o.n = n;
   o.omega = omega;
+  o.herm_preserving = exact_herm;
   const Complex coh{0.0, -(1.0 - omega)};
   const Complex rot{0.0, omega};
   const SparseMatrix ht = h.transpose();

@@ -140,6 +140,8 @@ def load_probability_file(path) -> np.ndarray:
         m = _NUMBER.match(tok)  # what `in >> x` accepts: no inf/nan words
         if m is None:
             break  # `in >> x` stops at the first token that is not a number
+        if re.match(r"[eE][+-]?(?![0-9])", tok[m.end():]):
+            break  # an exponent without digits ("1e", "1e+"): libstdc++ fails the whole extraction
         p.append(float(m.group(0)))
         if m.end() != len(tok):
             break  # a number followed by junk: the stream fails on the junk

@@ -136,3 +136,26 @@ def test_nccl_communicator_single_rank():
     assert np.array_equal(r.states, r0.states)
     del l
     del comm
+
+
+def test_non_hermitian_h_rot_disables_the_hermitian_tiles(port):
+    """With a rotating Hamiltonian that is not Hermitian (the reference never
+    checks H_rot, liouvillian.cpp:217-229) L does not map Hermitian X to
+    Hermitian L(X): the Hermitian tile kernels must stay off, and the result
+    must be the reference's full product."""
+    c = Case("gqsw_multi_rot")
+    rng = np.random.default_rng(3)
+    n = c.n
+    a = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.2)
+    from paper_2003_02450_b200.graphs import Csr
+    r_, c_ = np.nonzero(a)
+    hrot = Csr.from_coo(n, n, r_, c_, a[r_, c_] + 0.3j * a[r_, c_])  # not Hermitian
+    l = api.build_global(c.omega, c.h, c.ops, hrot, format="kron")
+    o = port.build_global(c.omega, c.h, c.ops, hrot)
+    t1, tq, q = c.series
+    v0 = rho0_vec(n, c.rho0)
+    r = api.series(l, l.state().upload(v0), t1, tq, int(q), states=True)
+    l._query()
+    assert not l.info.kron_hermitian
+    so, _, _ = o.series(v0, t1, tq, int(q))
+    assert np.abs(r.states - so).max() <= 1e-10 * max(1.0, np.abs(so).max())
