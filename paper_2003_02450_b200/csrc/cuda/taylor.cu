@@ -533,14 +533,60 @@ __device__ __forceinline__ void flush_element(const SeriesFlushArgs& a, const Fl
   }
 }
 
+// Norm maxima of the outputs a flush updates.  kReg: per-thread maxima of the
+// first 2 kSeriesRegD outputs in registers, reduced once per block (the
+// flush fused into the 64-register W kernel: c2 flush 8.0 -> 6.2 us per
+// term); otherwise (and past those outputs) a warp reduction per element,
+// which keeps the stand-alone streaming flush kernel at 46 registers (its
+// occupancy is its bandwidth: with the register maxima at 60-71 registers
+// the c5 flush went from 437 to 550-690 us per term).
+template <bool kReg>
+struct FlushMax {
+  unsigned long long m[2][kSeriesRegD];
+  __device__ __forceinline__ FlushMax() {
+    if constexpr (kReg) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int v = 0; v < kSeriesRegD; ++v) m[c][v] = 0;
+    }
+  }
+  // the norm of the output u0 + v (v a constant) from element value sv
+  __device__ __forceinline__ void add(FlushList& L, int u0, int v, double2 sv, bool valid) {
+    if (kReg && u0 == 0) {
+      if (valid) max_abs_bits(m[0][v], sv);
+    } else if (kReg && u0 == kSeriesRegD) {
+      if (valid) max_abs_bits(m[1][v], sv);
+    } else {
+      unsigned long long mk = valid ? dbits(cabs2(sv)) : 0ull;
+      mk = warp_max_bits(mk);
+      if ((threadIdx.x & 31) == 0 && mk) atomicMax(&L.smax[u0 + v], mk);
+    }
+  }
+  __device__ __forceinline__ void done(FlushList& L) {
+    if constexpr (kReg) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int v = 0; v < kSeriesRegD; ++v) {
+          const int u = c * kSeriesRegD + v;
+          if (u >= L.nm) continue;  // block-uniform
+          const unsigned long long mk = warp_max_bits(m[c][v]);
+          if ((threadIdx.x & 31) == 0 && mk) atomicMax(&L.smax[u], mk);
+        }
+    }
+  }
+};
+
 // The flush work of one block over all local rows (every thread calls it).
-template <bool kStrict, bool kCoop = false>
+template <bool kStrict, bool kCoop = false, bool kReg = false>
 __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
   __shared__ FlushList L;
   flush_prepare(a, L);
-  const int nm = L.nm, lane = threadIdx.x & 31;
+  const int nm = L.nm;
   const unsigned long long once = evict_first_policy();
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  FlushMax<kReg> fm;
   for (long long base = static_cast<long long>(blockIdx.x) * blockDim.x; base < a.rows; base += stride) {
     const long long row = base + threadIdx.x;
     const bool valid = row < a.rows;
@@ -552,16 +598,12 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
       for (int v = 0; v < kSeriesRegD; ++v) {
         const int u = u0 + v;
         if (u >= nm) break;  // block-uniform
-        unsigned long long mk = 0;
-        if (valid) {
-          st_hint(a.sums.s[L.list[u]] + row, sv[v], once);
-          mk = dbits(cabs2(sv[v]));
-        }
-        mk = warp_max_bits(mk);
-        if (lane == 0 && mk) atomicMax(&L.smax[u], mk);
+        if (valid) st_hint(a.sums.s[L.list[u]] + row, sv[v], once);
+        fm.add(L, u0, v, sv[v], valid);
       }
     }
   }
+  fm.done(L);
   flush_finish<kCoop>(a, L);
 }
 
@@ -573,60 +615,65 @@ __device__ __forceinline__ void flush_body(const SeriesFlushArgs& a) {
 // computes (conj is exact and the axpys are symmetric in the sign of the
 // imaginary parts), so the pending terms and sums are read for half the
 // elements only.
-__device__ __forceinline__ void flush_body_herm(const SeriesFlushArgs& a) {
-  __shared__ FlushList L;
-  __shared__ double2 tr[kSeriesRegD][8][33];
-  flush_prepare(a, L);
+// One upper 32 x 32 tile t of the Hermitian flush (in 32 x 8 sub-tiles).
+using FlushTr = double2[kSeriesRegD][8][33];
+template <bool kReg>
+__device__ __forceinline__ void flush_herm_tile(const SeriesFlushArgs& a, FlushList& L, FlushTr& tr, long long t,
+                                                FlushMax<kReg>& fm, unsigned long long once) {
   const int nm = L.nm, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int n = a.herm_n, nt = (n + 31) / 32;
-  const long long ntiles = static_cast<long long>(nt) * (nt + 1) / 2;
-  const unsigned long long once = evict_first_policy();
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
-    while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
-    while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
-    const int I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
+  const int n = a.herm_n;
+  int J = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
+  while (static_cast<long long>(J) * (J + 1) / 2 > t) --J;
+  while (static_cast<long long>(J + 1) * (J + 2) / 2 <= t) ++J;
+  const int I = static_cast<int>(t - static_cast<long long>(J) * (J + 1) / 2);
 #pragma unroll 1
-    for (int sub = 0; sub < 4; ++sub) {
-      const int i = I * 32 + lane, j = J * 32 + sub * 8 + w;
-      const bool upper = i < n && j < n && i <= j;
-      const long long row = static_cast<long long>(j) * n + i;
-      // mirror target of this thread after the transpose: row i2 of the
-      // sub-tile's columns, column j2 (8 consecutive j per 8 threads)
-      const int i2 = I * 32 + (threadIdx.x >> 3), j2 = J * 32 + sub * 8 + (threadIdx.x & 7);
-      const bool mirror = i2 < n && j2 < n && i2 < j2;
+  for (int sub = 0; sub < 4; ++sub) {
+    const int i = I * 32 + lane, j = J * 32 + sub * 8 + w;
+    const bool upper = i < n && j < n && i <= j;
+    const long long row = static_cast<long long>(j) * n + i;
+    // mirror target of this thread after the transpose: row i2 of the
+    // sub-tile's columns, column j2 (8 consecutive j per 8 threads)
+    const int i2 = I * 32 + (threadIdx.x >> 3), j2 = J * 32 + sub * 8 + (threadIdx.x & 7);
+    const bool mirror = i2 < n && j2 < n && i2 < j2;
 #pragma unroll 1
-      for (int u0 = 0; u0 < nm; u0 += kSeriesRegD) {
-        double2 sv[kSeriesRegD];
-        flush_element<false>(a, L, u0, row, upper, once, sv);
+    for (int u0 = 0; u0 < nm; u0 += kSeriesRegD) {
+      double2 sv[kSeriesRegD];
+      flush_element<false>(a, L, u0, row, upper, once, sv);
 #pragma unroll
-        for (int v = 0; v < kSeriesRegD; ++v) {
-          const int u = u0 + v;
-          if (u >= nm) break;  // block-uniform
-          unsigned long long mk = 0;
-          if (upper) {
-            st_hint(a.sums.s[L.list[u]] + row, sv[v], once);
-            mk = dbits(cabs2(sv[v]));
-          }
-          mk = warp_max_bits(mk);
-          if (lane == 0 && mk) atomicMax(&L.smax[u], mk);
-          tr[v][w][lane] = sv[v];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int v = 0; v < kSeriesRegD; ++v) {
-          const int u = u0 + v;
-          if (u >= nm) break;
-          if (mirror) {  // element (j2, i2) = conj of the computed (i2, j2)
-            const double2 m = tr[v][threadIdx.x & 7][threadIdx.x >> 3];
-            st_hint(a.sums.s[L.list[u]] + static_cast<long long>(i2) * n + j2, make_double2(m.x, -m.y), once);
-          }
-        }
-        __syncthreads();
+      for (int v = 0; v < kSeriesRegD; ++v) {
+        const int u = u0 + v;
+        if (u >= nm) break;  // block-uniform
+        if (upper) st_hint(a.sums.s[L.list[u]] + row, sv[v], once);
+        fm.add(L, u0, v, sv[v], upper);
+        tr[v][w][lane] = sv[v];
       }
+      __syncthreads();
+#pragma unroll
+      for (int v = 0; v < kSeriesRegD; ++v) {
+        const int u = u0 + v;
+        if (u >= nm) break;
+        if (mirror) {  // element (j2, i2) = conj of the computed (i2, j2)
+          const double2 m = tr[v][threadIdx.x & 7][threadIdx.x >> 3];
+          st_hint(a.sums.s[L.list[u]] + static_cast<long long>(i2) * n + j2, make_double2(m.x, -m.y), once);
+        }
+      }
+      __syncthreads();
     }
   }
-  flush_finish<false>(a, L);
+}
+
+template <bool kReg = false, bool kCoop = false>
+__device__ __forceinline__ void flush_body_herm(const SeriesFlushArgs& a) {
+  __shared__ FlushList L;
+  __shared__ FlushTr tr;
+  flush_prepare(a, L);
+  const int nt = (a.herm_n + 31) / 32;
+  const long long ntiles = static_cast<long long>(nt) * (nt + 1) / 2;
+  const unsigned long long once = evict_first_policy();
+  FlushMax<kReg> fm;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) flush_herm_tile(a, L, tr, t, fm, once);
+  fm.done(L);
+  flush_finish<kCoop>(a, L);
 }
 
 template <bool kStrict>
@@ -1328,6 +1375,9 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
 #ifndef QSWG_KRON_W_MIN_BLOCKS
 #define QSWG_KRON_W_MIN_BLOCKS 4
 #endif
+#ifndef QSWG_WFLUSH_REG
+#define QSWG_WFLUSH_REG 1  // the fused flush keeps its norm maxima in registers (FlushMax)
+#endif
 // kFlush: the same launch then runs the flush after the previous term
 // (series_flush; its HBM streaming overlaps the gathers of W).
 template <bool kHerm, bool kFlush>
@@ -1432,9 +1482,9 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
   if constexpr (kFlush) {
     if (flush_due(fa)) {
       if (fa.herm_n > 0) {
-        flush_body_herm(fa);
+        flush_body_herm<QSWG_WFLUSH_REG != 0>(fa);
       } else {
-        flush_body<false>(fa);
+        flush_body<false, false, QSWG_WFLUSH_REG != 0>(fa);
       }
       return;
     }

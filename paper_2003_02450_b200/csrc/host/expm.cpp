@@ -318,7 +318,8 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
     // launch that prepares W for term p + 1.
     const bool fused = ex.single && mat.format == dev::Format::Kron && mat.kron.nk > 0;
     const std::int64_t per_term =
-        (fused ? 1 : 2) + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + (mat.kron.factored && !mat.kron.herm)) : 0);
+        (fused ? 1 : 2) +
+        (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + (mat.kron.factored && !mat.kron.herm)) : 0);
     for (std::int64_t super = 0; super <= n_super; ++super) {
       const std::int64_t count = super < n_super ? d : remainder;
       if (count == 0) break;

@@ -334,6 +334,61 @@ MultiCsr strip_diagonal(const MultiCsr& m, std::vector<double2>& d) {
   return o;
 }
 
+// Launch order of the upper tiles (I <= J) of the Hermitian KRON kernels.
+// Concurrent blocks share L2: tile (I, J) gathers from row bands I and J of X
+// and of the work vectors (and, on lattices, from bands a fixed offset away),
+// so the order decides how much of x is re-read from HBM.
+//   jmajor   J outer, I inner (columns J shared by blocks launched together)
+//   blocked  B x B squares of tiles, J-major inside and between the squares:
+//            the bands a wave touches shrink from all of them to ~2B
+//   morton   Z-order of (I, J)
+// QSWG_KRON_ORDER / QSWG_KRON_TILE_BLOCK override (experiments).
+std::vector<int2> herm_tile_order(int nti) {
+  std::string order = "jmajor";
+  int bs = 16;
+  if (const char* e = std::getenv("QSWG_KRON_ORDER")) order = e;
+  if (const char* e = std::getenv("QSWG_KRON_TILE_BLOCK")) bs = std::max(1, std::atoi(e));
+  std::vector<int2> tl;
+  tl.reserve(static_cast<std::size_t>(nti) * (nti + 1) / 2);
+  if (order == "blocked") {
+    for (int J0 = 0; J0 < nti; J0 += bs)
+      for (int I0 = 0; I0 <= J0; I0 += bs)
+        for (int J = J0; J < std::min(nti, J0 + bs); ++J)
+          for (int I = I0; I < std::min(J + 1, I0 + bs); ++I) tl.push_back(make_int2(I, J));
+  } else if (order == "morton4") {  // tile index = q * D + r (lattice planes of D tiles): 4-D Z-order
+    int D = 18;
+    if (const char* e = std::getenv("QSWG_KRON_PERIOD")) D = std::max(1, std::atoi(e));
+    std::vector<std::pair<std::uint64_t, int2>> keyed;
+    for (int J = 0; J < nti; ++J)
+      for (int I = 0; I <= J; ++I) {
+        const unsigned c[4] = {static_cast<unsigned>(I % D), static_cast<unsigned>(I / D),
+                               static_cast<unsigned>(J % D), static_cast<unsigned>(J / D)};
+        std::uint64_t key = 0;
+        for (int b = 0; b < 15; ++b)
+          for (int d = 0; d < 4; ++d) key |= static_cast<std::uint64_t>((c[d] >> b) & 1u) << (4 * b + d);
+        keyed.push_back({key, make_int2(I, J)});
+      }
+    std::sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& k : keyed) tl.push_back(k.second);
+  } else if (order == "morton") {
+    std::vector<std::pair<std::uint64_t, int2>> keyed;
+    for (int J = 0; J < nti; ++J)
+      for (int I = 0; I <= J; ++I) {
+        std::uint64_t key = 0;
+        for (int b = 0; b < 16; ++b)
+          key |= (static_cast<std::uint64_t>((I >> b) & 1) << (2 * b)) |
+                 (static_cast<std::uint64_t>((J >> b) & 1) << (2 * b + 1));
+        keyed.push_back({key, make_int2(I, J)});
+      }
+    std::sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& k : keyed) tl.push_back(k.second);
+  } else {
+    for (int J = 0; J < nti; ++J)
+      for (int I = 0; I <= J; ++I) tl.push_back(make_int2(I, J));
+  }
+  return tl;
+}
+
 // kernels.hpp: value classes.  A list with no entries is "real" (no term).
 // With `cv`, kValConst is added when every entry equals one value (*cv).
 int value_class(const std::vector<double2>& v, double2* cv = nullptr) {
@@ -488,12 +543,8 @@ struct KronStore {
       for (auto* v : {&vk_p, &vk_q, &vk_r, &vk_s, &vk_u})
         for (int& x : *v) x &= 3;
     }
-    if (single) {  // the upper 32 x 32 tiles, J-major (kernels.hpp: KronTiles)
-      const int nti = static_cast<int>((host.n + 31) / 32);
-      std::vector<int2> tl;
-      tl.reserve(static_cast<std::size_t>(nti) * (nti + 1) / 2);
-      for (int J = 0; J < nti; ++J)
-        for (int I = 0; I <= J; ++I) tl.push_back(make_int2(I, J));
+    if (single) {  // the upper 32 x 32 tiles in launch order (kernels.hpp: KronTiles)
+      const std::vector<int2> tl = herm_tile_order(static_cast<int>((host.n + 31) / 32));
       herm_tiles.resize(tl.size());
       QSWG_CHECK(cudaMemcpyAsync(herm_tiles.get(), tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
     }
