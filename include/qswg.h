@@ -87,6 +87,8 @@ typedef struct {
   int64_t span_m_star, span_s, d, n_super, remainder, sub_m_star, spmvs;
   int64_t launches; /* qswg kernels enqueued by the call */
   double device_ms; /* CUDA-event time of the whole series on the library stream */
+  int64_t host_waits; /* several GPUs: host waits for a stop flag (bounded run-ahead); the
+                         stream is synchronised once per call, never per term */
 } qswg_series_info;
 
 const char* qswg_last_error(void);

@@ -102,7 +102,7 @@ class StepInfo(C.Structure):
 class SeriesInfo(C.Structure):
     _fields_ = [("path", C.c_int), ("span_m_star", i64), ("span_s", i64), ("d", i64), ("n_super", i64),
                 ("remainder", i64), ("sub_m_star", i64), ("spmvs", i64), ("launches", i64),
-                ("device_ms", C.c_double)]
+                ("device_ms", C.c_double), ("host_waits", i64)]
 
 
 # Every symbol include/qswg.h declares, with its ctypes signature.

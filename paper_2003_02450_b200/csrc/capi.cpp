@@ -684,6 +684,7 @@ int qswg_series_observe(const qswg_liouvillian* l, const qswg_state* v, double t
       info->spmvs = si.spmvs;
       info->launches = si.launches + si.emits;
       info->device_ms = ms;
+      info->host_waits = si.host_waits;
     }
   });
 }

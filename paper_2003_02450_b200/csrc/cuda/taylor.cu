@@ -1687,9 +1687,18 @@ __global__ void series_init_fin_kernel(SeriesCtl* ctl, int count, int pend_max) 
   pdl_trigger();
   series_init_apply(ctl, count, pend_max, bitsd(ctl->term_bits));
 }
+// The multi-GPU controls run after every term whether or not it ran (the
+// host enqueues without reading the stop flags): a term the stop test or an
+// error already skipped leaves the control block untouched.
 __global__ void step_control_kernel(StepCtl* ctl, int first_of_stage, int stage, double tol) {
   pdl_prologue();
   pdl_trigger();
+  if (ctl->error || (!first_of_stage && ctl->done)) {  // the term kernel skipped itself
+    ctl->term_bits = 0;
+    ctl->sum_bits = 0;
+    ctl->arrivals = 0;
+    return;
+  }
   step_control(ctl, first_of_stage, stage, tol);
 }
 __global__ void __launch_bounds__(kThreads) series_term_control_kernel(SeriesCtl* ctl, int p, int last, double tol) {
@@ -1697,9 +1706,31 @@ __global__ void __launch_bounds__(kThreads) series_term_control_kernel(SeriesCtl
   pdl_trigger();
   series_term_control(ctl, p, last, tol);
 }
+// After term p on several GPUs (one allreduce of [term_bits, sum_bits]): the
+// exact tests of the flush after term p - 1 when one ran, then term p's
+// control — unless term p is not part of the series (the series had ended,
+// or that flush stopped every output: the term ran speculatively and is
+// neither tested nor counted).
+__global__ void __launch_bounds__(kThreads) series_flush_term_control_kernel(SeriesCtl* ctl, int p, int last,
+                                                                            double tol) {
+  pdl_prologue();
+  pdl_trigger();
+  __shared__ int go;
+  if (*(volatile int*)&ctl->flush) series_flush_control(ctl, p - 1, tol);
+  __syncthreads();
+  if (threadIdx.x == 0) go = !ctl->error && ctl->n_active > 0;
+  __syncthreads();
+  if (go) {
+    series_term_control(ctl, p, last, tol);
+  } else if (threadIdx.x == 0) {
+    ctl->term_bits = 0;
+    ctl->arrivals = 0;
+  }
+}
 __global__ void __launch_bounds__(kThreads) series_flush_control_kernel(SeriesCtl* ctl, int p, double tol) {
   pdl_prologue();
   pdl_trigger();
+  if (!*(volatile int*)&ctl->flush) return;  // no flush was due (multi-GPU: enqueued unconditionally)
   series_flush_control(ctl, p, tol);
 }
 
@@ -1880,6 +1911,11 @@ void series_init_fin(SeriesCtl* ctl, int count, int pend_max, cudaStream_t s) {
 void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s) {
   launch_pdl(series_term_control_kernel, 1, kThreads, 0, s, ctl, p, last, tol);
   QSWG_LAUNCH_CHECK("series_term_control");
+}
+
+void series_flush_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s) {
+  launch_pdl(series_flush_term_control_kernel, 1, kThreads, 0, s, ctl, p, last, tol);
+  QSWG_LAUNCH_CHECK("series_flush_term_control");
 }
 
 void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {

@@ -18,6 +18,7 @@
 #include <cstddef>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -159,20 +160,6 @@ struct Exec {
       }
   }
 
-  // {n_active, flush} of a series control block in one device-to-host read.
-  std::pair<int, int> read_active_flush(const dev::SeriesCtl* ctl) const {
-    constexpr std::size_t lo = offsetof(dev::SeriesCtl, n_active), hi = offsetof(dev::SeriesCtl, flush);
-    static_assert(lo < hi, "n_active precedes flush");
-    unsigned char buf[hi - lo + sizeof(int)];
-    QSWG_CHECK(cudaMemcpyAsync(buf, reinterpret_cast<const unsigned char*>(ctl) + lo, sizeof(buf),
-                               cudaMemcpyDeviceToHost, s));
-    QSWG_CHECK(cudaStreamSynchronize(s));
-    int a = 0, f = 0;
-    std::memcpy(&a, buf, sizeof(int));
-    std::memcpy(&f, buf + (hi - lo), sizeof(int));
-    return {a, f};
-  }
-
   template <class T>
   T read(const T* dev_ptr) const {
     T v{};
@@ -182,10 +169,55 @@ struct Exec {
   }
 };
 
+// Several GPUs: the host enqueues every term without reading the stop flags
+// (each kernel and control skips itself once its stage or super-step is
+// done).  To stop enqueueing soon after the end, the flag of every term is
+// copied asynchronously into pinned memory behind an event; the host looks at
+// the copy from kLag terms back and waits for it only when the device is that
+// far behind — the stream never waits on the host.
+struct FlagPoll {
+  static constexpr int kLag = 4, kRing = 8;
+  cudaEvent_t ev[kRing] = {};
+  PinnedBuffer<int> flags{kRing};
+  int tags[kRing] = {};
+  long long recorded = 0;
+  std::int64_t waits = 0;  // host waits on an event (reported as SeriesInfo::host_waits)
+  FlagPoll() {
+    for (auto& e : ev) QSWG_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~FlagPoll() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  FlagPoll(const FlagPoll&) = delete;
+  FlagPoll& operator=(const FlagPoll&) = delete;
+  void record(const int* dev_flag, int tag, cudaStream_t s) {
+    const int k = static_cast<int>(recorded % kRing);
+    tags[k] = tag;
+    QSWG_CHECK(cudaMemcpyAsync(flags.get() + k, dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QSWG_CHECK(cudaEventRecord(ev[k], s));
+    ++recorded;
+  }
+  // The flag recorded kLag records ago (waiting for it if needed); false if
+  // there is none yet.
+  bool lagged(int& value, int& tag) {
+    if (recorded < kLag) return false;
+    const int k = static_cast<int>((recorded - kLag) % kRing);
+    if (cudaEventQuery(ev[k]) == cudaErrorNotReady) {
+      ++waits;
+      QSWG_CHECK(cudaEventSynchronize(ev[k]));
+    }
+    cudaGetLastError();
+    value = flags.get()[k];
+    tag = tags[k];
+    return true;
+  }
+};
+
 // Enqueues one step (expm.cpp:146-212).  `out` (local) receives the result;
 // scratch vectors come from the workspace.
 StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const TaylorParameters& params,
-                            double2* out, std::int64_t& launches) {
+                            double2* out, std::int64_t& launches, std::int64_t& host_waits) {
   const Liouvillian& l = ex.l;
   cudaStream_t s = ex.s;
   const StepParameters sp = select_parameters(l.one_norms().data(), t, params);
@@ -214,7 +246,13 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
     const double2* x_stage_full = ex.spmv_input(x_stage, kXStage);
     double2* acc = sums[st % 2];
     int pre = 0;  // own-column panels of this product already summed (overlapped exchange)
+    std::unique_ptr<FlagPoll> poll;
+    if (!ex.single) poll = std::make_unique<FlagPoll>();
     for (std::int64_t j = 1; j <= sp.m_star; ++j) {
+      if (!ex.single) {
+        int done = 0, tag = 0;
+        if (poll->lagged(done, tag) && done != 0) break;  // this stage stopped kLag terms ago
+      }
       const double2* x = j == 1 ? x_stage_full : term[(j - 1) % 2];
       double2* y = term[j % 2] + ex.row0;
       const double scale = t / (s_count * static_cast<double>(j));  // expm.cpp:174
@@ -226,12 +264,12 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
       pre = 0;
       if (!ex.single) {
         ex.comm->allreduce_max_u64(&ctl->term_bits, 2, s);  // term_bits, sum_bits
-        dev::step_control(ctl, j == 1, static_cast<int>(st), params.tolerance, s);
-        if (ex.read(&ctl->done)) break;  // expm.cpp:191-194 (error sets done)
+        dev::step_control(ctl, j == 1, static_cast<int>(st), params.tolerance, s);  // (error sets done)
+        poll->record(&ctl->done, static_cast<int>(j), s);
         if (j < sp.m_star) pre = ex.exchange_overlap(term[j % 2], mat, nullptr, ctl, 0);
       }
     }
-    if (!ex.single && ex.read(&ctl->error)) break;
+    if (poll) host_waits += poll->waits;
   }
   return sp;
 }
@@ -245,7 +283,8 @@ StepInfo step(const Liouvillian& l, const double2* v, double t, const TaylorPara
   reset_ctls(l, false);
   l.set_hermitian_input(v, herm_known);  // Hermitian input: the iterates stay Hermitian
   std::int64_t launches = 0;
-  const StepParameters sp = enqueue_step(ex, v, t, params, out, launches);
+  std::int64_t host_waits = 0;
+  const StepParameters sp = enqueue_step(ex, v, t, params, out, launches, host_waits);
   const Flags f = read_flags(l, false);
   if (f.error) throw NumericalError("non-finite values encountered in exponential action");
   return {sp.m_star, sp.s, f.spmvs, launches};
@@ -270,7 +309,7 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
 
   // states[0] = step(v, t1) (expm.cpp:225)
   double2* z = ex.local(kZ);
-  enqueue_step(ex, v, t1, params, z, info.launches);
+  enqueue_step(ex, v, t1, params, z, info.launches, info.host_waits);
   emit(0, z);
 
   const StepParameters span = select_parameters(l.one_norms().data(), tq - t1, params);
@@ -284,7 +323,7 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
     double2* cur = z;
     double2* nxt = ex.local(kNext);
     for (std::int64_t k = 1; k <= q; ++k) {
-      enqueue_step(ex, cur, h, params, nxt, info.launches);
+      enqueue_step(ex, cur, h, params, nxt, info.launches, info.host_waits);
       emit(k, nxt);
       std::swap(cur, nxt);
     }
@@ -333,10 +372,22 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
       for (std::int64_t k = 0; k < count; ++k) ss.s[k] = sums[static_cast<std::size_t>(k)];
       const double2* z_full = ex.spmv_input(z, kZFull);
       int pre = 0;  // own-column panels of this term already summed (overlapped exchange)
+      std::int64_t p_last = 0;  // the last term enqueued (several GPUs)
+      std::unique_ptr<FlagPoll> poll;
+      if (!ex.single) poll = std::make_unique<FlagPoll>();
       for (std::int64_t p = 1; p <= m_star; ++p) {
         const double2* x = p == 1 ? z_full : ring.k[(p - 1) % ring.slots];
         double2* kp = ring.k[p % ring.slots] + ex.row0;
         const bool last = p == m_star;
+        if (!ex.single) {
+          int active = 1, tag = 0;
+          if (poll->lagged(active, tag) && active == 0) break;  // the super-step ended kLag terms ago
+          if (p > 1)  // the flush after term p - 1 when its control asked for one (a no-op otherwise);
+                      // its norms join term p's allreduce
+            dev::series_flush(ring, ex.row0, ex.rows, z, ss, herm_n, static_cast<int>(p - 1), strict,
+                              params.tolerance, ctl, false, s);
+        }
+        p_last = p;
         if (!fused || p == 1) ex.prepare(mat, x);
         dev::DevMatrix mp = mat;
         mp.pre_done = pre;
@@ -351,23 +402,23 @@ SeriesInfo enqueue_series(const Liouvillian& l, const Exec& ex, const double2* v
                               params.tolerance, ctl, true, s);
           continue;
         }
-        ex.comm->allreduce_max_u64(&ctl->term_bits, 1, s);
-        dev::series_term_control(ctl, static_cast<int>(p), last ? 1 : 0, params.tolerance, s);
-        const auto [n_active, flush] = ex.read_active_flush(ctl);
-        if (n_active == 0) break;
-        if (flush) {
-          dev::series_flush(ring, ex.row0, ex.rows, z, ss, herm_n, static_cast<int>(p), strict,
-                            params.tolerance, ctl, false, s);
-          ex.comm->allreduce_max_u64(&ctl->sum_bits[0], static_cast<std::size_t>(count), s);
-          dev::series_flush_control(ctl, static_cast<int>(p), params.tolerance, s);
-          if (ex.read(&ctl->n_active) == 0) break;
-        }
+        // one allreduce: term p's maximum and the sums of the flush after p - 1 (adjacent fields)
+        ex.comm->allreduce_max_u64(&ctl->term_bits, 1 + static_cast<std::size_t>(count), s);
+        dev::series_flush_term_control(ctl, static_cast<int>(p), last ? 1 : 0, params.tolerance, s);
+        poll->record(&ctl->n_active, static_cast<int>(p), s);
         if (p < m_star) pre = ex.exchange_overlap(ring.k[p % ring.slots], mat, ctl, nullptr, 1);
       }
+      if (!ex.single && p_last > 0) {  // the flush after the last term enqueued (a no-op unless asked for)
+        dev::series_flush(ring, ex.row0, ex.rows, z, ss, herm_n, static_cast<int>(p_last), strict,
+                          params.tolerance, ctl, false, s);
+        ex.comm->allreduce_max_u64(&ctl->sum_bits[0], static_cast<std::size_t>(count), s);
+        dev::series_flush_control(ctl, static_cast<int>(p_last), params.tolerance, s);
+      }
+      if (poll) info.host_waits += poll->waits;
       for (std::int64_t k = 1; k <= count; ++k) emit(super * d + k, sums[static_cast<std::size_t>(k - 1)]);
       // the next super-step starts from states[(super + 1) d] = the last output
       std::swap(z, sums[static_cast<std::size_t>(count - 1)]);
-      if (!ex.single && ex.read(&ctl->error)) break;
+      // (an error skips every later kernel on the device; the call reports it at its end)
     }
   }
   return info;

@@ -31,6 +31,10 @@ struct SeriesInfo {
   std::int64_t launches = 0;  // kernels enqueued (emit() launches excluded)
   std::int64_t emits = 0;     // emit() calls
   bool graph = false;         // replayed from a captured CUDA graph
+  // Several GPUs: times the host waited for the device (an event of a term's
+  // stop flag kLag terms back, when the device was that far behind).  The
+  // stream itself is synchronised once per call (the error / SpMV counters).
+  std::int64_t host_waits = 0;
 };
 
 /// out = exp(t L) v.  `out` must not alias `v`.  Throws NumericalError on

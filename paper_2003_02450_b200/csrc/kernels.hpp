@@ -351,6 +351,10 @@ void series_init(const double2* z, std::int64_t n, int count, int pend_max, Seri
 void series_term(const DevMatrix& l, const double2* x, double2* kp, int p, bool last, double scale,
                  double tol, SeriesCtl* ctl, bool decide, cudaStream_t s);
 void series_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s);
+// Several GPUs, after term p and one allreduce of [term_bits, sum_bits]: the
+// exact tests of the flush after term p - 1 (when one ran), then term p's
+// control (skipped when term p is not part of the series).
+void series_flush_term_control(SeriesCtl* ctl, int p, int last, double tol, cudaStream_t s);
 // When ctl->flush: for every marked output k, S_k = (fresh_k ? Z : S_k) +
 // sum over its pending terms q of k^q K_q, in term order (expm.cpp:300-305),
 // then its exact stop test of term p (expm.cpp:306-316).  No-op otherwise.
