@@ -1094,6 +1094,75 @@ __device__ __forceinline__ void shfl_rows(const KronEll& e, double2 cv, int len,
   }
 }
 
+// W_0 = Q_0 X and AX = A X from the same gathers (KronView::ax): acc from
+// Q's values, aacc from A's values aligned to Q's entries; the same per-row
+// entry order as shfl_rows / uniform_rows, so each sum is the one its own
+// list would give.
+template <int KQ, bool CQ, int KA, bool CA, int L, class G>
+__device__ __forceinline__ void shfl_rows2_len(const KronEll& e, const double2* aval, double2 cvq, double2 cva, int len,
+                                               int base, int mycol, int l0, double2* acc, double2* aacc, G&& g) {
+  const int n_e = L > 0 ? L : len;
+#pragma unroll(L > 0 ? L : 2)
+  for (int k = 0; k < n_e; ++k) {
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const unsigned c = static_cast<unsigned>(__shfl_sync(0xffffffffu, mycol, kKR * k + r));
+      const double2 xv = g(c);
+      cfmak<KQ>(acc[r], opv<KQ, CQ>(e.val + base + 32 * k + l0 + r, cvq), xv);
+      cfmak<KA>(aacc[r], opv<KA, CA>(aval + base + 32 * k + l0 + r, cva), xv);
+    }
+  }
+}
+template <int KQ, bool CQ, int KA, bool CA, class G>
+__device__ __forceinline__ void shfl_rows2(const KronEll& e, const double2* aval, double2 cvq, double2 cva, int len,
+                                           int slice, int l0, double2* acc, double2* aacc, G&& g) {
+  const int lane = threadIdx.x & 31;
+  const int base = __ldg(e.sptr + slice);
+  const int kt = lane >> 2, rt = lane & 3;
+  const int mycol = kt < len ? __ldg(e.col + base + 32 * kt + l0 + rt) : 0;
+  if (len == 4) {
+    shfl_rows2_len<KQ, CQ, KA, CA, 4>(e, aval, cvq, cva, len, base, mycol, l0, acc, aacc, g);
+  } else if (len == 6) {
+    shfl_rows2_len<KQ, CQ, KA, CA, 6>(e, aval, cvq, cva, len, base, mycol, l0, acc, aacc, g);
+  } else {
+    shfl_rows2_len<KQ, CQ, KA, CA, 0>(e, aval, cvq, cva, len, base, mycol, l0, acc, aacc, g);
+  }
+}
+template <int KQ, bool CQ, int KA, bool CA, class G>
+__device__ __forceinline__ void uniform_rows2(const KronList& l, const double2* aval, double2 cvq, double2 cva,
+                                              const int* rows, double2* acc, double2* aacc, G&& g) {
+  if (l.ptr == nullptr) return;
+#pragma unroll
+  for (int r = 0; r < kKR; ++r) {
+    const int e1 = __ldg(l.ptr + rows[r] + 1);
+#pragma unroll kRowUnroll
+    for (int e = __ldg(l.ptr + rows[r]); e < e1; ++e) {
+      const double2 xv = g(static_cast<unsigned>(__ldg(l.col + e)));
+      cfmak<KQ>(acc[r], opv<KQ, CQ>(l.val + e, cvq), xv);
+      cfmak<KA>(aacc[r], opv<KA, CA>(aval + e, cva), xv);
+    }
+  }
+}
+// f(ValK<Q class>, ConstK<Q const>, ValK<A class>, ConstK<A const>) for the
+// AX combination (Q real, A imaginary; KronView::ax guarantees it).
+template <class F>
+__device__ __forceinline__ void by_kind_ax(int kq, int ka, F&& f) {
+  const bool cq = (kq & kValConst) != 0, ca = (ka & kValConst) != 0;
+  if (cq) {
+    if (ca) {
+      f(ValK<kValReal>{}, ConstK<true>{}, ValK<kValImag>{}, ConstK<true>{});
+    } else {
+      f(ValK<kValReal>{}, ConstK<true>{}, ValK<kValImag>{}, ConstK<false>{});
+    }
+  } else {
+    if (ca) {
+      f(ValK<kValReal>{}, ConstK<false>{}, ValK<kValImag>{}, ConstK<true>{});
+    } else {
+      f(ValK<kValReal>{}, ConstK<false>{}, ValK<kValImag>{}, ConstK<false>{});
+    }
+  }
+}
+
 // Row-indexed part, transposed (Hermitian path): acc[r] at (i[r], j), warp-
 // uniform rows i[r], lane = column j: A from conj X(j, c), R_k from the
 // row-major copy Wt_k (Wt_k[n b + j] = W_k(b, j)).  Column lists pre-scaled.
@@ -1105,15 +1174,20 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
   // rows i[r] = I*32 + 4w + r: lanes 4w .. 4w+3 of ELL slice I (clamped edge rows read
   // that slice's padding lanes, whose results are discarded)
   const int sl = i[0] >> 5, l0 = (threadIdx.x >> 5) * kKR;
-  by_kind(m.vk_a, [&](auto kc, auto cc) {
-    QSWG_KC(kc, cc);
-    const auto g = [&](unsigned cn) { return conj2(gat(xj, cn, xpol)); };
-    if (m.a_len > 0) {
-      shfl_rows<K, C>(m.a_ellu, m.cv_a, m.a_len, sl, l0, acc, g);
-    } else if (m.a_sc.ptr) {
-      uniform_rows<K, C>(m.a_sc, m.cv_a, i, acc, g);
-    }
-  });
+  if (m.ax) {  // A's part = AX(i, j), formed by the W kernel (KronView::ax)
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) acc[r] = gat(m.axt + j, static_cast<unsigned>(i[r]) * n, xpol);
+  } else {
+    by_kind(m.vk_a, [&](auto kc, auto cc) {
+      QSWG_KC(kc, cc);
+      const auto g = [&](unsigned cn) { return conj2(gat(xj, cn, xpol)); };
+      if (m.a_len > 0) {
+        shfl_rows<K, C>(m.a_ellu, m.cv_a, m.a_len, sl, l0, acc, g);
+      } else if (m.a_sc.ptr) {
+        uniform_rows<K, C>(m.a_sc, m.cv_a, i, acc, g);
+      }
+    });
+  }
   if constexpr (kF == 1) {
     for (int k = 0; k < m.nk; ++k) {
       const double2* wtj = m.wt[k] + j;
@@ -1148,7 +1222,7 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
       });
     }
   }
-  if (m.b_rows) {  // B(j, c) X(i, c) = B(j, c) conj x[n i + c], lane = j: padding-free ELL rows of B
+  if (m.b_rows && !m.ax) {  // B(j, c) X(i, c) = B(j, c) conj x[n i + c], lane = j: padding-free ELL rows of B
     const int sj = j >> 5, ln = j & 31;
     const KronEll& be = m.b_ell;
     const double2* xr[kKR];
@@ -1184,11 +1258,29 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
       });
     }
   }
-  if (m.b.ptr && !(kHerm && m.b_rows)) {  // B (x) I: coalesced columns c of X
+  if (kHerm && m.ax) {  // B's part = conj AX(j, i) (KronView::ax), added as one sum
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) {
+      const double2 b = gat(m.axt + i, static_cast<unsigned>(j[r]) * n, xpol);
+      acc[r].x += b.x;
+      acc[r].y -= b.y;
+    }
+  } else if (m.b.ptr && !(kHerm && m.b_rows)) {  // B (x) I: coalesced columns c of X
     const double2* xi = x + i;
     by_kind(m.vk_b, [&](auto kc, auto cc) {
       QSWG_KC(kc, cc);
-      uniform_rows<K, C>(m.b, m.cv_b, j, acc, [&](unsigned cn) { return gat(xi, cn, xpol); });
+      const auto g = [&](unsigned cn) { return gat(xi, cn, xpol); };
+      if (m.b_sep) {  // summed on its own, then added: the association of the AX path
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) {
+          double2 bs = make_double2(0.0, 0.0);
+          uniform_row<K, C>(m.b, m.cv_b, j[r], bs, g);
+          acc[r].x += bs.x;
+          acc[r].y += bs.y;
+        }
+      } else {
+        uniform_rows<K, C>(m.b, m.cv_b, j, acc, g);
+      }
     });
   }
   if constexpr (kF == 1) {
@@ -1403,7 +1495,33 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_W_MIN_BLOCKS) kron_w_kerne
       const int au = J * kKT + lane;  // column a (single GPU: c0 = 0)
       const double2* xa = x + (au < g.n ? au : g.n - 1);
       const auto gx = [&](unsigned bn) { return conj2(gat(xa, bn, xpol)); };  // q_ellu / q_sc hold b * n
-      if (m.q_len[k] > 0) {  // rows I*32 + 4w + r: lanes 4w .. 4w+3 of slice I
+      if (k == 0 && m.ax) {  // W_0 and AX from the same gathers (KronView::ax)
+        double2 aacc[kKR];
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) aacc[r] = make_double2(0.0, 0.0);
+        int ir[kKR];
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) {
+          const int iv = I * kKT + kKR * w + r;
+          ir[r] = iv < g.n ? iv : g.n - 1;
+        }
+        by_kind_ax(vk, m.vk_aq, [&](auto kq, auto cq, auto ka, auto ca) {
+          constexpr int KQ = decltype(kq)::value, KA = decltype(ka)::value;
+          constexpr bool CQ = decltype(cq)::value, CA = decltype(ca)::value;
+          if (m.q_len[0] > 0) {
+            shfl_rows2<KQ, CQ, KA, CA>(m.q_ellu[0], m.aq_ellu_val, cv, m.cv_aq, m.q_len[0], ir[0] >> 5, kKR * w, acc,
+                                       aacc, gx);
+          } else {
+            uniform_rows2<KQ, CQ, KA, CA>(m.q_sc[0], m.aq_sc_val, cv, m.cv_aq, ir, acc, aacc, gx);
+          }
+        });
+        const unsigned arow = static_cast<unsigned>(I * kKT + kKR * w) * n + static_cast<unsigned>(au);
+#pragma unroll
+        for (int r = 0; r < kKR; ++r) {
+          const int iv = I * kKT + kKR * w + r;
+          if (iv < g.n && au < g.n) st_hint(m.axt + (arow + static_cast<unsigned>(r) * n), aacc[r], xpol);
+        }
+      } else if (m.q_len[k] > 0) {  // rows I*32 + 4w + r: lanes 4w .. 4w+3 of slice I
         const int iv0 = I * kKT + kKR * w;
         by_kind(vk, [&](auto kc, auto cc) {
           QSWG_KC(kc, cc);

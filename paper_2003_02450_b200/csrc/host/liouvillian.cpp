@@ -406,6 +406,43 @@ int value_class(const std::vector<double2>& v, double2* cv = nullptr) {
   return k;
 }
 
+// Whether b(j, c) = conj a(j, c) entry by entry (same pattern and order).
+bool conj_pair(const MultiCsr& a, const MultiCsr& b) {
+  if (a.ptr != b.ptr || a.col != b.col || a.val.size() != b.val.size() || a.col.empty()) return false;
+  for (std::size_t k = 0; k < a.val.size(); ++k)
+    if (!(b.val[k].x == a.val[k].x && b.val[k].y == -a.val[k].y)) return false;
+  return true;
+}
+
+// Whether every entry of a lies on q's pattern (rows of both sorted by column).
+bool pattern_within(const MultiCsr& a, const MultiCsr& q) {
+  if (a.ptr.empty() || q.ptr.empty() || a.n != q.n) return false;
+  for (std::int64_t i = 0; i < a.n; ++i) {
+    int kq = q.ptr[static_cast<std::size_t>(i)];
+    const int eq = q.ptr[static_cast<std::size_t>(i) + 1];
+    for (int ka = a.ptr[static_cast<std::size_t>(i)]; ka < a.ptr[static_cast<std::size_t>(i) + 1]; ++ka) {
+      while (kq < eq && q.col[static_cast<std::size_t>(kq)] < a.col[static_cast<std::size_t>(ka)]) ++kq;
+      if (kq == eq || q.col[static_cast<std::size_t>(kq)] != a.col[static_cast<std::size_t>(ka)]) return false;
+      ++kq;
+    }
+  }
+  return true;
+}
+
+// q's pattern carrying a's values (0 where a has no entry); a within q.
+MultiCsr aligned_values(const MultiCsr& a, const MultiCsr& q) {
+  MultiCsr o = q;
+  for (std::int64_t i = 0; i < q.n; ++i) {
+    int ka = a.ptr[static_cast<std::size_t>(i)];
+    const int ea = a.ptr[static_cast<std::size_t>(i) + 1];
+    for (int kq = q.ptr[static_cast<std::size_t>(i)]; kq < q.ptr[static_cast<std::size_t>(i) + 1]; ++kq) {
+      const bool hit = ka < ea && a.col[static_cast<std::size_t>(ka)] == q.col[static_cast<std::size_t>(kq)];
+      o.val[static_cast<std::size_t>(kq)] = hit ? a.val[static_cast<std::size_t>(ka++)] : make_double2(0.0, 0.0);
+    }
+  }
+  return o;
+}
+
 // Column offsets pre-multiplied by n (kernels.hpp: KronView), for the lists
 // the kernels gather as base + c n: c n < n^2 = dim < 2^31.
 MultiCsr scaled(const MultiCsr& m) {
@@ -534,9 +571,20 @@ struct KronStore {
       p_sc.push_back(upload_list(scaled(host.p[k]), s));
       q_sc.push_back(upload_list(scaled(host.q[k]), s));
     }
+    // AX from the gathers of W_0 (kernels.hpp: KronView::ax)
+    ax = factored && single && host.q.size() == 1 && (vk_q[0] & 3) == dev::kValReal &&
+         (vk_a & 3) == dev::kValImag && conj_pair(a_host, b_host) && pattern_within(a_host, host.q[0]);
+    if (const char* e = std::getenv("QSWG_KRON_AX"); e && e[0] == '0') ax = false;  // experiment knob
+    if (ax) {
+      const MultiCsr aq = aligned_values(a_host, host.q[0]);  // Q_0's pattern, A's values (0 elsewhere)
+      vk_aq = value_class(aq.val, &cv_aq);
+      aq_sc_val = up(aq.val, s);
+      if (q_len[0] > 0) aq_ellu_val = up(to_ell(aq).val, s);  // the layout of q_ellu[0]
+    }
     if (const char* vk = std::getenv("QSWG_KRON_VALCLASS"); vk && vk[0] == '0') {  // experiment knob: all complex
       vk_a = vk_b = vk_t = vk_d = dev::kValComplex;
       for (auto* v : {&vk_p, &vk_q, &vk_r, &vk_s, &vk_u}) std::fill(v->begin(), v->end(), dev::kValComplex);
+      ax = false;
     } else if (vk && vk[0] == '1') {  // experiment knob: classes without the constant-value loads
       vk_a &= 3;
       vk_b &= 3;
@@ -582,6 +630,11 @@ struct KronStore {
   double2 cv_a{}, cv_b{};
   std::vector<double2> cv_p, cv_q, cv_r, cv_s;
   DeviceBuffer<int2> herm_tiles;               // one GPU: upper tiles in launch order
+  bool ax = false;                             // kernels.hpp: KronView::ax
+  int vk_aq = dev::kValComplex;
+  double2 cv_aq{};
+  const double2* aq_sc_val = nullptr;
+  const double2* aq_ellu_val = nullptr;
   dev::KronList a_sc;                          // A (as a_list) with columns scaled by n
   std::vector<dev::KronList> p_sc, q_sc, r_sc;  // P_k, Q_k, R_k with columns scaled by n
   dev::KronList af, bf;
@@ -684,6 +737,7 @@ void Liouvillian::adopt(Liouvillian& o) {
   std::swap(kron_v_, o.kron_v_);
   std::swap(herm_flag_, o.herm_flag_);
   std::swap(kron_wt_, o.kron_wt_);
+  std::swap(kron_axt_, o.kron_axt_);
   std::swap(ws_, o.ws_);  // drops captured series graphs and control blocks of the old operator
   herm_ = 0;
 }
@@ -858,6 +912,15 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.herm_flag = herm_flag_.get();
     m.kron.herm = herm_;
     for (std::size_t k = 0; k < kron_wt_.size(); ++k) m.kron.wt[k] = kron_wt_[k].get();
+    if (kron_->ax && kron_axt_.get()) {
+      m.kron.ax = 1;
+      m.kron.b_sep = 1;
+      m.kron.axt = kron_axt_.get();
+      m.kron.aq_ellu_val = kron_->aq_ellu_val;
+      m.kron.aq_sc_val = kron_->aq_sc_val;
+      m.kron.vk_aq = kron_->vk_aq;
+      m.kron.cv_aq = kron_->cv_aq;
+    }
   }
   return m;
 }
@@ -1215,6 +1278,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       QSWG_CHECK(cudaMemsetAsync(l->herm_flag_.get(), 0, sizeof(int), s));
       if (l->kron_->factored)
         for (std::size_t k = 0; k < hops.p.size(); ++k) l->kron_wt_.emplace_back(static_cast<std::size_t>(dim));
+      if (l->kron_->ax) l->kron_axt_.resize(static_cast<std::size_t>(dim));
     }
     QSWG_CHECK(cudaStreamSynchronize(s));
     grp.reset();

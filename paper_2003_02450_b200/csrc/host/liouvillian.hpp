@@ -179,6 +179,7 @@ class Liouvillian {
   mutable int herm_ = 0;         // the current call's input is Hermitian (kernels.hpp: KronView::herm)
   int herm_mode_ = 1;            // set_hermitian_mode
   std::vector<DeviceBuffer<double2>> kron_wt_;  // factored + one GPU: row-major W_k for the Hermitian path
+  DeviceBuffer<double2> kron_axt_;               // kernels.hpp: KronView::axt
   mutable Workspace ws_;
   // build_local / build_global inputs, re-run by set_omega on a fixed partition
   std::function<std::unique_ptr<Liouvillian>(double, const std::vector<std::int64_t>*)> rebuild_;

@@ -175,6 +175,21 @@ struct KronView {
   // (a, r, q, a_ell, q_ell, p_ell, b_ell and t hold plain columns).
   KronList a_sc, r_sc[kMaxKron], q_sc[kMaxKron];
   KronTiles tg;
+  // ax (one GPU, factored, one Lindblad operator): A's pattern lies inside
+  // Q_0's and B = conj(A) entrywise (a Hermitian H / H_rot).  The Hermitian W
+  // kernel then also forms AX = A X from the gathers of W_0 = Q_0 X (A's
+  // values aligned to Q_0's entries: aq_ellu_val / aq_sc_val, class vk_aq,
+  // constant cv_aq) into axt (row-major, axt[n i + j] = AX(i, j)); the
+  // Hermitian term kernel reads A's part as AX(i, j) and B's as conj AX(j, i)
+  // — Sum_c B(j, c) X(i, c) = conj Sum_c A(j, c) X(c, i) exactly, term by
+  // term.  b_sep: the general path sums B's part on its own before adding
+  // it, the association the Hermitian path has.
+  int ax = 0, b_sep = 0;
+  double2* axt = nullptr;
+  const double2* aq_ellu_val = nullptr;
+  const double2* aq_sc_val = nullptr;
+  int vk_aq = kValComplex;
+  double2 cv_aq{};
 };
 
 // The device superoperator block as the Taylor kernels see it.  group: CSR
