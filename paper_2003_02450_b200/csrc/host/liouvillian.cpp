@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -1181,6 +1182,54 @@ void kron_halos(const HostOperands& h, bool factored, std::int64_t n, const std:
 
 }  // namespace
 
+// Several GPUs, format "auto".  Row-partitioned, the
+// matrix-free action loses the Hermitian halving and exchanges x plus the
+// W_k (V_k) work vectors every term; the stored superoperator streams
+// 20 B/nnz of its own rows and exchanges x only.  Per rank and term, from the
+// one-GPU measurements:
+//   KRON  operand entries per element (+ W's) * 16 B * rows / 7 TB/s (the L2
+//         gather rate the KRON kernels reach on c2-c5), at least 1.5 us per
+//         entry (the dependent gather chain of one tile), + (x, W_k, V_k halos) / 900 GB/s
+//   SELL  (20 nnz + 48 rows) / (0.75 * 6.5 TB/s) (stored SpMV at 0.66-0.85 of
+//         HBM) + its x halo (the hull of x and W's) / 900 GB/s
+// Every input is rank-independent (totals / world, the halo tables of all
+// ranks), so every rank picks the same format; the stored copy must also fit
+// (20 B/nnz per rank within 40% of the device memory).  QSWG_MULTI_FORMAT=kron /
+// sell overrides.
+bool stored_beats_kron(const HostOperands& hops, std::int64_t n, std::int64_t nnz_total,
+                       const std::vector<std::int64_t>& starts) {
+  const int world = static_cast<int>(starts.size()) - 1;
+  if (const char* e = std::getenv("QSWG_MULTI_FORMAT")) return std::string(e) == "sell";
+  const HostOperands h = hops.summed();
+  const bool factored = h.has_factored && h.kron_cost(true, false) < 0.8 * h.kron_cost(false);
+  std::vector<std::vector<std::int64_t>> lo, hi, wlo, whi, vlo, vhi;
+  kron_halos(h, factored, n, starts, lo, hi, wlo, whi, vlo, vhi);
+  double kron_halo = 0.0, sell_halo = 0.0;
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) {
+      const auto R = static_cast<std::size_t>(r), Q = static_cast<std::size_t>(q);
+      const double x = static_cast<double>(hi[R][Q] - lo[R][Q]), wv = static_cast<double>(whi[R][Q] - wlo[R][Q]);
+      kron_halo += x + wv + static_cast<double>(vhi[R][Q] - vlo[R][Q]);
+      const std::int64_t slo = std::min(lo[R][Q] == hi[R][Q] ? wlo[R][Q] : lo[R][Q], wlo[R][Q] == whi[R][Q] ? lo[R][Q] : wlo[R][Q]);
+      const std::int64_t shi = std::max(hi[R][Q], whi[R][Q]);
+      sell_halo += static_cast<double>(shi - slo);
+    }
+  const double w = static_cast<double>(world), rows = static_cast<double>(n) * static_cast<double>(n) / w;
+  const double entries = h.kron_cost(factored, false);  // operand entries per output element
+  // (a latency floor: a KRON term is at least one tile's dependent gather
+  // chain, ~1.5 us per operand entry per element — c2 on one GPU, one wave)
+  const double t_kron = std::max(entries * 16.0 * rows / 7e12, 1.5e-6 * entries) + 16.0 * kron_halo / w / 9e11;
+  const double t_sell = (20.0 * static_cast<double>(nnz_total) / w + 48.0 * rows) / (0.75 * 6.5e12) +
+                        16.0 * sell_halo / w / 9e11;
+  std::size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);  // (the total: the same on every rank)
+  const bool fits = 20.0 * static_cast<double>(nnz_total) / w < 0.4 * static_cast<double>(total_b);
+  if (std::getenv("QSWG_DEBUG_FORMAT"))
+    std::fprintf(stderr, "qswg: world %d: modelled term KRON %.1f us, stored %.1f us%s\n", world, 1e6 * t_kron,
+                 1e6 * t_sell, fits ? "" : " (stored does not fit)");
+  return fits && t_sell < t_kron;
+}
+
 std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_t n, const HostOperands& hops,
                                                        const DeviceConfig& cfg,
                                                        const std::vector<std::int64_t>* fixed_starts) {
@@ -1258,9 +1307,11 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   }
 
   // ---- matrix-free Kronecker action: no superoperator stored ----
-  // (the default: fewest bytes and fastest on every BASELINE config; the
-  // bitwise reference-order mode needs a stored superoperator)
-  if ((cfg.format == 3 || (cfg.format == 0 && dim > kKronMinDim)) && cfg.group != 1) {
+  // (the default: fewest bytes and fastest on every BASELINE config on one
+  // GPU; the bitwise reference-order mode needs a stored superoperator; on
+  // several GPUs a cost model may pick the stored one)
+  if ((cfg.format == 3 || (cfg.format == 0 && dim > kKronMinDim && !(world > 1 && stored_beats_kron(hops, n, l->nnz_total_, l->starts_)))) &&
+      cfg.group != 1) {
     const std::int64_t j0 = l->block_.row0 / n, j1 = (l->block_.row0 + l->block_.rows) / n;
     l->nnz_local_ = colptr[static_cast<std::size_t>(j1)] - colptr[static_cast<std::size_t>(j0)];
     l->format_ = dev::Format::Kron;
