@@ -1191,7 +1191,7 @@ void kron_halos(const HostOperands& h, bool factored, std::int64_t n, const std:
 //         gather rate the KRON kernels reach on c2-c5), at least 1.5 us per
 //         entry (the dependent gather chain of one tile), + (x, W_k, V_k halos) / 900 GB/s
 //   SELL  (20 nnz + 48 rows) / (0.75 * 6.5 TB/s) (stored SpMV at 0.66-0.85 of
-//         HBM) + its x halo (the hull of x and W's) / 900 GB/s
+//         HBM), at least 60 us, + its x halo (the hull of x and W's) / 900 GB/s
 // Every input is rank-independent (totals / world, the halo tables of all
 // ranks), so every rank picks the same format; the stored copy must also fit
 // (20 B/nnz per rank within 40% of the device memory).  QSWG_MULTI_FORMAT=kron /
@@ -1219,7 +1219,9 @@ bool stored_beats_kron(const HostOperands& hops, std::int64_t n, std::int64_t nn
   // (a latency floor: a KRON term is at least one tile's dependent gather
   // chain, ~1.5 us per operand entry per element — c2 on one GPU, one wave)
   const double t_kron = std::max(entries * 16.0 * rows / 7e12, 1.5e-6 * entries) + 16.0 * kron_halo / w / 9e11;
-  const double t_sell = (20.0 * static_cast<double>(nnz_total) / w + 48.0 * rows) / (0.75 * 6.5e12) +
+  // (a floor as well: a sharded stored term with its panel and flush launches
+  // took 62 us per rank on c2 at N = 8, profiles/r02_scaling_sell.jsonl)
+  const double t_sell = std::max((20.0 * static_cast<double>(nnz_total) / w + 48.0 * rows) / (0.75 * 6.5e12), 60e-6) +
                         16.0 * sell_halo / w / 9e11;
   std::size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);  // (the total: the same on every rank)

@@ -6,9 +6,12 @@ in-process ranks, each rank's term is timed alone on the GPU (prepare + term
 kernel + flush, CUDA events; no rank ever waits on another), and the halo
 volume each rank receives per term comes from the real halo plan.
 
-  T_N (no overlap)   = max_r compute_r + max_r halo_r / B
-  T_N (overlap)      = max_r max(compute_r, halo_r / B)
-with B = 900 GB/s (NVLink 5 per direction; the exchange of the factored KRON
+  T_N (no overlap)   = max_r compute_r + max_r halo_r / B + L
+  T_N (overlap)      = max_r max(compute_r, halo_r / B) + L
+with L the per-term collective latency (one allreduce per term since round 2;
+reported for L = 0, 10, 20 us — it cannot be measured on one GPU) plus, for
+the round-1 flow, one host synchronisation per term (measured here: a stream
+synchronisation after a term's launches), and B = 900 GB/s (NVLink 5 per direction; the exchange of the factored KRON
 path also moves W, counted as a second x-sized halo).  Efficiency is against
 the measured one-GPU term (Hermitian path).  A model, not a measurement:
 DESIGN.md section 5 says so beside the numbers."""
@@ -27,6 +30,25 @@ ap.add_argument("--worlds", default="2,4,8")
 ap.add_argument("--format", default="auto")
 ap.add_argument("--bw", type=float, default=900e9)
 a = ap.parse_args()
+LAT_US = (0.0, 10.0, 20.0)
+
+
+def sync_latency_ms():
+    """Host round trip of one stream synchronisation after a small launch."""
+    import time
+    import numpy as np
+    w = graphs.config("c1", size=8)
+    l = api.build_local(w.omega, w.h, w.ops[0])
+    v = l.state().from_probabilities(w.rho0)
+    out = []
+    for _ in range(50):
+        t0 = time.perf_counter()
+        v.populations()  # one tiny kernel + D2H + synchronisation
+        out.append(time.perf_counter() - t0)
+    return 1e3 * float(np.median(out))
+
+
+SYNC_MS = sync_latency_ms()
 D = {"c1": 5, "c2": 6, "c3": 1, "c4": 2, "c5": 2}
 
 
@@ -72,9 +94,14 @@ for name in a.configs.split(","):
         t_comm = [h / a.bw * 1e3 for h in halo]
         no_ov = max(comp) + max(t_comm)
         ov = max(max(c, tc) for c, tc in zip(comp, t_comm))
+        eff = {f"L{int(lat)}us": {"overlap": t1 / (world * (ov + lat * 1e-3)),
+                                  "no_overlap": t1 / (world * (no_ov + lat * 1e-3)),
+                                  "round1_flow_overlap": t1 / (world * (ov + lat * 1e-3 + SYNC_MS))}
+               for lat in LAT_US}
         print(json.dumps({"config": name, "format": fmt, "world": world, "one_gpu_term_ms": t1,
+                          "one_gpu_format": fmt,
                           "rank_compute_ms": comp, "rank_halo_mb": [h / 1e6 for h in halo],
                           "model_term_ms_no_overlap": no_ov, "model_term_ms_overlap": ov,
-                          "efficiency_no_overlap": t1 / (world * no_ov), "efficiency_overlap": t1 / (world * ov)}),
+                          "host_sync_ms_measured": SYNC_MS, "efficiency": eff}),
               flush=True)
         del ranks, comms
