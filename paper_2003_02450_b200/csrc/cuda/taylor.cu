@@ -1330,7 +1330,16 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
       }
     }
   }
-  if (m.d_loc) {  // -0.5 (w (dl_i + dl_j) + ds_i + ds_j) X(i, j)
+  if (m.d_const) {  // a constant coefficient (regular graphs, no sources / sinks)
+    if (m.d_val != 0.0) {
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {
+        const double2 xg = ld_gather(xij[r], xpol);
+        acc[r].x = fma(-m.d_val, xg.x, acc[r].x);
+        acc[r].y = fma(-m.d_val, xg.y, acc[r].y);
+      }
+    }
+  } else if (m.d_loc) {  // -0.5 (w (dl_i + dl_j) + ds_i + ds_j) X(i, j)
     const double dli = __ldg(m.d_loc + i), dsi = __ldg(m.d_ss + i);
 #pragma unroll
     for (int r = 0; r < kKR; ++r) {
@@ -1430,6 +1439,12 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
     for (int r = 0; r < kKR; ++r) {
       const int jl = J * kKT + kKR * w + r;
       jg[r] = g.c0 + (jl < g.nc ? jl : g.nc - 1);
+    }
+    if (m.d_loc) {  // the decay term reads the tile's own elements last: start them towards L2 now
+#pragma unroll
+      for (int r = 0; r < kKR; ++r)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + (static_cast<unsigned>(jg[r]) * static_cast<unsigned>(g.n) +
+                                                          static_cast<unsigned>(i))));
     }
     double2 acc[kKR];
     if constexpr (kHerm) {

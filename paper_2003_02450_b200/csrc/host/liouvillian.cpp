@@ -582,6 +582,16 @@ struct KronStore {
       aq_sc_val = up(aq.val, s);
       if (q_len[0] > 0) aq_ellu_val = up(to_ell(aq).val, s);  // the layout of q_ellu[0]
     }
+    // a constant decay coefficient, as the kernels round it (kernels.hpp: d_const)
+    if (!host.d_loc.empty()) {
+      bool same = true;
+      for (std::size_t i = 0; i < host.d_loc.size() && same; ++i)
+        same = host.d_loc[i] == host.d_loc[0] && host.d_ss[i] == 0.0;
+      if (same) {
+        d_const = true;
+        d_val = 0.5 * ((host.omega * (host.d_loc[0] + host.d_loc[0]) + 0.0) + 0.0);
+      }
+    }
     if (const char* vk = std::getenv("QSWG_KRON_VALCLASS"); vk && vk[0] == '0') {  // experiment knob: all complex
       vk_a = vk_b = vk_t = vk_d = dev::kValComplex;
       for (auto* v : {&vk_p, &vk_q, &vk_r, &vk_s, &vk_u}) std::fill(v->begin(), v->end(), dev::kValComplex);
@@ -632,6 +642,8 @@ struct KronStore {
   std::vector<double2> cv_p, cv_q, cv_r, cv_s;
   DeviceBuffer<int2> herm_tiles;               // one GPU: upper tiles in launch order
   bool ax = false;                             // kernels.hpp: KronView::ax
+  bool d_const = false;                        // kernels.hpp: KronView::d_const
+  double d_val = 0.0;
   int vk_aq = dev::kValComplex;
   double2 cv_aq{};
   const double2* aq_sc_val = nullptr;
@@ -909,6 +921,8 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     m.kron.b_ell = kron_->b_rows ? kron_->b_ell : dev::KronEll{};
     m.kron.d_loc = o.d_loc;
     m.kron.d_ss = o.d_ss;
+    m.kron.d_const = kron_->d_const ? 1 : 0;
+    m.kron.d_val = kron_->d_val;
     m.kron.omega = o.omega;
     m.kron.herm_flag = herm_flag_.get();
     m.kron.herm = herm_;

@@ -184,6 +184,10 @@ struct KronView {
   // — Sum_c B(j, c) X(i, c) = conj Sum_c A(j, c) X(c, i) exactly, term by
   // term.  b_sep: the general path sums B's part on its own before adding
   // it, the association the Hermitian path has.
+  // d_const: every decay coefficient 0.5 (w (dl_i + dl_j) + ds_i + ds_j) is
+  // the same value d_val (constant dl, no sources / sinks: regular graphs)
+  int d_const = 0;
+  double d_val = 0.0;
   int ax = 0, b_sep = 0;
   double2* axt = nullptr;
   const double2* aq_ellu_val = nullptr;
