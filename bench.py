@@ -393,7 +393,8 @@ def main():
         s_ms = sp["term"]
         vs = ls.state().from_probabilities(w.rho0)
         api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)  # warm-up
-        rs = api.series(ls, vs, w.t1, w.tq, w.steps, populations=False)
+        rs = min((api.series(ls, vs, w.t1, w.tq, w.steps, populations=False) for _ in range(3)),
+                 key=lambda r: r.info.device_ms)  # best of 3 (a secondary number; shared boxes are noisy)
         sb = term_bytes(ls, n_lind)
         superop = {"format": ls.format, "kernel": "sell_series_term_kernel" if ls.format == "sell" else
                    "series_term_kernel", "bytes_per_launch": sb, "ms_per_launch": s_ms,
@@ -477,7 +478,7 @@ def config_block(name, peak):
     v = l.state().from_probabilities(w.rho0)
     # warm-up: allocates the workspace (term ring, sums) with a short series of the same plan shape
     api.series(l, v, w.t1, w.t1 + (w.tq - w.t1) / w.steps * 2, 2, populations=False)
-    reps = 1 if w.dim > 100_000_000 else 2  # c5: one 14 s series
+    reps = 1 if w.dim > 100_000_000 else 3  # best of 3 (c5: one 12 s series)
     best = None
     for _ in range(reps):
         r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
