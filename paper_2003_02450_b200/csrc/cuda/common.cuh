@@ -129,7 +129,10 @@ __device__ __forceinline__ double2 ld_gather(const double2* p, unsigned long lon
 #else
   (void)pol;  // plain read-only load: measured faster than the L2 evict-last hint (c2 1.38x, c3 1.24x)
 #ifdef QSWG_GATHER_FOLD  // experiment (wrong results): fold every 1 MB onto its first 512 B (L1-resident gathers)
-  p = reinterpret_cast<const double2*>(reinterpret_cast<unsigned long long>(p) & ~0xFFE00ull);
+#ifndef QSWG_GATHER_FOLD_MASK
+#define QSWG_GATHER_FOLD_MASK 0xFFE00ull
+#endif
+  p = reinterpret_cast<const double2*>(reinterpret_cast<unsigned long long>(p) & ~QSWG_GATHER_FOLD_MASK);
 #endif
   return __ldg(p);
 #endif

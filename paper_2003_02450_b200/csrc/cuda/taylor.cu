@@ -734,25 +734,310 @@ __device__ __forceinline__ double2 sell_dot(const SellView& m, long long b, int 
 }
 
 // Warp-uniform loop over slices; epi(row, acc, valid) runs on every lane.
-template <bool kStrict, class Epi>
-__device__ __forceinline__ void slice_loop(const SellView& m, const double2* __restrict__ x, Epi&& epi) {
-  const unsigned long long pol = evict_first_policy(), xpol = evict_last_policy();
-  const int lane = threadIdx.x & 31;
-  const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
-  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  for (long long sl = warp; sl < m.n_slices; sl += nwarps) {
-    const long long b = __ldg(m.slice_ptr + sl);
-    const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
-    double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
-    const long long slot = sl * kSlice + lane;
-    const bool valid = slot < m.rows;
-    const long long row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
-    if (m.part_in && valid) {  // earlier column panels first, then this one
-      const double2 pp = ld_once(m.part_in + row, pol);
-      acc = make_double2(pp.x + acc.x, pp.y + acc.y);
-    }
-    epi(row, acc, valid);
+//
+// Static path (SellView::work == nullptr): warp w takes slices w, w + nwarps,
+// ... and loads values and columns through registers (sell_dot).
+//
+// Streamed path (SellView::work): the matrix stream never passes through
+// registers.  Every warp owns a ring of kSellStages shared-memory stages; one
+// lane keeps the ring full with 1-D bulk copies (cp.async.bulk, completion on
+// an mbarrier per stage) of kSellPiece slots at a time — the values and
+// columns of consecutive slices are contiguous, so a chunk of slices is one
+// byte range — while the warp consumes the oldest stage: columns and values
+// from shared memory, the gathers of x from L2.  The bytes in flight per SM
+// (what an HBM-bound kernel needs: bandwidth x latency) are then set by the
+// ring depth instead of by registers and occupancy, and they no longer drain
+// at the end of every slice (the column panels of c4 have ~30 entries per row).
+// Chunks of consecutive slices are drawn from a device counter, so no warp
+// idles while another still holds a long share and the warps of the grid walk
+// the matrix (and the gathered columns of x) front to front; the first chunk
+// of a warp is its own index (no draw), the next chunk's descriptor is loaded
+// and the one after is drawn while the current one is processed.  Every warp
+// makes exactly one draw past the end, so the draw returning the launch's
+// last value zeroes the counter for the next launch.
+// Per row the entries are accumulated in slot order on both paths (identical
+// results).
+#ifndef QSWG_SELL_MIN_BLOCKS
+#define QSWG_SELL_MIN_BLOCKS 2  // two CTAs of 8 rings per SM (<= 128 registers: no spills)
+#endif
+#ifndef QSWG_SELL_PIECE
+#define QSWG_SELL_PIECE 4
+#endif
+constexpr int kSellPiece = QSWG_SELL_PIECE;                            // slots (32 entries each) per bulk copy
+#ifndef QSWG_SELL_STAGES
+#define QSWG_SELL_STAGES 4
+#endif
+constexpr int kSellStages = QSWG_SELL_STAGES;
+#ifndef QSWG_SELL_GROUP
+#define QSWG_SELL_GROUP 2
+#endif
+constexpr int kSellGroup = QSWG_SELL_GROUP;  // pieces consumed per round (their gathers in flight together)
+constexpr int kSellStageVal = kSellPiece * kSlice * 16;  // bytes of values per stage
+constexpr int kSellStageCol = kSellPiece * kSlice * 4;
+constexpr int kSellWarpBytes = kSellStages * (kSellStageVal + kSellStageCol);
+constexpr int kSellWarps = kThreads / 32;
+constexpr std::size_t kSellSmemBytes = static_cast<std::size_t>(kSellWarps) * (kSellWarpBytes + kSellStages * 8);
+constexpr int kSellTargetSlots = 96;  // slots per chunk aimed at
+constexpr int kSellMaxChunk = 31;     // slices per chunk (their slice_ptr entries fit one warp load)
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                          unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ unsigned draw_chunk(unsigned* ctr, int lane) {
+  unsigned v = 0;
+  if (lane == 0) v = atomicAdd(ctr, 1u);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+template <bool kStrict>
+__device__ __forceinline__ void sell_mac(double2& acc, double2 v, double2 xv) {
+  if constexpr (kStrict) {  // CSR order, separately rounded (liouvillian.cpp:120-124)
+    acc.x = __dadd_rn(acc.x, __dsub_rn(__dmul_rn(v.x, xv.x), __dmul_rn(v.y, xv.y)));
+    acc.y = __dadd_rn(acc.y, __dadd_rn(__dmul_rn(v.x, xv.y), __dmul_rn(v.y, xv.x)));
+  } else {
+    acc.x = fma(v.x, xv.x, acc.x);
+    acc.x = fma(-v.y, xv.y, acc.x);
+    acc.y = fma(v.x, xv.y, acc.y);
+    acc.y = fma(v.y, xv.x, acc.y);
   }
+}
+
+// A chunk of consecutive slices as the streamed path sees it.
+struct SellChunk {
+  long long s0 = 0;   // first slice
+  long long e0 = 0;   // first entry
+  int ns = 0;         // slices (0: no chunk)
+  int nslots = 0;     // 32-entry slots
+  int npieces = 0;
+  int issued = 0;     // pieces handed to the copy engine
+};
+
+template <bool kStrict, class Epi>
+__device__ __forceinline__ void slice_stream(const SellView& m, const double2* __restrict__ x, Epi&& epi) {
+  extern __shared__ __align__(128) unsigned char sell_smem[];
+  const unsigned long long pol = evict_first_policy();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* const ring = sell_smem + wib * kSellWarpBytes;
+  const double2* const sval = reinterpret_cast<const double2*>(ring);
+  const int* const scol = reinterpret_cast<const int*>(ring + kSellStages * kSellStageVal);
+  const unsigned ring_a = smem_addr(ring);
+  const unsigned bar_a = smem_addr(sell_smem + kSellWarps * kSellWarpBytes) + wib * kSellStages * 8;
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < kSellStages; ++st) mbar_init(bar_a + 8 * st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+  // Slices per chunk (grid-uniform): ~kSellTargetSlots slots, but at least ~8 chunks per warp.
+  const long long total_slots = __ldg(m.slice_ptr + m.n_slices) / kSlice;
+  long long chunk = total_slots > 0 ? (kSellTargetSlots * m.n_slices) / total_slots : kSellMaxChunk;
+  const long long fair = m.n_slices / (8 * nwarps);
+  if (chunk > fair) chunk = fair;
+  chunk = chunk < 1 ? 1 : (chunk > kSellMaxChunk ? kSellMaxChunk : chunk);
+  const long long n_chunks = (m.n_slices + chunk - 1) / chunk;
+  const unsigned last_draw =
+      static_cast<unsigned>((n_chunks > nwarps ? n_chunks - nwarps : 0) + nwarps - 1);
+
+  // Descriptor of chunk c; sp = this lane's slice_ptr entry (lane k: start of slice k of the chunk).
+  auto describe = [&](long long c, SellChunk& ch, long long& sp) {
+    ch = SellChunk{};
+    if (c >= n_chunks) return;
+    ch.s0 = c * chunk;
+    const long long left = m.n_slices - ch.s0;
+    ch.ns = static_cast<int>(left < chunk ? left : chunk);
+    sp = lane <= ch.ns ? __ldg(m.slice_ptr + ch.s0 + lane) : 0;
+    ch.e0 = __shfl_sync(0xffffffffu, sp, 0);
+    ch.nslots = static_cast<int>((__shfl_sync(0xffffffffu, sp, ch.ns) - ch.e0) / kSlice);
+    ch.npieces = (ch.nslots + kSellPiece - 1) / kSellPiece;
+  };
+  unsigned issued_total = 0, consumed_total = 0;  // running piece counters: stage = n % stages, parity = (n / stages) & 1
+  auto issue_piece = [&](SellChunk& ch) {
+    const int p = ch.issued++;
+    const int st = static_cast<int>(issued_total % kSellStages);
+    ++issued_total;
+    if (lane == 0) {
+      const int slots = ch.nslots - p * kSellPiece < kSellPiece ? ch.nslots - p * kSellPiece : kSellPiece;
+      const long long e = ch.e0 + static_cast<long long>(p) * (kSellPiece * kSlice);
+      const unsigned bar = bar_a + 8 * st;
+      mbar_expect_tx(bar, static_cast<unsigned>(slots) * (kSlice * 20));
+      bulk_load(ring_a + st * kSellStageVal, m.val + e, static_cast<unsigned>(slots) * (kSlice * 16), bar, pol);
+      bulk_load(ring_a + kSellStages * kSellStageVal + st * kSellStageCol, m.col + e,
+                static_cast<unsigned>(slots) * (kSlice * 4), bar, pol);
+    }
+  };
+
+  SellChunk cur, nxt;
+  long long sp_cur = 0, sp_nxt = 0;
+  describe(warp, cur, sp_cur);
+  unsigned raw = draw_chunk(m.work, lane);  // pending draw: the chunk after nxt
+  bool drawing = true;                      // false once a draw went past the end
+  auto take_draw = [&](SellChunk& ch, long long& sp) {  // turns the pending draw into a descriptor, draws again
+    ch = SellChunk{};
+    if (!drawing) return;
+    const long long c = static_cast<long long>(raw) + nwarps;
+    if (c < n_chunks) {
+      describe(c, ch, sp);
+      raw = draw_chunk(m.work, lane);
+    } else {
+      drawing = false;
+      if (lane == 0 && raw == last_draw) *m.work = 0u;
+    }
+  };
+  take_draw(nxt, sp_nxt);
+  auto refill = [&]() {  // fills the free stages while pieces are left
+#pragma unroll 1
+    while (issued_total - consumed_total < static_cast<unsigned>(kSellStages)) {
+      if (cur.issued < cur.npieces) {
+        issue_piece(cur);
+      } else if (nxt.issued < nxt.npieces) {
+        issue_piece(nxt);
+      } else {
+        break;
+      }
+    }
+  };
+  refill();
+
+  while (cur.ns > 0) {
+    // Walk the chunk: g = slot index in the chunk, k = slice in the chunk.
+    int k = 0, g = 0;
+    int slice_end = static_cast<int>((__shfl_sync(0xffffffffu, sp_cur, 1) - cur.e0) / kSlice);
+    long long slot = cur.s0 * kSlice + lane;
+    bool valid = slot < m.rows;
+    long long row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
+    double2 pp = m.part_in && valid ? ld_once(m.part_in + row, pol) : make_double2(0.0, 0.0);
+    double2 acc = make_double2(0.0, 0.0);
+    auto next_slice = [&]() {  // finishes slice k, starts slice k + 1
+      if (m.part_in) acc = make_double2(pp.x + acc.x, pp.y + acc.y);  // earlier column panels first, then this one
+      epi(row, acc, valid);
+      ++k;
+      acc = make_double2(0.0, 0.0);
+      if (k < cur.ns) {
+        slice_end = static_cast<int>((__shfl_sync(0xffffffffu, sp_cur, k + 1) - cur.e0) / kSlice);
+        slot = (cur.s0 + k) * kSlice + lane;
+        valid = slot < m.rows;
+        row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
+        pp = m.part_in && valid ? ld_once(m.part_in + row, pol) : make_double2(0.0, 0.0);
+      }
+    };
+    // kSellGroup pieces per round: their gathers are all in flight together.
+#pragma unroll 1
+    for (int p = 0; p < cur.npieces; p += kSellGroup) {
+      double2 v[kSellGroup][kSellPiece], xv[kSellGroup][kSellPiece];
+      const int left = cur.nslots - p * kSellPiece;  // slots of this round: min(left, group * piece)
+#pragma unroll
+      for (int q = 0; q < kSellGroup; ++q) {
+        if (q * kSellPiece < left) {
+          const unsigned n = consumed_total + q;
+          const int st = static_cast<int>(n % kSellStages);
+          mbar_wait(bar_a + 8 * st, (n / kSellStages) & 1u);
+          const int* pc = scol + st * (kSellPiece * kSlice) + lane;
+#pragma unroll
+          for (int u = 0; u < kSellPiece; ++u)
+            if (q * kSellPiece + u < left) xv[q][u] = ld_gather(x + pc[u * kSlice], 0ull);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kSellGroup; ++q) {
+        if (q * kSellPiece < left) {
+          const int st = static_cast<int>((consumed_total + q) % kSellStages);
+          const double2* pv = sval + st * (kSellPiece * kSlice) + lane;
+#pragma unroll
+          for (int u = 0; u < kSellPiece; ++u)
+            if (q * kSellPiece + u < left) v[q][u] = pv[u * kSlice];
+        }
+      }
+      __syncwarp();  // every lane has read the stages: they can be refilled
+      consumed_total += left > (kSellGroup - 1) * kSellPiece ? kSellGroup : (left + kSellPiece - 1) / kSellPiece;
+      refill();
+#pragma unroll
+      for (int q = 0; q < kSellGroup; ++q) {
+#pragma unroll
+        for (int u = 0; u < kSellPiece; ++u) {
+          if (q * kSellPiece + u < left) {
+            while (g == slice_end) next_slice();
+            sell_mac<kStrict>(acc, v[q][u], xv[q][u]);
+            ++g;
+          }
+        }
+      }
+    }
+    while (k < cur.ns) next_slice();  // the last slice and any empty ones after it
+    cur = nxt;
+    sp_cur = sp_nxt;
+    take_draw(nxt, sp_nxt);
+    refill();
+  }
+}
+
+template <bool kStrict, class Epi>
+__device__ __forceinline__ void slice_body(const SellView& m, const double2* __restrict__ x, long long sl, int lane,
+                                           unsigned long long pol, unsigned long long xpol, Epi&& epi) {
+  const long long b = __ldg(m.slice_ptr + sl);
+  const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
+  double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
+  const long long slot = sl * kSlice + lane;
+  const bool valid = slot < m.rows;
+  const long long row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
+  if (m.part_in && valid) {  // earlier column panels first, then this one
+    const double2 pp = ld_once(m.part_in + row, pol);
+    acc = make_double2(pp.x + acc.x, pp.y + acc.y);
+  }
+  epi(row, acc, valid);
+}
+
+// kStream: the kernel instance that streams the matrix through shared memory
+// (SellView::work set) — the SELL kernels are instantiated for both paths,
+// each with the register budget it was measured best at.
+template <bool kStrict, bool kStream, class Epi>
+__device__ __forceinline__ void slice_loop(const SellView& m, const double2* __restrict__ x, Epi&& epi) {
+  if constexpr (kStream) {
+    slice_stream<kStrict>(m, x, epi);
+  } else {
+    const unsigned long long pol = evict_first_policy(), xpol = evict_last_policy();
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    for (long long sl = warp; sl < m.n_slices; sl += nwarps) slice_body<kStrict>(m, x, sl, lane, pol, xpol, epi);
+  }
+}
+// Resident blocks per SM asked of ptxas: the streamed path holds its rings in
+// shared memory (2 blocks of 8 rings, <= 128 registers); the register path
+// hides the latency of its scattered gathers with warps (3 blocks, <= 85
+// registers: c3 0.79 -> 0.82 of HBM, c4 0.70 -> 0.74; 4 blocks: 0.78 / 0.72).
+#ifndef QSWG_SELL_REG_MIN_BLOCKS
+#define QSWG_SELL_REG_MIN_BLOCKS 3
+#endif
+template <bool kStream>
+constexpr int sell_min_blocks() {
+  return kStream ? QSWG_SELL_MIN_BLOCKS : QSWG_SELL_REG_MIN_BLOCKS;
 }
 
 // Skip test of the partial-panel kernels: the same early exits as the term
@@ -770,13 +1055,13 @@ __device__ __forceinline__ bool skip_now(const SkipCheck& k) {
 }
 
 // One earlier column panel: part[row] (=|+=) its row sums.
-template <bool kFirst>
-__global__ void __launch_bounds__(kThreads) sell_partial_kernel(SellView m, const double2* x, double2* part,
-                                                                SkipCheck sk) {
+template <bool kFirst, bool kStream>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
+    sell_partial_kernel(SellView m, const double2* x, double2* part, SkipCheck sk) {
   pdl_prologue();
   if (skip_now(sk)) return;
   const unsigned long long once = evict_first_policy();
-  slice_loop<false>(m, x, [&](long long row, double2 acc, bool valid) {
+  slice_loop<false, kStream>(m, x, [&](long long row, double2 acc, bool valid) {
     if (!valid) return;
     if constexpr (!kFirst) {
       const double2 pp = ld_once(part + row, once);
@@ -787,10 +1072,11 @@ __global__ void __launch_bounds__(kThreads) sell_partial_kernel(SellView m, cons
   pdl_trigger();
 }
 
-template <bool kStrict>
-__global__ void __launch_bounds__(kThreads) sell_spmv_kernel(SellView m, const double2* x, double2* y, double scale) {
+template <bool kStrict, bool kStream>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
+    sell_spmv_kernel(SellView m, const double2* x, double2* y, double scale) {
   pdl_prologue();
-  slice_loop<kStrict>(m, x, [&](long long row, double2 acc, bool valid) {
+  slice_loop<kStrict, kStream>(m, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
@@ -809,8 +1095,8 @@ struct SellStepArgs {
   int decide;
 };
 
-template <bool kStrict>
-__global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a) {
+template <bool kStrict, bool kStream>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>()) sell_step_term_kernel(SellStepArgs a) {
   pdl_prologue();
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
@@ -818,7 +1104,7 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0, smax = 0;
   const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  slice_loop<kStrict>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+  slice_loop<kStrict, kStream>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
     if (!valid) return;
     const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
     const double2 sv0 = ld_once(a.sum_in + row, once);
@@ -846,8 +1132,9 @@ __global__ void __launch_bounds__(kThreads) sell_step_term_kernel(SellStepArgs a
   }
 }
 
-template <bool kStrict>
-__global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermArgs a, SellView m) {
+template <bool kStrict, bool kStream>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
+    sell_series_term_kernel(SeriesTermArgs a, SellView m) {
   pdl_prologue();
   if (series_skip(a.ctl)) return;
   __shared__ unsigned long long red[32];
@@ -855,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads) sell_series_term_kernel(SeriesTermAr
   const unsigned long long keep = evict_last_policy();
   double2* const kp = a.kp;
   const double scale = a.scale;
-  slice_loop<kStrict>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  slice_loop<kStrict, kStream>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
   series_term_finish(a, tmax, red);
 }
 
@@ -1968,13 +2255,33 @@ int persistent_grid(K kernel, long long rows) {
   return static_cast<int>(want < cap ? want : cap);
 }
 
-template <class K>
-int sell_grid(K kernel, const SellView& m) {
-  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kernel));
+// Launch of a SELL kernel: persistent grid; the streamed path (SellView::work)
+// carries its rings in dynamic shared memory.
+template <class... KArgs, class... Args>
+void launch_sell(void (*kernel)(KArgs...), const SellView& m, cudaStream_t s, Args... args) {
+  const std::size_t smem = m.work ? kSellSmemBytes : 0;
+  const void* fn = reinterpret_cast<const void*>(kernel);
+  if (smem) {  // > 48 KB: opt in once per device and kernel
+    struct Key {
+      int dev;
+      const void* k;
+    };
+    static thread_local Key done[32];
+    static thread_local int used = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    bool seen = false;
+    for (int i = 0; i < used; ++i) seen = seen || (done[i].dev == dev && done[i].k == fn);
+    if (!seen) {
+      QSWG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      if (used < 32) done[used++] = {dev, fn};
+    }
+  }
+  const int per_sm = blocks_per_sm(fn, smem);
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
   long long want = (m.n_slices + kThreads / 32 - 1) / (kThreads / 32);
   if (want < 1) want = 1;
-  return static_cast<int>(want < cap ? want : cap);
+  launch_pdl(kernel, static_cast<int>(want < cap ? want : cap), kThreads, smem, s, args...);
 }
 
 // Persistent launch geometry of a Kron kernel (no dynamic shared memory).
@@ -2060,11 +2367,17 @@ void series_flush_control(SeriesCtl* ctl, int p, double tol, cudaStream_t s) {
 void sell_partials(const DevMatrix& m, const double2* x, const SkipCheck& sk, cudaStream_t s) {
   for (int q = m.pre_done; q < m.n_pre; ++q) {
     if (q == 0) {
-      launch_pdl(sell_partial_kernel<true>, sell_grid(sell_partial_kernel<true>, m.sell_pre[q]), kThreads, 0, s,
-                 m.sell_pre[q], x, m.part, sk);
+      if (m.sell_pre[q].work) {
+        launch_sell(sell_partial_kernel<true, true>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+      } else {
+        launch_sell(sell_partial_kernel<true, false>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+      }
     } else {
-      launch_pdl(sell_partial_kernel<false>, sell_grid(sell_partial_kernel<false>, m.sell_pre[q]), kThreads, 0, s,
-                 m.sell_pre[q], x, m.part, sk);
+      if (m.sell_pre[q].work) {
+        launch_sell(sell_partial_kernel<false, true>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+      } else {
+        launch_sell(sell_partial_kernel<false, false>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+      }
     }
     QSWG_LAUNCH_CHECK("sell_partials");
   }
@@ -2104,9 +2417,17 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
     sell_partials(m, x, SkipCheck{nullptr, ctl, first_of_stage ? 1 : 0}, s);
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
-      launch_pdl(sell_step_term_kernel<true>, sell_grid(sell_step_term_kernel<true>, m.sell), kThreads, 0, s, a);
+      if (m.sell.work) {
+        launch_sell(sell_step_term_kernel<true, true>, m.sell, s, a);
+      } else {
+        launch_sell(sell_step_term_kernel<true, false>, m.sell, s, a);
+      }
     } else {
-      launch_pdl(sell_step_term_kernel<false>, sell_grid(sell_step_term_kernel<false>, m.sell), kThreads, 0, s, a);
+      if (m.sell.work) {
+        launch_sell(sell_step_term_kernel<false, true>, m.sell, s, a);
+      } else {
+        launch_sell(sell_step_term_kernel<false, false>, m.sell, s, a);
+      }
     }
   } else {
     StepTermArgs a{m.csr, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
@@ -2146,9 +2467,17 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
   } else if (m.format == Format::Sell) {
     sell_partials(m, x, SkipCheck{ctl, nullptr, 1}, s);
     if (m.group == 1) {
-      launch_pdl(sell_series_term_kernel<true>, sell_grid(sell_series_term_kernel<true>, m.sell), kThreads, 0, s, a, m.sell);
+      if (m.sell.work) {
+        launch_sell(sell_series_term_kernel<true, true>, m.sell, s, a, m.sell);
+      } else {
+        launch_sell(sell_series_term_kernel<true, false>, m.sell, s, a, m.sell);
+      }
     } else {
-      launch_pdl(sell_series_term_kernel<false>, sell_grid(sell_series_term_kernel<false>, m.sell), kThreads, 0, s, a, m.sell);
+      if (m.sell.work) {
+        launch_sell(sell_series_term_kernel<false, true>, m.sell, s, a, m.sell);
+      } else {
+        launch_sell(sell_series_term_kernel<false, false>, m.sell, s, a, m.sell);
+      }
     }
   } else {
     dispatch_group<SeriesTermK>(m.group, m.csr.rows, s, a, m.csr);
@@ -2252,9 +2581,17 @@ void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaSt
   } else if (m.format == Format::Sell) {
     sell_partials(m, x, SkipCheck{}, s);
     if (m.group == 1) {
-      launch_pdl(sell_spmv_kernel<true>, sell_grid(sell_spmv_kernel<true>, m.sell), kThreads, 0, s, m.sell, x, y, scale);
+      if (m.sell.work) {
+        launch_sell(sell_spmv_kernel<true, true>, m.sell, s, m.sell, x, y, scale);
+      } else {
+        launch_sell(sell_spmv_kernel<true, false>, m.sell, s, m.sell, x, y, scale);
+      }
     } else {
-      launch_pdl(sell_spmv_kernel<false>, sell_grid(sell_spmv_kernel<false>, m.sell), kThreads, 0, s, m.sell, x, y, scale);
+      if (m.sell.work) {
+        launch_sell(sell_spmv_kernel<false, true>, m.sell, s, m.sell, x, y, scale);
+      } else {
+        launch_sell(sell_spmv_kernel<false, false>, m.sell, s, m.sell, x, y, scale);
+      }
     }
   } else {
     dispatch_group<SpmvK>(m.group, m.csr.rows, s, m.csr, x, y, scale);

@@ -41,6 +41,18 @@ int sell_sigma_setting() {
   }();
   return v;
 }
+// Streamed SELL kernels (taylor.cu: slice_stream).  QSWG_SELL_STREAM: 0 = the
+// register path everywhere, 1 = streamed everywhere; default: streamed for
+// unsorted (regular) superoperators, whose gathers are coalesced, and the
+// register path (more resident warps) for sigma-sorted (irregular) ones, whose
+// scattered gathers need the latency hiding (measured).
+int sell_stream_setting() {
+  static const int v = [] {
+    const char* e = std::getenv("QSWG_SELL_STREAM");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
 constexpr double kSellMaxPadding = 1.3;  // SELL if stored/nnz <= this (else CSR)
 // Column panels of a SELL superoperator: when the gathered vector (the
 // full-length x, also on every rank of a row-partitioned run) is larger than
@@ -733,6 +745,7 @@ void Liouvillian::adopt(Liouvillian& o) {
   std::swap(sigma_, o.sigma_);
   std::swap(pre_, o.pre_);
   std::swap(part_, o.part_);
+  std::swap(sell_work_, o.sell_work_);
   std::swap(main_c_lo_, o.main_c_lo_);
   std::swap(local_first_, o.local_first_);
   std::swap(rowptr_, o.rowptr_);
@@ -834,11 +847,16 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
   m.sell.row0 = block_.row0;
   m.sell.n_slices = n_slices_;
   m.sell.perm = perm_.size() ? perm_.get() : nullptr;
+  const int stream = sell_stream_setting();
+  const bool sorted = perm_.size() > 0 || (!pre_.empty() && pre_[0].perm.size() > 0);
+  if (format_ == dev::Format::Sell && sell_work_.size() && m.group != 1 && stream != 0 && (stream == 1 || !sorted))
+    m.sell.work = sell_work_.get() + pre_.size();
   if (!pre_.empty()) {  // column panels
     m.n_pre = static_cast<int>(pre_.size());
     for (std::size_t q = 0; q < pre_.size(); ++q) {
       dev::SellView& v = m.sell_pre[q];
       v = m.sell;
+      if (m.sell.work) v.work = sell_work_.get() + q;
       v.slice_ptr = pre_[q].slice_ptr.get();
       v.col = pre_[q].col.get();
       v.val = pre_[q].val.get();
@@ -1489,11 +1507,16 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       }
     }
     l->part_.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)));
+    l->sell_work_.resize(dev::kMaxSellPanels);  // scheduling counters of the streamed kernels, one per panel
+    QSWG_CHECK(cudaMemsetAsync(l->sell_work_.get(), 0, l->sell_work_.bytes(), s));
+    QSWG_CHECK(cudaStreamSynchronize(s));
     l->padding_ = static_cast<double>(stored) / static_cast<double>(l->nnz_local_);
     sell_entries = main_entries;  // the halo hull below walks the earlier panels separately
   } else if (use_sell) {
     l->format_ = dev::Format::Sell;
     l->padding_ = pad;
+    l->sell_work_.resize(dev::kMaxSellPanels);
+    QSWG_CHECK(cudaMemsetAsync(l->sell_work_.get(), 0, l->sell_work_.bytes(), s));
     l->col_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));
     l->val_.resize(static_cast<std::size_t>(std::max<std::int64_t>(sell_entries, 1)));
     dev::assemble_fill_sell(ops.get(), l->block_.row0, l->block_.rows, l->slice_ptr_.get(),

@@ -163,6 +163,7 @@ class Liouvillian {
   int sigma_ = dev::kSlice;
   std::vector<SellPanel> pre_;            // SELL column panels before the main arrays (one GPU)
   DeviceBuffer<double2> part_;            // their row sums
+  DeviceBuffer<unsigned> sell_work_;          // one scheduling counter per panel (dev::SellView::work)
   std::int64_t main_c_lo_ = 0;            // column range of the main SELL arrays
   int local_first_ = 0;                   // leading panels = this rank's own columns (overlap the halo exchange)
   mutable cudaStream_t side_ = nullptr;   // halo exchanges overlapped with the local panel

@@ -70,6 +70,10 @@ struct SellView {
   // Column panels: the row sums of the earlier panels, added to this
   // panel's sum (nullptr: a single panel).
   const double2* part_in = nullptr;
+  // Dynamic slice scheduling: a device counter the warps of one launch draw
+  // chunks of consecutive slices from (the launch's last draw zeroes it again);
+  // nullptr = the static grid-stride assignment.
+  unsigned* work = nullptr;
   std::int64_t rows = 0;
   std::int64_t row0 = 0;
   std::int64_t n_slices = 0;
