@@ -92,7 +92,8 @@ class LiouvillianInfo(C.Structure):
                 ("omega", C.c_double), ("one_norms", C.c_double * 9),
                 ("group", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("format", C.c_int), ("padding", C.c_double), ("kron_factored", C.c_int), ("kron_ell", C.c_int),
-                ("kron_term_vectors", C.c_int), ("sell_panels", C.c_int), ("kron_hermitian", C.c_int)]
+                ("kron_term_vectors", C.c_int), ("sell_panels", C.c_int), ("kron_hermitian", C.c_int),
+                ("kron_staged", C.c_int)]
 
 
 class StepInfo(C.Structure):

@@ -1381,6 +1381,21 @@ __device__ __forceinline__ void shfl_rows(const KronEll& e, double2 cv, int len,
   }
 }
 
+// shfl_rows with the slice's entry offset and this lane's column index
+// already in registers (the staged path loads them a tile ahead).
+template <int K, bool C, class G>
+__device__ __forceinline__ void shfl_rows_pre(const double2* val, double2 cv, int len, int base, int mycol, int l0,
+                                              double2* acc, G&& g) {
+  const KronEll e{nullptr, nullptr, val};
+  if (len == 4) {
+    shfl_rows_len<K, C, 4>(e, cv, len, base, mycol, l0, acc, g);
+  } else if (len == 6) {
+    shfl_rows_len<K, C, 6>(e, cv, len, base, mycol, l0, acc, g);
+  } else {
+    shfl_rows_len<K, C, 0>(e, cv, len, base, mycol, l0, acc, g);
+  }
+}
+
 // W_0 = Q_0 X and AX = A X from the same gathers (KronView::ax): acc from
 // Q's values, aacc from A's values aligned to Q's entries; the same per-row
 // entry order as shfl_rows / uniform_rows, so each sum is the one its own
@@ -1532,6 +1547,10 @@ __device__ __forceinline__ void kron_rows_uniform(const KronView& m, const doubl
 // Column-indexed part and diagonal terms at (i, j[r]), lane = row i.
 // kHerm: V_k = X L_k' = W_k' for Hermitian X, so V_k(i, a) = conj Wt_k[n a + i]
 // and no V_k is built.  (B, P_k, S_k lists and the S_k uniform ELL hold c * n.)
+template <class XL>
+__device__ __forceinline__ void kron_tail(const KronView& m, const double2* __restrict__ x, int i, const int* j,
+                                          double2* acc, unsigned long long xpol, XL&& xl);
+
 template <bool kHerm, int kF>
 __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __restrict__ x, int i, const int* j,
                                           double2* acc, unsigned long long xpol) {
@@ -1592,6 +1611,15 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
   const double2* xij[kKR];
 #pragma unroll
   for (int r = 0; r < kKR; ++r) xij[r] = x + (static_cast<unsigned>(j[r]) * n + static_cast<unsigned>(i));
+  kron_tail(m, x, i, j, acc, xpol, [&](int r) { return ld_gather(xij[r], xpol); });
+}
+
+// The diagonal terms at (i, j[r]), lane = row i, after the operand parts:
+// (A_ii + B_jj), T, decay.  xl(r) = X(i, j[r]) (a gather, or the staged tile).
+template <class XL>
+__device__ __forceinline__ void kron_tail(const KronView& m, const double2* __restrict__ x, int i, const int* j,
+                                          double2* acc, unsigned long long xpol, XL&& xl) {
+  const unsigned n = static_cast<unsigned>(m.n);
   if (m.da) {  // the diagonals of A and B: (A_ii + B_jj) X(i, j), one gather
     const double2 dai = __ldg(m.da + i);
     by_kind(m.vk_d & 3, [&](auto kc, auto) {
@@ -1600,7 +1628,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
       for (int r = 0; r < kKR; ++r) {
         const double2 dbj = __ldg(m.db + j[r]);
         const double2 c = make_double2(dai.x + dbj.x, dai.y + dbj.y);
-        if (c.x != 0.0 || c.y != 0.0) cfmak<K>(acc[r], c, ld_gather(xij[r], xpol));
+        if (c.x != 0.0 || c.y != 0.0) cfmak<K>(acc[r], c, xl(r));
       }
     });
   }
@@ -1621,7 +1649,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
     if (m.d_val != 0.0) {
 #pragma unroll
       for (int r = 0; r < kKR; ++r) {
-        const double2 xg = ld_gather(xij[r], xpol);
+        const double2 xg = xl(r);
         acc[r].x = fma(-m.d_val, xg.x, acc[r].x);
         acc[r].y = fma(-m.d_val, xg.y, acc[r].y);
       }
@@ -1634,7 +1662,7 @@ __device__ __forceinline__ void kron_cols(const KronView& m, const double2* __re
           0.5, __dadd_rn(__dadd_rn(__dmul_rn(m.omega, __dadd_rn(dli, __ldg(m.d_loc + j[r]))), dsi),
                          __ldg(m.d_ss + j[r])));
       if (d != 0.0) {
-        const double2 xg = ld_gather(xij[r], xpol);
+        const double2 xg = xl(r);
         acc[r].x = fma(-d, xg.x, acc[r].x);
         acc[r].y = fma(-d, xg.y, acc[r].y);
       }
@@ -1758,6 +1786,207 @@ __device__ __forceinline__ void kron_tiles(const KronView& m, const double2* __r
     kron_cols<kHerm, kF>(m, x, i, jg, acc, xpol);
     kron_tile_emit<kHerm>(g, I, J, acc, tile, epi);
   }
+}
+
+// ---- staged Hermitian tiles (KronView::staged) -------------------------------
+// 16-byte asynchronous copies global -> shared (LDGSTS; a warp moves one
+// 512-byte tile row per instruction).  512-byte cp.async.bulk copies were
+// measured first: the per-copy cost of the bulk engine (288 copies per tile)
+// made the c2 term 41.5 us against 23.7 us for the global gathers.
+__device__ __forceinline__ void cp_async16(double2* dst_smem, const double2* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+constexpr int kStageTile = kKT * kKT;  // elements of one staged tile (16 KB)
+
+// The upper tiles (I, J) of one block, each computed from shared memory.
+// Phase A of a tile: the tiles of F named by patterns 0 and 1 and (factored)
+// AXt(I, J); phase B: pattern 2, AXt(J, I) and the tile's own elements of x.
+// They are copied a tile ahead, as soon as their regions are free again —
+// phase A of the next tile once the transposed section of this one is done,
+// phase B after its emit — so the copies of tile t + 1 run under the second
+// half and the stores of tile t; the operand column indices of the next tile
+// are loaded into registers at the same distance.  With one block per SM (the
+// regions take 176 - 192 KB) nothing else hides a global-memory round trip,
+// so the arithmetic of a tile touches shared memory and registers only
+// (constant operand values; others are loaded).  Every thread commits one
+// copy group per phase in the order A, B, A, B, ...; "at most one group
+// pending" therefore means the older phase has landed.  The per-element order
+// of the sums is kron_tiles'.
+template <int kF, class Epi>
+__device__ __forceinline__ void kron_tiles_staged(const KronView& m, const double2* __restrict__ x, Epi&& epi) {
+  extern __shared__ __align__(128) unsigned char st_smem[];
+  __shared__ double2 tile[kKT][kKT + 1];
+  const unsigned long long xpol = evict_last_policy();
+  const TileGrid g = tile_grid(m, true);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, l0 = w * kKR;
+  const unsigned n = static_cast<unsigned>(m.n);
+  const double2* const F = kF == 1 ? m.wt[0] : x;
+  double2* const reg0 = reinterpret_cast<double2*>(st_smem);
+  double2* const reg1 = reg0 + m.st_slots[0] * kStageTile;
+  double2* const reg2 = reg1 + m.st_slots[1] * kStageTile;
+  double2* const d2 = reg2 + m.st_slots[2] * kStageTile;  // x(I-rows of columns J): [j][i]
+  double2* const d0 = d2 + kStageTile;                    // factored: AXt(I, J): [i][j]
+  double2* const d1 = d0 + kStageTile;                    // factored: AXt(J, I): [j][i]
+  const int len0 = m.st_len[0], len1 = m.st_len[1], len2 = m.st_len[2];
+  // The tile indices come in registers (loaded a phase earlier): a load
+  // between two copies would wait behind the copies' data in the load/store
+  // pipe and serialise them.
+  struct Next {
+    int t[3][kStageSlots];
+    int mycol0, mycol2, pcol[8];
+  };
+  const int kt = lane >> 2, rt = lane & 3;
+  const auto load_next = [&](int I, int J, Next& nx) {
+#pragma unroll
+    for (int q = 0; q < kStageSlots; ++q) {
+      nx.t[0][q] = q < m.st_slots[0] ? __ldg(m.st_nbr[0] + I * kStageSlots + q) : -1;
+      nx.t[1][q] = q < m.st_slots[1] ? __ldg(m.st_nbr[1] + J * kStageSlots + q) : -1;
+      nx.t[2][q] = q < m.st_slots[2] ? __ldg(m.st_nbr[2] + J * kStageSlots + q) : -1;
+    }
+    // (uniform ELL of constant row length: slice s starts at 32 s len)
+    nx.mycol0 = kt < len0 ? __ldg(m.st_col[0] + I * kKT * len0 + 32 * kt + l0 + rt) : 0;
+    nx.mycol2 = kt < len2 ? __ldg(m.st_col[2] + J * kKT * len2 + 32 * kt + l0 + rt) : 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) nx.pcol[e] = e < len1 ? __ldg(m.st_col[1] + J * kKT * len1 + 32 * e + lane) : 0;
+  };
+  // warp w copies rows w, w + 8, ... of every tile
+  const auto copy_tile = [&](double2* dst, const double2* src00) {  // src00: element (0, 0) of the 32 x 32 source tile
+#pragma unroll
+    for (int r = 0; r < kKT; r += kThreads / 32) {
+      const int row = r + w;
+      cp_async16(dst + row * kKT + lane, src00 + (static_cast<unsigned>(row) * n + static_cast<unsigned>(lane)));
+    }
+  };
+  const auto copy_a = [&](int I, int J, const Next& nx) {
+#pragma unroll
+    for (int q = 0; q < kStageSlots; ++q) {
+      if (nx.t[0][q] >= 0) copy_tile(reg0 + q * kStageTile, F + (static_cast<unsigned>(nx.t[0][q] * kKT) * n + static_cast<unsigned>(J * kKT)));
+    }
+#pragma unroll
+    for (int q = 0; q < kStageSlots; ++q) {
+      if (nx.t[1][q] >= 0) copy_tile(reg1 + q * kStageTile, F + (static_cast<unsigned>(I * kKT) * n + static_cast<unsigned>(nx.t[1][q] * kKT)));
+    }
+    if constexpr (kF == 1) copy_tile(d0, m.axt + (static_cast<unsigned>(I * kKT) * n + static_cast<unsigned>(J * kKT)));
+  };
+  const auto copy_b = [&](int I, int J, const Next& nx) {
+#pragma unroll
+    for (int q = 0; q < kStageSlots; ++q) {
+      if (nx.t[2][q] >= 0) copy_tile(reg2 + q * kStageTile, F + (static_cast<unsigned>(nx.t[2][q] * kKT) * n + static_cast<unsigned>(I * kKT)));
+    }
+    if constexpr (kF == 1) copy_tile(d1, m.axt + (static_cast<unsigned>(J * kKT) * n + static_cast<unsigned>(I * kKT)));
+    copy_tile(d2, x + (static_cast<unsigned>(J * kKT) * n + static_cast<unsigned>(I * kKT)));
+  };
+  long long t = blockIdx.x;
+  int I = 0, J = 0;
+  Next cur;
+  if (t < g.ntiles) {
+    tile_coords(m, g, true, t, I, J);
+    load_next(I, J, cur);
+    copy_a(I, J, cur);
+    cp_async_commit();
+    copy_b(I, J, cur);
+    cp_async_commit();
+  }
+  for (; t < g.ntiles; t += gridDim.x) {
+    const long long tn = t + gridDim.x;
+    const bool more = tn < g.ntiles;
+    int In = 0, Jn = 0;
+    Next nx;
+    if (more) {
+      tile_coords(m, g, true, tn, In, Jn);
+      load_next(In, Jn, nx);
+    }
+    const int i = I * kKT + lane;  // n % 32 == 0: no edge tiles
+    int jg[kKR];
+    double2 acc[kKR];
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) jg[r] = J * kKT + l0 + r;
+    cp_async_wait<1>();
+    __syncthreads();  // phase A of this tile is in shared memory
+    // ---- transposed section: warp-uniform rows i = I*32 + l0 + r, lane = column j
+    if constexpr (kF == 1) {
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) acc[r] = d0[(l0 + r) * kKT + lane];  // A's part = AX(i, j)
+      by_kind(m.vk_r[0], [&](auto kc, auto cc) {  // R_0: rows b of Wt_0
+        QSWG_KC(kc, cc);
+        const double2* r0 = reg0 + lane;
+        shfl_rows_pre<K, C>(m.r_ellu[0].val, m.cv_r[0], len0, I * kKT * len0, cur.mycol0, l0, acc,
+                            [&](unsigned o) { return r0[o]; });
+      });
+      by_kind(m.vk_p[0], [&](auto kc, auto cc) {  // P_0(j, a) Wt_0(i, a)
+        QSWG_KC(kc, cc);
+        const double2* r1 = reg1 + l0 * kKT;
+        const double2* pv = m.p_ell[0].val + J * kKT * len1 + lane;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e < len1) {
+            const double2 v = opv<K, C>(pv + 32 * e, m.cv_p[0]);
+#pragma unroll
+            for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, r1[cur.pcol[e] + r * kKT]);
+          }
+        }
+      });
+    } else {
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) acc[r] = make_double2(0.0, 0.0);
+      by_kind(m.vk_a, [&](auto kc, auto cc) {  // A(i, c) conj x[n c + j]
+        QSWG_KC(kc, cc);
+        const double2* r0 = reg0 + lane;
+        shfl_rows_pre<K, C>(m.a_ellu.val, m.cv_a, len0, I * kKT * len0, cur.mycol0, l0, acc,
+                            [&](unsigned o) { return conj2(r0[o]); });
+      });
+      by_kind(m.vk_b, [&](auto kc, auto cc) {  // B(j, c) conj x[n i + c]
+        QSWG_KC(kc, cc);
+        const double2* r1 = reg1 + l0 * kKT;
+        const double2* bv = m.b_ell.val + J * kKT * len1 + lane;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e < len1) {
+            const double2 v = opv<K, C>(bv + 32 * e, m.cv_b);
+#pragma unroll
+            for (int r = 0; r < kKR; ++r) cfmak<K>(acc[r], v, conj2(r1[cur.pcol[e] + r * kKT]));
+          }
+        }
+      });
+    }
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) tile[l0 + r][lane] = acc[r];
+    __syncthreads();  // the transposed sums are in `tile`; the phase-A regions are free
+    if (more) copy_a(In, Jn, nx);
+    cp_async_commit();
+#pragma unroll
+    for (int r = 0; r < kKR; ++r) acc[r] = tile[lane][l0 + r];
+    cp_async_wait<1>();
+    __syncthreads();  // phase B of this tile is in shared memory (and `tile` is free)
+    // ---- normal orientation: lane = row i, columns j = J*32 + l0 + r
+    if constexpr (kF == 1) {
+#pragma unroll
+      for (int r = 0; r < kKR; ++r) {  // B's part = conj AX(j, i), added as one sum
+        const double2 bb = d1[(l0 + r) * kKT + lane];
+        acc[r].x += bb.x;
+        acc[r].y -= bb.y;
+      }
+      by_kind(m.vk_s[0], [&](auto kc, auto cc) {  // S_0: rows a of Wt_0, conjugated
+        QSWG_KC(kc, cc);
+        const double2* r2 = reg2 + lane;
+        shfl_rows_pre<K, C>(m.s_ellu[0].val, m.cv_s[0], len2, J * kKT * len2, cur.mycol2, l0, acc,
+                            [&](unsigned o) { return conj2(r2[o]); });
+      });
+    }
+    kron_tail(m, x, i, jg, acc, xpol, [&](int r) { return d2[(l0 + r) * kKT + lane]; });
+    kron_tile_emit<true>(g, I, J, acc, tile, epi);  // (ends with a barrier: the phase-B regions are free)
+    if (more) copy_b(In, Jn, nx);
+    cp_async_commit();
+    I = In;
+    J = Jn;
+    cur = nx;
+  }
+  cp_async_wait<0>();
 }
 
 // W_k = Q_k X on the local columns (W_k(i, a) at w[n*a + i], global index)
@@ -2017,6 +2246,23 @@ __global__ void __launch_bounds__(kThreads, QSWG_KRON_MIN_BLOCKS) kron_series_te
   series_term_finish(a, tmax, red);
 }
 
+// The Hermitian series term on the staged tiles (one block per SM).
+template <int kF>
+__global__ void __launch_bounds__(kThreads, 1) kron_series_term_staged_kernel(SeriesTermArgs a, KronView m) {
+  pdl_prologue();
+  if (series_skip(a.ctl)) return;
+  __shared__ unsigned long long red[32];
+  unsigned long long tmax = 0;
+  const unsigned long long keep = evict_last_policy();
+  double2* const kp = a.kp;
+  const double scale = a.scale;
+  kron_tiles_staged<kF>(m, a.x, [&](unsigned row, double2 acc, bool valid, bool mirror) {
+    series_store(kp, scale, row, acc, valid && !mirror, keep, tmax);
+    if (valid && mirror) st_hint(kp + row, make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y)), keep);
+  });
+  series_term_finish(a, tmax, red);
+}
+
 // ------------------------------------------------------------ norm kernels
 // Grid-wide max |v| into *bits, last block runs `fin`.
 template <class Fin>
@@ -2255,28 +2501,30 @@ int persistent_grid(K kernel, long long rows) {
   return static_cast<int>(want < cap ? want : cap);
 }
 
+// Dynamic shared memory beyond 48 KB: opt in once per device, kernel and size.
+void allow_smem(const void* fn, std::size_t smem) {
+  struct Key {
+    int dev;
+    const void* k;
+    std::size_t bytes;
+  };
+  static thread_local Key done[64];
+  static thread_local int used = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < used; ++i)
+    if (done[i].dev == dev && done[i].k == fn && done[i].bytes >= smem) return;
+  QSWG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (used < 64) done[used++] = {dev, fn, smem};
+}
+
 // Launch of a SELL kernel: persistent grid; the streamed path (SellView::work)
 // carries its rings in dynamic shared memory.
 template <class... KArgs, class... Args>
 void launch_sell(void (*kernel)(KArgs...), const SellView& m, cudaStream_t s, Args... args) {
   const std::size_t smem = m.work ? kSellSmemBytes : 0;
   const void* fn = reinterpret_cast<const void*>(kernel);
-  if (smem) {  // > 48 KB: opt in once per device and kernel
-    struct Key {
-      int dev;
-      const void* k;
-    };
-    static thread_local Key done[32];
-    static thread_local int used = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    bool seen = false;
-    for (int i = 0; i < used; ++i) seen = seen || (done[i].dev == dev && done[i].k == fn);
-    if (!seen) {
-      QSWG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      if (used < 32) done[used++] = {dev, fn};
-    }
-  }
+  if (smem) allow_smem(fn, smem);
   const int per_sm = blocks_per_sm(fn, smem);
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
   long long want = (m.n_slices + kThreads / 32 - 1) / (kThreads / 32);
@@ -2447,7 +2695,23 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
                  double tol, SeriesCtl* ctl, bool decide, cudaStream_t s) {
   const SeriesTermArgs a{x, kp, p, last ? 1 : 0, scale, tol, ctl, decide ? 1 : 0};
   if (m.format == Format::Kron) {
-    if (m.kron.herm) {
+    if (m.kron.herm && m.kron.staged) {
+      const std::size_t smem = static_cast<std::size_t>(m.kron.st_slots[0] + m.kron.st_slots[1] + m.kron.st_slots[2] +
+                                                        (m.kron.factored ? 3 : 1)) *
+                               (kStageTile * 16);
+      const auto go = [&](auto kernel) {
+        const void* fn = reinterpret_cast<const void*>(kernel);
+        allow_smem(fn, smem);
+        const long long cap = static_cast<long long>(sm_count()) * blocks_per_sm(fn, smem);
+        const long long want = m.kron.tg.ntiles_herm < 1 ? 1 : m.kron.tg.ntiles_herm;
+        launch_pdl(kernel, static_cast<int>(want < cap ? want : cap), kThreads, smem, s, a, m.kron);
+      };
+      if (m.kron.factored) {
+        go(kron_series_term_staged_kernel<1>);
+      } else {
+        go(kron_series_term_staged_kernel<0>);
+      }
+    } else if (m.kron.herm) {
       if (m.kron.factored) {
         const auto g = kron_geom(kron_series_term_kernel<true, 1>, m.kron, true);
         launch_pdl(kron_series_term_kernel<true, 1>, g.first, kThreads, g.second, s, a, m.kron);

@@ -464,6 +464,44 @@ MultiCsr scaled(const MultiCsr& m) {
   return o;
 }
 
+// Staged tiles (kernels.hpp: KronView::staged).  For an operand m (rows r ->
+// columns c) the column tiles c / 32 named by the rows of each 32-row tile T,
+// in ascending order (nbr[T * kStageSlots + slot], -1 = none), and m with
+// every column replaced by its element offset inside the staged region:
+// (slot * 32 + c % 32) * 32 when the region holds rows c of the source
+// (by_rows), slot * 1024 + c % 32 when it holds its columns c.
+// false when some tile row names more than kStageSlots tiles.
+bool localize(const MultiCsr& m, bool by_rows, std::vector<int>& nbr, MultiCsr& local, int& slots) {
+  const std::int64_t nt = m.n / 32;
+  if (m.ptr.empty() || m.col.empty()) return false;
+  const int len = m.ptr[1] - m.ptr[0];  // one row length throughout (<= 8): slice s of the ELL copy starts at 32 s len
+  if (len < 1 || len > 8) return false;
+  for (std::int64_t r = 0; r < m.n; ++r)
+    if (m.ptr[static_cast<std::size_t>(r) + 1] - m.ptr[static_cast<std::size_t>(r)] != len) return false;
+  nbr.assign(static_cast<std::size_t>(nt) * dev::kStageSlots, -1);
+  local = m;
+  slots = 0;
+  for (std::int64_t T = 0; T < nt; ++T) {
+    std::vector<int> tiles;
+    for (std::int64_t r = 32 * T; r < 32 * T + 32; ++r)
+      for (int k = m.ptr[static_cast<std::size_t>(r)]; k < m.ptr[static_cast<std::size_t>(r) + 1]; ++k)
+        tiles.push_back(m.col[static_cast<std::size_t>(k)] / 32);
+    std::sort(tiles.begin(), tiles.end());
+    tiles.erase(std::unique(tiles.begin(), tiles.end()), tiles.end());
+    if (static_cast<int>(tiles.size()) > dev::kStageSlots) return false;
+    slots = std::max(slots, static_cast<int>(tiles.size()));
+    std::copy(tiles.begin(), tiles.end(), nbr.begin() + T * dev::kStageSlots);
+    for (std::int64_t r = 32 * T; r < 32 * T + 32; ++r) {
+      for (int k = m.ptr[static_cast<std::size_t>(r)]; k < m.ptr[static_cast<std::size_t>(r) + 1]; ++k) {
+        const int c = m.col[static_cast<std::size_t>(k)];
+        const int slot = static_cast<int>(std::lower_bound(tiles.begin(), tiles.end(), c / 32) - tiles.begin());
+        local.col[static_cast<std::size_t>(k)] = by_rows ? (slot * 32 + c % 32) * 32 : slot * 1024 + c % 32;
+      }
+    }
+  }
+  return true;
+}
+
 struct KronStore {
   // Sliced ELL copies unless they store more than kEllMaxPadding x the
   // nonzeros; whether the kernels use them is autotuned per operator set at
@@ -594,6 +632,39 @@ struct KronStore {
       aq_sc_val = up(aq.val, s);
       if (q_len[0] > 0) aq_ellu_val = up(to_ell(aq).val, s);  // the layout of q_ellu[0]
     }
+    // Staged Hermitian tiles (kernels.hpp: KronView::staged): a lattice-like
+    // operand set on one GPU.  Factored G-QSW with one Lindblad operator and
+    // the AX path (c2): R_0, P_0 and S_0 gather from Wt_0; L-QSW (c5): A and B
+    // gather from x.  Opt-in (QSWG_KRON_STAGED=1): bit-identical to the global
+    // gathers but measured slower — c2 term 27.7 us against 23.6 us, c5 2.92 ms
+    // against 2.23 ms: with the one block per SM its 176 - 192 KB allow, a
+    // tile costs ~340 KB of shared-memory reads and ~190 KB of copy writes
+    // through the same 128 B/clk port.
+    {
+      const char* sk = std::getenv("QSWG_KRON_STAGED");
+      const bool want = single && host.n % 32 == 0 && host.n >= 64 && sk && sk[0] == '1';
+      std::vector<int> nb[3];
+      MultiCsr lc[3];
+      int sl[3] = {0, 0, 0};
+      bool ok = false;
+      if (want && factored && host.q.size() == 1 && ax && p_rows && r_len[0] > 0 && s_len[0] > 0) {
+        ok = localize(host.r[0], true, nb[0], lc[0], sl[0]) && localize(host.p[0], false, nb[1], lc[1], sl[1]) &&
+             localize(host.sfac[0], true, nb[2], lc[2], sl[2]);
+      } else if (want && !factored && host.p.empty() && a_len > 0 && b_rows) {
+        ok = localize(a_host, true, nb[0], lc[0], sl[0]) && localize(b_host, false, nb[1], lc[1], sl[1]);
+      }
+      // 16 KB per tile — the patterns' and AXt(I, J), AXt(J, I), x(I, J) — next to the kernel's static 18 KB
+      if (ok && sl[0] + sl[1] + sl[2] + (factored ? 3 : 1) <= 12) {
+        staged = true;
+        for (int p3 = 0; p3 < 3; ++p3) {
+          st_slots[p3] = sl[p3];
+          if (sl[p3] == 0) continue;
+          st_len[p3] = lc[p3].ptr[1] - lc[p3].ptr[0];
+          st_nbr[p3] = up(nb[p3], s);
+          st_col[p3] = up(to_ell(lc[p3]).col, s);
+        }
+      }
+    }
     // a constant decay coefficient, as the kernels round it (kernels.hpp: d_const)
     if (!host.d_loc.empty()) {
       bool same = true;
@@ -653,6 +724,11 @@ struct KronStore {
   double2 cv_a{}, cv_b{};
   std::vector<double2> cv_p, cv_q, cv_r, cv_s;
   DeviceBuffer<int2> herm_tiles;               // one GPU: upper tiles in launch order
+  bool staged = false;                         // kernels.hpp: KronView::staged
+  int st_slots[3] = {0, 0, 0};
+  int st_len[3] = {0, 0, 0};
+  const int* st_nbr[3] = {nullptr, nullptr, nullptr};
+  const int* st_col[3] = {nullptr, nullptr, nullptr};
   bool ax = false;                             // kernels.hpp: KronView::ax
   bool d_const = false;                        // kernels.hpp: KronView::d_const
   double d_val = 0.0;
@@ -826,6 +902,9 @@ void fill_block(const dev::KronOperands& ops, const DeviceBuffer<std::int64_t>& 
 }  // namespace
 
 bool Liouvillian::kron_factored() const { return kron_ != nullptr && kron_->factored; }
+bool Liouvillian::kron_staged() const {
+  return kron_ != nullptr && kron_->staged && herm_flag_.size() > 0 && (!kron_->factored || (kron_->ax && kron_axt_.get()));
+}
 // Factored: Wt_k only when P_k is applied transposed (one GPU), else W_k and
 // Wt_k (one GPU) or W_k and V_k (row-partitioned); unfactored: W_k.
 int Liouvillian::kron_term_vectors() const {
@@ -953,6 +1032,15 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
       m.kron.aq_sc_val = kron_->aq_sc_val;
       m.kron.vk_aq = kron_->vk_aq;
       m.kron.cv_aq = kron_->cv_aq;
+    }
+    if (kron_->staged && (!kron_->factored || m.kron.ax)) {
+      m.kron.staged = 1;
+      for (int p = 0; p < 3; ++p) {
+        m.kron.st_slots[p] = kron_->st_slots[p];
+        m.kron.st_len[p] = kron_->st_len[p];
+        m.kron.st_nbr[p] = kron_->st_nbr[p];
+        m.kron.st_col[p] = kron_->st_col[p];
+      }
     }
   }
   return m;

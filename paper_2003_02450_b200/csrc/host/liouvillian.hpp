@@ -102,6 +102,8 @@ class Liouvillian {
   int kron_term_vectors() const;
   int kron_prepare_vectors() const;
   bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
+  /// The Hermitian series term runs on staged tiles (kernels.hpp: KronView::staged).
+  bool kron_staged() const;
 
   /// Local row block downloaded as CSR with global columns (parity / debug).
   void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,

@@ -11,6 +11,7 @@ namespace qswg::dev {
 inline constexpr int kMaxKron = 8;      // Lindblad operators per G-QSW
 inline constexpr int kMaxSeriesD = 128; // super-step outputs (d <= floor(1e280^(1/55)) = 123)
 inline constexpr int kSeriesRegD = 4;   // running sums updated per chunk in the series kernel
+inline constexpr int kStageSlots = 5;   // column tiles a 32-row tile of an operand may name on the staged path
 inline constexpr int kPendMax = 64;     // series terms held back before one batched sum update
 
 // A "multi-CSR" over the n x n operator space: rows sorted by column with
@@ -194,6 +195,29 @@ struct KronView {
   double d_val = 0.0;
   int ax = 0, b_sep = 0;
   double2* axt = nullptr;
+  // Staged Hermitian tiles (one GPU, n % 32 == 0, operands whose rows of one
+  // 32-row tile name at most kStageSlots column tiles: lattices in their
+  // natural labelling).  Every operand-weighted gather of a tile (I, J) then
+  // falls in a few 32 x 32 tiles of ONE row-major source F (Wt_0 for the
+  // factored G-QSW with one Lindblad operator, x itself for L-QSW):
+  //   pattern 0  F(T, J), T in st_nbr[0][I]   rows c of R_0 / A, lane = j
+  //   pattern 1  F(I, T), T in st_nbr[1][J]   columns a of P_0 / B, lane = j
+  //   pattern 2  F(T, I), T in st_nbr[2][J]   rows c of S_0, lane = i
+  // which the staged term kernel brings into shared memory with bulk copies
+  // (512-byte tile rows, one mbarrier per phase) before any arithmetic, so the
+  // operand-index -> gather -> FMA chains run against shared memory.
+  // st_col[p]: the operand's ELL column array (layout of r_ellu[0] / a_ellu,
+  // p_ell[0] / b_ell, s_ellu[0]) with every column replaced by its element
+  // offset inside the pattern's shared-memory region.
+  int staged = 0;
+  int st_slots[3] = {};           // tiles per region (max over the tile rows)
+  const int* st_nbr[3] = {};      // [n / 32][kStageSlots] tile indices, -1 = none
+  const int* st_col[3] = {};
+  int st_len[3] = {};             // row length of each pattern's operand (the same in every row, <= 8)
+  // The W kernel likewise (pattern 0 of F = x for Q_0).
+  int st_slots_q = 0;
+  const int* st_nbr_q = nullptr;
+  const int* st_col_q = nullptr;
   const double2* aq_ellu_val = nullptr;
   const double2* aq_sc_val = nullptr;
   int vk_aq = kValComplex;
