@@ -77,13 +77,16 @@ class ClockSampler:
         while not self.stop.wait(self.period):
             self._sample()
 
-    def __enter__(self):
-        if not self.enabled:
-            return self
+    def prepare(self):
+        """NVML start-up, long before the timed region: on a fresh box the first
+        nvmlInit of a process disturbed the GPU for the next second or so (the
+        first bench run of a box measured 40-45 ms per c2 series in the region
+        that followed it, 29 ms in every later run and in the region before it)."""
+        if not self.enabled or self.nvml is not None:
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
-            self.nvml = pynvml
             try:  # the NVML device behind this CUDA ordinal (CUDA_VISIBLE_DEVICES may remap)
                 import torch
                 pr = torch.cuda.get_device_properties(self.index)
@@ -91,6 +94,20 @@ class ClockSampler:
                 self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
             except Exception:
                 self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = pynvml
+            self._sample()
+            self.rows.clear()
+        except Exception:
+            self.nvml = None
+            self.enabled = False
+
+    def __enter__(self):
+        if not self.enabled:
+            return self
+        self.prepare()
+        if self.nvml is None:
+            return self
+        try:
             self._sample()
             self.stop = threading.Event()
             self.thread = threading.Thread(target=self._loop, daemon=True)
@@ -250,6 +267,8 @@ def main():
     from paper_2003_02450_b200 import api
 
     torch.cuda.set_device(local_rank)
+    clocks = ClockSampler(local_rank, enabled=not args.no_clocks)
+    clocks.prepare()
     comm = None
     if world > 1:
         import torch.distributed as dist
@@ -320,7 +339,7 @@ def main():
     # ---- device-resident timed region ----
     for _ in range(args.warmup):  # (re-)captures this call's series graph
         r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
-    with ClockSampler(local_rank, enabled=not args.no_clocks) as clocks:
+    with clocks:
         barrier()
         ev0.record(stream)
         launches = 0

@@ -79,7 +79,9 @@ typedef struct {
   int sell_panels;    /* SELL: column panels of the stored superoperator (1 = one pass; 0 other formats) */
   int kron_hermitian; /* KRON: the last product / step / series ran the Hermitian tile kernels */
   int kron_staged;    /* KRON: the Hermitian series term stages its operand tiles in shared memory
-                         (bulk copies; lattice-like operands, n a multiple of 32, one GPU) */
+                         (opt-in; lattice-like operands, n a multiple of 32, one GPU) */
+  int sell_fused;     /* SELL: the B (x) I entries are kept in natural row order beside the sorted rest
+                         (coalesced gathers; one GPU, sigma-sorted superoperators) */
 } qswg_liouvillian_info;
 
 typedef struct { int64_t m_star, s, spmvs, launches; } qswg_step_info;

@@ -93,7 +93,7 @@ class LiouvillianInfo(C.Structure):
                 ("group", C.c_int), ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("format", C.c_int), ("padding", C.c_double), ("kron_factored", C.c_int), ("kron_ell", C.c_int),
                 ("kron_term_vectors", C.c_int), ("sell_panels", C.c_int), ("kron_hermitian", C.c_int),
-                ("kron_staged", C.c_int)]
+                ("kron_staged", C.c_int), ("sell_fused", C.c_int)]
 
 
 class StepInfo(C.Structure):

@@ -375,6 +375,7 @@ int qswg_liouvillian_query(const qswg_liouvillian* l, qswg_liouvillian_info* inf
     info->kron_factored = L.kron_factored() ? 1 : 0;
     info->kron_ell = L.kron_ell() ? 1 : 0;
     info->kron_staged = L.kron_staged() ? 1 : 0;
+    info->sell_fused = L.sell_fused() ? 1 : 0;
     info->kron_term_vectors = L.kron_term_vectors();
     info->sell_panels = L.format() == qswg::dev::Format::Sell ? L.sell_panels() : 0;
     info->kron_hermitian = L.matrix().kron.herm;

@@ -690,15 +690,18 @@ __global__ void __launch_bounds__(kThreads) series_flush_kernel(SeriesFlushArgs 
 // ------------------------------------------------------------- SELL path
 // One warp per 32-row slice, one lane per row (kernels.hpp: SellView).
 template <bool kStrict>
-__device__ __forceinline__ double2 sell_dot(const SellView& m, long long b, int len, int lane,
-                                            const double2* __restrict__ x, unsigned long long pol,
+__device__ __forceinline__ double2 sell_dot(const int* __restrict__ col, const double2* __restrict__ val, long long b,
+                                            int len, int lane, const double2* __restrict__ x, unsigned long long pol,
                                             unsigned long long xpol) {
   double2 acc = make_double2(0.0, 0.0);
-  const int* cp = m.col + b + lane;
-  const double2* vp = m.val + b + lane;
+  const int* cp = col + b + lane;
+  const double2* vp = val + b + lane;
   int k = 0;
   if constexpr (!kStrict) {
-    constexpr int U = 4;
+#ifndef QSWG_SELL_U
+#define QSWG_SELL_U 4
+#endif
+    constexpr int U = QSWG_SELL_U;  // entries per lane in flight
     for (; k + U <= len; k += U) {
       int c[U];
       double2 v[U], xv[U];
@@ -1002,7 +1005,7 @@ __device__ __forceinline__ void slice_body(const SellView& m, const double2* __r
                                            unsigned long long pol, unsigned long long xpol, Epi&& epi) {
   const long long b = __ldg(m.slice_ptr + sl);
   const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
-  double2 acc = sell_dot<kStrict>(m, b, len, lane, x, pol, xpol);
+  double2 acc = sell_dot<kStrict>(m.col, m.val, b, len, lane, x, pol, xpol);
   const long long slot = sl * kSlice + lane;
   const bool valid = slot < m.rows;
   const long long row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
@@ -1013,19 +1016,81 @@ __device__ __forceinline__ void slice_body(const SellView& m, const double2* __r
   epi(row, acc, valid);
 }
 
-// kStream: the kernel instance that streams the matrix through shared memory
-// (SellView::work set) — the SELL kernels are instantiated for both paths,
-// each with the register budget it was measured best at.
-template <bool kStrict, bool kStream, class Epi>
+// Fused B (x) I windows (kernels.hpp: SellView::b_val).  Blocks draw windows
+// of win_slices slices from a device counter (first window = the block's own
+// index; the launch's last draw zeroes the counter).  Per window: the
+// natural-order B (x) I sums of its rows go to shared memory (every row once:
+// sums[row - window start]), then each sorted slice adds the sum of its row —
+// (B part) + (the rest), then the earlier panels' partial sum as on the other
+// paths.
+template <bool kStrict, class Epi>
+__device__ __forceinline__ void slice_windows(const SellView& m, const double2* __restrict__ x, int lane,
+                                              unsigned long long pol, unsigned long long xpol, Epi&& epi) {
+  __shared__ double2 sums[kSellWindowSlices * kSlice];
+  __shared__ long long next_window;
+  const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const long long n_windows = (m.n_slices + m.win_slices - 1) / m.win_slices;
+  const long long nb = gridDim.x;
+  const unsigned last_draw =
+      static_cast<unsigned>((n_windows > nb ? n_windows - nb : 0) + (n_windows < nb ? n_windows : nb) - 1);
+  long long win = blockIdx.x;
+  while (win < n_windows) {
+    const long long s0 = win * m.win_slices;
+    const long long s1 = s0 + m.win_slices < m.n_slices ? s0 + m.win_slices : m.n_slices;
+    for (long long sl = s0 + wib; sl < s1; sl += wpb) {  // natural order: slot = row
+      const long long b = __ldg(m.b_slice_ptr + sl);
+      const int len = static_cast<int>((__ldg(m.b_slice_ptr + sl + 1) - b) / kSlice);
+      sums[(sl - s0) * kSlice + lane] = sell_dot<kStrict>(m.b_col, m.b_val, b, len, lane, x, pol, xpol);
+    }
+    __syncthreads();
+    for (long long sl = s0 + wib; sl < s1; sl += wpb) {
+      const long long b = __ldg(m.slice_ptr + sl);
+      const int len = static_cast<int>((__ldg(m.slice_ptr + sl + 1) - b) / kSlice);
+      double2 acc = sell_dot<kStrict>(m.col, m.val, b, len, lane, x, pol, xpol);
+      const long long slot = sl * kSlice + lane;
+      const bool valid = slot < m.rows;
+      const long long row = m.perm && valid ? static_cast<long long>(__ldg(m.perm + slot)) : slot;
+      if (valid) {
+        const double2 bs = sums[row - s0 * kSlice];
+        acc = make_double2(bs.x + acc.x, bs.y + acc.y);
+        if (m.part_in) {
+          const double2 pp = ld_once(m.part_in + row, pol);
+          acc = make_double2(pp.x + acc.x, pp.y + acc.y);
+        }
+      }
+      epi(row, acc, valid);
+    }
+    __syncthreads();  // (the sums are read; the draw below is the block's)
+    if (threadIdx.x == 0) {
+      const unsigned r = atomicAdd(m.win_work, 1u);
+      const long long wn = static_cast<long long>(r) + nb;
+      if (wn >= n_windows && r == last_draw) *m.win_work = 0u;
+      next_window = wn;
+    }
+    __syncthreads();
+    win = next_window;
+  }
+}
+
+// kMode: the SELL kernels are instantiated per path, each with the register
+// budget it was measured best at: kSellReg (registers, grid-stride slices),
+// kSellStream (the matrix streamed through shared memory, SellView::work) and
+// kSellWindows (fused B (x) I windows, SellView::b_val).
+constexpr int kSellReg = 0, kSellStream = 1, kSellWindows = 2;
+template <bool kStrict, int kMode, class Epi>
 __device__ __forceinline__ void slice_loop(const SellView& m, const double2* __restrict__ x, Epi&& epi) {
-  if constexpr (kStream) {
+  if constexpr (kMode == kSellStream) {
     slice_stream<kStrict>(m, x, epi);
   } else {
     const unsigned long long pol = evict_first_policy(), xpol = evict_last_policy();
     const int lane = threadIdx.x & 31;
-    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
-    for (long long sl = warp; sl < m.n_slices; sl += nwarps) slice_body<kStrict>(m, x, sl, lane, pol, xpol, epi);
+    if constexpr (kMode == kSellWindows) {
+      slice_windows<kStrict>(m, x, lane, pol, xpol, epi);
+    } else {
+      const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+      const long long warp = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+      for (long long sl = warp; sl < m.n_slices; sl += nwarps) slice_body<kStrict>(m, x, sl, lane, pol, xpol, epi);
+    }
   }
 }
 // Resident blocks per SM asked of ptxas: the streamed path holds its rings in
@@ -1035,9 +1100,9 @@ __device__ __forceinline__ void slice_loop(const SellView& m, const double2* __r
 #ifndef QSWG_SELL_REG_MIN_BLOCKS
 #define QSWG_SELL_REG_MIN_BLOCKS 3
 #endif
-template <bool kStream>
+template <int kMode>
 constexpr int sell_min_blocks() {
-  return kStream ? QSWG_SELL_MIN_BLOCKS : QSWG_SELL_REG_MIN_BLOCKS;
+  return kMode == kSellStream ? QSWG_SELL_MIN_BLOCKS : QSWG_SELL_REG_MIN_BLOCKS;
 }
 
 // Skip test of the partial-panel kernels: the same early exits as the term
@@ -1055,13 +1120,13 @@ __device__ __forceinline__ bool skip_now(const SkipCheck& k) {
 }
 
 // One earlier column panel: part[row] (=|+=) its row sums.
-template <bool kFirst, bool kStream>
-__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
+template <bool kFirst, int kMode>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kMode>())
     sell_partial_kernel(SellView m, const double2* x, double2* part, SkipCheck sk) {
   pdl_prologue();
   if (skip_now(sk)) return;
   const unsigned long long once = evict_first_policy();
-  slice_loop<false, kStream>(m, x, [&](long long row, double2 acc, bool valid) {
+  slice_loop<false, kMode>(m, x, [&](long long row, double2 acc, bool valid) {
     if (!valid) return;
     if constexpr (!kFirst) {
       const double2 pp = ld_once(part + row, once);
@@ -1072,11 +1137,11 @@ __global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
   pdl_trigger();
 }
 
-template <bool kStrict, bool kStream>
-__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
+template <bool kStrict, int kMode>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kMode>())
     sell_spmv_kernel(SellView m, const double2* x, double2* y, double scale) {
   pdl_prologue();
-  slice_loop<kStrict, kStream>(m, x, [&](long long row, double2 acc, bool valid) {
+  slice_loop<kStrict, kMode>(m, x, [&](long long row, double2 acc, bool valid) {
     if (valid) y[row] = make_double2(__dmul_rn(scale, acc.x), __dmul_rn(scale, acc.y));
   });
 }
@@ -1095,8 +1160,8 @@ struct SellStepArgs {
   int decide;
 };
 
-template <bool kStrict, bool kStream>
-__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>()) sell_step_term_kernel(SellStepArgs a) {
+template <bool kStrict, int kMode>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kMode>()) sell_step_term_kernel(SellStepArgs a) {
   pdl_prologue();
   StepCtl* ctl = a.ctl;
   if (*(volatile int*)&ctl->error) return;
@@ -1104,7 +1169,7 @@ __global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>()) sell_ste
   __shared__ unsigned long long red[32];
   unsigned long long tmax = 0, smax = 0;
   const unsigned long long once = evict_first_policy(), keep = evict_last_policy();
-  slice_loop<kStrict, kStream>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
+  slice_loop<kStrict, kMode>(a.m, a.x, [&](long long row, double2 acc, bool valid) {
     if (!valid) return;
     const double2 yv = make_double2(__dmul_rn(a.scale, acc.x), __dmul_rn(a.scale, acc.y));
     const double2 sv0 = ld_once(a.sum_in + row, once);
@@ -1132,8 +1197,8 @@ __global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>()) sell_ste
   }
 }
 
-template <bool kStrict, bool kStream>
-__global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
+template <bool kStrict, int kMode>
+__global__ void __launch_bounds__(kThreads, sell_min_blocks<kMode>())
     sell_series_term_kernel(SeriesTermArgs a, SellView m) {
   pdl_prologue();
   if (series_skip(a.ctl)) return;
@@ -1142,7 +1207,7 @@ __global__ void __launch_bounds__(kThreads, sell_min_blocks<kStream>())
   const unsigned long long keep = evict_last_policy();
   double2* const kp = a.kp;
   const double scale = a.scale;
-  slice_loop<kStrict, kStream>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
+  slice_loop<kStrict, kMode>(m, a.x, [&](long long row, double2 acc, bool valid) { series_store(kp, scale, row, acc, valid, keep, tmax); });
   series_term_finish(a, tmax, red);
 }
 
@@ -2527,7 +2592,8 @@ void launch_sell(void (*kernel)(KArgs...), const SellView& m, cudaStream_t s, Ar
   if (smem) allow_smem(fn, smem);
   const int per_sm = blocks_per_sm(fn, smem);
   const long long cap = static_cast<long long>(sm_count()) * per_sm;
-  long long want = (m.n_slices + kThreads / 32 - 1) / (kThreads / 32);
+  long long want = m.b_val && !m.work ? (m.n_slices + m.win_slices - 1) / m.win_slices
+                                      : (m.n_slices + kThreads / 32 - 1) / (kThreads / 32);
   if (want < 1) want = 1;
   launch_pdl(kernel, static_cast<int>(want < cap ? want : cap), kThreads, smem, s, args...);
 }
@@ -2616,15 +2682,19 @@ void sell_partials(const DevMatrix& m, const double2* x, const SkipCheck& sk, cu
   for (int q = m.pre_done; q < m.n_pre; ++q) {
     if (q == 0) {
       if (m.sell_pre[q].work) {
-        launch_sell(sell_partial_kernel<true, true>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+        launch_sell(sell_partial_kernel<true, kSellStream>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+      } else if (m.sell_pre[q].b_val) {
+        launch_sell(sell_partial_kernel<true, kSellWindows>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
       } else {
-        launch_sell(sell_partial_kernel<true, false>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+        launch_sell(sell_partial_kernel<true, kSellReg>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
       }
     } else {
       if (m.sell_pre[q].work) {
-        launch_sell(sell_partial_kernel<false, true>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+        launch_sell(sell_partial_kernel<false, kSellStream>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+      } else if (m.sell_pre[q].b_val) {
+        launch_sell(sell_partial_kernel<false, kSellWindows>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
       } else {
-        launch_sell(sell_partial_kernel<false, false>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
+        launch_sell(sell_partial_kernel<false, kSellReg>, m.sell_pre[q], s, m.sell_pre[q], x, m.part, sk);
       }
     }
     QSWG_LAUNCH_CHECK("sell_partials");
@@ -2666,15 +2736,19 @@ void step_term(const DevMatrix& m, const double2* x, double2* y, const double2* 
     SellStepArgs a{m.sell, x, y, sum_in, sum_out, scale, tol, ctl, first_of_stage ? 1 : 0, stage, decide ? 1 : 0};
     if (m.group == 1) {
       if (m.sell.work) {
-        launch_sell(sell_step_term_kernel<true, true>, m.sell, s, a);
+        launch_sell(sell_step_term_kernel<true, kSellStream>, m.sell, s, a);
+      } else if (m.sell.b_val) {
+        launch_sell(sell_step_term_kernel<true, kSellWindows>, m.sell, s, a);
       } else {
-        launch_sell(sell_step_term_kernel<true, false>, m.sell, s, a);
+        launch_sell(sell_step_term_kernel<true, kSellReg>, m.sell, s, a);
       }
     } else {
       if (m.sell.work) {
-        launch_sell(sell_step_term_kernel<false, true>, m.sell, s, a);
+        launch_sell(sell_step_term_kernel<false, kSellStream>, m.sell, s, a);
+      } else if (m.sell.b_val) {
+        launch_sell(sell_step_term_kernel<false, kSellWindows>, m.sell, s, a);
       } else {
-        launch_sell(sell_step_term_kernel<false, false>, m.sell, s, a);
+        launch_sell(sell_step_term_kernel<false, kSellReg>, m.sell, s, a);
       }
     }
   } else {
@@ -2732,15 +2806,19 @@ void series_term(const DevMatrix& m, const double2* x, double2* kp, int p, bool 
     sell_partials(m, x, SkipCheck{ctl, nullptr, 1}, s);
     if (m.group == 1) {
       if (m.sell.work) {
-        launch_sell(sell_series_term_kernel<true, true>, m.sell, s, a, m.sell);
+        launch_sell(sell_series_term_kernel<true, kSellStream>, m.sell, s, a, m.sell);
+      } else if (m.sell.b_val) {
+        launch_sell(sell_series_term_kernel<true, kSellWindows>, m.sell, s, a, m.sell);
       } else {
-        launch_sell(sell_series_term_kernel<true, false>, m.sell, s, a, m.sell);
+        launch_sell(sell_series_term_kernel<true, kSellReg>, m.sell, s, a, m.sell);
       }
     } else {
       if (m.sell.work) {
-        launch_sell(sell_series_term_kernel<false, true>, m.sell, s, a, m.sell);
+        launch_sell(sell_series_term_kernel<false, kSellStream>, m.sell, s, a, m.sell);
+      } else if (m.sell.b_val) {
+        launch_sell(sell_series_term_kernel<false, kSellWindows>, m.sell, s, a, m.sell);
       } else {
-        launch_sell(sell_series_term_kernel<false, false>, m.sell, s, a, m.sell);
+        launch_sell(sell_series_term_kernel<false, kSellReg>, m.sell, s, a, m.sell);
       }
     }
   } else {
@@ -2846,15 +2924,19 @@ void spmv(const DevMatrix& m, const double2* x, double2* y, double scale, cudaSt
     sell_partials(m, x, SkipCheck{}, s);
     if (m.group == 1) {
       if (m.sell.work) {
-        launch_sell(sell_spmv_kernel<true, true>, m.sell, s, m.sell, x, y, scale);
+        launch_sell(sell_spmv_kernel<true, kSellStream>, m.sell, s, m.sell, x, y, scale);
+      } else if (m.sell.b_val) {
+        launch_sell(sell_spmv_kernel<true, kSellWindows>, m.sell, s, m.sell, x, y, scale);
       } else {
-        launch_sell(sell_spmv_kernel<true, false>, m.sell, s, m.sell, x, y, scale);
+        launch_sell(sell_spmv_kernel<true, kSellReg>, m.sell, s, m.sell, x, y, scale);
       }
     } else {
       if (m.sell.work) {
-        launch_sell(sell_spmv_kernel<false, true>, m.sell, s, m.sell, x, y, scale);
+        launch_sell(sell_spmv_kernel<false, kSellStream>, m.sell, s, m.sell, x, y, scale);
+      } else if (m.sell.b_val) {
+        launch_sell(sell_spmv_kernel<false, kSellWindows>, m.sell, s, m.sell, x, y, scale);
       } else {
-        launch_sell(sell_spmv_kernel<false, false>, m.sell, s, m.sell, x, y, scale);
+        launch_sell(sell_spmv_kernel<false, kSellReg>, m.sell, s, m.sell, x, y, scale);
       }
     }
   } else {

@@ -43,9 +43,11 @@ int sell_sigma_setting() {
 }
 // Streamed SELL kernels (taylor.cu: slice_stream).  QSWG_SELL_STREAM: 0 = the
 // register path everywhere, 1 = streamed everywhere; default: streamed for
-// unsorted (regular) superoperators, whose gathers are coalesced, and the
-// register path (more resident warps) for sigma-sorted (irregular) ones, whose
-// scattered gathers need the latency hiding (measured, DESIGN.md section 3).
+// unsorted (regular) superoperators with short rows, whose register-path warps
+// would drain at every slice boundary, and the register path (more resident
+// warps) otherwise — long rows, or sigma-sorted (irregular) matrices whose
+// scattered gathers need the latency hiding (measured, DESIGN.md section 2.3).
+constexpr double kStreamMaxRowLength = 24.0;
 int sell_stream_setting() {
   static const int v = [] {
     const char* e = std::getenv("QSWG_SELL_STREAM");
@@ -71,6 +73,13 @@ int sell_panel_count(int group, std::int64_t n, bool sorted) {
     if (xb > kPanelMinX) p = static_cast<int>(std::ceil(xb / kPanelX));
   }
   return static_cast<int>(std::clamp<std::int64_t>(p, 1, std::min<std::int64_t>(dev::kMaxSellPanels, n)));
+}
+
+// Fused B (x) I windows of the sorted SELL kernels (kernels.hpp: SellView::b_val);
+// QSWG_SELL_FUSE=0 keeps every entry in the sorted arrays.
+bool sell_fuse_setting() {
+  const char* e = std::getenv("QSWG_SELL_FUSE");
+  return !(e && e[0] == '0');
 }
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
@@ -167,6 +176,22 @@ MultiCsr canonical(const MultiCsr& m) {
 }  // namespace detail
 
 using namespace detail;
+
+// The diagonal (diag = true) or off-diagonal entries of a multi-CSR, order kept.
+MultiCsr filter_multi(const MultiCsr& m, bool diag) {
+  MultiCsr f;
+  f.n = m.n;
+  f.ptr.assign(m.ptr.size(), 0);
+  for (std::int64_t i = 0; i < m.n && !m.ptr.empty(); ++i) {
+    for (int k = m.ptr[static_cast<std::size_t>(i)]; k < m.ptr[static_cast<std::size_t>(i) + 1]; ++k) {
+      if ((m.col[static_cast<std::size_t>(k)] == i) != diag) continue;
+      f.col.push_back(m.col[static_cast<std::size_t>(k)]);
+      f.val.push_back(m.val[static_cast<std::size_t>(k)]);
+    }
+    f.ptr[static_cast<std::size_t>(i) + 1] = static_cast<int>(f.col.size());
+  }
+  return f;
+}
 
 // Operands of L = I(x)A + B(x)I + sum_k P_k(x)Q_k + T_diag + decay (kernels.hpp).
 struct HostOperands {
@@ -822,6 +847,7 @@ void Liouvillian::adopt(Liouvillian& o) {
   std::swap(pre_, o.pre_);
   std::swap(part_, o.part_);
   std::swap(sell_work_, o.sell_work_);
+  std::swap(fused_, o.fused_);
   std::swap(main_c_lo_, o.main_c_lo_);
   std::swap(local_first_, o.local_first_);
   std::swap(rowptr_, o.rowptr_);
@@ -926,20 +952,43 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
   m.sell.row0 = block_.row0;
   m.sell.n_slices = n_slices_;
   m.sell.perm = perm_.size() ? perm_.get() : nullptr;
+  // Per panel: streamed (a scheduling counter in SellView::work) for unsorted panels with
+  // short rows — a register-path warp drains its loads at every slice boundary (c5, 13 entries
+  // per row: 0.84 of HBM against 0.96-0.99 streamed) — and the register path otherwise: long
+  // rows keep it busy (c2, 41 per row: 0.94 at 3 blocks against 0.91 streamed), and sorted
+  // (irregular) panels need its resident warps for their scattered gathers.
   const int stream = sell_stream_setting();
-  const bool sorted = perm_.size() > 0 || (!pre_.empty() && pre_[0].perm.size() > 0);
-  if (format_ == dev::Format::Sell && sell_work_.size() && m.group != 1 && stream != 0 && (stream == 1 || !sorted))
+  const bool may_stream = format_ == dev::Format::Sell && sell_work_.size() && m.group != 1 && stream != 0;
+  const auto wants_stream = [&](bool sorted, std::int64_t entries) {
+    const double row_len = static_cast<double>(entries) / static_cast<double>(std::max<std::int64_t>(block_.rows, 1));
+    return may_stream && (stream == 1 || (!sorted && row_len <= kStreamMaxRowLength));
+  };
+  std::int64_t pre_entries = 0;
+  for (const SellPanel& pn : pre_) pre_entries += pn.entries;
+  if (wants_stream(perm_.size() > 0, static_cast<std::int64_t>(static_cast<double>(nnz_local_) * padding_) - pre_entries))
     m.sell.work = sell_work_.get() + pre_.size();
+  if (fused_.b_val.size() && !m.sell.work) {  // fused B (x) I windows (one GPU, sorted rows)
+    m.sell.b_slice_ptr = fused_.b_slice_ptr.get();
+    m.sell.b_col = fused_.b_col.get();
+    m.sell.b_val = fused_.b_val.get();
+    m.sell.win_slices = dev::kSellWindowSlices;
+    m.sell.win_work = sell_work_.get() + pre_.size();
+  }
   if (!pre_.empty()) {  // column panels
     m.n_pre = static_cast<int>(pre_.size());
     for (std::size_t q = 0; q < pre_.size(); ++q) {
       dev::SellView& v = m.sell_pre[q];
       v = m.sell;
-      if (m.sell.work) v.work = sell_work_.get() + q;
+      v.work = wants_stream(pre_[q].perm.size() > 0, pre_[q].entries) ? sell_work_.get() + q : nullptr;
       v.slice_ptr = pre_[q].slice_ptr.get();
       v.col = pre_[q].col.get();
       v.val = pre_[q].val.get();
       v.perm = pre_[q].perm.size() ? pre_[q].perm.get() : nullptr;
+      v.b_slice_ptr = pre_[q].b_val.size() && !v.work ? pre_[q].b_slice_ptr.get() : nullptr;
+      v.b_col = v.b_slice_ptr ? pre_[q].b_col.get() : nullptr;
+      v.b_val = v.b_slice_ptr ? pre_[q].b_val.get() : nullptr;
+      v.win_slices = v.b_slice_ptr ? dev::kSellWindowSlices : 0;
+      v.win_work = v.b_slice_ptr ? sell_work_.get() + q : nullptr;
     }
     m.part = part_.get();
     m.sell.part_in = part_.get();
@@ -1079,9 +1128,13 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
       const double2* val;
     };
     std::vector<std::pair<std::int64_t, View>> pv;  // (first column, panel), walked in column order
-    for (const SellPanel& pn : pre_)
+    for (const SellPanel& pn : pre_) {
       pv.push_back({pn.c_lo, {pn.slice_ptr.get(), pn.perm.size() ? pn.perm.get() : nullptr, pn.col.get(), pn.val.get()}});
+      if (pn.b_val.size()) pv.push_back({pn.c_lo, {pn.b_slice_ptr.get(), nullptr, pn.b_col.get(), pn.b_val.get()}});
+    }
     pv.push_back({main_c_lo_, {slice_ptr_.get(), perm_.size() ? perm_.get() : nullptr, col_.get(), val_.get()}});
+    if (fused_.b_val.size())
+      pv.push_back({main_c_lo_, {fused_.b_slice_ptr.get(), nullptr, fused_.b_col.get(), fused_.b_val.get()}});
     std::stable_sort(pv.begin(), pv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
     std::vector<View> views;
     for (const auto& e : pv) views.push_back(e.second);
@@ -1114,6 +1167,21 @@ void Liouvillian::download(std::vector<std::int64_t>& rowptr, std::vector<std::i
           rc[r].push_back(c32[e]);
           rv[r].push_back(v[e]);
         }
+      }
+    }
+    if (fused_.b_val.size()) {  // a row's B (x) I entries and its other entries are stored apart: back to column order
+      for (std::size_t r = 0; r < rows; ++r) {
+        std::vector<std::size_t> o(rc[r].size());
+        std::iota(o.begin(), o.end(), std::size_t{0});
+        std::stable_sort(o.begin(), o.end(), [&](std::size_t a, std::size_t b) { return rc[r][a] < rc[r][b]; });
+        std::vector<int> c2(o.size());
+        std::vector<Complex> v2(o.size());
+        for (std::size_t k = 0; k < o.size(); ++k) {
+          c2[k] = rc[r][o[k]];
+          v2[k] = rv[r][o[k]];
+        }
+        rc[r].swap(c2);
+        rv[r].swap(v2);
       }
     }
     rowptr.assign(rows + 1, 0);
@@ -1543,10 +1611,42 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
     for (int q = 0; panels > 1 && q < panels; ++q)
       ranges.push_back({n * (static_cast<std::int64_t>(q) * n / panels), n * (static_cast<std::int64_t>(q + 1) * n / panels)});
   }
+  // Fused B (x) I windows (one GPU, sigma-sorted rows; kernels.hpp: SellView::b_val).  The
+  // B (x) I entries of row (i, j) sit at columns n c + i, c in row j of B: for the 32
+  // consecutive rows of a natural-order slice they are the same list and their gathers one
+  // coalesced 512-byte segment (4 L1 wavefronts) — until the sigma sort scatters the rows of a
+  // slice, after which every lane's gather is its own 32-byte sector and wavefront, the bound
+  // of the irregular configs (about one sector per clock and SM).  So every panel keeps those
+  // entries in a second, natural-order sliced ELL (no padding inside a rho column: every row
+  // has row j's count) and sorts only the rest, inside windows of kSellWindowSlices slices
+  // whose natural-order sums a block holds in shared memory.  B's diagonal stays with the
+  // rest (it shares its position with A's diagonal), and every Q_k must be diagonal-free so
+  // that no position is stored twice.
+  bool fuse = use_sell && world == 1 && cfg.group != 1 && l->perm_.size() > 0 && !hops.b.empty() && sell_fuse_setting();
+  for (const MultiCsr& qk : hops.q)
+    for (std::int64_t i = 0; fuse && i < qk.n; ++i)
+      for (int k = qk.ptr[static_cast<std::size_t>(i)]; k < qk.ptr[static_cast<std::size_t>(i) + 1]; ++k)
+        if (qk.col[static_cast<std::size_t>(k)] == i) fuse = false;
+  std::unique_ptr<DeviceOperands> ops_boff, ops_rest;
+  if (fuse) {
+    HostOperands hb;
+    hb.n = hops.n;
+    hb.omega = hops.omega;
+    hb.b = filter_multi(hops.b, false);
+    HostOperands hr = hops;
+    hr.b = filter_multi(hops.b, true);
+    fuse = !hb.b.col.empty();
+    if (fuse) {
+      ops_boff = std::make_unique<DeviceOperands>(hb, s);
+      ops_rest = std::make_unique<DeviceOperands>(hr, s);
+      if (ranges.size() < 2) ranges.assign(1, {0, dim});
+      l->sigma_ = dev::kSellWindowSlices * dev::kSlice;
+    }
+  }
   const int panels = ranges.size() > 1 ? static_cast<int>(ranges.size()) : 1;
   std::int64_t main_entries = 0;
   l->local_first_ = panels > 1 ? std::min(local_first, panels - 1) : 0;
-  if (use_sell && panels > 1) {
+  if (use_sell && (panels > 1 || fuse)) {
     // ---- column panels: x slices that stay in L2 while their entries stream ----
     l->format_ = dev::Format::Sell;
     const std::int64_t rows = l->block_.rows;
@@ -1561,8 +1661,26 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       SellPanel pn;
       pn.c_lo = ranges[static_cast<std::size_t>(q)].first;
       pn.c_hi = ranges[static_cast<std::size_t>(q)].second;
+      const dev::KronOperands& po = fuse ? ops_rest->get() : ops.get();
+      if (fuse) {  // the B (x) I entries of this column range: natural row order, no permutation
+        QSWG_CHECK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+        dev::assemble_count(ops_boff->get(), l->block_.row0, rows, cnt.get(), s, pn.c_lo, pn.c_hi);
+        dev::exclusive_scan(cnt.get(), g.get(), rows + 1, tmp.get(), tmp_bytes, s);
+        QSWG_CHECK(cudaMemsetAsync(se.get(), 0, se.bytes(), s));
+        dev::sell_slice_entries(g.get(), rows, nullptr, se.get(), s);
+        pn.b_slice_ptr.resize(static_cast<std::size_t>(l->n_slices_) + 1);
+        dev::exclusive_scan(se.get(), pn.b_slice_ptr.get(), l->n_slices_ + 1, tmp.get(), tmp_bytes, s);
+        std::int64_t eb = 0;
+        QSWG_CHECK(cudaMemcpyAsync(&eb, pn.b_slice_ptr.get() + l->n_slices_, sizeof(std::int64_t), cudaMemcpyDeviceToHost, s));
+        QSWG_CHECK(cudaStreamSynchronize(s));
+        stored += eb;
+        pn.b_col.resize(static_cast<std::size_t>(std::max<std::int64_t>(eb, 1)));
+        pn.b_val.resize(static_cast<std::size_t>(std::max<std::int64_t>(eb, 1)));
+        dev::assemble_fill_sell(ops_boff->get(), l->block_.row0, rows, pn.b_slice_ptr.get(), nullptr, pn.b_col.get(),
+                                pn.b_val.get(), s, pn.c_lo, pn.c_hi);
+      }
       QSWG_CHECK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
-      dev::assemble_count(ops.get(), l->block_.row0, rows, cnt.get(), s, pn.c_lo, pn.c_hi);
+      dev::assemble_count(po, l->block_.row0, rows, cnt.get(), s, pn.c_lo, pn.c_hi);
       dev::exclusive_scan(cnt.get(), g.get(), rows + 1, tmp.get(), tmp_bytes, s);
       if (l->sigma_ > dev::kSlice) {
         pn.perm.resize(static_cast<std::size_t>(rows));
@@ -1579,7 +1697,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       pn.entries = e;
       pn.col.resize(static_cast<std::size_t>(std::max<std::int64_t>(e, 1)));
       pn.val.resize(static_cast<std::size_t>(std::max<std::int64_t>(e, 1)));
-      dev::assemble_fill_sell(ops.get(), l->block_.row0, rows, pn.slice_ptr.get(),
+      dev::assemble_fill_sell(po, l->block_.row0, rows, pn.slice_ptr.get(),
                               pn.perm.size() ? pn.perm.get() : nullptr, pn.col.get(), pn.val.get(), s, pn.c_lo,
                               pn.c_hi);
       QSWG_CHECK(cudaStreamSynchronize(s));
@@ -1592,6 +1710,9 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
         l->val_ = std::move(pn.val);
         l->main_c_lo_ = pn.c_lo;
         main_entries = e;
+        l->fused_.b_slice_ptr = std::move(pn.b_slice_ptr);
+        l->fused_.b_col = std::move(pn.b_col);
+        l->fused_.b_val = std::move(pn.b_val);
       }
     }
     l->part_.resize(static_cast<std::size_t>(std::max<std::int64_t>(rows, 1)));

@@ -56,6 +56,10 @@ struct SellPanel {
   DeviceBuffer<double2> val;
   std::int64_t c_lo = 0, c_hi = 0;  // global column range
   std::int64_t entries = 0;          // stored entries (padding included)
+  // fused B (x) I part in natural row order (dev::SellView::b_val); empty: none
+  DeviceBuffer<std::int64_t> b_slice_ptr;
+  DeviceBuffer<int> b_col;
+  DeviceBuffer<double2> b_val;
 };
 
 struct RowBlock {
@@ -104,6 +108,8 @@ class Liouvillian {
   bool kron_ell() const { return kron_ != nullptr && kron_ell_; }
   /// The Hermitian series term runs on staged tiles (kernels.hpp: KronView::staged).
   bool kron_staged() const;
+  /// SELL with the fused natural-order B (x) I arrays (kernels.hpp: SellView::b_val).
+  bool sell_fused() const { return format_ == dev::Format::Sell && fused_.b_val.size() > 0; }
 
   /// Local row block downloaded as CSR with global columns (parity / debug).
   void download(std::vector<std::int64_t>& rowptr, std::vector<std::int64_t>& col,
@@ -165,6 +171,7 @@ class Liouvillian {
   int sigma_ = dev::kSlice;
   std::vector<SellPanel> pre_;            // SELL column panels before the main arrays (one GPU)
   DeviceBuffer<double2> part_;            // their row sums
+  SellPanel fused_;                       // the main panel's fused B (x) I arrays (b_* only)
   DeviceBuffer<unsigned> sell_work_;          // one scheduling counter per panel (dev::SellView::work)
   std::int64_t main_c_lo_ = 0;            // column range of the main SELL arrays
   int local_first_ = 0;                   // leading panels = this rank's own columns (overlap the halo exchange)

@@ -75,6 +75,21 @@ struct SellView {
   // chunks of consecutive slices from (the launch's last draw zeroes it again);
   // nullptr = the static grid-stride assignment.
   unsigned* work = nullptr;
+  // Fused B (x) I part (one GPU, sigma-sorted rows; nullptr = none): the
+  // panel's B (x) I entries — for the 32 consecutive rows (i .. i + 31, j) of a
+  // slice the same operand row j, their gathers x[n c + i .. i + 31] one
+  // coalesced 512-byte segment — kept in a second sliced ELL in NATURAL row
+  // order (no padding between rows of one rho column), while col / val hold
+  // the remaining entries in the sorted order.  A block works through
+  // windows of win_slices slices (sigma = 32 win_slices rows, so the sort
+  // permutes inside a window): the natural-order sums of the window go to
+  // shared memory, then the sorted slices add them to theirs.  win_work: the
+  // device counter the blocks draw windows from.
+  const std::int64_t* b_slice_ptr = nullptr;
+  const int* b_col = nullptr;
+  const double2* b_val = nullptr;
+  int win_slices = 0;
+  unsigned* win_work = nullptr;
   std::int64_t rows = 0;
   std::int64_t row0 = 0;
   std::int64_t n_slices = 0;
@@ -230,6 +245,7 @@ struct KronView {
 // SELL split into column panels (one GPU, x beyond L2): the earlier panels
 // accumulate row sums in `part`; the last one (DevMatrix::sell) adds them.
 inline constexpr int kMaxSellPanels = 16;
+inline constexpr int kSellWindowSlices = 64;  // fused B (x) I windows: 2048 rows, 32 KB of sums per block
 
 struct DevMatrix {
   Format format = Format::Csr;

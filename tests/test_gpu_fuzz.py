@@ -60,10 +60,10 @@ def random_hermitian(rng, n, density):
     return Csr.from_coo(n, n, r, c, d[r, c])
 
 
-def instance(seed):
+def instance(seed, sizes=(1, 2, 3, 5, 17, 31, 32, 33, 40, 47), mean_degree=None):
     rng = np.random.default_rng(1000 + seed)
-    n = int(rng.choice([1, 2, 3, 5, 17, 31, 32, 33, 40, 47]))
-    density = float(rng.choice([0.0, 0.05, 0.2, 0.6]))
+    n = int(rng.choice(list(sizes)))
+    density = float(rng.choice([0.0, 0.05, 0.2, 0.6])) if mean_degree is None else mean_degree / n
     omega = float(rng.choice([0.0, 1.0, round(float(rng.random()), 3)]))
     g = random_digraph(rng, n, density)
     gu = api.symmetrize(g)
@@ -81,8 +81,9 @@ def instance(seed):
         inst.update(kind="local", h=pad(h), ml=pad(ml), src=src, snk=snk, N=total)
     else:  # G-QSW with 1-2 complex Lindblad operators, sometimes a rotating Hamiltonian
         h = api.generator_matrix(float(0.5 + rng.random()), gu).to_csr()
-        ls = [random_complex(rng, n, 0.3) for _ in range(int(rng.integers(1, 3)))]
-        hrot = random_hermitian(rng, n, 0.2) if rng.random() < 0.4 else None
+        ld = 0.3 if mean_degree is None else mean_degree / n
+        ls = [random_complex(rng, n, ld) for _ in range(int(rng.integers(1, 3)))]
+        hrot = random_hermitian(rng, n, 0.2 if mean_degree is None else 1.0 / n) if rng.random() < 0.4 else None
         inst.update(kind="global", h=h, ls=ls, hrot=hrot, N=n)
     N = inst["N"]
     if rng.random() < 0.5:
@@ -121,6 +122,34 @@ def test_random_walk_parity(port, seed):
     want, n_step = o.step(inst["v0"], tq)
     L_ref = o.csr()
     for fmt, group in MODES:
+        l = build_gpu(inst, fmt, group)
+        np.testing.assert_allclose(l.one_norms(), o.norms, rtol=1e-12, atol=1e-300)
+        r = api.series(l, l.state().upload(inst["v0"]), t1, tq, q, states=True)
+        err = float(np.abs(r.states - so).max())
+        assert err <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, group, err)
+        got, info = api.step(l, l.state().upload(inst["v0"]), tq)
+        assert np.abs(got.gather() - want).max() <= RHO_TOL * max(1.0, float(np.abs(want).max())), (seed, fmt)
+        if group == 1:
+            same_L = bool(np.array_equal(l.gather_full().data, L_ref.data))
+            slack_series, slack_step = (0, 0) if same_L else (q, int(info.s))
+            assert abs(int(r.info.spmvs) - n_ref) <= slack_series, (seed, fmt, r.info.spmvs, n_ref, same_L)
+            assert abs(int(info.spmvs) - n_step) <= slack_step, (seed, fmt, info.spmvs, n_step, same_L)
+
+
+@pytest.mark.parametrize("seed", range(100, 108))
+def test_random_walk_parity_several_tiles(port, seed):
+    """The same sweep at sizes where the KRON tile grid has 2 - 5 tile rows with
+    ragged edges (n = 64 ... 150), the sliced-ELL rows span several slices and
+    sigma windows, and the series plans take more than one super-step: sparse
+    random digraphs of mean degree 4, every default-arithmetic path and one
+    bitwise one."""
+    inst = instance(seed, sizes=(64, 65, 96, 97, 128, 150), mean_degree=4.0)
+    t1, tq, q = inst["times"]
+    o = build_oracle(port, inst)
+    so, po, n_ref = o.series(inst["v0"], t1, tq, q)
+    want, n_step = o.step(inst["v0"], tq)
+    L_ref = o.csr()
+    for fmt, group in [("kron", 0), ("sell", 0), ("csr", 1)]:
         l = build_gpu(inst, fmt, group)
         np.testing.assert_allclose(l.one_norms(), o.norms, rtol=1e-12, atol=1e-300)
         r = api.series(l, l.state().upload(inst["v0"]), t1, tq, q, states=True)

@@ -71,3 +71,36 @@ def test_panelled_sell_sharded(name, world, monkeypatch):
     keep = c.z["series_keep"]
     assert np.abs(states[keep] - c.z["series_states"]).max() <= RHO_TOL
     assert np.abs(parts[0][2] - c.z["series_pops"]).max() <= RHO_TOL
+
+
+@pytest.mark.parametrize("cfg,size,panels", [("c3", 256, 1), ("c3", 200, 3), ("c4", 160, 2)])
+def test_fused_natural_order_b_part(cfg, size, panels, monkeypatch):
+    """Sigma-sorted SELL on one GPU keeps the B (x) I entries in a second,
+    natural-order sliced ELL (coalesced gathers) that a block sums per window
+    in shared memory before the sorted slices add theirs (kernels.hpp:
+    SellView::b_val).  Same canonical matrix, same products and series as with
+    every entry in the sorted arrays (QSWG_SELL_FUSE=0) up to the order of the
+    sums, over several windows and with column panels."""
+    from paper_2003_02450_b200 import graphs
+    w = graphs.config(cfg, size=size)
+    monkeypatch.setenv("QSWG_SELL_PANELS", str(panels))
+    build = (lambda: api.build_local(w.omega, w.h, w.ops[0], format="sell")) if w.kind == "local" else \
+        (lambda: api.build_global(w.omega, w.h, w.ops, format="sell"))
+    monkeypatch.setenv("QSWG_SELL_FUSE", "1")
+    lf = build()
+    monkeypatch.setenv("QSWG_SELL_FUSE", "0")
+    l0 = build()
+    assert bool(lf.info.sell_fused) and not bool(l0.info.sell_fused)
+    assert int(lf.info.sell_panels) == panels
+    Lf, L0 = lf.gather_full(), l0.gather_full()
+    assert np.array_equal(Lf.indptr, L0.indptr) and np.array_equal(Lf.indices, L0.indices)
+    assert np.array_equal(Lf.data, L0.data)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(w.dim) + 1j * rng.standard_normal(w.dim)
+    yf, y0 = lf.spmv(x), l0.spmv(x)
+    assert np.abs(yf - y0).max() <= 1e-13 * np.abs(y0).max()
+    rf = api.series(lf, lf.state().from_probabilities(w.rho0), w.t1, w.tq, 6, states=True)
+    r0 = api.series(l0, l0.state().from_probabilities(w.rho0), w.t1, w.tq, 6, states=True)
+    assert rf.info.spmvs == r0.info.spmvs
+    assert np.abs(rf.states - r0.states).max() <= 1e-13
+    assert np.abs(rf.populations.sum(axis=1) - 1).max() <= 1e-12
