@@ -62,15 +62,19 @@ constexpr double kSellMaxPadding = 1.3;  // SELL if stored/nnz <= this (else CSR
 // split the columns so each panel's slice of x (about kPanelX) stays in L2
 // while the panel's entries stream.  QSWG_SELL_PANELS forces a count
 // (tests); lattices and the bitwise mode keep one pass.
-constexpr double kPanelMinX = 96e6, kPanelX = 40e6;
-int sell_panel_count(int group, std::int64_t n, bool sorted) {
+// With the fused natural-order B (x) I arrays (one GPU) a third to a half of
+// the gathers are coalesced segments, the L2 carries less sector traffic, and
+// larger panels win (c4: 4 panels of 67 MB 0.755 of HBM, 5: 0.747, 7: 0.727,
+// 3: 0.745, 2: 0.71, 1: 0.62; without the fused arrays 6-7 panels of 40 MB).
+constexpr double kPanelMinX = 96e6, kPanelX = 40e6, kPanelXFused = 70e6;
+int sell_panel_count(int group, std::int64_t n, bool sorted, bool fused = false) {
   if (group == 1) return 1;
   int p = 1;
   if (const char* e = std::getenv("QSWG_SELL_PANELS")) {
     p = std::atoi(e);
   } else if (sorted) {
     const double xb = 16.0 * static_cast<double>(n) * static_cast<double>(n);
-    if (xb > kPanelMinX) p = static_cast<int>(std::ceil(xb / kPanelX));
+    if (xb > kPanelMinX) p = static_cast<int>(std::ceil(xb / (fused ? kPanelXFused : kPanelX)));
   }
   return static_cast<int>(std::clamp<std::int64_t>(p, 1, std::min<std::int64_t>(dev::kMaxSellPanels, n)));
 }
@@ -1607,7 +1611,12 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       chunk *= 2;
     } while (static_cast<int>(ranges.size()) > dev::kMaxSellPanels);
   } else if (use_sell) {
-    const int panels = sell_panel_count(cfg.group, n, l->perm_.size() > 0);
+    bool fuse_ok = world == 1 && cfg.group != 1 && l->perm_.size() > 0 && !hops.b.empty() && sell_fuse_setting();
+    for (const MultiCsr& qk : hops.q)  // (the conditions of the fused B (x) I arrays below)
+      for (std::int64_t i = 0; fuse_ok && i < qk.n; ++i)
+        for (int k = qk.ptr[static_cast<std::size_t>(i)]; k < qk.ptr[static_cast<std::size_t>(i) + 1]; ++k)
+          if (qk.col[static_cast<std::size_t>(k)] == i) fuse_ok = false;
+    const int panels = sell_panel_count(cfg.group, n, l->perm_.size() > 0, fuse_ok);
     for (int q = 0; panels > 1 && q < panels; ++q)
       ranges.push_back({n * (static_cast<std::int64_t>(q) * n / panels), n * (static_cast<std::int64_t>(q + 1) * n / panels)});
   }
