@@ -320,6 +320,19 @@ bool uniform_slices(const MultiCsr& m) {
   return true;
 }
 
+// The entry count every row of m has, or 0 when the rows differ (or m is
+// empty).  The shuffled operand rows of the KRON kernels (KronView::a_len,
+// q_len, r_len, s_len) take ONE length for the whole operand: slices that are
+// uniform inside but differ from one another (a graph whose first 32 vertices
+// have degree 2 and the next 32 degree 4) must not take that path.
+int uniform_row_length(const MultiCsr& m) {
+  if (m.col.empty() || m.ptr.size() < 2) return 0;
+  const int len = m.ptr[1] - m.ptr[0];
+  for (std::int64_t i = 0; i < m.n; ++i)
+    if (m.ptr[static_cast<std::size_t>(i) + 1] - m.ptr[static_cast<std::size_t>(i)] != len) return 0;
+  return len;
+}
+
 EllHost to_ell(const MultiCsr& m) {
   EllHost e;
   const std::int64_t ns = (m.n + 31) / 32;
@@ -603,15 +616,16 @@ struct KronStore {
     // so a warp fetches all their column indices in one load and hands them
     // out by shuffle (the index -> gather chain starts without an L1 round trip).
     const char* ash = std::getenv("QSWG_KRON_ASHFL");  // experiment knob: 0 = no shuffled operand rows
-    if (single && !(ash && ash[0] == '0') && uniform_slices(a_host) && a_host.ptr[1] - a_host.ptr[0] <= 8) {
+    if (const int al = uniform_row_length(a_host); single && !(ash && ash[0] == '0') && al > 0 && al <= 8) {
       a_ellu = upload_ell(to_ell(scaled(a_host)), s);
-      a_len = a_host.ptr[1] - a_host.ptr[0];
+      a_len = al;
     }
     for (std::size_t k = 0; k < host.q.size(); ++k) {  // Q_k, and R_k / S_k when factored
       const auto shfl = [&](const MultiCsr& m, dev::KronEll& e, int& len) {
-        if (!single || (ash && ash[0] == '0') || !uniform_slices(m) || m.ptr[1] - m.ptr[0] > 8) return;
+        const int ul = uniform_row_length(m);
+        if (!single || (ash && ash[0] == '0') || ul < 1 || ul > 8) return;
         e = upload_ell(to_ell(scaled(m)), s);
-        len = m.ptr[1] - m.ptr[0];
+        len = ul;
       };
       dev::KronEll e;
       int len = 0;

@@ -159,3 +159,33 @@ def test_non_hermitian_h_rot_disables_the_hermitian_tiles(port):
     assert not l.info.kron_hermitian
     so, _, _ = o.series(v0, t1, tq, int(q))
     assert np.abs(r.states - so).max() <= 1e-10 * max(1.0, np.abs(so).max())
+
+
+@pytest.mark.parametrize("kind", ["local", "global"])
+def test_slices_of_different_row_length(kind, port):
+    """Operand slices that are uniform inside but differ from one another: 32
+    vertices on a cycle (degree 2) and 32 on a 4-regular circulant.  The
+    shuffled operand rows of the KRON kernels take one row length for the
+    whole operand, so such operands must stay on the per-row paths (a round-2
+    regression: the Hermitian tiles dropped the longer slices' last entries)."""
+    from paper_2003_02450_b200.graphs import Csr
+    n, r, c = 64, [], []
+    for i in range(32):
+        for d in (1, -1):
+            r.append(i)
+            c.append((i + d) % 32)
+        for d in (1, -1, 2, -2):
+            r.append(32 + i)
+            c.append(32 + (i + d) % 32)
+    g = Csr.from_coo(n, n, r, c, [1.0] * len(r))
+    h, m = graphs.generator_matrix(1.0, g), graphs.markov_chain_matrix(g)
+    p = np.zeros(n)
+    p[0] = p[40] = 0.5
+    v0 = rho0_vec(n, p)
+    o = port.build_local(0.3, h, m, [], []) if kind == "local" else port.build_global(0.3, h, [m], None)
+    so, _, ns = o.series(v0, 0.0, 3.0, 4)
+    for fmt in ("kron", "sell", "csr"):
+        l = api.build_local(0.3, h, m, format=fmt) if kind == "local" else api.build_global(0.3, h, [m], format=fmt)
+        res = api.series(l, l.state().upload(v0), 0.0, 3.0, 4, states=True)
+        assert res.info.spmvs == ns, fmt
+        assert np.abs(res.states - so).max() <= 1e-10, fmt
