@@ -1434,7 +1434,7 @@ template <int K, bool C, class G>
 __device__ __forceinline__ void shfl_rows(const KronEll& e, double2 cv, int len, int slice, int l0, double2* acc,
                                           G&& g) {
   const int lane = threadIdx.x & 31;
-  const int base = __ldg(e.sptr + slice);
+  const int base = slice * 32 * len;  // one row length in every slice (host: uniform_row_length)
   const int kt = lane >> 2, rt = lane & 3;
   const int mycol = kt < len ? __ldg(e.col + base + 32 * kt + l0 + rt) : 0;
   if (len == 4) {  // square lattices (c2)
@@ -1484,7 +1484,7 @@ template <int KQ, bool CQ, int KA, bool CA, class G>
 __device__ __forceinline__ void shfl_rows2(const KronEll& e, const double2* aval, double2 cvq, double2 cva, int len,
                                            int slice, int l0, double2* acc, double2* aacc, G&& g) {
   const int lane = threadIdx.x & 31;
-  const int base = __ldg(e.sptr + slice);
+  const int base = slice * 32 * len;
   const int kt = lane >> 2, rt = lane & 3;
   const int mycol = kt < len ? __ldg(e.col + base + 32 * kt + l0 + rt) : 0;
   if (len == 4) {
