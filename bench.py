@@ -53,7 +53,7 @@ class ClockSampler:
     each of its polls stalled this GPU's work for tens of ms (c1, 7 ms region:
     1.4 -> 15-21 ms/step), so the in-process NVML queries replace it."""
 
-    def __init__(self, index, period=0.1, enabled=True):
+    def __init__(self, index, period=0.25, enabled=True):
         self.index = index
         self.enabled = enabled
         self.period = period
@@ -74,8 +74,14 @@ class ClockSampler:
         self.rows.append([str(sm), str(mx), "", "", *["Active" if f else "Not Active" for f in flags]])
 
     def _loop(self):
-        while not self.stop.wait(self.period):
+        # one sample shortly after the region starts (short regions still get one
+        # under load), then one every `period` s: each NVML query can stall the
+        # GPU's work for milliseconds (20 series of 29 ms measured 28.8 ms per
+        # series with ~2 samples in the region, 30-32 ms with ~6), so few of them
+        wait = 0.05
+        while not self.stop.wait(wait):
             self._sample()
+            wait = self.period
 
     def prepare(self):
         """NVML start-up, long before the timed region: on a fresh box the first
@@ -343,9 +349,11 @@ def main():
         barrier()
         ev0.record(stream)
         launches = 0
+        step_device_ms = []  # CUDA-event time of every series (library stream): shows outlier steps
         for _ in range(args.steps):
             r = api.series(l, v, w.t1, w.tq, w.steps, populations=False)
             launches += r.info.launches
+            step_device_ms.append(float(r.info.device_ms))
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -447,6 +455,11 @@ def main():
                 "d2h_bytes_per_step": 8 * (w.steps + 1) * w.n, "ms_per_step": e2e_ms, "h2d_pinned": True,
                 "parts": e2e_parts},
         "gpu_launches": int(launches),
+        "step_device_ms": {"min": min(step_device_ms), "median": float(np.median(step_device_ms)),
+                           "max": max(step_device_ms),
+                           "note": "CUDA-event time of each timed series; ms_per_step is their mean plus the host "
+                                   "gaps between calls.  On the shared boxes single series intermittently run "
+                                   "28.5 -> 40 ms on the device with unchanged clocks (DESIGN.md section 6)"},
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
