@@ -136,7 +136,7 @@ def test_random_walk_parity(port, seed):
             assert abs(int(info.spmvs) - n_step) <= slack_step, (seed, fmt, info.spmvs, n_step, same_L)
 
 
-@pytest.mark.parametrize("seed", range(100, 108))
+@pytest.mark.parametrize("seed", range(100, 100 + int(__import__("os").environ.get("QSWG_FUZZ_SEEDS", "8"))))
 def test_random_walk_parity_several_tiles(port, seed):
     """The same sweep at sizes where the KRON tile grid has 2 - 5 tile rows with
     ragged edges (n = 64 ... 150), the sliced-ELL rows span several slices and
@@ -233,3 +233,36 @@ def test_random_walk_sharded(port, seed, fmt, world):
     parts = sorted(run_ranks(world, rank_fn), key=lambda p: p[0])
     states = np.concatenate([p[1] for p in parts], axis=1)
     assert np.abs(states - so).max() <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, world)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("QSWG_FUZZ_SEEDS", "6"))))
+def test_random_circulant_parity(port, seed):
+    """Random circulant graphs (d-regular, uniform operand rows of 2 - 8
+    entries: the shuffled-row, transposed-P/B and constant-value paths of the
+    KRON kernels on graphs that are not lattices), sizes with full and ragged
+    tiles, L-QSW and G-QSW, against the C oracle on every default path."""
+    from paper_2003_02450_b200 import graphs
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.choice([64, 70, 96, 128, 131]))
+    k = int(rng.integers(1, 5))
+    offs = rng.choice(np.arange(1, n // 2), size=k, replace=False)
+    r, c = [], []
+    for i in range(n):
+        for o in offs:
+            for sgn in (1, -1):
+                r.append(i)
+                c.append((i + sgn * int(o)) % n)
+    g = Csr.from_coo(n, n, r, c, [1.0] * len(r))
+    h, m = graphs.generator_matrix(1.0, g), graphs.markov_chain_matrix(g)
+    omega = float(rng.choice([0.1, 0.5, 0.9]))
+    p = rng.random(n)
+    v0 = rho0_vec(n, p / p.sum())
+    t1, tq, q = 0.0, float(1 + 3 * rng.random()), int(rng.integers(2, 6))
+    local = seed % 2 == 0
+    o = port.build_local(omega, h, m, [], []) if local else port.build_global(omega, h, [m], None)
+    so, _, n_ref = o.series(v0, t1, tq, q)
+    for fmt in ("kron", "sell"):
+        l = api.build_local(omega, h, m, format=fmt) if local else api.build_global(omega, h, [m], format=fmt)
+        res = api.series(l, l.state().upload(v0), t1, tq, q, states=True)
+        assert int(res.info.spmvs) == n_ref, (seed, fmt)
+        assert np.abs(res.states - so).max() <= RHO_TOL, (seed, fmt, n, k)
