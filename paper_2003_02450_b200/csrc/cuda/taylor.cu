@@ -245,8 +245,15 @@ __device__ void series_term_control(SeriesCtl* ctl, int p, int last, double tol)
   static_assert(kMaxSeriesD <= kThreads, "one thread per output");
   __shared__ int pmin_sh;
   const int k = threadIdx.x;
+  // every field this step reads, loaded up front: the control block sits in L2 and
+  // this step is the tail of the term kernel that the next kernel's blocks wait for, so
+  // its global round trips are taken once, in parallel, instead of one after another
   const double tn = bitsd(*(volatile unsigned long long*)&ctl->term_bits);
   const int count = ctl->count;
+  const int slots_l = ctl->slots, pend_max_l = ctl->pend_max;
+  const int kk = k < kMaxSeriesD ? k : 0;
+  const int active_l = ctl->active[kk], pending_l = ctl->pending[kk], p0_l = ctl->p0[kk];
+  const double factor_l = ctl->factor[kk], bound_l = ctl->bound[kk], nf_last_l = ctl->nf_last[kk], c1_l = ctl->c1[kk];
   if (k == 0) pmin_sh = p;
   __syncthreads();
   if (!isfinite(tn)) {  // expm.cpp:293-295
@@ -259,25 +266,25 @@ __device__ void series_term_control(SeriesCtl* ctl, int p, int last, double tol)
     }
     return;
   }
-  const int slot = p % ctl->slots;
-  const bool act = k < count && ctl->active[k];
-  const bool pend = k < count && ctl->pending[k];
-  if (act || pend) atomicMin(&pmin_sh, ctl->p0[k]);
+  const int slot = p % slots_l;
+  const bool act = k < count && active_l;
+  const bool pend = k < count && pending_l;
+  if (act || pend) atomicMin(&pmin_sh, p0_l);
   __syncthreads();
   // the next term must not overwrite a pending one
-  const bool full = last || p - pmin_sh + 1 >= ctl->pend_max;
+  const bool full = last || p - pmin_sh + 1 >= pend_max_l;
   double f = 0.0;
   bool und = false, stop = false;
   if (act) {
-    f = ctl->factor[k];
+    f = factor_l;
     ctl->fac_ring[slot][k] = f;
-    const double bnd = __dadd_ru(ctl->bound[k], __dmul_ru(f, tn));
+    const double bnd = __dadd_ru(bound_l, __dmul_ru(f, tn));
     ctl->bound[k] = bnd;
-    const double nf0 = ctl->nf_last[k];
+    const double nf0 = nf_last_l;
     const double ub = __dmul_ru(__dadd_ru(nf0, bnd), 1.0 + 0x1p-30);
-    if (!(ctl->c1[k] + f * tn > tol * ub)) {  // "continue" not settled (expm.cpp:310, 315)
+    if (!(c1_l + f * tn > tol * ub)) {  // "continue" not settled (expm.cpp:310, 315)
       const double lb = bnd <= nf0 * 0x1p-20 ? __dmul_rd(__dsub_rd(nf0, bnd), 1.0 - 0x1p-30) : 0.0;
-      stop = __dadd_rn(ctl->c1[k], __dmul_rn(f, tn)) <= __dmul_rd(tol, lb);  // c1 + c2 as expm.cpp:310-315 rounds it
+      stop = __dadd_rn(c1_l, __dmul_rn(f, tn)) <= __dmul_rd(tol, lb);  // c1 + c2 as expm.cpp:310-315 rounds it
 #ifdef QSWG_NO_SETTLED_STOP  // experiment: every stop through a flush and the exact test
       stop = false;
 #endif

@@ -79,11 +79,17 @@ int sell_panel_count(int group, std::int64_t n, bool sorted, bool fused = false)
   return static_cast<int>(std::clamp<std::int64_t>(p, 1, std::min<std::int64_t>(dev::kMaxSellPanels, n)));
 }
 
-// Fused B (x) I windows of the sorted SELL kernels (kernels.hpp: SellView::b_val);
-// QSWG_SELL_FUSE=0 keeps every entry in the sorted arrays.
-bool sell_fuse_setting() {
+// Fused B (x) I windows of the sorted SELL kernels (kernels.hpp: SellView::b_val).  A block
+// takes a whole window of 64 slices, so small superoperators would leave SMs idle (c1,
+// 128 slices: 2 blocks, 1.3 -> 3.6 ms per series): by default only from kFuseMinWindows
+// windows (2 per SM of a B200) on.  QSWG_SELL_FUSE=0 keeps every entry in the sorted arrays,
+// =1 fuses at any size (tests).
+constexpr std::int64_t kFuseMinWindows = 296;
+bool sell_fuse_setting(std::int64_t n_slices) {
   const char* e = std::getenv("QSWG_SELL_FUSE");
-  return !(e && e[0] == '0');
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return n_slices >= kFuseMinWindows * dev::kSellWindowSlices;
 }
 
 double hermiticity_tolerance(const SparseMatrix& m) { return 1e-15 * std::max(1.0, m.max_abs()); }
@@ -983,7 +989,9 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
   };
   std::int64_t pre_entries = 0;
   for (const SellPanel& pn : pre_) pre_entries += pn.entries;
-  if (wants_stream(perm_.size() > 0, static_cast<std::int64_t>(static_cast<double>(nnz_local_) * padding_) - pre_entries))
+  // (a panel with fused B (x) I arrays always takes the window path: they hold part of its entries)
+  if (!fused_.b_val.size() &&
+      wants_stream(perm_.size() > 0, static_cast<std::int64_t>(static_cast<double>(nnz_local_) * padding_) - pre_entries))
     m.sell.work = sell_work_.get() + pre_.size();
   if (fused_.b_val.size() && !m.sell.work) {  // fused B (x) I windows (one GPU, sorted rows)
     m.sell.b_slice_ptr = fused_.b_slice_ptr.get();
@@ -997,7 +1005,8 @@ dev::DevMatrix Liouvillian::matrix(int group_override) const {
     for (std::size_t q = 0; q < pre_.size(); ++q) {
       dev::SellView& v = m.sell_pre[q];
       v = m.sell;
-      v.work = wants_stream(pre_[q].perm.size() > 0, pre_[q].entries) ? sell_work_.get() + q : nullptr;
+      v.work = !pre_[q].b_val.size() && wants_stream(pre_[q].perm.size() > 0, pre_[q].entries) ? sell_work_.get() + q
+                                                                                                    : nullptr;
       v.slice_ptr = pre_[q].slice_ptr.get();
       v.col = pre_[q].col.get();
       v.val = pre_[q].val.get();
@@ -1625,7 +1634,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
       chunk *= 2;
     } while (static_cast<int>(ranges.size()) > dev::kMaxSellPanels);
   } else if (use_sell) {
-    bool fuse_ok = world == 1 && cfg.group != 1 && l->perm_.size() > 0 && !hops.b.empty() && sell_fuse_setting();
+    bool fuse_ok = world == 1 && cfg.group != 1 && l->perm_.size() > 0 && !hops.b.empty() && sell_fuse_setting(l->n_slices_);
     for (const MultiCsr& qk : hops.q)  // (the conditions of the fused B (x) I arrays below)
       for (std::int64_t i = 0; fuse_ok && i < qk.n; ++i)
         for (int k = qk.ptr[static_cast<std::size_t>(i)]; k < qk.ptr[static_cast<std::size_t>(i) + 1]; ++k)
@@ -1645,7 +1654,7 @@ std::unique_ptr<Liouvillian> LiouvillianBuilder::build(double omega, std::int64_
   // whose natural-order sums a block holds in shared memory.  B's diagonal stays with the
   // rest (it shares its position with A's diagonal), and every Q_k must be diagonal-free so
   // that no position is stored twice.
-  bool fuse = use_sell && world == 1 && cfg.group != 1 && l->perm_.size() > 0 && !hops.b.empty() && sell_fuse_setting();
+  bool fuse = use_sell && world == 1 && cfg.group != 1 && l->perm_.size() > 0 && !hops.b.empty() && sell_fuse_setting(l->n_slices_);
   for (const MultiCsr& qk : hops.q)
     for (std::int64_t i = 0; fuse && i < qk.n; ++i)
       for (int k = qk.ptr[static_cast<std::size_t>(i)]; k < qk.ptr[static_cast<std::size_t>(i) + 1]; ++k)

@@ -137,7 +137,7 @@ def test_random_walk_parity(port, seed):
 
 
 @pytest.mark.parametrize("seed", range(100, 100 + int(__import__("os").environ.get("QSWG_FUZZ_SEEDS", "8"))))
-def test_random_walk_parity_several_tiles(port, seed):
+def test_random_walk_parity_several_tiles(port, seed, monkeypatch):
     """The same sweep at sizes where the KRON tile grid has 2 - 5 tile rows with
     ragged edges (n = 64 ... 150), the sliced-ELL rows span several slices and
     sigma windows, and the series plans take more than one super-step: sparse
@@ -149,14 +149,20 @@ def test_random_walk_parity_several_tiles(port, seed):
     so, po, n_ref = o.series(inst["v0"], t1, tq, q)
     want, n_step = o.step(inst["v0"], tq)
     L_ref = o.csr()
-    for fmt, group in [("kron", 0), ("sell", 0), ("csr", 1)]:
+    # ("sell", 0) twice: the size-gated default, and with the fused natural-order B (x) I
+    # arrays forced (QSWG_SELL_FUSE=1; by default only large superoperators take them)
+    for fmt, group, fuse in [("kron", 0, None), ("sell", 0, None), ("sell", 0, "1"), ("csr", 1, None)]:
+        if fuse is None:
+            monkeypatch.delenv("QSWG_SELL_FUSE", raising=False)
+        else:
+            monkeypatch.setenv("QSWG_SELL_FUSE", fuse)
         l = build_gpu(inst, fmt, group)
         np.testing.assert_allclose(l.one_norms(), o.norms, rtol=1e-12, atol=1e-300)
         r = api.series(l, l.state().upload(inst["v0"]), t1, tq, q, states=True)
         err = float(np.abs(r.states - so).max())
-        assert err <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, group, err)
+        assert err <= RHO_TOL * max(1.0, float(np.abs(so).max())), (seed, fmt, group, fuse, err)
         got, info = api.step(l, l.state().upload(inst["v0"]), tq)
-        assert np.abs(got.gather() - want).max() <= RHO_TOL * max(1.0, float(np.abs(want).max())), (seed, fmt)
+        assert np.abs(got.gather() - want).max() <= RHO_TOL * max(1.0, float(np.abs(want).max())), (seed, fmt, fuse)
         if group == 1:
             same_L = bool(np.array_equal(l.gather_full().data, L_ref.data))
             slack_series, slack_step = (0, 0) if same_L else (q, int(info.s))

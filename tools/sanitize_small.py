@@ -28,8 +28,8 @@ def run(cfg, size, fmt, steps, **env):
 
 run("c5", 4, "sell", 3)                                   # streamed (short regular rows)
 run("c2", 8, "sell", 3)                                   # register path (long regular rows)
-run("c3", 96, "sell", 2)                                  # fused windows, several windows
-run("c4", 96, "sell", 2, QSWG_SELL_PANELS="3")            # fused windows + column panels
+run("c3", 96, "sell", 2, QSWG_SELL_FUSE="1")              # fused windows, several windows
+run("c4", 96, "sell", 2, QSWG_SELL_PANELS="3", QSWG_SELL_FUSE="1")  # fused windows + column panels
 run("c4", 96, "sell", 2, QSWG_SELL_PANELS="2", QSWG_SELL_FUSE="0")  # sorted register path + panels
 run("c2", 8, "kron", 3, QSWG_KRON_STAGED="1")             # staged tiles, factored
 run("c5", 4, "kron", 3, QSWG_KRON_STAGED="1")             # staged tiles, L-QSW
