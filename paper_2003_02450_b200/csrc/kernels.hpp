@@ -218,9 +218,10 @@ struct KronView {
   //   pattern 0  F(T, J), T in st_nbr[0][I]   rows c of R_0 / A, lane = j
   //   pattern 1  F(I, T), T in st_nbr[1][J]   columns a of P_0 / B, lane = j
   //   pattern 2  F(T, I), T in st_nbr[2][J]   rows c of S_0, lane = i
-  // which the staged term kernel brings into shared memory with bulk copies
-  // (512-byte tile rows, one mbarrier per phase) before any arithmetic, so the
-  // operand-index -> gather -> FMA chains run against shared memory.
+  // which the staged term kernel copies into shared memory a tile ahead
+  // (cp.async, 16 bytes per thread, one copy group per phase), so the
+  // operand-index -> gather -> FMA chains run against shared memory.  Opt-in
+  // (QSWG_KRON_STAGED=1): measured slower than the global gathers.
   // st_col[p]: the operand's ELL column array (layout of r_ellu[0] / a_ellu,
   // p_ell[0] / b_ell, s_ellu[0]) with every column replaced by its element
   // offset inside the pattern's shared-memory region.
@@ -229,10 +230,6 @@ struct KronView {
   const int* st_nbr[3] = {};      // [n / 32][kStageSlots] tile indices, -1 = none
   const int* st_col[3] = {};
   int st_len[3] = {};             // row length of each pattern's operand (the same in every row, <= 8)
-  // The W kernel likewise (pattern 0 of F = x for Q_0).
-  int st_slots_q = 0;
-  const int* st_nbr_q = nullptr;
-  const int* st_col_q = nullptr;
   const double2* aq_ellu_val = nullptr;
   const double2* aq_sc_val = nullptr;
   int vk_aq = kValComplex;
