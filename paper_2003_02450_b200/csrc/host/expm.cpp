@@ -240,7 +240,23 @@ StepParameters enqueue_step(const Exec& ex, const double2* v, double t, const Ta
   }
   launches += 1 + sp.s * sp.m_star * (1 + (mat.format == dev::Format::Kron ? mat.kron.nk * (1 + (mat.kron.factored && !mat.kron.herm)) : 0));
   const double s_count = static_cast<double>(sp.s);
+  // One GPU, very many stages (a huge ||t L||: test_expm.cpp:234-244 reaches 10^5 stages before
+  // it overflows): the error flag is polled every kErrStride stages, lagged like the stop
+  // flags of several GPUs, so a step that has already failed stops being enqueued.  Not under
+  // stream capture (events of a capture cannot be queried).
+  constexpr std::int64_t kErrStride = 64, kErrMinStages = 512;
+  std::unique_ptr<FlagPoll> err_poll;
+  if (ex.single && sp.s >= kErrMinStages) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    QSWG_CHECK(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusNone) err_poll = std::make_unique<FlagPoll>();
+  }
   for (std::int64_t st = 0; st < sp.s; ++st) {
+    if (err_poll && st % kErrStride == 0) {
+      int err = 0, tag = 0;
+      if (err_poll->lagged(err, tag) && err != 0) break;  // failed kLag polls ago: step() reports it
+      err_poll->record(&ctl->error, static_cast<int>(st / kErrStride), s);
+    }
     // stage input: v, then the previous stage's sum (term = sum, expm.cpp:197-205)
     const double2* x_stage = st == 0 ? v : sums[(st - 1) % 2];
     const double2* x_stage_full = ex.spmv_input(x_stage, kXStage);
